@@ -1,0 +1,230 @@
+/*
+ * vsb200.h -- C ABI of the B200-native SLAMCast hot path (libvsb200.so).
+ *
+ * This is the drop-in boundary for three pieces of the reference package
+ * `voxelstream` (pure Python, /root/reference/pkg/src/voxelstream):
+ *
+ *   1. the concurrent block hash set / map      (concurrent_hash.py:49-491)
+ *   2. the Marching-Cubes block encoder         (mc_encoding.py:83-172,
+ *      TSDF block layout voxel_model.py:23-72)
+ *   3. the per-client stream-set update         (server.py:49-95, 221-249,
+ *      299-315, 425-436)
+ *
+ * Conventions
+ *   - Every pointer argument is a DEVICE pointer unless its name ends in
+ *     `_host`.  Keys are int32[n][3] (x, y, z), little-endian, exactly the
+ *     wire layout `<3i` (wire.py:37).
+ *   - Every call is asynchronous on the given CUDA stream (pass NULL for the
+ *     legacy default stream) unless documented as synchronous.
+ *   - All operations on ONE table must be stream-ordered (one stream, or
+ *     streams ordered with events): erased excess entries are recycled into
+ *     the free-list stack only between launches, which is what makes the
+ *     lock-free readers inside a launch safe ("hash").
+ *     Within a launch, any mix of insert / find / erase on any keys is
+ *     thread-safe and keeps keys unique.
+ *   - Status codes are returned, never thrown.  vs_last_error() gives a
+ *     thread-local message for the last non-OK status.
+ */
+#ifndef VSB200_H
+#define VSB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *vs_stream_t; /* == cudaStream_t */
+
+typedef int32_t vs_status;
+enum {
+  VS_OK = 0,
+  VS_ERR_CAPACITY = 1, /* CapacityExhausted (concurrent_hash.py:45-46,193-197) */
+  VS_ERR_INVALID = 2,  /* ValueError (concurrent_hash.py:96-101)             */
+  VS_ERR_CUDA = 3,     /* CUDA runtime failure                               */
+  VS_ERR_OVERFLOW = 4  /* an output buffer was too small; output truncated   */
+};
+
+/* Op codes of vs_table_apply (mixed batches). */
+enum { VS_OP_INSERT = 0, VS_OP_FIND = 1, VS_OP_ERASE = 2 };
+
+/* Sizes of the data formats (voxel_model.py:23-31, mc_encoding.py:34-37). */
+#define VS_BLOCK_VOXELS 512
+#define VS_TSDF_BLOCK_BYTES 6144 /* 512 x {f32 tsdf, f32 weight, u8 rgb[3], u8 pad} */
+#define VS_MC_BLOCK_BYTES 2048   /* 512 x {u8 index, u8 rgb[3]}                      */
+
+const char *vs_last_error(void);
+int32_t vs_abi_version(void);
+
+/* ---------------------------------------------------------------- hash --- */
+
+/* hash_key (concurrent_hash.py:49-59): bucket = (x*p1 ^ y*p2 ^ z*p3) mod n,
+ * products wrapping in uint32.  out[i] in [0, bucket_count). */
+vs_status vs_hash_keys(const int32_t *keys, uint64_t n, uint32_t bucket_count,
+                       uint32_t *out, vs_stream_t stream);
+
+/* One table serves both BlockHashSet and BlockHashMap (the reference shares
+ * _HashCore, concurrent_hash.py:85-120).  Map payloads live in caller-owned
+ * arrays indexed by the returned entry position, exactly as the reference's
+ * parallel `_values` list (concurrent_hash.py:112; SPEC.md "Map payloads live
+ * in a parallel array indexed like entries").  Positions are stable while a
+ * key is present (concurrent_hash.py:8-13).
+ *
+ * bucket_count >= 1, excess_capacity >= 1 (else VS_ERR_INVALID, like
+ * concurrent_hash.py:96-99); bucket_count + excess_capacity < 2^31 and
+ * excess_capacity < 2^29 (entry-offset field width). */
+typedef struct vs_table vs_table;
+
+vs_status vs_table_create(uint64_t bucket_count, uint64_t excess_capacity,
+                          int device, vs_table **out);
+vs_status vs_table_destroy(vs_table *t);
+vs_status vs_table_info(const vs_table *t, uint64_t *bucket_count_host,
+                        uint64_t *excess_capacity_host, uint64_t *capacity_host);
+
+/* _insert_pos / BlockHashSet.insert / BlockHashMap.insert
+ * (concurrent_hash.py:159-208, 361-364, 418-425).  created[i] = 1 for the
+ * LOWEST input index among in-batch duplicates of a key that was absent
+ * before the batch (= sequential replay); index[i] = entry position.  An op
+ * that needed an excess entry when the free list was empty gets index -1,
+ * created 0, and the table's sticky capacity flag is raised (see
+ * vs_table_check).  The table is unchanged for that op. */
+vs_status vs_table_insert(vs_table *t, const int32_t *keys, uint64_t n,
+                          uint8_t *created, int32_t *index, vs_stream_t stream);
+
+/* _find / __contains__ / BlockHashMap.get (concurrent_hash.py:146-157,
+ * 297-298, 449-460).  Read-only.  index[i] = position or -1. */
+vs_status vs_table_find(vs_table *t, const int32_t *keys, uint64_t n,
+                        uint8_t *found, int32_t *index, vs_stream_t stream);
+
+/* remove (concurrent_hash.py:251-295).  erased[i] = 1 if the key was present;
+ * index[i] = the position it occupied (so map payload slots can be cleared),
+ * else -1. */
+vs_status vs_table_erase(vs_table *t, const int32_t *keys, uint64_t n,
+                         uint8_t *erased, int32_t *index, vs_stream_t stream);
+
+/* Mixed batch in ONE launch: ops[i] in {VS_OP_INSERT, VS_OP_FIND, VS_OP_ERASE};
+ * result[i] = created / found / erased.  Per-op results equal a sequential
+ * replay when no key whose membership changes in the batch appears in any
+ * other op except duplicate inserts of itself; any batch
+ * is safe (keys stay unique). */
+vs_status vs_table_apply(vs_table *t, const int32_t *keys, const uint8_t *ops,
+                         uint64_t n, uint8_t *result, int32_t *index,
+                         vs_stream_t stream);
+
+/* SYNCHRONOUS: returns VS_ERR_CAPACITY (and clears the flag) if any insert
+ * since the last check hit an empty free list, else VS_OK. */
+vs_status vs_table_check(vs_table *t, vs_stream_t stream);
+
+/* approx_size (concurrent_hash.py:311-313): live-key count, device counter.
+ * size_dev may be NULL; size_host (may be NULL) makes the call synchronous. */
+vs_status vs_table_size(vs_table *t, uint64_t *size_dev, uint64_t *size_host,
+                        vs_stream_t stream);
+/* Free excess entries (len(free_stack)), synchronous. */
+vs_status vs_table_free_count(vs_table *t, uint64_t *free_host, vs_stream_t stream);
+
+/* clear (concurrent_hash.py:315-322): quiescent bulk reset. */
+vs_status vs_table_clear(vs_table *t, vs_stream_t stream);
+
+/* snapshot_keys / snapshot_items (concurrent_hash.py:300-309, 483-491):
+ * live keys in ascending entry-position order.  Writes at most `cap` records;
+ * *n_dev = number of live keys (may exceed cap -> VS_ERR_OVERFLOW is NOT
+ * reported asynchronously; compare *n_dev with cap). index_out may be NULL. */
+vs_status vs_table_snapshot(vs_table *t, int32_t *keys_out, int32_t *index_out,
+                            uint64_t cap, uint64_t *n_dev, vs_stream_t stream);
+
+/* extract_batch (concurrent_hash.py:366-402): remove and return up to max_n
+ * keys, scanning occupied entries from a rotating start position derived from
+ * `seed` (the reference uses random.randrange).  *n_dev = number returned. */
+vs_status vs_table_extract(vs_table *t, uint64_t max_n, uint64_t seed,
+                           int32_t *keys_out, uint64_t *n_dev, vs_stream_t stream);
+
+/* Integrity check for tests (replaces the reference's white-box checks,
+ * tests/test_concurrent_hash.py:113,124-126,379-383).  SYNCHRONOUS.
+ * out_host[0] = live entries found by a full scan
+ * out_host[1] = entries reachable from bucket chains (excess, any occupancy)
+ * out_host[2] = free-list stack size
+ * out_host[3] = duplicate live keys found (must be 0)
+ * out_host[4] = live entries NOT reachable from their own bucket (must be 0)
+ * out_host[5] = free-list entries that are also reachable (must be 0)  */
+vs_status vs_table_audit(vs_table *t, uint64_t out_host[6], vs_stream_t stream);
+
+/* ------------------------------------------------------------ MC encode --- */
+
+/* TSDF pool: caller-owned rows of VS_TSDF_BLOCK_BYTES in the wire layout
+ * (TsdfBlock.to_bytes, voxel_model.py:55-60); row r at pool + r*6144, 16-byte
+ * aligned.  nbr[i][c] = pool row of TSDF block key_i + (c&1, c>>1&1, c>>2&1)
+ * or -1 if absent (c = 0 is the block itself).
+ *
+ * recompute_mc_block (mc_encoding.py:145-172) for n blocks:
+ *   mc_out[i]  : 2048 B McBlock.to_bytes() (interleaved {index, r, g, b})
+ *   q_out[i]   : 512 int8 quantised TSDF of block i (A17; NEW)
+ *   counts[i]  : number of voxels with index != 0
+ * Any of mc_out / q_out / counts may be NULL to skip that output. */
+vs_status vs_mc_encode(const uint8_t *pool, const int32_t *nbr, uint64_t n,
+                       uint8_t *mc_out, int8_t *q_out, uint32_t *counts,
+                       vs_stream_t stream);
+
+/* Same, but the neighbour rows come from hash lookups of keys[i] + delta in
+ * `tsdf_table`, whose entry positions index `pool` (the TSDF map's parallel
+ * payload array).  This is where the hash feeds the encoder. */
+vs_status vs_mc_encode_keys(const vs_table *tsdf_table, const uint8_t *pool,
+                            const int32_t *keys, uint64_t n, uint8_t *mc_out,
+                            int8_t *q_out, uint32_t *counts, vs_stream_t stream);
+
+/* Neighbour table only: nbr_out[i][c] as defined above (8 batched finds). */
+vs_status vs_mc_neighbors(const vs_table *tsdf_table, const int32_t *keys,
+                          uint64_t n, int32_t *nbr_out, vs_stream_t stream);
+
+/* Stream compaction of non-empty cells (NEW format):
+ * offsets[0..n] = exclusive prefix of counts (offsets[n] = total);
+ * cell_flat[j] = flat voxel index (x + 8y + 64z), cell_mc[j] = the 4 MC
+ * bytes {index, r, g, b} as a little-endian u32; blocks in input order,
+ * cells in ascending flat index.  Reads mc (dense) and counts.  Writes at
+ * most cell_cap cells.  work_dev: scratch of >= vs_scan_workspace_bytes(n). */
+vs_status vs_mc_compact(const uint8_t *mc, const uint32_t *counts, uint64_t n,
+                        uint64_t *offsets, uint16_t *cell_flat, uint32_t *cell_mc,
+                        uint64_t cell_cap, void *work_dev, vs_stream_t stream);
+uint64_t vs_scan_workspace_bytes(uint64_t n);
+
+/* ----------------------------------------------------------- stream sets --- */
+
+/* affected_mc_blocks (mc_encoding.py:108-115) for u updated keys, with the
+ * ordered first-occurrence dedup of Server.on_tsdf_batch (server.py:304-307).
+ * out_keys receives <= 8u keys; *n_dev = count.  `scratch` is a table used
+ * as the dedup set; it is cleared by the call. */
+vs_status vs_affected_dedup(vs_table *scratch, const int32_t *updated, uint64_t u,
+                            int32_t *out_keys, uint64_t *n_dev, vs_stream_t stream);
+
+/* StreamSet.insert_many over C client sets (server.py:62-69, 314-315):
+ * inserts the same n keys into every set; created[c*n + i] per client; each
+ * client's newly created keys are appended, in input order, to its
+ * generation-order FIFO ring (server.py:63-64).
+ * fifo_keys[c]  : device int32[fifo_cap[c]][3] ring of client c
+ * fifo_tail     : device uint64[C] (absolute, monotonically increasing)
+ * n_created     : device uint64[C] (may be NULL). */
+vs_status vs_stream_insert_many(vs_table *const *sets_host, int n_sets,
+                                const int32_t *keys, uint64_t n, uint8_t *created,
+                                int32_t *const *fifo_keys_host,
+                                const uint64_t *fifo_cap_host, uint64_t *fifo_tail,
+                                uint64_t *n_created, vs_stream_t stream);
+
+/* Bulk remove of n keys from every one of n_sets tables (on_reset_blocks,
+ * server.py:425-436).  erased may be NULL or device uint8[n_sets*n]. */
+vs_status vs_stream_remove_many(vs_table *const *sets_host, int n_sets,
+                                const int32_t *keys, uint64_t n, uint8_t *erased,
+                                vs_stream_t stream);
+
+/* extract_ordered (server.py:86-95): pop keys from the FIFO ring
+ * [*head, tail), keep those whose removal from `set` succeeds, stop after
+ * max_n successes.  Exact deque semantics, stale entries skipped.
+ * head_host/tail_host are in/out (synchronous call). */
+vs_status vs_stream_extract_ordered(vs_table *set, const int32_t *fifo_keys,
+                                    uint64_t fifo_cap, uint64_t *head_host,
+                                    uint64_t tail_host, uint64_t max_n,
+                                    int32_t *keys_out, uint64_t *n_out_host,
+                                    vs_table *scratch, vs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VSB200_H */

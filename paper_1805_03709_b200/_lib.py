@@ -1,0 +1,140 @@
+"""ctypes binding of libvsb200.so (the C ABI declared in include/vsb200.h).
+
+The shared library is built in-tree by ``paper_1805_03709_b200.build``.  There
+is deliberately no CPU fallback: if the library or a CUDA device is missing,
+every product entry point raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import threading
+
+LIB_PATH = pathlib.Path(__file__).resolve().with_name("libvsb200.so")
+HEADER_PATH = pathlib.Path(__file__).resolve().parent.parent / "include" / "vsb200.h"
+
+VS_OK = 0
+VS_ERR_CAPACITY = 1
+VS_ERR_INVALID = 2
+VS_ERR_CUDA = 3
+VS_ERR_OVERFLOW = 4
+
+VS_OP_INSERT = 0
+VS_OP_FIND = 1
+VS_OP_ERASE = 2
+
+
+class NativeUnavailable(RuntimeError):
+    """libvsb200.so (or a CUDA device) is not available; no fallback exists."""
+
+
+class CapacityExhausted(RuntimeError):
+    """Raised when an insert needs an excess entry and the free list is empty.
+
+    Same name and base class as the reference (concurrent_hash.py:45-46).
+    """
+
+
+_vp = ctypes.c_void_p
+_u64 = ctypes.c_uint64
+_u32 = ctypes.c_uint32
+_i32 = ctypes.c_int32
+_pu64 = ctypes.POINTER(ctypes.c_uint64)
+
+# name -> (restype, argtypes); mirrors include/vsb200.h one to one
+SIGNATURES: dict[str, tuple] = {
+    "vs_last_error": (ctypes.c_char_p, []),
+    "vs_abi_version": (_i32, []),
+    "vs_hash_keys": (_i32, [_vp, _u64, _u32, _vp, _vp]),
+    "vs_table_create": (_i32, [_u64, _u64, ctypes.c_int, ctypes.POINTER(_vp)]),
+    "vs_table_destroy": (_i32, [_vp]),
+    "vs_table_info": (_i32, [_vp, _pu64, _pu64, _pu64]),
+    "vs_table_insert": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp]),
+    "vs_table_find": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp]),
+    "vs_table_erase": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp]),
+    "vs_table_apply": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),
+    "vs_table_check": (_i32, [_vp, _vp]),
+    "vs_table_size": (_i32, [_vp, _vp, _pu64, _vp]),
+    "vs_table_free_count": (_i32, [_vp, _pu64, _vp]),
+    "vs_table_clear": (_i32, [_vp, _vp]),
+    "vs_table_snapshot": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp]),
+    "vs_table_extract": (_i32, [_vp, _u64, _u64, _vp, _vp, _vp]),
+    "vs_table_audit": (_i32, [_vp, ctypes.POINTER(ctypes.c_uint64 * 6), _vp]),
+    "vs_mc_encode": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp, _vp]),
+    "vs_mc_encode_keys": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
+    "vs_mc_neighbors": (_i32, [_vp, _vp, _u64, _vp, _vp]),
+    "vs_mc_compact": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp, _u64, _vp, _vp]),
+    "vs_scan_workspace_bytes": (_u64, [_u64]),
+    "vs_affected_dedup": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp]),
+    "vs_stream_insert_many": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _vp, _u64, _vp,
+                                     ctypes.POINTER(_vp), _pu64, _vp, _vp, _vp]),
+    "vs_stream_remove_many": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _vp, _u64, _vp, _vp]),
+    "vs_stream_extract_ordered": (_i32, [_vp, _vp, _u64, _pu64, _u64, _u64, _vp, _pu64, _vp, _vp]),
+}
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+
+def load() -> ctypes.CDLL:
+    """Load (once) and type the native library; raise loudly if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise NativeUnavailable(
+                f"{LIB_PATH} is missing: run `python -m paper_1805_03709_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    msg = load().vs_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a vs_status to the reference's exception types."""
+    if status == VS_OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if status == VS_ERR_CAPACITY:
+        raise CapacityExhausted(msg)
+    if status == VS_ERR_INVALID:
+        raise ValueError(msg)
+    raise RuntimeError(f"libvsb200 status {status}: {msg}")
+
+
+def require_cuda():
+    """Import torch and insist on a CUDA device (the product path is GPU-only)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device: libvsb200 has no CPU fallback")
+    load()
+    return torch
+
+
+def ptr(t) -> ctypes.c_void_p:
+    """Raw data pointer of a torch tensor (or None for NULL)."""
+    if t is None:
+        return ctypes.c_void_p(None)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def stream_of(device) -> ctypes.c_void_p:
+    import torch
+
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)

@@ -1,0 +1,132 @@
+// common.cuh -- shared device definitions for libvsb200 (sm_100a).
+//
+// Entry layout (one 16-byte aligned entry per table position):
+//   int32 x, y, z   the block key (full int32 range; no sentinel value exists,
+//                   SURVEY.md §7.3 item 1, so all state lives in `meta`)
+//   uint32 meta     bit 31 LOCK   per-bucket writer lock (bucket entries only)
+//                   bit 30 OCC    occupied           (reference `_occ`, concurrent_hash.py:108)
+//                   bit 29 FRESH  created in the running launch (created-flag fixup)
+//                   bits 0-28 NEXT  excess offset + 1 of the next chain entry,
+//                                 0 = end of chain   (reference `_next`, :109-111)
+// Positions [0, n) are buckets, [n, n + excess) the excess region, exactly as
+// the reference (concurrent_hash.py:104-115).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vsb {
+
+constexpr uint32_t kLock = 0x80000000u;
+constexpr uint32_t kOcc = 0x40000000u;
+constexpr uint32_t kFresh = 0x20000000u;
+constexpr uint32_t kNext = 0x1FFFFFFFu;
+
+// Spatial hash primes, concurrent_hash.py:38-40 (normative).
+constexpr uint32_t kP1 = 73856093u;
+constexpr uint32_t kP2 = 19349669u;
+constexpr uint32_t kP3 = 83492791u;
+
+struct __align__(16) Entry {
+  int32_t x, y, z;
+  uint32_t meta;
+};
+
+// Device control block of one table.
+struct Ctl {
+  long long free_top;            // entries in the free-list stack
+  unsigned long long retired_n;  // excess entries erased in the running launch
+  unsigned long long size;       // live keys (approx_size)
+  unsigned int error;            // sticky: bit 0 = capacity exhausted
+  unsigned int pad;
+  unsigned long long aux[4];     // scratch counters for multi-kernel ops
+};
+
+// By-value view passed to kernels.
+struct TableView {
+  Entry* e;
+  uint32_t* free_stack;  // [excess] absolute positions
+  uint32_t* retired;     // [excess] erased excess positions, recycled after the launch
+  int32_t* first_op;     // [cap] lowest op index per freshly created entry
+  Ctl* ctl;
+  uint32_t n;            // bucket_count
+  uint32_t excess;
+  uint64_t magic;        // Lemire fastmod constant for n
+};
+
+// hash_key (concurrent_hash.py:49-59): uint32 wrapping products, XOR.
+__host__ __device__ __forceinline__ uint32_t hash_raw(int32_t x, int32_t y, int32_t z) {
+  return ((uint32_t)x * kP1) ^ ((uint32_t)y * kP2) ^ ((uint32_t)z * kP3);
+}
+
+__host__ __forceinline__ uint64_t fastmod_magic(uint32_t d) {
+  return UINT64_C(0xFFFFFFFFFFFFFFFF) / d + 1;
+}
+
+// a mod d for 32-bit a, d (exact; Lemire et al. 2019).
+__device__ __forceinline__ uint32_t fastmod(uint32_t a, uint64_t M, uint32_t d) {
+  uint64_t lowbits = M * a;
+  return (uint32_t)__umul64hi(lowbits, (uint64_t)d);
+}
+
+__device__ __forceinline__ uint32_t bucket_of(const TableView& T, int32_t x, int32_t y, int32_t z) {
+  return fastmod(hash_raw(x, y, z), T.magic, T.n);
+}
+
+// ---- memory access helpers (L2-coherent; the table mutates inside a launch)
+
+__device__ __forceinline__ int4 ld_entry(const Entry* p) {
+  int4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_entry(Entry* p, int32_t x, int32_t y, int32_t z, uint32_t meta) {
+  asm volatile("st.relaxed.gpu.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(x), "r"(y),
+               "r"(z), "r"(meta)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t atom_or_acquire(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acquire.gpu.global.or.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ uint32_t atom_and_release(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.release.gpu.global.and.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ uint32_t atom_exch_release(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ bool key_eq(const int4& s, int32_t x, int32_t y, int32_t z) {
+  return s.x == x && s.y == y && s.z == z;
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+inline unsigned grid_for(uint64_t n, unsigned block) {
+  uint64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+}  // namespace vsb

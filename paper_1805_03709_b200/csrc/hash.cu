@@ -1,0 +1,672 @@
+// hash.cu -- batched kernels and C ABI of the block hash set/map.
+//
+// Reference: concurrent_hash.py (all of it).  Per-op algorithms live in
+// hash_ops.cuh; this file holds the launches: one thread per op, every op
+// type in one launch if wanted (vs_table_apply), followed by
+//   k_fixup_created  -- gives `created` to the lowest op index among in-batch
+//                       duplicates, i.e. the sequential-replay answer;
+//   k_flush_retired  -- recycles erased excess entries into the free stack
+//                       (FreeListStack.push, concurrent_hash.py:72-73).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "hash_ops.cuh"
+#include "table.h"
+
+namespace vsb {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+vs_status cuda_status(cudaError_t err, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(err);
+  return VS_ERR_CUDA;
+}
+
+constexpr int kOpBlock = 256;
+
+// ---------------------------------------------------------------- kernels
+
+__global__ void k_hash_keys(const int32_t* __restrict__ keys, uint64_t n, uint32_t nb,
+                            uint32_t* __restrict__ out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = hash_raw(keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]) % nb;
+}
+
+__global__ void k_init_free(uint32_t* __restrict__ stack, uint32_t n, uint32_t excess) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < excess;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    stack[i] = n + (uint32_t)i;  // FreeListStack(range(n, cap)): first pop = cap-1
+}
+
+__global__ void k_reset_ctl(Ctl* ctl, uint32_t excess) {
+  ctl->free_top = excess;
+  ctl->retired_n = 0;
+  ctl->size = 0;
+  ctl->error = 0;
+}
+
+__global__ void __launch_bounds__(kOpBlock) k_insert(TableView T, const int32_t* __restrict__ keys, uint64_t n,
+                                                     uint8_t* __restrict__ created, int32_t* __restrict__ index) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int delta = 0;
+  if (i < n) {
+    const int32_t x = keys[3 * i], y = keys[3 * i + 1], z = keys[3 * i + 2];
+    const InsertResult r = insert_key(T, x, y, z, (int32_t)i);
+    created[i] = r.created;
+    index[i] = r.pos;
+    delta = r.created;
+  }
+  add_size(T, delta);
+}
+
+__global__ void __launch_bounds__(kOpBlock) k_find(TableView T, const int32_t* __restrict__ keys, uint64_t n,
+                                                   uint8_t* __restrict__ found, int32_t* __restrict__ index) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t x = keys[3 * i], y = keys[3 * i + 1], z = keys[3 * i + 2];
+  uint32_t meta;
+  const int32_t pos = find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
+  found[i] = pos >= 0;
+  index[i] = pos;
+}
+
+__global__ void __launch_bounds__(kOpBlock) k_erase(TableView T, const int32_t* __restrict__ keys, uint64_t n,
+                                                    const uint64_t* __restrict__ n_dev,
+                                                    uint8_t* __restrict__ erased, int32_t* __restrict__ index) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n_dev) n = *n_dev < n ? *n_dev : n;
+  int delta = 0;
+  if (i < n) {
+    const int32_t pos = erase_key(T, keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]);
+    if (erased) erased[i] = pos >= 0;
+    if (index) index[i] = pos;
+    delta = -(pos >= 0);
+  }
+  add_size(T, delta);
+}
+
+__global__ void __launch_bounds__(kOpBlock) k_apply(TableView T, const int32_t* __restrict__ keys,
+                                                    const uint8_t* __restrict__ ops, uint64_t n,
+                                                    uint8_t* __restrict__ result, int32_t* __restrict__ index) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int delta = 0;
+  if (i < n) {
+    const int32_t x = keys[3 * i], y = keys[3 * i + 1], z = keys[3 * i + 2];
+    const uint8_t op = ops[i];
+    int32_t pos;
+    uint8_t res;
+    if (op == VS_OP_INSERT) {
+      const InsertResult r = insert_key(T, x, y, z, (int32_t)i);
+      pos = r.pos;
+      res = r.created;
+      delta = r.created;
+    } else if (op == VS_OP_ERASE) {
+      pos = erase_key(T, x, y, z);
+      res = pos >= 0;
+      delta = -(int)res;
+    } else {
+      uint32_t meta;
+      pos = find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
+      res = pos >= 0;
+    }
+    result[i] = res;
+    index[i] = pos;
+  }
+  add_size(T, delta);
+}
+
+// created[i] goes to the lowest op index that inserted the same key in this
+// batch (sequential replay: the first occurrence creates, later ones find).
+__global__ void k_fixup_created(TableView T, const int32_t* __restrict__ keys, const uint8_t* __restrict__ ops,
+                                uint64_t n, uint8_t* __restrict__ created, const int32_t* __restrict__ index) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (ops && ops[i] != VS_OP_INSERT) return;
+  if (!created[i]) return;
+  const int32_t pos = index[i];
+  atomicAnd(&T.e[pos].meta, ~kFresh);
+  const int32_t m = T.first_op[pos];
+  if (m >= 0 && (uint64_t)m < i && keys[3 * (uint64_t)m] == keys[3 * i] &&
+      keys[3 * (uint64_t)m + 1] == keys[3 * i + 1] && keys[3 * (uint64_t)m + 2] == keys[3 * i + 2]) {
+    created[i] = 0;
+    created[m] = 1;
+  }
+}
+
+__global__ void k_flush_retired(TableView T) {
+  const unsigned long long r = T.ctl->retired_n;
+  const long long top = T.ctl->free_top;
+  for (unsigned long long j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < r;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    T.free_stack[top + (long long)j] = T.retired[j];
+}
+
+__global__ void k_flush_final(Ctl* ctl) {
+  ctl->free_top += (long long)ctl->retired_n;
+  ctl->retired_n = 0;
+}
+
+// ---- ordered compaction of live entries (snapshot_keys / extract_batch)
+
+__global__ void __launch_bounds__(256) k_chunk_count(TableView T, uint32_t cap, uint32_t* __restrict__ counts) {
+  const uint64_t base = (uint64_t)blockIdx.x * kChunk;
+  uint32_t c = 0;
+  for (uint32_t j = threadIdx.x; j < kChunk; j += blockDim.x) {
+    const uint64_t p = base + j;
+    if (p < cap) c += (T.e[p].meta & kOcc) ? 1u : 0u;
+  }
+  __shared__ uint32_t red[8];
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane_id() == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s = 0;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    counts[blockIdx.x] = s;
+  }
+}
+
+// Single-CTA exclusive scan of a u32 array into u64 offsets[0..n].
+__global__ void __launch_bounds__(1024) k_scan_u32(const uint32_t* __restrict__ in, uint64_t n,
+                                                   uint64_t* __restrict__ out) {
+  __shared__ uint64_t warp_sums[32];
+  __shared__ uint64_t carry_s;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (uint64_t base = 0; base < n; base += 1024) {
+    const uint64_t i = base + threadIdx.x;
+    const uint64_t v = i < n ? in[i] : 0;
+    uint64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((int)lane_id() >= o) x += y;
+    }
+    if (lane_id() == 31) warp_sums[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint64_t w = warp_sums[threadIdx.x];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if ((int)lane_id() >= o) w += y;
+      }
+      warp_sums[threadIdx.x] = w;  // inclusive
+    }
+    __syncthreads();
+    const uint64_t carry = carry_s;
+    const uint64_t wpre = (threadIdx.x >> 5) ? warp_sums[(threadIdx.x >> 5) - 1] : 0;
+    if (i < n) out[i] = carry + wpre + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + warp_sums[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry_s;
+}
+
+__global__ void __launch_bounds__(256) k_chunk_write(TableView T, uint32_t cap, const uint64_t* __restrict__ offsets,
+                                                     int32_t* __restrict__ keys_out, int32_t* __restrict__ pos_out,
+                                                     uint64_t out_cap) {
+  __shared__ uint32_t wcnt[8];
+  const uint64_t base = (uint64_t)blockIdx.x * kChunk;
+  uint64_t running = offsets[blockIdx.x];
+  const uint32_t warp = threadIdx.x >> 5;
+  for (uint32_t j = 0; j < kChunk; j += 256) {
+    const uint64_t p = base + j + threadIdx.x;
+    int4 s = make_int4(0, 0, 0, 0);
+    bool occ = false;
+    if (p < cap) {
+      s = ld_entry(T.e + p);
+      occ = ((uint32_t)s.w & kOcc) != 0;
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, occ);
+    if (lane_id() == 0) wcnt[warp] = __popc(bal);
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+    for (uint32_t w = 0; w < 8; ++w) {
+      const uint32_t c = wcnt[w];
+      before += (w < warp) ? c : 0;
+      total += c;
+    }
+    if (occ) {
+      const uint64_t o = running + before + __popc(bal & lanemask_lt());
+      if (o < out_cap) {
+        if (keys_out) {
+          keys_out[3 * o] = s.x;
+          keys_out[3 * o + 1] = s.y;
+          keys_out[3 * o + 2] = s.z;
+        }
+        if (pos_out) pos_out[o] = (int32_t)p;
+      }
+    }
+    running += total;
+    __syncthreads();
+  }
+}
+
+__global__ void k_copy_total(const uint64_t* __restrict__ offsets, uint32_t nchunks, uint64_t* __restrict__ n_dev) {
+  *n_dev = offsets[nchunks];
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// extract_batch selection (concurrent_hash.py:387-399): rotate the ascending
+// list of live positions at a random start and take the first max_n.
+__global__ void k_extract_select(TableView T, uint32_t cap, const int32_t* __restrict__ pos,
+                                 const uint64_t* __restrict__ total_p, uint64_t max_n, uint64_t seed,
+                                 int32_t* __restrict__ keys_out, uint64_t* __restrict__ n_out) {
+  __shared__ uint64_t split_s;
+  const uint64_t total = *total_p;
+  const uint64_t m = total < max_n ? total : max_n;
+  if (threadIdx.x == 0) {
+    const uint32_t start = (uint32_t)(splitmix64(seed) % cap);
+    uint64_t lo = 0, hi = total;  // first index with pos >= start (np.searchsorted)
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if ((uint32_t)pos[mid] < start) lo = mid + 1; else hi = mid;
+    }
+    split_s = lo;
+    if (blockIdx.x == 0) *n_out = m;
+  }
+  __syncthreads();
+  const uint64_t split = split_s;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k = split + j;
+    if (k >= total) k -= total;
+    const int4 s = ld_entry(T.e + pos[k]);
+    keys_out[3 * j] = s.x;
+    keys_out[3 * j + 1] = s.y;
+    keys_out[3 * j + 2] = s.z;
+  }
+}
+
+// ---- audit (white-box invariants; tests only)
+
+__global__ void k_audit(TableView T, uint32_t cap, uint8_t* __restrict__ reach, unsigned long long* __restrict__ out) {
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  // chains: mark reachable excess entries
+  for (uint64_t b = tid; b < T.n; b += stride) {
+    uint32_t meta = T.e[b].meta;
+    uint32_t hops = 0;
+    while ((meta & kNext) && hops < T.excess + 1) {
+      const uint32_t e = T.n + (meta & kNext) - 1;
+      if (reach[e]) atomicAdd(&out[6], 1ull);  // reached twice: chains merged
+      reach[e] = 1;
+      atomicAdd(&out[1], 1ull);
+      meta = T.e[e].meta;
+      ++hops;
+    }
+  }
+  // live entries: unique and reachable from their own bucket
+  for (uint64_t p = tid; p < cap; p += stride) {
+    const Entry s = T.e[p];
+    if (!(s.meta & kOcc)) continue;
+    atomicAdd(&out[0], 1ull);
+    const uint32_t b = bucket_of(T, s.x, s.y, s.z);
+    uint32_t e = b, copies = 0, hops = 0;
+    bool seen_self = false;
+    for (;;) {
+      const Entry c = T.e[e];
+      if ((c.meta & kOcc) && c.x == s.x && c.y == s.y && c.z == s.z) {
+        ++copies;
+        if (e == p) seen_self = true;
+      }
+      if (!(c.meta & kNext) || ++hops > T.excess + 1) break;
+      e = T.n + (c.meta & kNext) - 1;
+    }
+    if (copies != 1) atomicAdd(&out[3], 1ull);
+    if (!seen_self) atomicAdd(&out[4], 1ull);
+  }
+}
+
+__global__ void k_audit_free(TableView T, const uint8_t* __restrict__ reach, unsigned long long* __restrict__ out) {
+  const long long top = T.ctl->free_top;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < top; j += (long long)gridDim.x * blockDim.x) {
+    const uint32_t e = T.free_stack[j];
+    if (e < T.n || e >= T.n + T.excess || reach[e]) atomicAdd(&out[5], 1ull);
+  }
+}
+
+// ------------------------------------------------------------ host helpers
+
+vs_status flush_retired(vs_table* t, cudaStream_t s) {
+  k_flush_retired<<<148, 256, 0, s>>>(t->view());
+  k_flush_final<<<1, 1, 0, s>>>(t->ctl);
+  VS_CK_LAUNCH("flush_retired");
+  return VS_OK;
+}
+
+vs_status erase_device_count(vs_table* t, const int32_t* keys, const uint64_t* n_dev, uint64_t max_n,
+                             cudaStream_t s) {
+  if (max_n == 0) return VS_OK;
+  k_erase<<<grid_for(max_n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, max_n, n_dev, nullptr, nullptr);
+  VS_CK_LAUNCH("k_erase");
+  return flush_retired(t, s);
+}
+
+static vs_status compact_live(vs_table* t, int32_t* keys_out, int32_t* pos_out, uint64_t cap_out, cudaStream_t s) {
+  const TableView v = t->view();
+  k_chunk_count<<<t->nchunks, 256, 0, s>>>(v, t->cap, t->chunk_counts);
+  k_scan_u32<<<1, 1024, 0, s>>>(t->chunk_counts, t->nchunks, t->chunk_offsets);
+  k_chunk_write<<<t->nchunks, 256, 0, s>>>(v, t->cap, t->chunk_offsets, keys_out, pos_out, cap_out);
+  VS_CK_LAUNCH("compact_live");
+  return VS_OK;
+}
+
+}  // namespace vsb
+
+using namespace vsb;
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" {
+
+const char* vs_last_error(void) { return g_last_error.c_str(); }
+int32_t vs_abi_version(void) { return 1; }
+
+vs_status vs_hash_keys(const int32_t* keys, uint64_t n, uint32_t bucket_count, uint32_t* out, vs_stream_t stream) {
+  if (bucket_count < 1) {
+    set_error("bucket_count must be >= 1");
+    return VS_ERR_INVALID;
+  }
+  if (n == 0) return VS_OK;
+  k_hash_keys<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(keys, n, bucket_count, out);
+  VS_CK_LAUNCH("k_hash_keys");
+  return VS_OK;
+}
+
+vs_status vs_table_create(uint64_t bucket_count, uint64_t excess_capacity, int device, vs_table** out) {
+  if (!out) {
+    set_error("out is NULL");
+    return VS_ERR_INVALID;
+  }
+  *out = nullptr;
+  if (bucket_count < 1) {
+    set_error("bucket_count must be >= 1");
+    return VS_ERR_INVALID;
+  }
+  if (excess_capacity < 1) {
+    set_error("excess_capacity must be >= 1");
+    return VS_ERR_INVALID;
+  }
+  if (excess_capacity > kNext - 1 || bucket_count + excess_capacity >= (1ull << 31)) {
+    set_error("table too large: need excess < 2^29 and bucket_count + excess < 2^31");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(device);
+  vs_table* t = new vs_table();
+  t->device = device;
+  t->n = (uint32_t)bucket_count;
+  t->excess = (uint32_t)excess_capacity;
+  t->cap = t->n + t->excess;
+  t->magic = fastmod_magic(t->n);
+  t->nchunks = (t->cap + kChunk - 1) / kChunk;
+  cudaError_t err = cudaSuccess;
+  auto A = [&](void** p, size_t bytes) {
+    if (err == cudaSuccess) err = cudaMalloc(p, bytes);
+  };
+  A((void**)&t->e, sizeof(Entry) * (size_t)t->cap);
+  A((void**)&t->free_stack, sizeof(uint32_t) * (size_t)t->excess);
+  A((void**)&t->retired, sizeof(uint32_t) * (size_t)t->excess);
+  A((void**)&t->first_op, sizeof(int32_t) * (size_t)t->cap);
+  A((void**)&t->ctl, sizeof(Ctl));
+  A((void**)&t->chunk_counts, sizeof(uint32_t) * (size_t)t->nchunks);
+  A((void**)&t->chunk_offsets, sizeof(uint64_t) * ((size_t)t->nchunks + 1));
+  if (err != cudaSuccess) {
+    vs_table_destroy(t);
+    return cuda_status(err, "vs_table_create: cudaMalloc");
+  }
+  vs_status st = vs_table_clear(t, nullptr);
+  if (st == VS_OK) {
+    cudaError_t e2 = cudaStreamSynchronize(nullptr);
+    if (e2 != cudaSuccess) st = cuda_status(e2, "vs_table_create: sync");
+  }
+  if (st != VS_OK) {
+    vs_table_destroy(t);
+    return st;
+  }
+  *out = t;
+  return VS_OK;
+}
+
+vs_status vs_table_destroy(vs_table* t) {
+  if (!t) return VS_OK;
+  DeviceGuard g(t->device);
+  cudaFree(t->e);
+  cudaFree(t->free_stack);
+  cudaFree(t->retired);
+  cudaFree(t->first_op);
+  cudaFree(t->ctl);
+  cudaFree(t->chunk_counts);
+  cudaFree(t->chunk_offsets);
+  cudaFree(t->pos_work);
+  delete t;
+  return VS_OK;
+}
+
+vs_status vs_table_info(const vs_table* t, uint64_t* nb, uint64_t* ex, uint64_t* cap) {
+  if (!t) {
+    set_error("table is NULL");
+    return VS_ERR_INVALID;
+  }
+  if (nb) *nb = t->n;
+  if (ex) *ex = t->excess;
+  if (cap) *cap = t->cap;
+  return VS_OK;
+}
+
+static vs_status check_batch(const vs_table* t, uint64_t n) {
+  if (!t) {
+    set_error("table is NULL");
+    return VS_ERR_INVALID;
+  }
+  if (n >= (1ull << 31)) {
+    set_error("batch too large (n must be < 2^31)");
+    return VS_ERR_INVALID;
+  }
+  return VS_OK;
+}
+
+vs_status vs_table_insert(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* created, int32_t* index,
+                          vs_stream_t stream) {
+  vs_status st = check_batch(t, n);
+  if (st != VS_OK || n == 0) return st;
+  if (!keys || !created || !index) {
+    set_error("keys/created/index must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const TableView v = t->view();
+  k_insert<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, created, index);
+  k_fixup_created<<<grid_for(n, 256), 256, 0, s>>>(v, keys, nullptr, n, created, index);
+  VS_CK_LAUNCH("vs_table_insert");
+  return VS_OK;
+}
+
+vs_status vs_table_find(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* found, int32_t* index,
+                        vs_stream_t stream) {
+  vs_status st = check_batch(t, n);
+  if (st != VS_OK || n == 0) return st;
+  if (!keys || !found || !index) {
+    set_error("keys/found/index must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  k_find<<<grid_for(n, kOpBlock), kOpBlock, 0, (cudaStream_t)stream>>>(t->view(), keys, n, found, index);
+  VS_CK_LAUNCH("vs_table_find");
+  return VS_OK;
+}
+
+vs_status vs_table_erase(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* erased, int32_t* index,
+                         vs_stream_t stream) {
+  vs_status st = check_batch(t, n);
+  if (st != VS_OK || n == 0) return st;
+  if (!keys) {
+    set_error("keys must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  k_erase<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, n, nullptr, erased, index);
+  VS_CK_LAUNCH("vs_table_erase");
+  return flush_retired(t, s);
+}
+
+vs_status vs_table_apply(vs_table* t, const int32_t* keys, const uint8_t* ops, uint64_t n, uint8_t* result,
+                         int32_t* index, vs_stream_t stream) {
+  vs_status st = check_batch(t, n);
+  if (st != VS_OK || n == 0) return st;
+  if (!keys || !ops || !result || !index) {
+    set_error("keys/ops/result/index must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const TableView v = t->view();
+  k_apply<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, ops, n, result, index);
+  k_fixup_created<<<grid_for(n, 256), 256, 0, s>>>(v, keys, ops, n, result, index);
+  VS_CK_LAUNCH("vs_table_apply");
+  return flush_retired(t, s);
+}
+
+vs_status vs_table_check(vs_table* t, vs_stream_t stream) {
+  if (!t) {
+    set_error("table is NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  unsigned int err = 0;
+  VS_CK(cudaMemcpyAsync(&err, &t->ctl->error, sizeof(err), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  VS_CK(cudaStreamSynchronize((cudaStream_t)stream));
+  if (err & 1u) {
+    VS_CK(cudaMemsetAsync(&t->ctl->error, 0, sizeof(unsigned int), (cudaStream_t)stream));
+    VS_CK(cudaStreamSynchronize((cudaStream_t)stream));
+    set_error("excess list exhausted (" + std::to_string(t->excess) + " entries)");
+    return VS_ERR_CAPACITY;
+  }
+  return VS_OK;
+}
+
+vs_status vs_table_size(vs_table* t, uint64_t* size_dev, uint64_t* size_host, vs_stream_t stream) {
+  if (!t) {
+    set_error("table is NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (size_dev) VS_CK(cudaMemcpyAsync(size_dev, &t->ctl->size, 8, cudaMemcpyDeviceToDevice, s));
+  if (size_host) {
+    VS_CK(cudaMemcpyAsync(size_host, &t->ctl->size, 8, cudaMemcpyDeviceToHost, s));
+    VS_CK(cudaStreamSynchronize(s));
+  }
+  return VS_OK;
+}
+
+vs_status vs_table_free_count(vs_table* t, uint64_t* free_host, vs_stream_t stream) {
+  if (!t || !free_host) {
+    set_error("table/free_host is NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  long long top = 0;
+  VS_CK(cudaMemcpyAsync(&top, &t->ctl->free_top, 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  VS_CK(cudaStreamSynchronize((cudaStream_t)stream));
+  *free_host = top < 0 ? 0 : (uint64_t)top;
+  return VS_OK;
+}
+
+vs_status vs_table_clear(vs_table* t, vs_stream_t stream) {
+  if (!t) {
+    set_error("table is NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  VS_CK(cudaMemsetAsync(t->e, 0, sizeof(Entry) * (size_t)t->cap, s));
+  k_init_free<<<grid_for(t->excess, 256) < 4096 ? grid_for(t->excess, 256) : 4096, 256, 0, s>>>(
+      t->free_stack, t->n, t->excess);
+  k_reset_ctl<<<1, 1, 0, s>>>(t->ctl, t->excess);
+  VS_CK_LAUNCH("vs_table_clear");
+  return VS_OK;
+}
+
+vs_status vs_table_snapshot(vs_table* t, int32_t* keys_out, int32_t* index_out, uint64_t cap, uint64_t* n_dev,
+                            vs_stream_t stream) {
+  if (!t || !n_dev) {
+    set_error("table/n_dev is NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  vs_status st = compact_live(t, keys_out, index_out, cap, s);
+  if (st != VS_OK) return st;
+  k_copy_total<<<1, 1, 0, s>>>(t->chunk_offsets, t->nchunks, n_dev);
+  VS_CK_LAUNCH("vs_table_snapshot");
+  return VS_OK;
+}
+
+vs_status vs_table_extract(vs_table* t, uint64_t max_n, uint64_t seed, int32_t* keys_out, uint64_t* n_dev,
+                           vs_stream_t stream) {
+  if (!t || !n_dev) {
+    set_error("table/n_dev is NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (max_n == 0) {
+    VS_CK(cudaMemsetAsync(n_dev, 0, 8, s));
+    return VS_OK;
+  }
+  if (!t->pos_work) VS_CK(cudaMalloc((void**)&t->pos_work, sizeof(int32_t) * (size_t)t->cap));
+  vs_status st = compact_live(t, nullptr, t->pos_work, t->cap, s);
+  if (st != VS_OK) return st;
+  const uint64_t m = max_n < t->cap ? max_n : t->cap;
+  unsigned grid = grid_for(m, 256);
+  if (grid > 1184) grid = 1184;
+  k_extract_select<<<grid, 256, 0, s>>>(t->view(), t->cap, t->pos_work, t->chunk_offsets + t->nchunks, max_n, seed,
+                                        keys_out, n_dev);
+  VS_CK_LAUNCH("k_extract_select");
+  return erase_device_count(t, keys_out, n_dev, m, s);
+}
+
+vs_status vs_table_audit(vs_table* t, uint64_t out_host[6], vs_stream_t stream) {
+  if (!t || !out_host) {
+    set_error("table/out is NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* reach = nullptr;
+  unsigned long long* out = nullptr;
+  VS_CK(cudaMalloc((void**)&reach, t->cap));
+  VS_CK(cudaMalloc((void**)&out, 8 * 8));
+  VS_CK(cudaMemsetAsync(reach, 0, t->cap, s));
+  VS_CK(cudaMemsetAsync(out, 0, 64, s));
+  k_audit<<<1184, 256, 0, s>>>(t->view(), t->cap, reach, out);
+  k_audit_free<<<148, 256, 0, s>>>(t->view(), reach, out);
+  unsigned long long h[8];
+  long long top = 0;
+  VS_CK(cudaMemcpyAsync(h, out, 64, cudaMemcpyDeviceToHost, s));
+  VS_CK(cudaMemcpyAsync(&top, &t->ctl->free_top, 8, cudaMemcpyDeviceToHost, s));
+  VS_CK(cudaStreamSynchronize(s));
+  cudaFree(reach);
+  cudaFree(out);
+  out_host[0] = h[0];
+  out_host[1] = h[1];
+  out_host[2] = top < 0 ? 0 : (uint64_t)top;
+  out_host[3] = h[3];
+  out_host[4] = h[4];
+  out_host[5] = h[5] + h[6];
+  return VS_OK;
+}
+
+}  // extern "C"

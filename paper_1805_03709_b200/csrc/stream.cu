@@ -1,0 +1,406 @@
+// stream.cu -- per-client stream-set updates on the GPU.
+//
+// Reference (server.py):
+//   StreamSet            :49-95   hash set + generation-order deque of NEWLY
+//                                 created keys (stale entries tolerated)
+//   on_tsdf_batch        :299-315 affected = ordered first-occurrence dedup of
+//                                 affected_mc_blocks(k) for every updated k,
+//                                 then insert_many(affected) into EVERY client
+//   _attach_session      :221-249 fresh client: new set filled with
+//                                 mc_map.snapshot_keys()
+//   on_reset_blocks      :425-436 remove keys from every client set
+// B200 design: all clients' inserts are ONE launch over a (key, client) grid;
+// the per-client "created" subset (= the set difference affected \ pending_c)
+// is placed into each client's FIFO ring by ONE exclusive scan over the
+// C x n created flags (segment c starts at c*n), so the FIFO append order is
+// the affected order, exactly the deque.append order of the reference.
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "hash_ops.cuh"
+#include "scan.cuh"
+#include "table.h"
+
+namespace vsb {
+
+constexpr int kMaxSets = 32;
+
+struct SetViews {
+  TableView v[kMaxSets];
+};
+
+struct FifoViews {
+  int32_t* keys[kMaxSets];
+  uint64_t cap[kMaxSets];
+};
+
+__global__ void __launch_bounds__(256) k_multi_insert(const __grid_constant__ SetViews V,
+                                                      const int32_t* __restrict__ keys, uint64_t n,
+                                                      uint8_t* __restrict__ created, int32_t* __restrict__ index) {
+  const int c = blockIdx.y;
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const TableView& T = V.v[c];
+  int delta = 0;
+  if (i < n) {
+    const InsertResult r = insert_key(T, keys[3 * i], keys[3 * i + 1], keys[3 * i + 2], (int32_t)i);
+    created[(uint64_t)c * n + i] = r.created;
+    index[(uint64_t)c * n + i] = r.pos;
+    delta = r.created;
+  }
+  add_size(T, delta);
+}
+
+__global__ void k_multi_fixup(const __grid_constant__ SetViews V, const int32_t* __restrict__ keys, uint64_t n,
+                              uint8_t* __restrict__ created, const int32_t* __restrict__ index) {
+  const int c = blockIdx.y;
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t* cr = created + (uint64_t)c * n;
+  if (!cr[i]) return;
+  const TableView& T = V.v[c];
+  const int32_t pos = index[(uint64_t)c * n + i];
+  atomicAnd(&T.e[pos].meta, ~kFresh);
+  const int32_t m = T.first_op[pos];
+  if (m >= 0 && (uint64_t)m < i && keys[3 * (uint64_t)m] == keys[3 * i] &&
+      keys[3 * (uint64_t)m + 1] == keys[3 * i + 1] && keys[3 * (uint64_t)m + 2] == keys[3 * i + 2]) {
+    cr[i] = 0;
+    cr[m] = 1;
+  }
+}
+
+__global__ void k_fifo_append(const __grid_constant__ FifoViews F, const int32_t* __restrict__ keys, uint64_t n,
+                              const uint8_t* __restrict__ created, const uint64_t* __restrict__ off,
+                              const uint64_t* __restrict__ tails) {
+  const int c = blockIdx.y;
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t j = (uint64_t)c * n + i;
+  if (!created[j]) return;
+  const uint64_t rank = off[j] - off[(uint64_t)c * n];
+  const uint64_t p = (tails[c] + rank) % F.cap[c];
+  int32_t* dst = F.keys[c] + 3 * p;
+  dst[0] = keys[3 * i];
+  dst[1] = keys[3 * i + 1];
+  dst[2] = keys[3 * i + 2];
+}
+
+__global__ void k_fifo_tail(const uint64_t* __restrict__ off, uint64_t n, int C, uint64_t* __restrict__ tails,
+                            uint64_t* __restrict__ n_created) {
+  const int c = threadIdx.x;
+  if (c >= C) return;
+  const uint64_t cnt = off[(uint64_t)(c + 1) * n] - off[(uint64_t)c * n];
+  if (tails) tails[c] += cnt;
+  if (n_created) n_created[c] = cnt;
+}
+
+__global__ void __launch_bounds__(256) k_multi_erase(const __grid_constant__ SetViews V,
+                                                     const int32_t* __restrict__ keys, uint64_t n,
+                                                     uint8_t* __restrict__ erased) {
+  const int c = blockIdx.y;
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const TableView& T = V.v[c];
+  int delta = 0;
+  if (i < n) {
+    const int32_t pos = erase_key(T, keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]);
+    if (erased) erased[(uint64_t)c * n + i] = pos >= 0;
+    delta = -(pos >= 0);
+  }
+  add_size(T, delta);
+}
+
+__global__ void k_multi_flush(const __grid_constant__ SetViews V) {
+  const TableView& T = V.v[blockIdx.y];
+  const unsigned long long r = T.ctl->retired_n;
+  const long long top = T.ctl->free_top;
+  for (unsigned long long j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < r;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    T.free_stack[top + (long long)j] = T.retired[j];
+}
+
+__global__ void k_multi_flush_final(const __grid_constant__ SetViews V, int C) {
+  const int c = threadIdx.x;
+  if (c >= C) return;
+  Ctl* ctl = V.v[c].ctl;
+  ctl->free_top += (long long)ctl->retired_n;
+  ctl->retired_n = 0;
+}
+
+// affected_mc_blocks order: itertools.product((0, -1), repeat=3) -> dx slowest
+__global__ void k_expand_affected(const int32_t* __restrict__ updated, uint64_t u, int32_t* __restrict__ out) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= 8 * u) return;
+  const uint64_t i = j >> 3;
+  const int d = (int)(j & 7);
+  out[3 * j] = updated[3 * i] - ((d >> 2) & 1);
+  out[3 * j + 1] = updated[3 * i + 1] - ((d >> 1) & 1);
+  out[3 * j + 2] = updated[3 * i + 2] - (d & 1);
+}
+
+__global__ void k_scatter_flagged(const int32_t* __restrict__ keys, uint64_t n, const uint8_t* __restrict__ flag,
+                                  const uint64_t* __restrict__ off, int32_t* __restrict__ out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !flag[i]) return;
+  const uint64_t o = off[i];
+  out[3 * o] = keys[3 * i];
+  out[3 * o + 1] = keys[3 * i + 1];
+  out[3 * o + 2] = keys[3 * i + 2];
+}
+
+__global__ void k_copy_u64(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst) { *dst = *src; }
+
+__global__ void k_gather_ring(const int32_t* __restrict__ ring, uint64_t cap, uint64_t head, uint64_t w,
+                              int32_t* __restrict__ out) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= w) return;
+  const uint64_t p = (head + j) % cap;
+  out[3 * j] = ring[3 * p];
+  out[3 * j + 1] = ring[3 * p + 1];
+  out[3 * j + 2] = ring[3 * p + 2];
+}
+
+__global__ void k_candidates(const uint8_t* __restrict__ first, const uint8_t* __restrict__ present, uint64_t w,
+                             uint8_t* __restrict__ cand) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < w) cand[j] = first[j] & present[j];
+}
+
+// position of the need-th candidate (1-based) -> *cut
+__global__ void k_find_cut(const uint8_t* __restrict__ cand, const uint64_t* __restrict__ off, uint64_t w,
+                           uint64_t need, uint64_t* __restrict__ cut) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < w && cand[j] && off[j] + 1 == need) *cut = j;
+}
+
+__global__ void k_clip_flags(uint8_t* __restrict__ flag, uint64_t w, uint64_t cut) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < w && j > cut) flag[j] = 0;
+}
+
+static vs_status fill_views(vs_table* const* sets, int n_sets, SetViews& V) {
+  if (n_sets < 1 || n_sets > kMaxSets) {
+    set_error("n_sets must be in [1, 32] per call");
+    return VS_ERR_INVALID;
+  }
+  for (int c = 0; c < n_sets; ++c) {
+    if (!sets[c]) {
+      set_error("set handle is NULL");
+      return VS_ERR_INVALID;
+    }
+    V.v[c] = sets[c]->view();
+  }
+  return VS_OK;
+}
+
+static vs_status flush_multi(const SetViews& V, int C, cudaStream_t s) {
+  k_multi_flush<<<dim3(64, C), 256, 0, s>>>(V);
+  k_multi_flush_final<<<1, 32, 0, s>>>(V, C);
+  VS_CK_LAUNCH("flush_multi");
+  return VS_OK;
+}
+
+}  // namespace vsb
+
+using namespace vsb;
+
+extern "C" {
+
+vs_status vs_affected_dedup(vs_table* scratch, const int32_t* updated, uint64_t u, int32_t* out_keys,
+                            uint64_t* n_dev, vs_stream_t stream) {
+  if (!scratch || !n_dev || (u && (!updated || !out_keys))) {
+    set_error("scratch/updated/out_keys/n_dev must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(scratch->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (u == 0) {
+    VS_CK(cudaMemsetAsync(n_dev, 0, 8, s));
+    return VS_OK;
+  }
+  const uint64_t m = 8 * u;
+  int32_t* all = nullptr;
+  uint8_t* created = nullptr;
+  int32_t* index = nullptr;
+  uint64_t *off = nullptr, *work = nullptr;
+  VS_CK(cudaMallocAsync((void**)&all, 12 * m, s));
+  VS_CK(cudaMallocAsync((void**)&created, m, s));
+  VS_CK(cudaMallocAsync((void**)&index, 4 * m, s));
+  VS_CK(cudaMallocAsync((void**)&off, 8 * (m + 1), s));
+  VS_CK(cudaMallocAsync((void**)&work, 8 * (scan_tiles(m) + 1), s));
+  vs_status st = vs_table_clear(scratch, stream);
+  if (st == VS_OK) {
+    k_expand_affected<<<grid_for(m, 256), 256, 0, s>>>(updated, u, all);
+    st = vs_table_insert(scratch, all, m, created, index, stream);
+  }
+  if (st == VS_OK) {
+    cudaError_t e = exclusive_scan<uint8_t>(created, m, off, work, s);
+    if (e != cudaSuccess) st = cuda_status(e, "exclusive_scan");
+  }
+  if (st == VS_OK) {
+    k_scatter_flagged<<<grid_for(m, 256), 256, 0, s>>>(all, m, created, off, out_keys);
+    k_copy_u64<<<1, 1, 0, s>>>(off + m, n_dev);
+  }
+  cudaFreeAsync(all, s);
+  cudaFreeAsync(created, s);
+  cudaFreeAsync(index, s);
+  cudaFreeAsync(off, s);
+  cudaFreeAsync(work, s);
+  if (st != VS_OK) return st;
+  VS_CK_LAUNCH("vs_affected_dedup");
+  return VS_OK;
+}
+
+vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const int32_t* keys, uint64_t n,
+                                uint8_t* created, int32_t* const* fifo_keys_host, const uint64_t* fifo_cap_host,
+                                uint64_t* fifo_tail, uint64_t* n_created, vs_stream_t stream) {
+  SetViews V;
+  if (!sets_host) {
+    set_error("sets is NULL");
+    return VS_ERR_INVALID;
+  }
+  vs_status st = fill_views(sets_host, n_sets, V);
+  if (st != VS_OK) return st;
+  if (n >= (1ull << 31)) {
+    set_error("batch too large");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(sets_host[0]->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) {
+    if (n_created) VS_CK(cudaMemsetAsync(n_created, 0, 8 * n_sets, s));
+    return VS_OK;
+  }
+  if (!keys || !created) {
+    set_error("keys/created must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  const uint64_t total = (uint64_t)n_sets * n;
+  int32_t* index = nullptr;
+  uint64_t *off = nullptr, *work = nullptr;
+  VS_CK(cudaMallocAsync((void**)&index, 4 * total, s));
+  VS_CK(cudaMallocAsync((void**)&off, 8 * (total + 1), s));
+  VS_CK(cudaMallocAsync((void**)&work, 8 * (scan_tiles(total) + 1), s));
+  const dim3 grid(grid_for(n, 256), n_sets);
+  k_multi_insert<<<grid, 256, 0, s>>>(V, keys, n, created, index);
+  k_multi_fixup<<<grid, 256, 0, s>>>(V, keys, n, created, index);
+  cudaError_t e = exclusive_scan<uint8_t>(created, total, off, work, s);
+  if (e == cudaSuccess && fifo_keys_host && fifo_cap_host && fifo_tail) {
+    FifoViews F;
+    for (int c = 0; c < n_sets; ++c) {
+      F.keys[c] = fifo_keys_host[c];
+      F.cap[c] = fifo_cap_host[c] ? fifo_cap_host[c] : 1;
+    }
+    k_fifo_append<<<grid, 256, 0, s>>>(F, keys, n, created, off, fifo_tail);
+  }
+  if (e == cudaSuccess) k_fifo_tail<<<1, 32, 0, s>>>(off, n, n_sets, fifo_tail, n_created);
+  cudaFreeAsync(index, s);
+  cudaFreeAsync(off, s);
+  cudaFreeAsync(work, s);
+  if (e != cudaSuccess) return cuda_status(e, "vs_stream_insert_many");
+  VS_CK_LAUNCH("vs_stream_insert_many");
+  return VS_OK;
+}
+
+vs_status vs_stream_remove_many(vs_table* const* sets_host, int n_sets, const int32_t* keys, uint64_t n,
+                                uint8_t* erased, vs_stream_t stream) {
+  SetViews V;
+  if (!sets_host) {
+    set_error("sets is NULL");
+    return VS_ERR_INVALID;
+  }
+  vs_status st = fill_views(sets_host, n_sets, V);
+  if (st != VS_OK) return st;
+  if (n == 0) return VS_OK;
+  if (!keys) {
+    set_error("keys must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(sets_host[0]->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  k_multi_erase<<<dim3(grid_for(n, 256), n_sets), 256, 0, s>>>(V, keys, n, erased);
+  VS_CK_LAUNCH("k_multi_erase");
+  return flush_multi(V, n_sets, s);
+}
+
+vs_status vs_stream_extract_ordered(vs_table* set, const int32_t* fifo_keys, uint64_t fifo_cap, uint64_t* head_host,
+                                    uint64_t tail_host, uint64_t max_n, int32_t* keys_out, uint64_t* n_out_host,
+                                    vs_table* scratch, vs_stream_t stream) {
+  if (!set || !scratch || !head_host || !n_out_host || (max_n && (!fifo_keys || !keys_out))) {
+    set_error("set/scratch/fifo/head/keys_out/n_out must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(set->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t head = *head_host, out = 0;
+  *n_out_host = 0;
+  if (max_n == 0 || head >= tail_host) return VS_OK;
+  // window buffers sized to the scratch table (the dedup set of a window)
+  const uint64_t wmax = std::max<uint64_t>(1, std::min<uint64_t>(scratch->n, 1u << 20));
+  int32_t* wkeys = nullptr;
+  uint8_t *first = nullptr, *present = nullptr, *cand = nullptr;
+  int32_t* idx = nullptr;
+  uint64_t *off = nullptr, *work = nullptr, *cut_dev = nullptr;
+  VS_CK(cudaMallocAsync((void**)&wkeys, 12 * wmax, s));
+  VS_CK(cudaMallocAsync((void**)&first, wmax, s));
+  VS_CK(cudaMallocAsync((void**)&present, wmax, s));
+  VS_CK(cudaMallocAsync((void**)&cand, wmax, s));
+  VS_CK(cudaMallocAsync((void**)&idx, 4 * wmax, s));
+  VS_CK(cudaMallocAsync((void**)&off, 8 * (wmax + 1), s));
+  VS_CK(cudaMallocAsync((void**)&work, 8 * (scan_tiles(wmax) + 1), s));
+  VS_CK(cudaMallocAsync((void**)&cut_dev, 8, s));
+  vs_status st = VS_OK;
+  while (st == VS_OK && out < max_n && head < tail_host) {
+    const uint64_t need = max_n - out;
+    uint64_t w = std::min<uint64_t>(tail_host - head, std::max<uint64_t>(need, 1024));
+    w = std::min(w, wmax);
+    k_gather_ring<<<grid_for(w, 256), 256, 0, s>>>(fifo_keys, fifo_cap, head, w, wkeys);
+    // first occurrence inside the window (later duplicates are stale by
+    // construction: the earlier entry either delivers the key or finds it gone)
+    st = vs_table_clear(scratch, stream);
+    if (st == VS_OK) st = vs_table_insert(scratch, wkeys, w, first, idx, stream);
+    if (st == VS_OK) st = vs_table_find(set, wkeys, w, present, idx, stream);
+    if (st != VS_OK) break;
+    k_candidates<<<grid_for(w, 256), 256, 0, s>>>(first, present, w, cand);
+    cudaError_t e = exclusive_scan<uint8_t>(cand, w, off, work, s);
+    if (e != cudaSuccess) {
+      st = cuda_status(e, "exclusive_scan");
+      break;
+    }
+    uint64_t total = 0;
+    if ((e = cudaMemcpyAsync(&total, off + w, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess) {
+      st = cuda_status(e, "extract_ordered: total");
+      break;
+    }
+    uint64_t cut = w - 1, taken = total;
+    if (total >= need) {
+      k_find_cut<<<grid_for(w, 256), 256, 0, s>>>(cand, off, w, need, cut_dev);
+      if ((e = cudaMemcpyAsync(&cut, cut_dev, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+          (e = cudaStreamSynchronize(s)) != cudaSuccess) {
+        st = cuda_status(e, "extract_ordered: cut");
+        break;
+      }
+      taken = need;
+      k_clip_flags<<<grid_for(w, 256), 256, 0, s>>>(cand, w, cut);
+    }
+    k_scatter_flagged<<<grid_for(w, 256), 256, 0, s>>>(wkeys, w, cand, off, keys_out + 3 * out);
+    if (taken) st = vs_table_erase(set, keys_out + 3 * out, taken, nullptr, nullptr, stream);
+    out += taken;
+    head += cut + 1;
+  }
+  cudaFreeAsync(wkeys, s);
+  cudaFreeAsync(first, s);
+  cudaFreeAsync(present, s);
+  cudaFreeAsync(cand, s);
+  cudaFreeAsync(idx, s);
+  cudaFreeAsync(off, s);
+  cudaFreeAsync(work, s);
+  cudaFreeAsync(cut_dev, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (st == VS_OK && e != cudaSuccess) st = cuda_status(e, "extract_ordered");
+  *head_host = head;
+  *n_out_host = out;
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// table.h -- host-side table object and shared host helpers of libvsb200.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "../../include/vsb200.h"
+
+struct vs_table {
+  int device = 0;
+  uint32_t n = 0, excess = 0, cap = 0;
+  vsb::Entry* e = nullptr;
+  uint32_t* free_stack = nullptr;
+  uint32_t* retired = nullptr;
+  int32_t* first_op = nullptr;
+  vsb::Ctl* ctl = nullptr;
+  uint64_t magic = 0;
+  // ordered-compaction workspace (snapshot / extract)
+  uint32_t nchunks = 0;
+  uint32_t* chunk_counts = nullptr;
+  uint64_t* chunk_offsets = nullptr;  // nchunks + 1
+  int32_t* pos_work = nullptr;        // lazily allocated, cap entries
+
+  vsb::TableView view() const {
+    vsb::TableView v;
+    v.e = e;
+    v.free_stack = free_stack;
+    v.retired = retired;
+    v.first_op = first_op;
+    v.ctl = ctl;
+    v.n = n;
+    v.excess = excess;
+    v.magic = magic;
+    return v;
+  }
+};
+
+namespace vsb {
+
+constexpr uint32_t kChunk = 4096;  // entries per CTA in ordered compaction
+
+void set_error(const std::string& msg);
+vs_status cuda_status(cudaError_t err, const char* what);
+
+// RAII: make `dev` current for the duration of a call.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// internal entry points shared across translation units
+vs_status flush_retired(vs_table* t, cudaStream_t s);
+vs_status erase_device_count(vs_table* t, const int32_t* keys, const uint64_t* n_dev, uint64_t max_n,
+                             cudaStream_t s);
+
+}  // namespace vsb
+
+#define VS_CK(call)                                            \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return vsb::cuda_status(_e, #call); \
+  } while (0)
+
+#define VS_CK_LAUNCH(what) VS_CK(cudaGetLastError())

@@ -1,0 +1,323 @@
+"""GPU stream sets and the server's data-parallel update path.
+
+Mirrors the hot half of the reference server (server.py):
+  StreamSet        :49-95    device hash set + device generation-order FIFO
+  fan_out          :314-315  insert_many of the recomputed keys into EVERY
+                             client set in one launch (set difference +
+                             ordered FIFO append per client)
+  GpuServerCore    :221-249, 299-315, 425-436
+                   on_tsdf_batch (TSDF put -> affected dedup -> MC recompute
+                   -> MC put -> fan-out), fresh/returning attach, resets.
+The control plane (sockets, negotiation, pose/texture relays, stats) stays
+in the reference and is out of scope.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from typing import Callable, Optional, Sequence
+
+from . import _lib
+from ._lib import check, ptr
+from .concurrent_hash import BlockHashSet, BlockKey, _as_keys
+from .mc_encoding import MC_BLOCK_BYTES, Q_BLOCK_BYTES, encode_keys
+from .voxel_model import TSDF_BLOCK_BYTES
+
+_MAX_SETS_PER_LAUNCH = 32
+
+
+class StreamSet:
+    """Per-destination pending-update set with a generation-order queue
+    (server.py:49-95).  The queue is a device ring of keys that keeps stale
+    entries exactly like the reference's deque; ``extract_ordered`` skips
+    them by validating membership."""
+
+    def __init__(self, buckets: int = 1 << 16, excess: int = 1 << 16, *, device=None,
+                 fifo_capacity: Optional[int] = None) -> None:
+        torch = _lib.require_cuda()
+        self._torch = torch
+        self._set = BlockHashSet(buckets, excess, device=device)
+        self.device = self._set.device
+        cap = fifo_capacity or max(1024, min(buckets + excess, 1 << 20))
+        self._fifo = torch.empty((cap, 3), dtype=torch.int32, device=self.device)
+        self._head = 0
+        self._tail = 0
+        self._scratch: Optional[BlockHashSet] = None
+
+    # -- FIFO ring management (host-authoritative head/tail) ---------------
+
+    @property
+    def fifo_capacity(self) -> int:
+        return self._fifo.shape[0]
+
+    def _ring_view(self):
+        """Pending FIFO entries [head, tail) in order (device tensor)."""
+        torch = self._torch
+        cap = self.fifo_capacity
+        idx = (torch.arange(self._head, self._tail, device=self.device) % cap)
+        return self._fifo[idx]
+
+    def _ensure_fifo(self, extra: int) -> None:
+        need = (self._tail - self._head) + extra
+        if need <= self.fifo_capacity:
+            return
+        torch = self._torch
+        cap = max(2 * self.fifo_capacity, need)
+        live = self._ring_view()
+        fifo = torch.empty((cap, 3), dtype=torch.int32, device=self.device)
+        fifo[: live.shape[0]] = live
+        self._fifo = fifo
+        self._tail -= self._head
+        self._head = 0
+
+    def fifo_entries(self) -> list[BlockKey]:
+        """The generation-order queue incl. stale entries (tests/inspection)."""
+        return [tuple(k) for k in self._ring_view().cpu().tolist()]
+
+    # -- reference API ------------------------------------------------------
+
+    def insert(self, key: BlockKey) -> bool:
+        return self.insert_many([key]) == 1
+
+    def insert_many(self, keys) -> int:
+        return fan_out([self], keys)[0]
+
+    def remove(self, key: BlockKey) -> bool:
+        return self._set.remove(key)
+
+    def remove_many(self, keys) -> int:
+        erased, _ = self._set.erase_keys(keys)
+        return int(erased.sum().item())
+
+    def size(self) -> int:
+        return self._set.approx_size()
+
+    def snapshot(self) -> list[BlockKey]:
+        return self._set.snapshot_keys()
+
+    def extract_random(self, max_n: int) -> list[BlockKey]:
+        return self._set.extract_batch(max_n)
+
+    def extract_matching(self, max_n: int, predicate: Callable) -> list[BlockKey]:
+        return self._set.extract_matching(max_n, predicate)
+
+    def extract_ordered(self, max_n: int) -> list[BlockKey]:
+        keys = self.extract_ordered_keys(max_n)
+        return [tuple(k) for k in keys.cpu().tolist()]
+
+    def extract_ordered_keys(self, max_n: int):
+        """Device version of extract_ordered (server.py:86-95) -> int32[m,3]."""
+        torch = self._torch
+        if max_n <= 0 or self._head >= self._tail:
+            return torch.empty((0, 3), dtype=torch.int32, device=self.device)
+        if self._scratch is None:
+            self._scratch = BlockHashSet(1 << 12, 1 << 12, device=self.device)
+        out = torch.empty((max_n, 3), dtype=torch.int32, device=self.device)
+        head = ctypes.c_uint64(self._head)
+        n_out = ctypes.c_uint64(0)
+        s = _order_streams([self._set, self._scratch])
+        check(_lib.load().vs_stream_extract_ordered(
+            self._set.handle, ptr(self._fifo), self.fifo_capacity, ctypes.byref(head), self._tail, max_n,
+            ptr(out), ctypes.byref(n_out), self._scratch.handle, ctypes.c_void_p(s.cuda_stream)),
+            "extract_ordered")
+        _mark_done([self._set, self._scratch], s)
+        self._head = int(head.value)
+        return out[: int(n_out.value)]
+
+    def clear(self) -> None:
+        """Bulk reset (fresh reconnect of a retained client)."""
+        self._set.clear()
+        self._head = self._tail = 0
+
+
+def _order_streams(tables):
+    """Current stream, made to wait for the last launch on every table."""
+    s = tables[0]._torch.cuda.current_stream(tables[0].device)
+    for t in tables:
+        if t._event is not None:
+            s.wait_event(t._event)
+    return s
+
+
+def _mark_done(tables, s) -> None:
+    ev = tables[0]._torch.cuda.Event()
+    ev.record(s)
+    for t in tables:
+        t._event = ev
+
+
+def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True):
+    """``for s in sets: s.insert_many(keys)`` in one launch per 32 clients.
+
+    For each client the newly created keys (the set difference keys \\
+    pending) are appended to its FIFO in input order, exactly like the
+    reference's per-key deque.append.  Returns the created count per client
+    (synchronising), or the device counts when sync=False.
+    """
+    if not sets:
+        return []
+    torch = sets[0]._torch
+    dev = sets[0].device
+    k = _as_keys(keys, dev)
+    n = k.shape[0]
+    if n == 0:
+        return [0] * len(sets) if sync else torch.zeros(len(sets), dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    counts = torch.empty(len(sets), dtype=torch.int64, device=dev)
+    created = torch.empty(min(len(sets), _MAX_SETS_PER_LAUNCH) * n, dtype=torch.uint8, device=dev)
+    for g0 in range(0, len(sets), _MAX_SETS_PER_LAUNCH):
+        group = list(sets[g0:g0 + _MAX_SETS_PER_LAUNCH])
+        C = len(group)
+        for st in group:
+            st._ensure_fifo(n)
+        tables = [st._set for st in group]
+        handles = (ctypes.c_void_p * C)(*[t.handle.value for t in tables])
+        fifos = (ctypes.c_void_p * C)(*[st._fifo.data_ptr() for st in group])
+        caps = (ctypes.c_uint64 * C)(*[st.fifo_capacity for st in group])
+        tails = torch.tensor([st._tail for st in group], dtype=torch.int64).to(dev, non_blocking=True)
+        s = _order_streams(tables)
+        check(lib.vs_stream_insert_many(handles, C, ptr(k), n, ptr(created), fifos, caps, ptr(tails),
+                                        ptr(counts[g0:g0 + C]), ctypes.c_void_p(s.cuda_stream)), "fan_out")
+        _mark_done(tables, s)
+    if not sync:
+        return counts
+    host = counts.cpu().tolist()
+    for st, c in zip(sets, host):
+        st._tail += int(c)
+    return [int(c) for c in host]
+
+
+def remove_everywhere(sets: Sequence[StreamSet], keys) -> None:
+    """Remove keys from every client set (server.py:433-435), one launch per 32."""
+    if not sets:
+        return
+    dev = sets[0].device
+    k = _as_keys(keys, dev)
+    if k.shape[0] == 0:
+        return
+    lib = _lib.load()
+    for g0 in range(0, len(sets), _MAX_SETS_PER_LAUNCH):
+        tables = [st._set for st in sets[g0:g0 + _MAX_SETS_PER_LAUNCH]]
+        handles = (ctypes.c_void_p * len(tables))(*[t.handle.value for t in tables])
+        s = _order_streams(tables)
+        check(lib.vs_stream_remove_many(handles, len(tables), ptr(k), k.shape[0], None,
+                                        ctypes.c_void_p(s.cuda_stream)), "remove_everywhere")
+        _mark_done(tables, s)
+
+
+class GpuServerCore:
+    """Device-resident TSDF model, MC model and client stream sets.
+
+    tsdf_map / mc_map are hash tables whose entry positions index the device
+    payload pools (the reference's parallel ``_values`` array,
+    concurrent_hash.py:112): tsdf_pool uint8[cap,6144] (wire rows),
+    mc_pool uint8[cap,2048] (McBlock.to_bytes), q_pool int8[cap,512].
+    """
+
+    def __init__(self, buckets: int = 1 << 20, excess: int = 1 << 20, *, stream_buckets: int = 1 << 16,
+                 stream_excess: int = 1 << 16, retention_s: float = 3600.0, max_batch: int = 4096,
+                 device=None) -> None:
+        torch = _lib.require_cuda()
+        self._torch = torch
+        self.tsdf_map = BlockHashSet(buckets, excess, device=device)
+        self.device = self.tsdf_map.device
+        self.mc_map = BlockHashSet(buckets, excess, device=self.device)
+        cap = buckets + excess
+        self.tsdf_pool = torch.zeros((cap, TSDF_BLOCK_BYTES), dtype=torch.uint8, device=self.device)
+        self.mc_pool = torch.zeros((cap, MC_BLOCK_BYTES), dtype=torch.uint8, device=self.device)
+        self.q_pool = torch.zeros((cap, Q_BLOCK_BYTES), dtype=torch.int8, device=self.device)
+        self._dedup = BlockHashSet(16 * max_batch, 16 * max_batch, device=self.device)
+        self._stream_sizes = (stream_buckets, stream_excess)
+        self.retention_s = retention_s
+        self.sessions: dict[bytes, dict] = {}
+
+    # -- sessions (server.py:221-249) ---------------------------------------
+
+    def attach(self, client_id: bytes) -> StreamSet:
+        """Returning client within retention keeps its set; otherwise a new
+        set filled with every MC key (snapshot order)."""
+        now = time.monotonic()
+        sess = self.sessions.get(client_id)
+        if sess is not None and (sess["connected"] or now - sess["disconnected_at"] <= self.retention_s):
+            sess["connected"] = True
+            return sess["stream"]
+        stream = StreamSet(*self._stream_sizes, device=self.device)
+        self.sessions[client_id] = {"stream": stream, "connected": True, "disconnected_at": 0.0}
+        keys, _ = self.mc_map.snapshot_tensor()
+        fan_out([stream], keys)
+        return stream
+
+    def detach(self, client_id: bytes) -> None:
+        sess = self.sessions.get(client_id)
+        if sess is not None:
+            sess["connected"] = False
+            sess["disconnected_at"] = time.monotonic()
+
+    def streams(self) -> list[StreamSet]:
+        return [s["stream"] for s in self.sessions.values()]
+
+    # -- model updates (server.py:299-315) ----------------------------------
+
+    def on_tsdf_batch(self, keys, rows):
+        """Ingest U TSDF blocks (int32[U,3], uint8[U,6144] wire rows) and
+        propagate: affected MC keys are recomputed, stored and queued into
+        every client.  Returns the affected keys (device int32[A,3])."""
+        torch = self._torch
+        dev = self.device
+        k = _as_keys(keys, dev)
+        rows = torch.as_tensor(rows).to(dev, torch.uint8).reshape(-1, TSDF_BLOCK_BYTES)
+        U = k.shape[0]
+        if U == 0:
+            return k
+        # tsdf_map.put: latest write wins (sequential put order)
+        self.tsdf_map.insert_many_exact(k)
+        _, pos = self.tsdf_map.find_keys(k)
+        pos = pos.to(torch.int64)
+        last = torch.full((self.tsdf_map.capacity,), -1, dtype=torch.int64, device=dev)
+        order = torch.arange(U, device=dev)
+        last.scatter_reduce_(0, pos, order, reduce="amax")
+        win = last[pos] == order
+        self.tsdf_pool[pos[win]] = rows[win]
+        # affected = ordered first-occurrence dedup of the 8 affected blocks per key
+        if 8 * U > self._dedup.bucket_count:
+            self._dedup = BlockHashSet(16 * U, 16 * U, device=dev)
+        affected = torch.empty((8 * U, 3), dtype=torch.int32, device=dev)
+        n_dev = torch.empty(1, dtype=torch.int64, device=dev)
+        s = _order_streams([self._dedup])
+        check(_lib.load().vs_affected_dedup(self._dedup.handle, ptr(k), U, ptr(affected), ptr(n_dev),
+                                            ctypes.c_void_p(s.cuda_stream)), "affected_dedup")
+        _mark_done([self._dedup], s)
+        self._dedup.check_capacity()
+        A = int(n_dev.item())
+        affected = affected[:A]
+        # recompute + mc_map.put
+        self.mc_map.insert_many_exact(affected)
+        _, mpos = self.mc_map.find_keys(affected)
+        mpos = mpos.to(torch.int64)
+        mc, q, _ = encode_keys(self.tsdf_map, self.tsdf_pool, affected, counts=False)
+        self.mc_pool[mpos] = mc
+        self.q_pool[mpos] = q
+        fan_out(self.streams(), affected)
+        return affected
+
+    def on_reset_blocks(self, keys) -> None:
+        """server.py:425-436: remove from both maps and every client set."""
+        k = _as_keys(keys, self.device)
+        if k.shape[0] == 0:
+            return
+        _, tpos = self.tsdf_map.erase_keys(k)
+        _, mpos = self.mc_map.erase_keys(k)
+        remove_everywhere(self.streams(), k)
+
+    def mc_payload(self, key: BlockKey) -> Optional[bytes]:
+        found, pos = self.mc_map.find_keys([key])
+        if not bool(found[0].item()):
+            return None
+        return bytes(self.mc_pool[int(pos[0].item())].cpu().numpy().tobytes())
+
+    def tsdf_payload(self, key: BlockKey) -> Optional[bytes]:
+        found, pos = self.tsdf_map.find_keys([key])
+        if not bool(found[0].item()):
+            return None
+        return bytes(self.tsdf_pool[int(pos[0].item())].cpu().numpy().tobytes())

@@ -1,0 +1,175 @@
+"""GPU parity tests of the MC block encoder (+ quantised TSDF, compaction).
+
+Bar: bit-exact MC bytes against the reference's recorded outputs and the
+C oracle; quantised TSDF bit-exact against the normative oracle (A17);
+compaction scatters back to the dense bytes (A19).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1805_03709_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(a, dev):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def gpu_encode(pool, nbr, dev):
+    from paper_1805_03709_b200 import encode_blocks
+
+    mc, q, c = encode_blocks(_t(pool, dev), _t(nbr, dev))
+    return mc.cpu().numpy(), q.cpu().numpy(), c.cpu().numpy().astype(np.uint32)
+
+
+def table_with_pool(tsdf_keys, rows, dev, n=1 << 12, excess=1 << 12):
+    """A BlockHashMap-style table whose positions index a device pool."""
+    import torch
+
+    from paper_1805_03709_b200 import BlockHashSet
+
+    t = BlockHashSet(n, excess)
+    created, pos = t.insert_keys(tsdf_keys)
+    t.check_capacity()
+    pool = torch.zeros((t.capacity, 6144), dtype=torch.uint8, device=dev)
+    pool[pos.long()] = _t(rows, dev)
+    return t, pool
+
+
+def test_random_fields_vs_reference(dev, golden):
+    d = np.load(golden / "mc_random.npz")
+    pool = oracle.make_pool(d["tsdf"], d["weight"], d["color"])
+    nbr = oracle.neighbor_table(d["mc_keys"], d["tsdf_keys"])
+    mc, q, counts = gpu_encode(pool, nbr, dev)
+    assert np.array_equal(mc, d["mc"])  # reference recompute_mc_block bytes
+    omc, oq, oc = oracle.mc_encode(pool, nbr)
+    assert np.array_equal(q, oq) and np.array_equal(counts, oc)
+
+
+def test_fused_hash_lookup_path_vs_reference(dev, golden):
+    from paper_1805_03709_b200 import encode_keys, neighbors
+
+    d = np.load(golden / "mc_random.npz")
+    rows = oracle.make_pool(d["tsdf"], d["weight"], d["color"])
+    t, pool = table_with_pool(d["tsdf_keys"], rows, dev)
+    mc, q, c = encode_keys(t, pool, d["mc_keys"])
+    assert np.array_equal(mc.cpu().numpy(), d["mc"])
+    nbr = neighbors(t, d["mc_keys"]).cpu().numpy()
+    ref_nbr = oracle.neighbor_table(d["mc_keys"], d["tsdf_keys"])
+    assert np.array_equal(nbr >= 0, ref_nbr >= 0)
+
+
+def test_ieee_edge_cases(dev, golden):
+    for c in json.loads((golden / "mc_edge.json").read_text()):
+        tsdf = np.full((8, 512), 0.5, np.float32)
+        weight = np.ones((8, 512), np.float32)
+        color = np.full((8, 512, 3), 7, np.uint8)
+        tsdf[0, 1] = -0.5
+        tsdf[0, 0] = np.float32(float(c["tsdf0"]))
+        weight[0, 0] = np.float32(float(c["weight0"]))
+        pool = oracle.make_pool(tsdf, weight, color)
+        nbr = oracle.neighbor_table([(0, 0, 0)], [(k & 1, (k >> 1) & 1, (k >> 2) & 1) for k in range(8)])
+        mc, q, _ = gpu_encode(pool, nbr, dev)
+        assert mc[0, 0] == c["index0"], c
+        assert hashlib.sha256(mc[0].tobytes()).hexdigest() == c["mc_sha"], c
+        assert np.array_equal(q, oracle.mc_encode(pool, nbr)[1])
+
+
+def test_fused_sphere_reproduces_manifest_model_sha256(dev, golden):
+    """The reference's pipeline golden (pkg/fixtures/protocol/manifest.json):
+    760 sorted-key MC payloads of the fused sphere hash to model_sha256."""
+    from paper_1805_03709_b200 import encode_keys
+
+    d = np.load(golden / "mc_sphere.npz")
+    meta = json.loads((golden / "mc_sphere.json").read_text())
+    rows = oracle.make_pool(d["tsdf"], d["weight"], d["color"])
+    t, pool = table_with_pool(d["keys"], rows, dev)
+    mc, _, _ = encode_keys(t, pool, d["keys"])
+    assert hashlib.sha256(mc.cpu().numpy().tobytes()).hexdigest() == meta["model_sha256"]
+
+
+@pytest.mark.parametrize("field", ["random", "smooth"])
+def test_config1_mc_10k_blocks_vs_oracle(dev, field):
+    keys = workloads.config1_mc_keys()
+    if field == "random":
+        tsdf, weight, color = workloads.random_field(len(keys))
+    else:
+        tsdf, weight, color = workloads.smooth_field(keys)
+    pool = oracle.make_pool(tsdf, weight, color)
+    # MC keys = the TSDF keys plus the -1 shell (absent centres -> zero blocks)
+    mkeys = np.concatenate([keys, keys[:200] - 1])
+    nbr = oracle.neighbor_table(mkeys, keys)
+    mc, q, counts = gpu_encode(pool, nbr, dev)
+    omc, oq, oc = oracle.mc_encode(pool, nbr, threads=8)
+    assert np.array_equal(mc, omc)
+    assert np.array_equal(q, oq)
+    assert np.array_equal(counts, oc)
+    assert counts.sum() > 0
+
+
+def test_compaction_vs_oracle_and_scatter_back(dev):
+    import torch
+
+    from paper_1805_03709_b200 import compact, encode_blocks
+
+    keys = workloads.config1_mc_keys()[:3000]
+    tsdf, weight, color = workloads.random_field(len(keys), seed=5)
+    pool = oracle.make_pool(tsdf, weight, color)
+    nbr = oracle.neighbor_table(keys, keys)
+    mc, _, counts = encode_blocks(_t(pool, dev), _t(nbr, dev))
+    offsets, flat, cells = compact(mc, counts)
+    oo, of, oc = oracle.mc_compact(mc.cpu().numpy())
+    assert np.array_equal(offsets.cpu().numpy().astype(np.uint64), oo)
+    assert np.array_equal(flat.cpu().numpy().view(np.uint16), of)
+    assert np.array_equal(cells.cpu().numpy().view(np.uint32), oc)
+    dense = torch.zeros((len(keys), 512), dtype=torch.int32, device=dev)
+    blk = torch.repeat_interleave(torch.arange(len(keys), device=dev), counts.long())
+    dense[blk, flat.long() & 0xFFFF] = cells
+    assert torch.equal(dense.view(torch.uint8).reshape(mc.shape), mc)
+
+
+def test_recompute_mc_block_api_with_host_blocks(dev, golden):
+    from paper_1805_03709_b200 import TsdfBlock, recompute_mc_block, recompute_mc_blocks
+
+    d = np.load(golden / "mc_random.npz")
+    blocks = {}
+    for i, k in enumerate(d["tsdf_keys"].tolist()):
+        b = TsdfBlock(tuple(k))
+        b.tsdf, b.weight, b.color = d["tsdf"][i], d["weight"][i], d["color"][i]
+        blocks[tuple(k)] = b
+    keys = [tuple(k) for k in d["mc_keys"].tolist()]
+    out = recompute_mc_blocks(keys, blocks.get)
+    assert b"".join(m.to_bytes() for m in out) == d["mc"].tobytes()
+    one = recompute_mc_block(keys[5], blocks.get)
+    assert one.to_bytes() == d["mc"][5].tobytes()
+    assert recompute_mc_block((40, 40, 40), blocks.get).is_empty()
+
+
+def test_room_sample_vs_oracle(dev):
+    """Config 3 geometry: a 60k-block slab of the room, GPU vs oracle."""
+    import torch
+
+    from paper_1805_03709_b200 import encode_keys
+
+    keys = workloads.room_block_keys()[:60_000]
+    kt = torch.from_numpy(keys).to(dev)
+    rows = workloads.room_tsdf_rows(kt)
+    t, pool = table_with_pool(keys, rows.cpu().numpy(), dev, n=1 << 16, excess=1 << 16)
+    mc, q, c = encode_keys(t, pool, keys)
+    rows_np = rows.cpu().numpy()
+    nbr = oracle.neighbor_table(keys, keys)
+    omc, oq, oc = oracle.mc_encode(rows_np, nbr, threads=8)
+    assert np.array_equal(mc.cpu().numpy(), omc)
+    assert np.array_equal(q.cpu().numpy(), oq)
+    assert np.array_equal(c.cpu().numpy().astype(np.uint32), oc)
+    assert oc.sum() > 0

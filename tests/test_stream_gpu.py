@@ -1,0 +1,152 @@
+"""GPU parity tests of the per-client stream sets and the server update path
+against golden sequences recorded from the reference server (tests/golden/).
+
+Bar: each client's pending set bit-exact (sorted); the generation-order
+FIFO append order bit-exact (server.py:62-66); extract_ordered results
+bit-exact incl. stale-entry skipping (server.py:86-95).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def test_streamset_sequences_vs_reference(dev, golden):
+    from paper_1805_03709_b200 import StreamSet
+
+    g = json.loads((golden / "stream_seq.json").read_text())
+    for name in ("fifo_example", "random"):
+        ss = StreamSet(256, 1024)
+        for op, arg, want in g[name]:
+            if op in ("insert", "remove"):
+                assert getattr(ss, op)(tuple(arg)) == want, (op, arg)
+            elif op == "insert_many":
+                assert ss.insert_many([tuple(a) for a in arg]) == want
+            else:
+                assert [list(k) for k in ss.extract_ordered(arg)] == want, (op, arg)
+    assert sorted(list(k) for k in ss.snapshot()) == g["random_final"]
+
+
+def test_fifo_keeps_stale_entries_like_the_deque(dev):
+    from paper_1805_03709_b200 import StreamSet
+
+    ss = StreamSet(64, 64)
+    for k in [(1, 0, 0), (2, 0, 0), (3, 0, 0)]:
+        ss.insert(k)
+    ss.remove((1, 0, 0))
+    ss.insert((4, 0, 0))
+    ss.insert((1, 0, 0))
+    assert ss.fifo_entries() == [(1, 0, 0), (2, 0, 0), (3, 0, 0), (4, 0, 0), (1, 0, 0)]
+    assert ss.extract_ordered(2) == [(1, 0, 0), (2, 0, 0)]
+    assert ss.extract_ordered(2) == [(3, 0, 0), (4, 0, 0)]
+    assert ss.extract_ordered(2) == []
+
+
+def test_fifo_growth_and_long_drain(dev):
+    from paper_1805_03709_b200 import StreamSet
+
+    rng = np.random.default_rng(2)
+    ss = StreamSet(1 << 12, 1 << 12, fifo_capacity=1024)
+    o = oracle.OracleStreamSet()
+    for step in range(30):
+        ks = [tuple(int(v) for v in r) for r in rng.integers(0, 40, (300, 3))]
+        assert ss.insert_many(ks) == o.insert_many(ks)
+        for k in ks[:20]:
+            assert ss.remove(k) == o.remove(k)
+        n = int(rng.integers(0, 200))
+        assert ss.extract_ordered(n) == o.extract_ordered(n)
+    assert ss.extract_ordered(10 ** 6) == o.extract_ordered(10 ** 6)
+    assert ss.size() == o.size() == 0
+
+
+def test_fan_out_40_clients_vs_oracle(dev):
+    """insert_many into > 32 clients (two launches) == per-client oracle."""
+    from paper_1805_03709_b200 import StreamSet, fan_out, remove_everywhere
+
+    rng = np.random.default_rng(3)
+    sets = [StreamSet(1 << 10, 1 << 10) for _ in range(40)]
+    oracles = [oracle.OracleStreamSet() for _ in range(40)]
+    for c in range(40):  # different pending state per client
+        pre = [tuple(int(v) for v in r) for r in rng.integers(0, 12, (c * 3, 3))]
+        sets[c].insert_many(pre)
+        oracles[c].insert_many(pre)
+    for step in range(5):
+        upd = [tuple(int(v) for v in r) for r in rng.integers(0, 12, (64, 3))]
+        affected = oracle.affected_dedup(upd)
+        got = fan_out(sets, affected)
+        want = [o.insert_many(affected) for o in oracles]
+        assert got == want
+        for s, o in zip(sets, oracles):
+            assert s.fifo_entries() == list(o.order)
+        victims = affected[:5]
+        remove_everywhere(sets, victims)
+        for o in oracles:
+            for v in victims:
+                o.remove(v)
+    for s, o in zip(sets, oracles):
+        assert set(s.snapshot()) == o.set
+
+
+def test_affected_dedup_order(dev):
+    import ctypes
+
+    import torch
+
+    from paper_1805_03709_b200 import BlockHashSet, _lib
+
+    rng = np.random.default_rng(9)
+    upd = rng.integers(-5, 5, (700, 3)).astype(np.int32)
+    scratch = BlockHashSet(1 << 14, 1 << 14)
+    out = torch.empty((8 * 700, 3), dtype=torch.int32, device=dev)
+    n = torch.empty(1, dtype=torch.int64, device=dev)
+    k = torch.from_numpy(upd).to(dev)
+    _lib.check(_lib.load().vs_affected_dedup(scratch.handle, _lib.ptr(k), 700, _lib.ptr(out), _lib.ptr(n),
+                                             _lib.stream_of(dev)))
+    got = [tuple(r) for r in out[: int(n.item())].cpu().tolist()]
+    assert got == oracle.affected_dedup(upd.tolist())
+
+
+def test_server_core_replays_reference_server(dev, golden):
+    """Server.on_tsdf_batch / on_reset_blocks / fresh attach, replayed on the
+    GPU core with the reference's exact TSDF bytes (server_blocks.npz)."""
+    from paper_1805_03709_b200 import GpuServerCore
+
+    g = json.loads((golden / "server_seq.json").read_text())
+    d = np.load(golden / "server_blocks.npz")
+    core = GpuServerCore(1 << 12, 1 << 12, stream_buckets=1 << 10, stream_excess=1 << 10)
+    clients = [core.attach(bytes([i]) * 16) for i in range(3)]
+    for step, entry in enumerate(g["steps"]):
+        sel = d["step"] == step
+        keys = d["keys"][sel]
+        assert keys.tolist() == entry["updated"]
+        before = [len(c.fifo_entries()) for c in clients]
+        core.on_tsdf_batch(keys, d["blocks"][sel])
+        for c, cl in enumerate(clients):
+            assert [list(k) for k in cl.fifo_entries()[before[c]:]] == entry["appended"][c]
+            assert sorted(list(k) for k in cl.snapshot()) == entry["pending"][c]
+        if "pending_after_extract_c1" in entry:
+            keep = {tuple(k) for k in entry["pending_after_extract_c1"]}
+            drop = [k for k in clients[1].snapshot() if k not in keep]
+            clients[1].remove_many(drop)  # adopt the reference's random subset
+        if "reset" in entry:
+            core.on_reset_blocks([tuple(v) for v in entry["reset"]])
+            for c, cl in enumerate(clients):
+                assert sorted(list(k) for k in cl.snapshot()) == entry["pending_after_reset"][c]
+    keys, _ = core.mc_map.snapshot_tensor()
+    got = sorted(tuple(k) for k in keys.cpu().tolist())
+    assert [list(k) for k in got] == g["mc_keys"]
+    for k in got:
+        digest = hashlib.sha256(core.mc_payload(k)).hexdigest()
+        assert digest == g["mc_digest"][",".join(map(str, k))], k
+    fresh = core.attach(b"\x09" * 16)
+    assert sorted(list(k) for k in fresh.snapshot()) == g["fresh_pending"]
+    # a returning client keeps its set (server.py:225-239)
+    assert core.attach(bytes([0]) * 16) is clients[0]
