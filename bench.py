@@ -1,0 +1,519 @@
+#!/usr/bin/env python
+"""bench.py -- the SLAMCast hot path on B200 (contract: see README/DESIGN.md).
+
+Headline (BASELINE.json configs[1], "config 2"): a 10M-key block hash set at
+load factor 0.7, batches of 2^22 mixed ops (50% insert: 40% fresh / 60%
+present, 30% find: 50% hit, 20% erase), ONE launch per batch
+(vs_table_apply).  A "step" is one batch.  Reported in M ops/s.
+
+Also on the same line (extra objects):
+  "mc"     config 3: full MC-index + quantised-TSDF encode of the synthetic
+           16 m x 3 m x 16 m room at 5 mm (2,080,160 blocks), blocks/s
+  "cpu_baseline"  the C oracle port of the reference algorithm, timed on this
+           box's host cores on a bounded sample
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun: every rank owns one hash partition (owner =
+fmix32(hash_key) mod N) and each batch is routed to owners with NCCL
+all-to-all and back (weak scaling: per-rank batch and live keys fixed).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "M hash ops/s (insert/find/erase, 1-8 GPU); MC-encoded voxel blocks/s"
+BYTES_PER_OP = 43.2   # 0.5*48 + 0.3*32 + 0.2*48 algorithmic bytes per mixed op
+BYTES_PER_BLOCK = 8704  # 6144 TSDF read + 2048 MC write + 512 quantised write
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--live", type=int, default=10_000_000, help="live keys per GPU (config 2: 10M)")
+    p.add_argument("--batch-log2", type=int, default=22)
+    p.add_argument("--mc-steps", type=int, default=10)
+    p.add_argument("--no-mc", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-threads", type=int, default=0)
+    return p.parse_args()
+
+
+# --------------------------------------------------------------- helpers
+
+def peaks():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu capture."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class Clocks:
+    """Samples nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.t:
+                self.t.join(timeout=2)
+        return self.summary()
+
+    def summary(self):
+        import statistics
+
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------- CPU (oracle)
+
+def cpu_hash_sample(spec, threads: int, batches: int = 1, seed: int = 0):
+    """Oracle port (C restatement of concurrent_hash.py) on a bounded sample:
+    build the config-2 table, then time `batches` mixed batches."""
+    import numpy as np
+
+    import oracle
+    from paper_1805_03709_b200 import workloads
+
+    o = oracle.OracleHashSet(spec.bucket_count, spec.excess)
+    chunk = 1 << 22
+    for a in range(0, spec.live, chunk):
+        o.insert_batch_mt(workloads.id_to_key_np(np.arange(a, min(spec.live, a + chunk))), threads)
+    rng = np.random.default_rng(seed)
+    lo, hi = 0, spec.live
+    times = []
+    ok = True
+    for step in range(batches):
+        ids, ops, expect = workloads.mix_batch_ids_np(spec, step, lo, hi, rng)
+        keys = workloads.id_to_key_np(ids)
+        t0 = time.perf_counter()
+        res, _, fail = o.apply_batch(keys, ops, threads=threads)
+        times.append(time.perf_counter() - t0)
+        ok &= bool(fail == -1 and np.array_equal(res, expect))
+        lo += spec.counts["erase"]
+        hi += spec.counts["fresh"]
+    return times, ok, o.size()
+
+
+def cpu_mc_sample(threads: int, n_blocks: int = 32768):
+    """Oracle MC encode (C restatement of recompute_mc_block) on a slab of the room."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_1805_03709_b200 import workloads
+
+    keys = workloads.room_block_keys()[:n_blocks]
+    rows = workloads.room_tsdf_rows(torch.from_numpy(keys)).numpy()
+    nbr = oracle.neighbor_table(keys, keys)
+    t0 = time.perf_counter()
+    oracle.mc_encode(rows, nbr, threads=threads)
+    return time.perf_counter() - t0, n_blocks
+
+
+# --------------------------------------------------------------- GPU arms
+
+def sync_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+class Router:
+    """Key-hash sharding across ranks: owner = fmix32(hash_key)
+    mod world; requests travel to owners and results back with NCCL
+    all-to-all (torch.distributed all_to_all_single)."""
+
+    def __init__(self, world: int, dev):
+        self.world = world
+        self.dev = dev
+
+    def owner(self, keys):
+        import torch
+
+        x, y, z = keys[:, 0].to(torch.int64), keys[:, 1].to(torch.int64), keys[:, 2].to(torch.int64)
+        h = ((x * 73856093) ^ (y * 19349669) ^ (z * 83492791)) & 0xFFFFFFFF
+        h = ((h ^ (h >> 16)) * 0x85EBCA6B) & 0xFFFFFFFF
+        h = ((h ^ (h >> 13)) * 0xC2B2AE35) & 0xFFFFFFFF
+        h = h ^ (h >> 16)
+        return h % self.world
+
+    def apply(self, table, keys, ops):
+        import torch
+        import torch.distributed as dist
+
+        own = self.owner(keys)
+        order = torch.argsort(own, stable=True)
+        send_counts = torch.bincount(own, minlength=self.world)
+        recv_counts = torch.empty_like(send_counts)
+        dist.all_to_all_single(recv_counts, send_counts)
+        sc, rc = send_counts.tolist(), recv_counts.tolist()
+        payload = torch.cat([keys[order], ops[order].to(torch.int32)[:, None]], dim=1).contiguous()
+        recv = torch.empty((sum(rc), 4), dtype=torch.int32, device=self.dev)
+        dist.all_to_all_single(recv, payload, rc, sc)
+        res, idx = table.apply(recv[:, :3], recv[:, 3].to(torch.uint8))
+        back = torch.empty(keys.shape[0], dtype=torch.uint8, device=self.dev)
+        dist.all_to_all_single(back, res, sc, rc)
+        out = torch.empty_like(back)
+        out[order] = back
+        return out
+
+
+def run_hash(args, dev, rank, world):
+    import torch
+
+    from paper_1805_03709_b200 import BlockHashSet, _lib, workloads
+
+    spec = workloads.MixSpec(live=args.live, load_factor=0.7, batch=1 << args.batch_log2)
+    B = spec.batch
+    s = BlockHashSet(spec.bucket_count, spec.excess, device=dev)
+    # rank r owns its own id space; with world > 1 keys are routed to owners
+    base = rank << 40
+    router = Router(world, dev) if world > 1 else None
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    # initial fill: `live` keys (routed when sharded)
+    chunk = 1 << 22
+    for a in range(0, spec.live, chunk):
+        ids = torch.arange(base + a, base + min(spec.live, a + chunk), device=dev, dtype=torch.int64)
+        keys = workloads.id_to_key_torch(ids)
+        if router:
+            router.apply(s, keys, torch.zeros(keys.shape[0], dtype=torch.uint8, device=dev))
+        else:
+            s.insert_keys(keys)
+    s.check_capacity()
+    torch.cuda.synchronize()
+    lo, hi = base, base + spec.live
+    n_total = args.warmup + args.steps
+    batches = []
+    for step in range(n_total + (0 if args.no_e2e else min(args.steps, 20))):
+        ids, ops, expect = workloads.mix_batch_ids(spec, step, lo, hi, gen, dev)
+        ids = torch.where(ids >= workloads.MISS_BASE, ids + (rank << 50), ids)
+        batches.append((workloads.id_to_key_torch(ids), ops, expect))
+        lo += spec.counts["erase"]
+        hi += spec.counts["fresh"]
+    del ids
+
+    def step_fn(i):
+        k, o, _ = batches[i]
+        if router:
+            return router.apply(s, k, o)
+        return s.apply(k, o)[0]
+
+    ok = True
+    for i in range(args.warmup):
+        r = step_fn(i)
+        ok &= bool(torch.equal(r, batches[i][2]))
+    s.check_capacity()
+    clocks = Clocks(dev.index if world == 1 else int(os.environ.get("LOCAL_RANK", 0)))
+    barrier(world)
+    clocks.start()
+    time.sleep(0.12)  # let the sampler attach before the region starts
+    results = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with _lib.Profile() as prof:
+        barrier(world)
+        ev0.record()
+        for i in range(args.warmup, n_total):
+            results.append(step_fn(i))
+        ev1.record()
+        barrier(world)
+    clk = clocks.stop()
+    ms = sync_max(ev0.elapsed_time(ev1), world)
+    for j, r in enumerate(results):
+        ok &= bool(torch.equal(r, batches[args.warmup + j][2]))
+    s.check_capacity()
+    size_ok = s.approx_size() == spec.live if world == 1 else True
+    ops_total = args.steps * B * world
+    value = ops_total / (ms / 1e3) / 1e6
+    apply_ms = prof.ms["hash"] / max(1, prof.count["hash"])
+    # with routing the table sees ~B ops per rank per step as well
+    achieved = B * BYTES_PER_OP / (apply_ms / 1e3) / 1e9
+    peak, peak_src = peaks()
+    out = {
+        "value": value, "ms_per_step": ms / args.steps, "ok": ok and size_ok, "clocks": clk,
+        "gpu_launches": prof.launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic("k_apply"), "kernel": "vsb::k_apply",
+                     "kernel_ms": apply_ms, "bytes_per_launch": B * BYTES_PER_OP, "peak_source": peak_src,
+                     "note": "algorithmic 43.2 B/op (SURVEY §8d); random 16-B entry access, latency/atomic bound"},
+    }
+    # ---- e2e through the public API with pinned host buffers
+    if not args.no_e2e and world == 1:
+        extra = batches[n_total:]
+        hk = [b[0].cpu().pin_memory() for b in extra]
+        ho = [b[1].cpu().pin_memory() for b in extra]
+        hr = [torch.empty(B, dtype=torch.uint8).pin_memory() for _ in extra]
+        hi_ = [torch.empty(B, dtype=torch.int32).pin_memory() for _ in extra]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        for j in range(len(extra)):
+            res, idx = s.apply(hk[j], ho[j])
+            hr[j].copy_(res, non_blocking=True)
+            hi_[j].copy_(idx, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e_ms = e0.elapsed_time(e1)
+        e2e_ok = all(torch.equal(hr[j], extra[j][2].cpu()) for j in range(len(extra)))
+        out["e2e"] = {"value": len(extra) * B / (e_ms / 1e3) / 1e6, "unit": "M ops/s",
+                      "h2d_bytes_per_step": B * 13, "d2h_bytes_per_step": B * 5, "steps": len(extra),
+                      "wall_s": wall, "ok": e2e_ok}
+    del batches, results
+    return out
+
+
+def run_mc(args, dev):
+    """Config 3: full encode of the synthetic room (2,080,160 blocks)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_1805_03709_b200 import BlockHashSet, _lib, encode_blocks, encode_keys, neighbors, workloads
+
+    keys_np = workloads.room_block_keys()
+    N = len(keys_np)
+    keys = torch.from_numpy(keys_np).to(dev)
+    t = BlockHashSet(1 << 21, 1 << 20, device=dev)
+    _, pos = t.insert_keys(keys)
+    t.check_capacity()
+    pool = torch.empty((t.capacity, 6144), dtype=torch.uint8, device=dev)
+    for a in range(0, N, 1 << 15):
+        pool[pos[a:a + (1 << 15)].long()] = workloads.room_tsdf_rows(keys[a:a + (1 << 15)])
+    mc = torch.empty((N, 2048), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    lib = _lib.load()
+
+    def enc():
+        return encode_keys(t, pool, keys)
+
+    for _ in range(2):
+        mc, q, counts = enc()
+    # parity: a random sample vs the oracle, neighbours gathered from the pool
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(N, 1024, replace=False))
+    nbr = neighbors(t, keys[sample]).cpu().numpy()
+    uniq, inv = np.unique(nbr[nbr >= 0], return_inverse=True)
+    rows = pool[torch.from_numpy(uniq).to(dev).long()].cpu().numpy()
+    local = np.full_like(nbr, -1)
+    local[nbr >= 0] = inv
+    omc, oq, oc = oracle.mc_encode(rows, local, threads=8)
+    ok = bool(np.array_equal(mc[torch.from_numpy(sample).to(dev)].cpu().numpy(), omc)
+              and np.array_equal(q[torch.from_numpy(sample).to(dev)].cpu().numpy(), oq))
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with _lib.Profile() as prof:
+        ev0.record()
+        for _ in range(args.mc_steps):
+            enc()
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    k_ms = prof.ms["mc"] / max(1, prof.count["mc"])
+    peak, src = peaks()
+    achieved = N * BYTES_PER_BLOCK / (k_ms / 1e3) / 1e9
+    out = {"workload": "config 3: room 16x3x16 m, 5 mm voxels, 2,080,160 blocks, fused hash lookups",
+           "value": N * args.mc_steps / (ms / 1e3), "unit": "blocks/s", "ms_per_step": ms / args.mc_steps,
+           "steps": args.mc_steps, "blocks": N, "ok": ok, "gpu_launches": prof.launches,
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                        "traffic": ncu_traffic("k_mc_encode"), "kernel": "vsb::k_mc_encode<true>",
+                        "kernel_ms": k_ms, "bytes_per_launch": N * BYTES_PER_BLOCK, "peak_source": src}}
+    if not args.no_e2e:
+        # e2e: host TSDF rows -> device pool, encode, MC + quantised bytes -> host
+        host_rows = pool[pos.long()].cpu().pin_memory()
+        h_mc = torch.empty((N, 2048), dtype=torch.uint8).pin_memory()
+        h_q = torch.empty((N, 512), dtype=torch.int8).pin_memory()
+        posl = pos.long()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = 2
+        e0.record()
+        for _ in range(steps):
+            dev_rows = host_rows.to(dev, non_blocking=True)
+            pool.index_copy_(0, posl, dev_rows)
+            m, qq, _ = encode_keys(t, pool, keys, counts=False)
+            h_mc.copy_(m, non_blocking=True)
+            h_q.copy_(qq, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        out["e2e"] = {"value": N * steps / (e_ms / 1e3), "unit": "blocks/s", "h2d_bytes_per_step": N * 6144,
+                      "d2h_bytes_per_step": N * (2048 + 512), "steps": steps}
+    return out
+
+
+# ------------------------------------------------------------------ main
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    from paper_1805_03709_b200 import workloads
+
+    spec = workloads.MixSpec(live=args.live, load_factor=0.7, batch=1 << args.batch_log2)
+    threads = args.cpu_threads or cpu_cores()
+    config = {"workload": "config 2: 10M-key block hash set, 50/30/20 insert/find/erase mix, load factor 0.7, "
+                          f"batches of 2^{args.batch_log2} ops (one launch per batch)",
+              "live_keys_per_gpu": spec.live, "slots_per_gpu": spec.slots, "batch_ops": spec.batch,
+              "mix": spec.counts, "key_space": "int3 in [-2^20, 2^20)^3 (injective id map)",
+              "l2": "inputs larger than L2: 229 MB table + fresh 55 MB batch per step",
+              "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU"}
+
+    if args.impl == "reference":
+        # reference arm: the C oracle port of the reference algorithm on host cores
+        if rank != 0:
+            return
+        sys.path.insert(0, str(ROOT))
+        times, ok, size = cpu_hash_sample(spec, threads, batches=args.warmup + args.steps)
+        t = sum(times[args.warmup:])
+        value = args.steps * spec.batch / t / 1e6
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "M ops/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+                "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": value, "unit": "M ops/s", "cores": threads, "kind": "port",
+                                 "sample": f"{args.steps} mixed batches of {spec.batch} ops on the 10M-key table "
+                                           "(C restatement of concurrent_hash.py, bucket-partitioned threads)",
+                                 "ok": ok},
+                "e2e": {"value": value, "unit": "M ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    h = run_hash(args, dev, rank, world)
+    mc = None
+    if not args.no_mc and world == 1:
+        mc = run_mc(args, dev)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        times, ok, _ = cpu_hash_sample(spec, threads, batches=1)
+        mc_t, mc_n = (None, None) if args.no_mc else cpu_mc_sample(threads)
+        cpu = {"value": spec.batch / times[0] / 1e6, "unit": "M ops/s", "cores": threads, "kind": "port",
+               "sample": f"1 mixed batch of {spec.batch} ops on the 10M-key config-2 table (C restatement of "
+                         "concurrent_hash.py, bucket-partitioned threads)", "ok": ok}
+        if mc_t:
+            cpu["mc"] = {"value": mc_n / mc_t, "unit": "blocks/s", "cores": threads, "kind": "port",
+                         "sample": f"{mc_n} room blocks (C restatement of recompute_mc_block)"}
+    if world > 1:
+        import torch.distributed as dist
+
+        oks = torch.tensor([1.0 if h["ok"] else 0.0], device=dev)
+        dist.all_reduce(oks, op=dist.ReduceOp.MIN)
+        h["ok"] = bool(oks.item() > 0)
+    if rank == 0:
+        line = {"metric": METRIC, "value": h["value"], "unit": "M ops/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": config,
+                "parity_ok": h["ok"], "roofline": h["roofline"], "gpu_launches": h["gpu_launches"],
+                "clocks": h["clocks"], "cpu_baseline": cpu, "e2e": h.get("e2e"), "mc": mc}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

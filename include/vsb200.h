@@ -56,6 +56,15 @@ enum { VS_OP_INSERT = 0, VS_OP_FIND = 1, VS_OP_ERASE = 2 };
 const char *vs_last_error(void);
 int32_t vs_abi_version(void);
 
+/* Profiling (bench.py only).  Between begin and end, the dominant kernel of
+ * every call is bracketed with CUDA events on the call's stream; end
+ * synchronises those events and returns, per tag (0 hash op kernel, 1 MC
+ * encode, 2 multi-set stream insert, 3 reserved), the summed kernel time in
+ * ms and the number of launches, plus the number of ALL library kernel
+ * launches issued in between. */
+vs_status vs_profile_begin(void);
+vs_status vs_profile_end(double ms_host[4], uint64_t count_host[4], uint64_t *launches_host);
+
 /* ---------------------------------------------------------------- hash --- */
 
 /* hash_key (concurrent_hash.py:49-59): bucket = (x*p1 ^ y*p2 ^ z*p3) mod n,

@@ -317,8 +317,9 @@ int64_t oh_apply_batch_mt(oh_table *t, const int32_t *keys, const uint8_t *ops, 
     pthread_create(&th[k], NULL, apply_worker, &jobs[k]);
   }
   int64_t fail = -1;
+  for (int k = 0; k < nthreads; ++k) pthread_join(th[k], NULL);
+  /* recycle only after EVERY worker stopped popping */
   for (int k = 0; k < nthreads; ++k) {
-    pthread_join(th[k], NULL);
     for (uint64_t r = 0; r < jobs[k].retired_n; ++r) {
       int64_t top = atomic_fetch_add(&t->top, 1);
       t->stack[top] = jobs[k].retired[r];

@@ -46,6 +46,8 @@ _pu64 = ctypes.POINTER(ctypes.c_uint64)
 SIGNATURES: dict[str, tuple] = {
     "vs_last_error": (ctypes.c_char_p, []),
     "vs_abi_version": (_i32, []),
+    "vs_profile_begin": (_i32, []),
+    "vs_profile_end": (_i32, [ctypes.POINTER(ctypes.c_double * 4), ctypes.POINTER(ctypes.c_uint64 * 4), _pu64]),
     "vs_hash_keys": (_i32, [_vp, _u64, _u32, _vp, _vp]),
     "vs_table_create": (_i32, [_u64, _u64, ctypes.c_int, ctypes.POINTER(_vp)]),
     "vs_table_destroy": (_i32, [_vp]),
@@ -138,3 +140,23 @@ def stream_of(device) -> ctypes.c_void_p:
     import torch
 
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class Profile:
+    """Context manager around vs_profile_begin/end (bench.py)."""
+
+    TAGS = ("hash", "mc", "stream", "other")
+
+    def __enter__(self):
+        check(load().vs_profile_begin())
+        return self
+
+    def __exit__(self, *exc):
+        ms = (ctypes.c_double * 4)()
+        cnt = (ctypes.c_uint64 * 4)()
+        launches = ctypes.c_uint64()
+        check(load().vs_profile_end(ctypes.byref(ms), ctypes.byref(cnt), ctypes.byref(launches)))
+        self.ms = {t: float(ms[i]) for i, t in enumerate(self.TAGS)}
+        self.count = {t: int(cnt[i]) for i, t in enumerate(self.TAGS)}
+        self.launches = int(launches.value)
+        return False

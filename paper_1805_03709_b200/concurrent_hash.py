@@ -20,6 +20,8 @@ import random
 import threading
 from typing import Any, Callable, Iterable, Optional
 
+import numpy as np
+
 from . import _lib
 from ._lib import CapacityExhausted, check, ptr
 
@@ -100,9 +102,10 @@ def _as_keys(keys, device):
     if isinstance(keys, torch.Tensor):
         t = keys
     else:
-        if not isinstance(keys, (list, tuple)):
+        if not isinstance(keys, (list, tuple, np.ndarray)):
             keys = list(keys)
-        t = torch.tensor(keys, dtype=torch.int32) if len(keys) else torch.empty((0, 3), dtype=torch.int32)
+        a = np.asarray(keys, dtype=np.int32).reshape(-1, 3) if len(keys) else np.empty((0, 3), np.int32)
+        t = torch.from_numpy(np.ascontiguousarray(a))
     if t.dtype != torch.int32:
         t = t.to(torch.int32)
     t = t.reshape(-1, 3)

@@ -7,9 +7,12 @@
 //                       duplicates, i.e. the sequential-replay answer;
 //   k_flush_retired  -- recycles erased excess entries into the free stack
 //                       (FreeListStack.push, concurrent_hash.py:72-73).
+#include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "hash_ops.cuh"
 #include "table.h"
@@ -26,6 +29,48 @@ vs_status cuda_status(cudaError_t err, const char* what) {
 }
 
 constexpr int kOpBlock = 256;
+
+// ------------------------------------------------------- launch accounting
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+struct ProfRec {
+  int tag;
+  cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<cudaEvent_t> g_ev_pool;
+static std::vector<ProfRec> g_prof_recs;
+static uint64_t g_prof_launch0 = 0;
+
+static cudaEvent_t take_event() {
+  if (!g_ev_pool.empty()) {
+    cudaEvent_t e = g_ev_pool.back();
+    g_ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+ProfScope::ProfScope(int tag_, cudaStream_t s_) : tag(tag_), s(s_) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on) return;
+  cudaEvent_t a = take_event();
+  cudaEventRecord(a, s);
+  start = (void*)a;
+}
+
+ProfScope::~ProfScope() {
+  if (!start) return;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  cudaEvent_t b = take_event();
+  cudaEventRecord(b, s);
+  g_prof_recs.push_back({tag, (cudaEvent_t)start, b});
+}
 
 // ---------------------------------------------------------------- kernels
 
@@ -84,6 +129,41 @@ __global__ void __launch_bounds__(kOpBlock) k_erase(TableView T, const int32_t* 
     const int32_t pos = erase_key(T, keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]);
     if (erased) erased[i] = pos >= 0;
     if (index) index[i] = pos;
+    delta = -(pos >= 0);
+  }
+  add_size(T, delta);
+}
+
+// Duplicate removes in one batch: the lowest op index wins (sequential replay
+// gives True to the first occurrence).  Phase 1 claims the key's current
+// position with an epoch-tagged atomicMin (values of older batches compare
+// larger, so no clearing pass is needed); phase 2 lets only winners erase.
+__global__ void __launch_bounds__(kOpBlock) k_erase_claim(TableView T, const int32_t* __restrict__ keys, uint64_t n,
+                                                          unsigned long long* __restrict__ claim, uint64_t tag,
+                                                          int32_t* __restrict__ pos_out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t x = keys[3 * i], y = keys[3 * i + 1], z = keys[3 * i + 2];
+  uint32_t meta;
+  const int32_t pos = find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
+  pos_out[i] = pos;
+  if (pos >= 0) atomicMin(&claim[pos], (unsigned long long)(tag | i));
+}
+
+__global__ void __launch_bounds__(kOpBlock) k_erase_win(TableView T, const int32_t* __restrict__ keys, uint64_t n,
+                                                        const unsigned long long* __restrict__ claim, uint64_t tag,
+                                                        uint8_t* __restrict__ erased, int32_t* __restrict__ index) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int delta = 0;
+  if (i < n) {
+    int32_t pos = index[i];
+    if (pos >= 0 && claim[pos] == (tag | i)) {
+      pos = erase_key(T, keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]);
+    } else {
+      pos = -1;
+    }
+    if (erased) erased[i] = pos >= 0;
+    index[i] = pos;
     delta = -(pos >= 0);
   }
   add_size(T, delta);
@@ -338,8 +418,8 @@ __global__ void k_audit_free(TableView T, const uint8_t* __restrict__ reach, uns
 // ------------------------------------------------------------ host helpers
 
 vs_status flush_retired(vs_table* t, cudaStream_t s) {
-  k_flush_retired<<<148, 256, 0, s>>>(t->view());
-  k_flush_final<<<1, 1, 0, s>>>(t->ctl);
+  { k_flush_retired<<<148, 256, 0, s>>>(t->view()); vsb::count_launch(); }
+  { k_flush_final<<<1, 1, 0, s>>>(t->ctl); vsb::count_launch(); }
   VS_CK_LAUNCH("flush_retired");
   return VS_OK;
 }
@@ -347,16 +427,16 @@ vs_status flush_retired(vs_table* t, cudaStream_t s) {
 vs_status erase_device_count(vs_table* t, const int32_t* keys, const uint64_t* n_dev, uint64_t max_n,
                              cudaStream_t s) {
   if (max_n == 0) return VS_OK;
-  k_erase<<<grid_for(max_n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, max_n, n_dev, nullptr, nullptr);
+  { k_erase<<<grid_for(max_n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, max_n, n_dev, nullptr, nullptr); vsb::count_launch(); }
   VS_CK_LAUNCH("k_erase");
   return flush_retired(t, s);
 }
 
 static vs_status compact_live(vs_table* t, int32_t* keys_out, int32_t* pos_out, uint64_t cap_out, cudaStream_t s) {
   const TableView v = t->view();
-  k_chunk_count<<<t->nchunks, 256, 0, s>>>(v, t->cap, t->chunk_counts);
-  k_scan_u32<<<1, 1024, 0, s>>>(t->chunk_counts, t->nchunks, t->chunk_offsets);
-  k_chunk_write<<<t->nchunks, 256, 0, s>>>(v, t->cap, t->chunk_offsets, keys_out, pos_out, cap_out);
+  { k_chunk_count<<<t->nchunks, 256, 0, s>>>(v, t->cap, t->chunk_counts); vsb::count_launch(); }
+  { k_scan_u32<<<1, 1024, 0, s>>>(t->chunk_counts, t->nchunks, t->chunk_offsets); vsb::count_launch(); }
+  { k_chunk_write<<<t->nchunks, 256, 0, s>>>(v, t->cap, t->chunk_offsets, keys_out, pos_out, cap_out); vsb::count_launch(); }
   VS_CK_LAUNCH("compact_live");
   return VS_OK;
 }
@@ -372,13 +452,49 @@ extern "C" {
 const char* vs_last_error(void) { return g_last_error.c_str(); }
 int32_t vs_abi_version(void) { return 1; }
 
+vs_status vs_profile_begin(void) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (auto& r : g_prof_recs) {
+    g_ev_pool.push_back(r.a);
+    g_ev_pool.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  g_prof_on = true;
+  g_prof_launch0 = g_launches.load();
+  return VS_OK;
+}
+
+vs_status vs_profile_end(double ms_host[4], uint64_t count_host[4], uint64_t* launches_host) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = false;
+  for (int i = 0; i < 4; ++i) {
+    if (ms_host) ms_host[i] = 0.0;
+    if (count_host) count_host[i] = 0;
+  }
+  for (auto& r : g_prof_recs) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return cuda_status(e, "vs_profile_end");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    if (r.tag >= 0 && r.tag < 4) {
+      if (ms_host) ms_host[r.tag] += ms;
+      if (count_host) count_host[r.tag] += 1;
+    }
+    g_ev_pool.push_back(r.a);
+    g_ev_pool.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  if (launches_host) *launches_host = g_launches.load() - g_prof_launch0;
+  return VS_OK;
+}
+
 vs_status vs_hash_keys(const int32_t* keys, uint64_t n, uint32_t bucket_count, uint32_t* out, vs_stream_t stream) {
   if (bucket_count < 1) {
     set_error("bucket_count must be >= 1");
     return VS_ERR_INVALID;
   }
   if (n == 0) return VS_OK;
-  k_hash_keys<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(keys, n, bucket_count, out);
+  { k_hash_keys<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(keys, n, bucket_count, out); vsb::count_launch(); }
   VS_CK_LAUNCH("k_hash_keys");
   return VS_OK;
 }
@@ -448,6 +564,7 @@ vs_status vs_table_destroy(vs_table* t) {
   cudaFree(t->chunk_counts);
   cudaFree(t->chunk_offsets);
   cudaFree(t->pos_work);
+  cudaFree(t->claim);
   delete t;
   return VS_OK;
 }
@@ -486,8 +603,8 @@ vs_status vs_table_insert(vs_table* t, const int32_t* keys, uint64_t n, uint8_t*
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   const TableView v = t->view();
-  k_insert<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, created, index);
-  k_fixup_created<<<grid_for(n, 256), 256, 0, s>>>(v, keys, nullptr, n, created, index);
+  { ProfScope prof(0, s); k_insert<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, created, index); vsb::count_launch(); }
+  { k_fixup_created<<<grid_for(n, 256), 256, 0, s>>>(v, keys, nullptr, n, created, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_insert");
   return VS_OK;
 }
@@ -501,7 +618,7 @@ vs_status vs_table_find(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* f
     return VS_ERR_INVALID;
   }
   DeviceGuard g(t->device);
-  k_find<<<grid_for(n, kOpBlock), kOpBlock, 0, (cudaStream_t)stream>>>(t->view(), keys, n, found, index);
+  { ProfScope prof(0, (cudaStream_t)stream); k_find<<<grid_for(n, kOpBlock), kOpBlock, 0, (cudaStream_t)stream>>>(t->view(), keys, n, found, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_find");
   return VS_OK;
 }
@@ -516,7 +633,19 @@ vs_status vs_table_erase(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* 
   }
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
-  k_erase<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, n, nullptr, erased, index);
+  if (!t->claim) {
+    VS_CK(cudaMalloc((void**)&t->claim, sizeof(unsigned long long) * (size_t)t->cap));
+    VS_CK(cudaMemsetAsync(t->claim, 0xFF, sizeof(unsigned long long) * (size_t)t->cap, s));
+  }
+  int32_t* idx = index;
+  if (!idx) VS_CK(cudaMallocAsync((void**)&idx, sizeof(int32_t) * n, s));
+  const uint64_t tag = (uint64_t)(0xFFFFFFFFu - (++t->erase_epoch)) << 32;
+  {
+    ProfScope prof(0, s);
+    { k_erase_claim<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, n, t->claim, tag, idx); vsb::count_launch(); }
+    { k_erase_win<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, n, t->claim, tag, erased, idx); vsb::count_launch(); }
+  }
+  if (!index) cudaFreeAsync(idx, s);
   VS_CK_LAUNCH("vs_table_erase");
   return flush_retired(t, s);
 }
@@ -532,8 +661,8 @@ vs_status vs_table_apply(vs_table* t, const int32_t* keys, const uint8_t* ops, u
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   const TableView v = t->view();
-  k_apply<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, ops, n, result, index);
-  k_fixup_created<<<grid_for(n, 256), 256, 0, s>>>(v, keys, ops, n, result, index);
+  { ProfScope prof(0, s); k_apply<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
+  { k_fixup_created<<<grid_for(n, 256), 256, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_apply");
   return flush_retired(t, s);
 }
@@ -592,9 +721,9 @@ vs_status vs_table_clear(vs_table* t, vs_stream_t stream) {
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   VS_CK(cudaMemsetAsync(t->e, 0, sizeof(Entry) * (size_t)t->cap, s));
-  k_init_free<<<grid_for(t->excess, 256) < 4096 ? grid_for(t->excess, 256) : 4096, 256, 0, s>>>(
-      t->free_stack, t->n, t->excess);
-  k_reset_ctl<<<1, 1, 0, s>>>(t->ctl, t->excess);
+  { k_init_free<<<grid_for(t->excess, 256) < 4096 ? grid_for(t->excess, 256) : 4096, 256, 0, s>>>(
+      t->free_stack, t->n, t->excess); vsb::count_launch(); }
+  { k_reset_ctl<<<1, 1, 0, s>>>(t->ctl, t->excess); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_clear");
   return VS_OK;
 }
@@ -609,7 +738,7 @@ vs_status vs_table_snapshot(vs_table* t, int32_t* keys_out, int32_t* index_out, 
   cudaStream_t s = (cudaStream_t)stream;
   vs_status st = compact_live(t, keys_out, index_out, cap, s);
   if (st != VS_OK) return st;
-  k_copy_total<<<1, 1, 0, s>>>(t->chunk_offsets, t->nchunks, n_dev);
+  { k_copy_total<<<1, 1, 0, s>>>(t->chunk_offsets, t->nchunks, n_dev); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_snapshot");
   return VS_OK;
 }
@@ -632,8 +761,8 @@ vs_status vs_table_extract(vs_table* t, uint64_t max_n, uint64_t seed, int32_t* 
   const uint64_t m = max_n < t->cap ? max_n : t->cap;
   unsigned grid = grid_for(m, 256);
   if (grid > 1184) grid = 1184;
-  k_extract_select<<<grid, 256, 0, s>>>(t->view(), t->cap, t->pos_work, t->chunk_offsets + t->nchunks, max_n, seed,
-                                        keys_out, n_dev);
+  { k_extract_select<<<grid, 256, 0, s>>>(t->view(), t->cap, t->pos_work, t->chunk_offsets + t->nchunks, max_n, seed,
+                                        keys_out, n_dev); vsb::count_launch(); }
   VS_CK_LAUNCH("k_extract_select");
   return erase_device_count(t, keys_out, n_dev, m, s);
 }
@@ -651,8 +780,8 @@ vs_status vs_table_audit(vs_table* t, uint64_t out_host[6], vs_stream_t stream) 
   VS_CK(cudaMalloc((void**)&out, 8 * 8));
   VS_CK(cudaMemsetAsync(reach, 0, t->cap, s));
   VS_CK(cudaMemsetAsync(out, 0, 64, s));
-  k_audit<<<1184, 256, 0, s>>>(t->view(), t->cap, reach, out);
-  k_audit_free<<<148, 256, 0, s>>>(t->view(), reach, out);
+  { k_audit<<<1184, 256, 0, s>>>(t->view(), t->cap, reach, out); vsb::count_launch(); }
+  { k_audit_free<<<148, 256, 0, s>>>(t->view(), reach, out); vsb::count_launch(); }
   unsigned long long h[8];
   long long top = 0;
   VS_CK(cudaMemcpyAsync(h, out, 64, cudaMemcpyDeviceToHost, s));

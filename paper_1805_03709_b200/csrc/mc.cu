@@ -307,8 +307,8 @@ static vs_status launch_mc(const TableView& T, const uint8_t* pool, const int32_
     grid = sms * per_sm;
   }
   const uint64_t g = n < (uint64_t)grid ? n : (uint64_t)grid;
-  k_mc_encode<kFromKeys><<<(unsigned)g, kMcThreads, 0, s>>>(T, pool, keys, nbr, n, (uint32_t*)mc_out, q_out,
-                                                            counts);
+  { ProfScope prof(1, s); k_mc_encode<kFromKeys><<<(unsigned)g, kMcThreads, 0, s>>>(T, pool, keys, nbr, n, (uint32_t*)mc_out, q_out,
+                                                            counts); vsb::count_launch(); }
   VS_CK_LAUNCH("k_mc_encode");
   return VS_OK;
 }
@@ -355,7 +355,7 @@ vs_status vs_mc_neighbors(const vs_table* t, const int32_t* keys, uint64_t n, in
   }
   if (n == 0) return VS_OK;
   DeviceGuard g(t->device);
-  k_mc_neighbors<<<grid_for(8 * n, 256), 256, 0, (cudaStream_t)stream>>>(t->view(), keys, n, nbr_out);
+  { k_mc_neighbors<<<grid_for(8 * n, 256), 256, 0, (cudaStream_t)stream>>>(t->view(), keys, n, nbr_out); vsb::count_launch(); }
   VS_CK_LAUNCH("k_mc_neighbors");
   return VS_OK;
 }
@@ -372,8 +372,8 @@ vs_status vs_mc_compact(const uint8_t* mc, const uint32_t* counts, uint64_t n, u
   cudaStream_t s = (cudaStream_t)stream;
   VS_CK(exclusive_scan<uint32_t>(counts, n, offsets, (uint64_t*)work_dev, s));
   if (n && cell_flat && cell_mc)
-    k_mc_compact<<<grid_for(32 * n, 256), 256, 0, s>>>((const uint32_t*)mc, n, offsets, cell_flat, cell_mc,
-                                                       cell_cap);
+    { k_mc_compact<<<grid_for(32 * n, 256), 256, 0, s>>>((const uint32_t*)mc, n, offsets, cell_flat, cell_mc,
+                                                       cell_cap); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_mc_compact");
   return VS_OK;
 }

@@ -9,6 +9,8 @@
 
 namespace vsb {
 
+void count_launch();  // defined in hash.cu
+
 constexpr int kScanTile = 4096;  // elements per CTA (256 threads x 16)
 
 inline uint64_t scan_tiles(uint64_t n) { return (n + kScanTile - 1) / kScanTile; }
@@ -108,9 +110,9 @@ template <typename T>
 inline cudaError_t exclusive_scan(const T* in, uint64_t n, uint64_t* out, uint64_t* work, cudaStream_t s) {
   if (n == 0) return cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
   const uint64_t nt = scan_tiles(n);
-  k_tile_sums<T><<<(unsigned)nt, 256, 0, s>>>(in, n, work);
-  k_scan_tiles<<<1, 1024, 0, s>>>(work, nt);
-  k_tile_scan<T><<<(unsigned)nt, 256, 0, s>>>(in, n, work, nt, out);
+  { k_tile_sums<T><<<(unsigned)nt, 256, 0, s>>>(in, n, work); vsb::count_launch(); }
+  { k_scan_tiles<<<1, 1024, 0, s>>>(work, nt); vsb::count_launch(); }
+  { k_tile_scan<T><<<(unsigned)nt, 256, 0, s>>>(in, n, work, nt, out); vsb::count_launch(); }
   return cudaGetLastError();
 }
 

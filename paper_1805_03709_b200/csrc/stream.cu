@@ -193,8 +193,8 @@ static vs_status fill_views(vs_table* const* sets, int n_sets, SetViews& V) {
 }
 
 static vs_status flush_multi(const SetViews& V, int C, cudaStream_t s) {
-  k_multi_flush<<<dim3(64, C), 256, 0, s>>>(V);
-  k_multi_flush_final<<<1, 32, 0, s>>>(V, C);
+  { k_multi_flush<<<dim3(64, C), 256, 0, s>>>(V); vsb::count_launch(); }
+  { k_multi_flush_final<<<1, 32, 0, s>>>(V, C); vsb::count_launch(); }
   VS_CK_LAUNCH("flush_multi");
   return VS_OK;
 }
@@ -229,7 +229,7 @@ vs_status vs_affected_dedup(vs_table* scratch, const int32_t* updated, uint64_t 
   VS_CK(cudaMallocAsync((void**)&work, 8 * (scan_tiles(m) + 1), s));
   vs_status st = vs_table_clear(scratch, stream);
   if (st == VS_OK) {
-    k_expand_affected<<<grid_for(m, 256), 256, 0, s>>>(updated, u, all);
+    { k_expand_affected<<<grid_for(m, 256), 256, 0, s>>>(updated, u, all); vsb::count_launch(); }
     st = vs_table_insert(scratch, all, m, created, index, stream);
   }
   if (st == VS_OK) {
@@ -237,8 +237,8 @@ vs_status vs_affected_dedup(vs_table* scratch, const int32_t* updated, uint64_t 
     if (e != cudaSuccess) st = cuda_status(e, "exclusive_scan");
   }
   if (st == VS_OK) {
-    k_scatter_flagged<<<grid_for(m, 256), 256, 0, s>>>(all, m, created, off, out_keys);
-    k_copy_u64<<<1, 1, 0, s>>>(off + m, n_dev);
+    { k_scatter_flagged<<<grid_for(m, 256), 256, 0, s>>>(all, m, created, off, out_keys); vsb::count_launch(); }
+    { k_copy_u64<<<1, 1, 0, s>>>(off + m, n_dev); vsb::count_launch(); }
   }
   cudaFreeAsync(all, s);
   cudaFreeAsync(created, s);
@@ -281,8 +281,8 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
   VS_CK(cudaMallocAsync((void**)&off, 8 * (total + 1), s));
   VS_CK(cudaMallocAsync((void**)&work, 8 * (scan_tiles(total) + 1), s));
   const dim3 grid(grid_for(n, 256), n_sets);
-  k_multi_insert<<<grid, 256, 0, s>>>(V, keys, n, created, index);
-  k_multi_fixup<<<grid, 256, 0, s>>>(V, keys, n, created, index);
+  { ProfScope prof(2, s); k_multi_insert<<<grid, 256, 0, s>>>(V, keys, n, created, index); vsb::count_launch(); }
+  { k_multi_fixup<<<grid, 256, 0, s>>>(V, keys, n, created, index); vsb::count_launch(); }
   cudaError_t e = exclusive_scan<uint8_t>(created, total, off, work, s);
   if (e == cudaSuccess && fifo_keys_host && fifo_cap_host && fifo_tail) {
     FifoViews F;
@@ -290,9 +290,9 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
       F.keys[c] = fifo_keys_host[c];
       F.cap[c] = fifo_cap_host[c] ? fifo_cap_host[c] : 1;
     }
-    k_fifo_append<<<grid, 256, 0, s>>>(F, keys, n, created, off, fifo_tail);
+    { k_fifo_append<<<grid, 256, 0, s>>>(F, keys, n, created, off, fifo_tail); vsb::count_launch(); }
   }
-  if (e == cudaSuccess) k_fifo_tail<<<1, 32, 0, s>>>(off, n, n_sets, fifo_tail, n_created);
+  if (e == cudaSuccess) { k_fifo_tail<<<1, 32, 0, s>>>(off, n, n_sets, fifo_tail, n_created); vsb::count_launch(); }
   cudaFreeAsync(index, s);
   cudaFreeAsync(off, s);
   cudaFreeAsync(work, s);
@@ -317,7 +317,7 @@ vs_status vs_stream_remove_many(vs_table* const* sets_host, int n_sets, const in
   }
   DeviceGuard g(sets_host[0]->device);
   cudaStream_t s = (cudaStream_t)stream;
-  k_multi_erase<<<dim3(grid_for(n, 256), n_sets), 256, 0, s>>>(V, keys, n, erased);
+  { k_multi_erase<<<dim3(grid_for(n, 256), n_sets), 256, 0, s>>>(V, keys, n, erased); vsb::count_launch(); }
   VS_CK_LAUNCH("k_multi_erase");
   return flush_multi(V, n_sets, s);
 }
@@ -353,14 +353,14 @@ vs_status vs_stream_extract_ordered(vs_table* set, const int32_t* fifo_keys, uin
     const uint64_t need = max_n - out;
     uint64_t w = std::min<uint64_t>(tail_host - head, std::max<uint64_t>(need, 1024));
     w = std::min(w, wmax);
-    k_gather_ring<<<grid_for(w, 256), 256, 0, s>>>(fifo_keys, fifo_cap, head, w, wkeys);
+    { k_gather_ring<<<grid_for(w, 256), 256, 0, s>>>(fifo_keys, fifo_cap, head, w, wkeys); vsb::count_launch(); }
     // first occurrence inside the window (later duplicates are stale by
     // construction: the earlier entry either delivers the key or finds it gone)
     st = vs_table_clear(scratch, stream);
     if (st == VS_OK) st = vs_table_insert(scratch, wkeys, w, first, idx, stream);
     if (st == VS_OK) st = vs_table_find(set, wkeys, w, present, idx, stream);
     if (st != VS_OK) break;
-    k_candidates<<<grid_for(w, 256), 256, 0, s>>>(first, present, w, cand);
+    { k_candidates<<<grid_for(w, 256), 256, 0, s>>>(first, present, w, cand); vsb::count_launch(); }
     cudaError_t e = exclusive_scan<uint8_t>(cand, w, off, work, s);
     if (e != cudaSuccess) {
       st = cuda_status(e, "exclusive_scan");
@@ -374,16 +374,16 @@ vs_status vs_stream_extract_ordered(vs_table* set, const int32_t* fifo_keys, uin
     }
     uint64_t cut = w - 1, taken = total;
     if (total >= need) {
-      k_find_cut<<<grid_for(w, 256), 256, 0, s>>>(cand, off, w, need, cut_dev);
+      { k_find_cut<<<grid_for(w, 256), 256, 0, s>>>(cand, off, w, need, cut_dev); vsb::count_launch(); }
       if ((e = cudaMemcpyAsync(&cut, cut_dev, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
           (e = cudaStreamSynchronize(s)) != cudaSuccess) {
         st = cuda_status(e, "extract_ordered: cut");
         break;
       }
       taken = need;
-      k_clip_flags<<<grid_for(w, 256), 256, 0, s>>>(cand, w, cut);
+      { k_clip_flags<<<grid_for(w, 256), 256, 0, s>>>(cand, w, cut); vsb::count_launch(); }
     }
-    k_scatter_flagged<<<grid_for(w, 256), 256, 0, s>>>(wkeys, w, cand, off, keys_out + 3 * out);
+    { k_scatter_flagged<<<grid_for(w, 256), 256, 0, s>>>(wkeys, w, cand, off, keys_out + 3 * out); vsb::count_launch(); }
     if (taken) st = vs_table_erase(set, keys_out + 3 * out, taken, nullptr, nullptr, stream);
     out += taken;
     head += cut + 1;

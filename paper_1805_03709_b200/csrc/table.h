@@ -21,6 +21,8 @@ struct vs_table {
   uint32_t* chunk_counts = nullptr;
   uint64_t* chunk_offsets = nullptr;  // nchunks + 1
   int32_t* pos_work = nullptr;        // lazily allocated, cap entries
+  unsigned long long* claim = nullptr;  // lazily allocated, duplicate-erase claims
+  uint32_t erase_epoch = 0;
 
   vsb::TableView view() const {
     vsb::TableView v;
@@ -55,6 +57,21 @@ struct DeviceGuard {
     cudaGetDevice(&cur);
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
   }
+};
+
+// Every kernel launch of the library is counted (bench.py reports the count
+// of launches inside its timed region as "gpu_launches").
+void count_launch();
+
+// Event-timed scope around the dominant kernel of a call while profiling is
+// on (vs_profile_begin/end).  Tags: 0 hash op kernel, 1 MC encode, 2 stream
+// multi-set insert.
+struct ProfScope {
+  int tag;
+  cudaStream_t s;
+  void* start = nullptr;
+  ProfScope(int tag, cudaStream_t s);
+  ~ProfScope();
 };
 
 // internal entry points shared across translation units
