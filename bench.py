@@ -367,7 +367,10 @@ def run_mc(args, dev):
     keys_np = workloads.room_block_keys()
     N = len(keys_np)
     keys = torch.from_numpy(keys_np).to(dev)
-    t = BlockHashSet(1 << 21, 1 << 20, device=dev)
+    # the normative spatial hash (concurrent_hash.py:49-59) collides heavily on
+    # structured room keys (1.35M distinct values for 2.08M keys): ~1.08M keys
+    # land in the excess region whatever the bucket count, so size it 2^21
+    t = BlockHashSet(1 << 21, 1 << 21, device=dev)
     _, pos = t.insert_keys(keys)
     t.check_capacity()
     pool = torch.empty((t.capacity, 6144), dtype=torch.uint8, device=dev)

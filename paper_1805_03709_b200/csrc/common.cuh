@@ -33,24 +33,27 @@ struct __align__(16) Entry {
 
 // Device control block of one table.
 struct Ctl {
-  long long free_top;            // entries in the free-list stack
-  unsigned long long retired_n;  // excess entries erased in the running launch
-  unsigned long long size;       // live keys (approx_size)
-  unsigned int error;            // sticky: bit 0 = capacity exhausted
+  unsigned long long size;  // live keys (approx_size)
+  unsigned int error;       // sticky: bit 0 = capacity exhausted
   unsigned int pad;
-  unsigned long long aux[4];     // scratch counters for multi-kernel ops
 };
+
+constexpr uint32_t kMaxStripes = 32;  // free-list stripes
+constexpr uint32_t kTopStride = 32;   // long longs between stripe tops (256 B)
 
 // By-value view passed to kernels.
 struct TableView {
   Entry* e;
-  uint32_t* free_stack;  // [excess] absolute positions
-  uint32_t* retired;     // [excess] erased excess positions, recycled after the launch
-  int32_t* first_op;     // [cap] lowest op index per freshly created entry
+  uint32_t* free_stack;      // [stripes * stripe_cap] absolute excess positions
+  long long* tops;           // [stripes * kTopStride] entries per stripe
+  unsigned long long* claim; // [cap] epoch-tagged lowest op index (created / erase dedup)
   Ctl* ctl;
-  uint32_t n;            // bucket_count
+  uint32_t n;                // bucket_count
   uint32_t excess;
-  uint64_t magic;        // Lemire fastmod constant for n
+  uint32_t stripes;
+  uint32_t stripe_cap;
+  uint64_t magic;            // Lemire fastmod constant for n
+  unsigned long long tag;    // (0xFFFFFFFF - launch epoch) << 32
 };
 
 // hash_key (concurrent_hash.py:49-59): uint32 wrapping products, XOR.

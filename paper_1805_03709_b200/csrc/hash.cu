@@ -5,8 +5,11 @@
 // type in one launch if wanted (vs_table_apply), followed by
 //   k_fixup_created  -- gives `created` to the lowest op index among in-batch
 //                       duplicates, i.e. the sequential-replay answer;
-//   k_flush_retired  -- recycles erased excess entries into the free stack
-//                       (FreeListStack.push, concurrent_hash.py:72-73).
+//   k_recycle        -- pushes the excess entries vacated by erases back onto
+//                       the striped free list (FreeListStack.push,
+//                       concurrent_hash.py:72-73), from the ops' vacated
+//                       positions, so the op kernel itself needs no atomics
+//                       for it.
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -81,17 +84,24 @@ __global__ void k_hash_keys(const int32_t* __restrict__ keys, uint64_t n, uint32
   out[i] = hash_raw(keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]) % nb;
 }
 
-__global__ void k_init_free(uint32_t* __restrict__ stack, uint32_t n, uint32_t excess) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < excess;
+// Free list: stripe s holds excess positions n + [s*C, min((s+1)*C, excess)).
+__global__ void k_init_free(TableView T) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T.excess;
        i += (uint64_t)gridDim.x * blockDim.x)
-    stack[i] = n + (uint32_t)i;  // FreeListStack(range(n, cap)): first pop = cap-1
+    T.free_stack[i] = T.n + (uint32_t)i;  // stripe s, slot i - s*C == i (contiguous layout)
 }
 
-__global__ void k_reset_ctl(Ctl* ctl, uint32_t excess) {
-  ctl->free_top = excess;
-  ctl->retired_n = 0;
-  ctl->size = 0;
-  ctl->error = 0;
+__global__ void k_reset_ctl(TableView T) {
+  for (uint32_t s = threadIdx.x; s < T.stripes; s += blockDim.x) {
+    const long long lo = (long long)s * T.stripe_cap;
+    long long c = (long long)T.excess - lo;
+    if (c > (long long)T.stripe_cap) c = T.stripe_cap;
+    T.tops[(size_t)s * kTopStride] = c < 0 ? 0 : c;
+  }
+  if (threadIdx.x == 0) {
+    T.ctl->size = 0;
+    T.ctl->error = 0;
+  }
 }
 
 __global__ void __launch_bounds__(kOpBlock) k_insert(TableView T, const int32_t* __restrict__ keys, uint64_t n,
@@ -105,7 +115,7 @@ __global__ void __launch_bounds__(kOpBlock) k_insert(TableView T, const int32_t*
     index[i] = r.pos;
     delta = r.created;
   }
-  add_size(T, delta);
+  add_size_cta(T, delta);
 }
 
 __global__ void __launch_bounds__(kOpBlock) k_find(TableView T, const int32_t* __restrict__ keys, uint64_t n,
@@ -119,19 +129,18 @@ __global__ void __launch_bounds__(kOpBlock) k_find(TableView T, const int32_t* _
   index[i] = pos;
 }
 
+// Single-pass erase for batches of DISTINCT keys (internal: extract paths).
 __global__ void __launch_bounds__(kOpBlock) k_erase(TableView T, const int32_t* __restrict__ keys, uint64_t n,
-                                                    const uint64_t* __restrict__ n_dev,
-                                                    uint8_t* __restrict__ erased, int32_t* __restrict__ index) {
+                                                    const uint64_t* __restrict__ n_dev, int32_t* __restrict__ index) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n_dev) n = *n_dev < n ? *n_dev : n;
   int delta = 0;
   if (i < n) {
     const int32_t pos = erase_key(T, keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]);
-    if (erased) erased[i] = pos >= 0;
-    if (index) index[i] = pos;
+    index[i] = pos;
     delta = -(pos >= 0);
   }
-  add_size(T, delta);
+  add_size_cta(T, delta);
 }
 
 // Duplicate removes in one batch: the lowest op index wins (sequential replay
@@ -139,7 +148,6 @@ __global__ void __launch_bounds__(kOpBlock) k_erase(TableView T, const int32_t* 
 // position with an epoch-tagged atomicMin (values of older batches compare
 // larger, so no clearing pass is needed); phase 2 lets only winners erase.
 __global__ void __launch_bounds__(kOpBlock) k_erase_claim(TableView T, const int32_t* __restrict__ keys, uint64_t n,
-                                                          unsigned long long* __restrict__ claim, uint64_t tag,
                                                           int32_t* __restrict__ pos_out) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -147,17 +155,16 @@ __global__ void __launch_bounds__(kOpBlock) k_erase_claim(TableView T, const int
   uint32_t meta;
   const int32_t pos = find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
   pos_out[i] = pos;
-  if (pos >= 0) atomicMin(&claim[pos], (unsigned long long)(tag | i));
+  if (pos >= 0) atomicMin(&T.claim[pos], T.tag | (unsigned long long)i);
 }
 
 __global__ void __launch_bounds__(kOpBlock) k_erase_win(TableView T, const int32_t* __restrict__ keys, uint64_t n,
-                                                        const unsigned long long* __restrict__ claim, uint64_t tag,
                                                         uint8_t* __restrict__ erased, int32_t* __restrict__ index) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int delta = 0;
   if (i < n) {
     int32_t pos = index[i];
-    if (pos >= 0 && claim[pos] == (tag | i)) {
+    if (pos >= 0 && T.claim[pos] == (T.tag | (unsigned long long)i)) {
       pos = erase_key(T, keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]);
     } else {
       pos = -1;
@@ -166,7 +173,7 @@ __global__ void __launch_bounds__(kOpBlock) k_erase_win(TableView T, const int32
     index[i] = pos;
     delta = -(pos >= 0);
   }
-  add_size(T, delta);
+  add_size_cta(T, delta);
 }
 
 __global__ void __launch_bounds__(kOpBlock) k_apply(TableView T, const int32_t* __restrict__ keys,
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(kOpBlock) k_apply(TableView T, const int32_t* 
     result[i] = res;
     index[i] = pos;
   }
-  add_size(T, delta);
+  add_size_cta(T, delta);
 }
 
 // created[i] goes to the lowest op index that inserted the same key in this
@@ -209,7 +216,7 @@ __global__ void k_fixup_created(TableView T, const int32_t* __restrict__ keys, c
   if (!created[i]) return;
   const int32_t pos = index[i];
   atomicAnd(&T.e[pos].meta, ~kFresh);
-  const int32_t m = T.first_op[pos];
+  const int32_t m = (int32_t)(uint32_t)(T.claim[pos] & 0xFFFFFFFFull);
   if (m >= 0 && (uint64_t)m < i && keys[3 * (uint64_t)m] == keys[3 * i] &&
       keys[3 * (uint64_t)m + 1] == keys[3 * i + 1] && keys[3 * (uint64_t)m + 2] == keys[3 * i + 2]) {
     created[i] = 0;
@@ -217,17 +224,16 @@ __global__ void k_fixup_created(TableView T, const int32_t* __restrict__ keys, c
   }
 }
 
-__global__ void k_flush_retired(TableView T) {
-  const unsigned long long r = T.ctl->retired_n;
-  const long long top = T.ctl->free_top;
-  for (unsigned long long j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < r;
-       j += (uint64_t)gridDim.x * blockDim.x)
-    T.free_stack[top + (long long)j] = T.retired[j];
-}
-
-__global__ void k_flush_final(Ctl* ctl) {
-  ctl->free_top += (long long)ctl->retired_n;
-  ctl->retired_n = 0;
+// Push vacated excess positions back onto the striped free list (warp-
+// aggregated reservations; a full stripe hands the lanes to the next one).
+__global__ void k_recycle(TableView T, const int32_t* __restrict__ pos, const uint8_t* __restrict__ flag,
+                          const uint8_t* __restrict__ ops, const uint64_t* __restrict__ n_dev, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n_dev) n = *n_dev < n ? *n_dev : n;
+  if (i >= n) return;
+  const int32_t e = pos[i];
+  if (e < (int32_t)T.n || (flag && !flag[i]) || (ops && ops[i] != VS_OP_ERASE)) return;
+  push_free(T, (uint32_t)e);
 }
 
 // ---- ordered compaction of live entries (snapshot_keys / extract_batch)
@@ -408,28 +414,35 @@ __global__ void k_audit(TableView T, uint32_t cap, uint8_t* __restrict__ reach, 
 }
 
 __global__ void k_audit_free(TableView T, const uint8_t* __restrict__ reach, unsigned long long* __restrict__ out) {
-  const long long top = T.ctl->free_top;
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < top; j += (long long)gridDim.x * blockDim.x) {
-    const uint32_t e = T.free_stack[j];
-    if (e < T.n || e >= T.n + T.excess || reach[e]) atomicAdd(&out[5], 1ull);
+  for (uint32_t s = blockIdx.x; s < T.stripes; s += gridDim.x) {
+    const long long top = T.tops[(size_t)s * kTopStride];
+    if (threadIdx.x == 0) atomicAdd(&out[2], (unsigned long long)(top < 0 ? 0 : top));
+    for (long long j = threadIdx.x; j < top; j += blockDim.x) {
+      const uint32_t e = T.free_stack[(size_t)s * T.stripe_cap + (size_t)j];
+      if (e < T.n || e >= T.n + T.excess || reach[e]) atomicAdd(&out[5], 1ull);
+    }
   }
 }
 
 // ------------------------------------------------------------ host helpers
 
-vs_status flush_retired(vs_table* t, cudaStream_t s) {
-  { k_flush_retired<<<148, 256, 0, s>>>(t->view()); vsb::count_launch(); }
-  { k_flush_final<<<1, 1, 0, s>>>(t->ctl); vsb::count_launch(); }
-  VS_CK_LAUNCH("flush_retired");
-  return VS_OK;
+void launch_recycle(const TableView& v, const int32_t* pos, const uint8_t* flag, const uint8_t* ops,
+                    const uint64_t* n_dev, uint64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  { k_recycle<<<grid_for(n, 256), 256, 0, s>>>(v, pos, flag, ops, n_dev, n); vsb::count_launch(); }
 }
 
 vs_status erase_device_count(vs_table* t, const int32_t* keys, const uint64_t* n_dev, uint64_t max_n,
                              cudaStream_t s) {
   if (max_n == 0) return VS_OK;
-  { k_erase<<<grid_for(max_n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, max_n, n_dev, nullptr, nullptr); vsb::count_launch(); }
-  VS_CK_LAUNCH("k_erase");
-  return flush_retired(t, s);
+  int32_t* idx = nullptr;
+  VS_CK(cudaMallocAsync((void**)&idx, sizeof(int32_t) * max_n, s));
+  const TableView v = t->next_view();
+  { k_erase<<<grid_for(max_n, kOpBlock), kOpBlock, 0, s>>>(v, keys, max_n, n_dev, idx); vsb::count_launch(); }
+  launch_recycle(v, idx, nullptr, nullptr, n_dev, max_n, s);
+  cudaFreeAsync(idx, s);
+  VS_CK_LAUNCH("erase_device_count");
+  return VS_OK;
 }
 
 static vs_status compact_live(vs_table* t, int32_t* keys_out, int32_t* pos_out, uint64_t cap_out, cudaStream_t s) {
@@ -523,6 +536,8 @@ vs_status vs_table_create(uint64_t bucket_count, uint64_t excess_capacity, int d
   t->n = (uint32_t)bucket_count;
   t->excess = (uint32_t)excess_capacity;
   t->cap = t->n + t->excess;
+  t->stripes = t->excess < kMaxStripes ? t->excess : kMaxStripes;
+  t->stripe_cap = (t->excess + t->stripes - 1) / t->stripes;
   t->magic = fastmod_magic(t->n);
   t->nchunks = (t->cap + kChunk - 1) / kChunk;
   cudaError_t err = cudaSuccess;
@@ -530,9 +545,9 @@ vs_status vs_table_create(uint64_t bucket_count, uint64_t excess_capacity, int d
     if (err == cudaSuccess) err = cudaMalloc(p, bytes);
   };
   A((void**)&t->e, sizeof(Entry) * (size_t)t->cap);
-  A((void**)&t->free_stack, sizeof(uint32_t) * (size_t)t->excess);
-  A((void**)&t->retired, sizeof(uint32_t) * (size_t)t->excess);
-  A((void**)&t->first_op, sizeof(int32_t) * (size_t)t->cap);
+  A((void**)&t->free_stack, sizeof(uint32_t) * (size_t)t->stripes * t->stripe_cap);
+  A((void**)&t->tops, sizeof(long long) * (size_t)t->stripes * kTopStride);
+  A((void**)&t->claim, sizeof(unsigned long long) * (size_t)t->cap);
   A((void**)&t->ctl, sizeof(Ctl));
   A((void**)&t->chunk_counts, sizeof(uint32_t) * (size_t)t->nchunks);
   A((void**)&t->chunk_offsets, sizeof(uint64_t) * ((size_t)t->nchunks + 1));
@@ -558,13 +573,12 @@ vs_status vs_table_destroy(vs_table* t) {
   DeviceGuard g(t->device);
   cudaFree(t->e);
   cudaFree(t->free_stack);
-  cudaFree(t->retired);
-  cudaFree(t->first_op);
+  cudaFree(t->tops);
+  cudaFree(t->claim);
   cudaFree(t->ctl);
   cudaFree(t->chunk_counts);
   cudaFree(t->chunk_offsets);
   cudaFree(t->pos_work);
-  cudaFree(t->claim);
   delete t;
   return VS_OK;
 }
@@ -602,8 +616,11 @@ vs_status vs_table_insert(vs_table* t, const int32_t* keys, uint64_t n, uint8_t*
   }
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
-  const TableView v = t->view();
-  { ProfScope prof(0, s); k_insert<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, created, index); vsb::count_launch(); }
+  const TableView v = t->next_view();
+  {
+    ProfScope prof(0, s);
+    { k_insert<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, created, index); vsb::count_launch(); }
+  }
   { k_fixup_created<<<grid_for(n, 256), 256, 0, s>>>(v, keys, nullptr, n, created, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_insert");
   return VS_OK;
@@ -618,7 +635,11 @@ vs_status vs_table_find(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* f
     return VS_ERR_INVALID;
   }
   DeviceGuard g(t->device);
-  { ProfScope prof(0, (cudaStream_t)stream); k_find<<<grid_for(n, kOpBlock), kOpBlock, 0, (cudaStream_t)stream>>>(t->view(), keys, n, found, index); vsb::count_launch(); }
+  cudaStream_t s = (cudaStream_t)stream;
+  {
+    ProfScope prof(0, s);
+    { k_find<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, n, found, index); vsb::count_launch(); }
+  }
   VS_CK_LAUNCH("vs_table_find");
   return VS_OK;
 }
@@ -633,21 +654,18 @@ vs_status vs_table_erase(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* 
   }
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (!t->claim) {
-    VS_CK(cudaMalloc((void**)&t->claim, sizeof(unsigned long long) * (size_t)t->cap));
-    VS_CK(cudaMemsetAsync(t->claim, 0xFF, sizeof(unsigned long long) * (size_t)t->cap, s));
-  }
   int32_t* idx = index;
   if (!idx) VS_CK(cudaMallocAsync((void**)&idx, sizeof(int32_t) * n, s));
-  const uint64_t tag = (uint64_t)(0xFFFFFFFFu - (++t->erase_epoch)) << 32;
+  const TableView v = t->next_view();
   {
     ProfScope prof(0, s);
-    { k_erase_claim<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, n, t->claim, tag, idx); vsb::count_launch(); }
-    { k_erase_win<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(t->view(), keys, n, t->claim, tag, erased, idx); vsb::count_launch(); }
+    { k_erase_claim<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, idx); vsb::count_launch(); }
+    { k_erase_win<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, erased, idx); vsb::count_launch(); }
   }
+  launch_recycle(v, idx, nullptr, nullptr, nullptr, n, s);
   if (!index) cudaFreeAsync(idx, s);
   VS_CK_LAUNCH("vs_table_erase");
-  return flush_retired(t, s);
+  return VS_OK;
 }
 
 vs_status vs_table_apply(vs_table* t, const int32_t* keys, const uint8_t* ops, uint64_t n, uint8_t* result,
@@ -660,11 +678,15 @@ vs_status vs_table_apply(vs_table* t, const int32_t* keys, const uint8_t* ops, u
   }
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
-  const TableView v = t->view();
-  { ProfScope prof(0, s); k_apply<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
+  const TableView v = t->next_view();
+  {
+    ProfScope prof(0, s);
+    { k_apply<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
+  }
   { k_fixup_created<<<grid_for(n, 256), 256, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
+  launch_recycle(v, index, result, ops, nullptr, n, s);
   VS_CK_LAUNCH("vs_table_apply");
-  return flush_retired(t, s);
+  return VS_OK;
 }
 
 vs_status vs_table_check(vs_table* t, vs_stream_t stream) {
@@ -706,10 +728,16 @@ vs_status vs_table_free_count(vs_table* t, uint64_t* free_host, vs_stream_t stre
     return VS_ERR_INVALID;
   }
   DeviceGuard g(t->device);
-  long long top = 0;
-  VS_CK(cudaMemcpyAsync(&top, &t->ctl->free_top, 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  std::vector<long long> tops((size_t)t->stripes * kTopStride);
+  VS_CK(cudaMemcpyAsync(tops.data(), t->tops, sizeof(long long) * tops.size(), cudaMemcpyDeviceToHost,
+                        (cudaStream_t)stream));
   VS_CK(cudaStreamSynchronize((cudaStream_t)stream));
-  *free_host = top < 0 ? 0 : (uint64_t)top;
+  uint64_t sum = 0;
+  for (uint32_t s = 0; s < t->stripes; ++s) {
+    const long long v = tops[(size_t)s * kTopStride];
+    sum += v < 0 ? 0 : (uint64_t)v;
+  }
+  *free_host = sum;
   return VS_OK;
 }
 
@@ -721,9 +749,12 @@ vs_status vs_table_clear(vs_table* t, vs_stream_t stream) {
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   VS_CK(cudaMemsetAsync(t->e, 0, sizeof(Entry) * (size_t)t->cap, s));
-  { k_init_free<<<grid_for(t->excess, 256) < 4096 ? grid_for(t->excess, 256) : 4096, 256, 0, s>>>(
-      t->free_stack, t->n, t->excess); vsb::count_launch(); }
-  { k_reset_ctl<<<1, 1, 0, s>>>(t->ctl, t->excess); vsb::count_launch(); }
+  VS_CK(cudaMemsetAsync(t->claim, 0xFF, sizeof(unsigned long long) * (size_t)t->cap, s));
+  t->epoch = 0;
+  const TableView v = t->view();
+  const unsigned g_init = grid_for(t->excess, 256) < 4096 ? grid_for(t->excess, 256) : 4096;
+  { k_init_free<<<g_init, 256, 0, s>>>(v); vsb::count_launch(); }
+  { k_reset_ctl<<<1, 32, 0, s>>>(v); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_clear");
   return VS_OK;
 }
@@ -783,15 +814,13 @@ vs_status vs_table_audit(vs_table* t, uint64_t out_host[6], vs_stream_t stream) 
   { k_audit<<<1184, 256, 0, s>>>(t->view(), t->cap, reach, out); vsb::count_launch(); }
   { k_audit_free<<<148, 256, 0, s>>>(t->view(), reach, out); vsb::count_launch(); }
   unsigned long long h[8];
-  long long top = 0;
   VS_CK(cudaMemcpyAsync(h, out, 64, cudaMemcpyDeviceToHost, s));
-  VS_CK(cudaMemcpyAsync(&top, &t->ctl->free_top, 8, cudaMemcpyDeviceToHost, s));
   VS_CK(cudaStreamSynchronize(s));
   cudaFree(reach);
   cudaFree(out);
   out_host[0] = h[0];
   out_host[1] = h[1];
-  out_host[2] = top < 0 ? 0 : (uint64_t)top;
+  out_host[2] = h[2];
   out_host[3] = h[3];
   out_host[4] = h[4];
   out_host[5] = h[5] + h[6];

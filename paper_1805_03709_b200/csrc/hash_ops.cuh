@@ -6,63 +6,100 @@
 //   * one thread per op, thousands of ops in flight per SM; entries are read
 //     with single 16-byte L2-coherent vector loads (key + meta together);
 //   * the reference's 1024 striped try-locks + seqlock versions become ONE
-//     lock bit in each bucket entry's meta word (atom.or.acquire /
-//     atom.exch.release), so a lock costs no extra memory traffic;
+//     lock bit in each bucket entry's meta word, so a lock costs no extra
+//     memory traffic;
 //   * readers need no version validation: chains change only by tail append
-//     (published last, release) and by unlinking (victim keeps its stale NEXT,
-//     like concurrent_hash.py:286-288), and unlinked excess entries are NOT
-//     reused inside the launch -- they go to `retired` and rejoin the free
-//     stack between launches, which removes the ABA case the seqlock guards;
-//   * free-list pops are warp-aggregated (one atomic per warp, not per op).
+//     (published last) and by unlinking (victim keeps its stale NEXT, like
+//     concurrent_hash.py:286-288), and unlinked excess entries are NOT reused
+//     inside the launch -- they are recycled into the free list by a separate
+//     launch, which removes the ABA case the seqlock guards;
+//   * memory ordering is paid only where something is published: a claim of
+//     an empty bucket is ONE 16-byte store (key + meta + unlock), lock
+//     acquisition orders the re-scan through a data dependency on the lock
+//     word, and release fences remain only around excess-entry links;
+//   * the free-list stack is striped over kStripes counters (separate L2
+//     sectors) with warp-aggregated pops; a pop fails (CapacityExhausted)
+//     only after every stripe was seen empty, so exhaustion stays exact;
+//   * "created" for in-batch duplicates goes to the lowest op index through
+//     an epoch-tagged 64-bit atomicMin (no ordering, no clearing pass).
 #pragma once
 #include "common.cuh"
 
 namespace vsb {
 
-// Pop one excess entry from the free-list stack (FreeListStack.pop,
-// concurrent_hash.py:75-79), aggregated over the lanes that reach this call
-// together.  Returns -1 when the stack is empty (CapacityExhausted).
-__device__ __forceinline__ int64_t pop_free(const TableView& T) {
-  const uint32_t m = __activemask();
-  const uint32_t lane = lane_id();
-  const int leader = __ffs(m) - 1;
-  const int cnt = __popc(m);
-  const int rank = __popc(m & lanemask_lt());
-  long long old = 0;
-  if ((int)lane == leader)
-    old = (long long)atomicAdd((unsigned long long*)&T.ctl->free_top, (unsigned long long)(-(long long)cnt));
-  old = __shfl_sync(m, old, leader);
-  const long long t = old - 1 - rank;
-  if (t < 0) {
-    // give the failed ticket back; the stack top never rises above the
-    // number of entries not yet handed out
-    atomicAdd((unsigned long long*)&T.ctl->free_top, 1ull);
-    return -1;
-  }
-  return (int64_t)T.free_stack[t];
-}
-
-// Record an unlinked excess entry for recycling after the launch.
-__device__ __forceinline__ void retire(const TableView& T, uint32_t pos) {
-  const uint32_t m = __activemask();
-  const uint32_t lane = lane_id();
-  const int leader = __ffs(m) - 1;
-  const int cnt = __popc(m);
-  const int rank = __popc(m & lanemask_lt());
-  unsigned long long base = 0;
-  if ((int)lane == leader) base = atomicAdd(&T.ctl->retired_n, (unsigned long long)cnt);
-  base = __shfl_sync(m, base, leader);
-  T.retired[base + rank] = pos;
-}
-
 __device__ __forceinline__ uint32_t next_pos(const TableView& T, uint32_t meta) {
   return T.n + (meta & kNext) - 1u;
 }
 
+__device__ __forceinline__ uint32_t atom_or_relaxed(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.relaxed.gpu.global.or.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ uint32_t atom_exch_relaxed(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.relaxed.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Pop one excess entry (FreeListStack.pop, concurrent_hash.py:75-79) from the
+// striped free list, aggregated over the lanes that reach the call together.
+// Returns -1 only when every stripe is empty (CapacityExhausted).
+__device__ __forceinline__ int64_t pop_free(const TableView& T) {
+  uint32_t s = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % T.stripes;
+#pragma unroll 1
+  for (uint32_t k = 0; k < T.stripes; ++k) {
+    const uint32_t m = __activemask();
+    const int leader = __ffs(m) - 1;
+    const int cnt = __popc(m);
+    const int rank = __popc(m & lanemask_lt());
+    long long* top = T.tops + (size_t)s * kTopStride;
+    long long old = 0;
+    if ((int)lane_id() == leader) old = (long long)atomicAdd((unsigned long long*)top, (unsigned long long)(-(long long)cnt));
+    old = __shfl_sync(m, old, leader);
+    const long long t = old - 1 - rank;
+    if (t >= 0) return (int64_t)T.free_stack[(size_t)s * T.stripe_cap + (size_t)t];
+    // this stripe ran dry for this lane: give the ticket back, try the next
+    atomicAdd((unsigned long long*)top, 1ull);
+    s = (s + 1 == T.stripes) ? 0 : s + 1;
+  }
+  return -1;
+}
+
+// Push one vacated excess position onto the striped free list (used only by
+// recycle launches, never concurrently with pops).  Warp-aggregated
+// reservations; a full stripe hands the lanes on to the next stripe.
+__device__ __forceinline__ void push_free(const TableView& T, uint32_t e) {
+  uint32_t s = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % T.stripes;
+#pragma unroll 1
+  for (;;) {
+    const uint32_t m = __activemask();
+    const int leader = __ffs(m) - 1;
+    const int cnt = __popc(m);
+    const int rank = __popc(m & lanemask_lt());
+    long long* top = T.tops + (size_t)s * kTopStride;
+    long long old = 0;
+    if ((int)lane_id() == leader) old = (long long)atomicAdd((unsigned long long*)top, (unsigned long long)cnt);
+    old = __shfl_sync(m, old, leader);
+    const long long slot = old + rank;
+    if (slot < (long long)T.stripe_cap) {
+      T.free_stack[(size_t)s * T.stripe_cap + (size_t)slot] = e;
+      return;
+    }
+    atomicAdd((unsigned long long*)top, (unsigned long long)(-1ll));  // undo the overshoot
+    s = (s + 1 == T.stripes) ? 0 : s + 1;
+  }
+}
+
 // Lock-free retrieval (_find + _scan_chain, concurrent_hash.py:127-157).
 // Returns the position or -1; *meta_out = meta of the matching entry.
-__device__ __forceinline__ int32_t find_pos(const TableView& T, int32_t x, int32_t y, int32_t z,
-                                            uint32_t b, uint32_t* meta_out) {
+__device__ __forceinline__ int32_t find_pos(const TableView& T, int32_t x, int32_t y, int32_t z, uint32_t b,
+                                           uint32_t* meta_out) {
   uint32_t e = b;
 #pragma unroll 1
   for (;;) {
@@ -77,43 +114,44 @@ __device__ __forceinline__ int32_t find_pos(const TableView& T, int32_t x, int32
   }
 }
 
-// A duplicate insert of a key created earlier in this launch: compete for
-// the "created" flag by lowest op index (resolved by k_fixup_created).
-__device__ __forceinline__ void note_duplicate(const TableView& T, int32_t pos, uint32_t meta, int32_t op) {
-  if (meta & kFresh) atomicMin(&T.first_op[pos], op);
+// Compete for the "created" flag of an entry created in this launch: lowest
+// op index wins (resolved by the fixup launch).
+__device__ __forceinline__ void claim_min(const TableView& T, int32_t pos, int32_t op) {
+  atomicMin(&T.claim[pos], T.tag | (unsigned long long)(uint32_t)op);
 }
 
 struct InsertResult {
-  int32_t pos;   // -1 on capacity failure
+  int32_t pos;  // -1 on capacity failure
   uint8_t created;
 };
 
 // _insert_pos (concurrent_hash.py:159-208): loop of non-blocking attempts;
 // each retry starts with a fresh lock-free retrieval.
-__device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x, int32_t y, int32_t z,
-                                                   int32_t op) {
+__device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x, int32_t y, int32_t z, int32_t op) {
   const uint32_t b = bucket_of(T, x, y, z);
   uint32_t* bmeta = &T.e[b].meta;
 #pragma unroll 1
   for (int attempt = 0;; ++attempt) {
     uint32_t fmeta;
-    int32_t pos = find_pos(T, x, y, z, b, &fmeta);
+    const int32_t pos = find_pos(T, x, y, z, b, &fmeta);
     if (pos >= 0) {
-      note_duplicate(T, pos, fmeta, op);
+      if (fmeta & kFresh) claim_min(T, pos, op);
       return {pos, 0};
     }
-    const uint32_t old = atom_or_acquire(bmeta, kLock);
+    const uint32_t old = atom_or_relaxed(bmeta, kLock);
     if (old & kLock) {
       if (attempt > 4) __nanosleep(64);
       continue;
     }
-    // --- chain lock held: re-validate (concurrent_hash.py:180-184)
+    // --- chain lock held.  The re-scan's first load depends on `old`, so it
+    // is issued only after the lock word came back (acquire by dependency).
+    const uint32_t dep = (old >> 31) & 1u;  // always 0 here
     uint32_t tail = b, tail_meta = old;
     {
-      const int4 s = ld_entry(T.e + b);
+      const int4 s = ld_entry(T.e + b + dep);
       if ((old & kOcc) && key_eq(s, x, y, z)) {
-        atom_and_release(bmeta, ~kLock);
-        note_duplicate(T, (int32_t)b, old, op);
+        atom_exch_relaxed(bmeta, old);  // unlock; nothing was modified
+        if (old & kFresh) claim_min(T, (int32_t)b, op);
         return {(int32_t)b, 0};
       }
       uint32_t meta = old;
@@ -122,8 +160,8 @@ __device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x
         const int4 t = ld_entry(T.e + e);
         meta = (uint32_t)t.w;
         if ((meta & kOcc) && key_eq(t, x, y, z)) {
-          atom_and_release(bmeta, ~kLock);
-          note_duplicate(T, (int32_t)e, meta, op);
+          atom_exch_relaxed(bmeta, old);
+          if (meta & kFresh) claim_min(T, (int32_t)e, op);
           return {(int32_t)e, 0};
         }
         tail = e;
@@ -131,33 +169,34 @@ __device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x
       }
     }
     if (!(old & kOcc)) {
-      // claim the free bucket entry; its NEXT link is kept (:185-192)
-      T.first_op[b] = op;
-      st_entry(T.e + b, x, y, z, old | kLock);  // meta unchanged (still locked)
-      atom_exch_release(bmeta, (old & ~kLock) | kOcc | kFresh);
+      // claim the free bucket entry: key, OCC and unlock in ONE 16-byte
+      // store; its NEXT link is kept (:185-192)
+      claim_min(T, (int32_t)b, op);
+      st_entry(T.e + b, x, y, z, (old & kNext) | kOcc | kFresh);
       return {(int32_t)b, 1};
     }
     const int64_t ne = pop_free(T);
     if (ne < 0) {
-      atom_and_release(bmeta, ~kLock);
+      atom_exch_relaxed(bmeta, old);
       atomicOr(&T.ctl->error, 1u);
       return {-1, 0};
     }
     const uint32_t e = (uint32_t)ne;
-    T.first_op[e] = op;
-    st_entry(T.e + e, x, y, z, kOcc | kFresh);  // NEXT = 0: clears the stale offset (:200)
+    claim_min(T, (int32_t)e, op);
+    st_entry(T.e + e, x, y, z, kOcc | kFresh);  // NEXT = 0 clears the stale offset (:200)
     const uint32_t link = e - T.n + 1u;
     if (tail == b) {
-      atom_exch_release(bmeta, (old & ~(kLock | kNext)) | link);  // publish + unlock
+      atom_exch_release(bmeta, (old & ~kNext) | link);  // publish + unlock
     } else {
       st_release_u32(&T.e[tail].meta, (tail_meta & ~kNext) | link);  // publish last (:204)
-      atom_and_release(bmeta, ~kLock);
+      atom_exch_release(bmeta, old);                                   // unlock after the link
     }
     return {(int32_t)e, 1};
   }
 }
 
 // remove (concurrent_hash.py:251-295).  Returns the vacated position or -1.
+// Vacated EXCESS positions are recycled by the caller's recycle launch.
 __device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int32_t y, int32_t z) {
   const uint32_t b = bucket_of(T, x, y, z);
   uint32_t* bmeta = &T.e[b].meta;
@@ -165,15 +204,16 @@ __device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int3
   for (int attempt = 0;; ++attempt) {
     uint32_t fmeta;
     if (find_pos(T, x, y, z, b, &fmeta) < 0) return -1;
-    const uint32_t old = atom_or_acquire(bmeta, kLock);
+    const uint32_t old = atom_or_relaxed(bmeta, kLock);
     if (old & kLock) {
       if (attempt > 4) __nanosleep(64);
       continue;
     }
-    const int4 s = ld_entry(T.e + b);
+    const uint32_t dep = (old >> 31) & 1u;
+    const int4 s = ld_entry(T.e + b + dep);
     if ((old & kOcc) && key_eq(s, x, y, z)) {
       // bucket case: clear occupancy only; NEXT and the chain stay (:266-275)
-      atom_exch_release(bmeta, old & ~(kLock | kOcc | kFresh));
+      atom_exch_relaxed(bmeta, old & ~(kOcc | kFresh));
       return (int32_t)b;
     }
     uint32_t prev = b, prev_meta = old, meta = old;
@@ -183,35 +223,39 @@ __device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int3
       meta = (uint32_t)t.w;
       if ((meta & kOcc) && key_eq(t, x, y, z)) {
         // excess case: clear the victim but keep its stale NEXT (:280-289)
-        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(&T.e[e].meta),
-                     "r"(meta & ~(kOcc | kFresh))
-                     : "memory");
+        st_relaxed_u32(&T.e[e].meta, meta & ~(kOcc | kFresh));
         const uint32_t vnext = meta & kNext;
         if (prev == b) {
-          atom_exch_release(bmeta, (old & ~(kLock | kNext)) | vnext);
+          atom_exch_relaxed(bmeta, (old & ~kNext) | vnext);  // relink + unlock, one word
         } else {
-          st_release_u32(&T.e[prev].meta, (prev_meta & ~kNext) | vnext);
-          atom_and_release(bmeta, ~kLock);
+          st_relaxed_u32(&T.e[prev].meta, (prev_meta & ~kNext) | vnext);
+          atom_exch_release(bmeta, old);  // unlock only after the relink
         }
-        retire(T, e);
         return (int32_t)e;
       }
       prev = e;
       prev_meta = meta;
     }
     // key vanished between the find and the lock; re-check (:293)
-    atom_and_release(bmeta, ~kLock);
+    atom_exch_relaxed(bmeta, old);
   }
 }
 
-// Warp-aggregated update of the live-key counter.  Every lane of the warp
-// must call it (kernels keep out-of-range lanes alive with delta 0).
-__device__ __forceinline__ void add_size(const TableView& T, int delta) {
-  __syncwarp();
+// CTA-aggregated update of the live-key counter: one atomic per CTA.  Every
+// thread of the CTA must call it exactly once (out-of-range threads with 0).
+__device__ __forceinline__ void add_size_cta(const TableView& T, int delta) {
+  __shared__ int red[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o);
-  if (lane_id() == 0 && delta != 0)
-    atomicAdd(&T.ctl->size, (unsigned long long)(long long)delta);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane_id() == 0) red[w] = delta;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    if (s) atomicAdd(&T.ctl->size, (unsigned long long)(long long)s);
+  }
 }
 
 }  // namespace vsb

@@ -110,16 +110,18 @@ __device__ __forceinline__ void halo_item(int i, int& c, int& flat, int& row, in
   }
 }
 
+constexpr int kLook = kMcThreads / 8;  // blocks per batched neighbour lookup (16)
+
 struct McSmem {
   alignas(128) uint8_t buf[2][VS_TSDF_BLOCK_BYTES];
   alignas(8) uint64_t mbar[2];
   uint32_t grid_in[2][81];
   uint32_t grid_ob[2][81];
-  int32_t nb[2][8];
+  int32_t nb[2][kLook][8];  // neighbour rows of two lookup batches
   uint32_t cnt[2][4];
 };
 
-// Neighbour rows of block `blk` for corner-block c (threads 0..7).
+// Neighbour row of block `blk` for corner-block c.
 template <bool kFromKeys>
 __device__ __forceinline__ int32_t load_nbr(const TableView& T, const int32_t* __restrict__ keys,
                                             const int32_t* __restrict__ nbr, uint64_t blk, int c) {
@@ -132,6 +134,18 @@ __device__ __forceinline__ int32_t load_nbr(const TableView& T, const int32_t* _
   } else {
     return __ldg(&nbr[8 * blk + c]);
   }
+}
+
+// All 128 threads resolve the 8 neighbour rows of the CTA's next kLook
+// blocks at once (iterations j0 .. j0+15): one chain-walk latency per 16
+// blocks instead of one per block.
+template <bool kFromKeys>
+__device__ __forceinline__ void lookup_batch(McSmem& sm, int buf, const TableView& T, const int32_t* keys,
+                                             const int32_t* nbr, uint64_t n, uint64_t j0) {
+  const int t = threadIdx.x;
+  const int slot = t >> 3, c = t & 7;
+  const uint64_t blk = blockIdx.x + (j0 + slot) * (uint64_t)gridDim.x;
+  sm.nb[buf][slot][c] = blk < n ? load_nbr<kFromKeys>(T, keys, nbr, blk, c) : -1;
 }
 
 template <bool kFromKeys>
@@ -151,29 +165,36 @@ __global__ void __launch_bounds__(kMcThreads) k_mc_encode(TableView T, const uin
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   uint64_t blk = blockIdx.x;
-  if (t < 8 && blk < n) sm.nb[0][t] = load_nbr<kFromKeys>(T, keys, nbr, blk, t);
+  lookup_batch<kFromKeys>(sm, 0, T, keys, nbr, n, 0);
   __syncthreads();
-  if (t == 0 && blk < n && sm.nb[0][0] >= 0) {
+  if (t == 0 && blk < n && sm.nb[0][0][0] >= 0) {
     mbar_arrive_expect_tx(&sm.mbar[0], VS_TSDF_BLOCK_BYTES);
-    tma_load_1d(sm.buf[0], pool + (uint64_t)sm.nb[0][0] * VS_TSDF_BLOCK_BYTES, VS_TSDF_BLOCK_BYTES, &sm.mbar[0]);
+    tma_load_1d(sm.buf[0], pool + (uint64_t)sm.nb[0][0][0] * VS_TSDF_BLOCK_BYTES, VS_TSDF_BLOCK_BYTES,
+                &sm.mbar[0]);
   }
   uint32_t phases = 0u;  // bit s = parity of mbar[s]
 
-  for (int it = 0; blk < n; ++it, blk += G) {
-    const int s = it & 1;
+  for (uint64_t j = 0; blk < n; ++j, blk += G) {
+    const int s = (int)(j & 1);
+    const int slot = (int)(j % kLook);
+    const int bb = (int)((j / kLook) & 1);
     const uint64_t next = blk + G;
-    if (t < 8 && next < n) sm.nb[s ^ 1][t] = load_nbr<kFromKeys>(T, keys, nbr, next, t);
-    const int32_t centre = sm.nb[s][0];  // stable since (A) of the previous iteration
+    const int32_t* nbc = sm.nb[bb][slot];
+    const int32_t centre = nbc[0];
+    if (slot == kLook - 1 && next < n) lookup_batch<kFromKeys>(sm, bb ^ 1, T, keys, nbr, n, j + 1);
     for (int r = t; r < 81; r += kMcThreads) {
       sm.grid_in[s][r] = 0u;
       sm.grid_ob[s][r] = 0u;
     }
-    __syncthreads();  // (A) nb[s^1] ready, grids zeroed, buf[s^1] no longer read
-    if (t == 0 && next < n && sm.nb[s ^ 1][0] >= 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_expect_tx(&sm.mbar[s ^ 1], VS_TSDF_BLOCK_BYTES);
-      tma_load_1d(sm.buf[s ^ 1], pool + (uint64_t)sm.nb[s ^ 1][0] * VS_TSDF_BLOCK_BYTES, VS_TSDF_BLOCK_BYTES,
-                  &sm.mbar[s ^ 1]);
+    __syncthreads();  // (A) next lookups ready, grids zeroed, buf[s^1] no longer read
+    if (t == 0 && next < n) {
+      const int32_t nrow = (slot == kLook - 1) ? sm.nb[bb ^ 1][0][0] : sm.nb[bb][slot + 1][0];
+      if (nrow >= 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&sm.mbar[s ^ 1], VS_TSDF_BLOCK_BYTES);
+        tma_load_1d(sm.buf[s ^ 1], pool + (uint64_t)nrow * VS_TSDF_BLOCK_BYTES, VS_TSDF_BLOCK_BYTES,
+                    &sm.mbar[s ^ 1]);
+      }
     }
     uint32_t* mc_blk = mc_out ? mc_out + blk * VS_BLOCK_VOXELS : nullptr;
     int8_t* q_blk = q_out ? q_out + blk * VS_BLOCK_VOXELS : nullptr;
@@ -181,8 +202,8 @@ __global__ void __launch_bounds__(kMcThreads) k_mc_encode(TableView T, const uin
     if (centre < 0) {
       // absent centre: every cube's origin lives here -> all zero (:152-156)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int v = j * kMcThreads + t;
+      for (int k = 0; k < 4; ++k) {
+        const int v = k * kMcThreads + t;
         if (mc_blk) __stcs(mc_blk + v, 0u);
         if (q_blk) __stcs((char*)q_blk + v, (char)-128);
       }
@@ -197,7 +218,7 @@ __global__ void __launch_bounds__(kMcThreads) k_mc_encode(TableView T, const uin
       if (i < 217) {
         int c, flat, row, bit;
         halo_item(i, c, flat, row, bit);
-        const int32_t nrow = sm.nb[s][c];
+        const int32_t nrow = nbc[c];
         if (nrow >= 0) {
           const uint32_t* src = (const uint32_t*)(pool + (uint64_t)nrow * VS_TSDF_BLOCK_BYTES + 12u * flat);
           const uint32_t tb = __ldg(src), wb = __ldg(src + 1);
@@ -213,15 +234,15 @@ __global__ void __launch_bounds__(kMcThreads) k_mc_encode(TableView T, const uin
     const uint32_t* b32 = (const uint32_t*)sm.buf[s];
     uint32_t tb[4], wb[4], rgb[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int v = j * kMcThreads + t;
-      tb[j] = b32[3 * v];
-      wb[j] = b32[3 * v + 1];
-      rgb[j] = b32[3 * v + 2] & 0x00FFFFFFu;
-      const uint32_t bin = __ballot_sync(0xffffffffu, inside_bit(tb[j]));
-      const uint32_t bob = __ballot_sync(0xffffffffu, observed_bit(wb[j]));
+    for (int k = 0; k < 4; ++k) {
+      const int v = k * kMcThreads + t;
+      tb[k] = b32[3 * v];
+      wb[k] = b32[3 * v + 1];
+      rgb[k] = b32[3 * v + 2] & 0x00FFFFFFu;
+      const uint32_t bin = __ballot_sync(0xffffffffu, inside_bit(tb[k]));
+      const uint32_t bob = __ballot_sync(0xffffffffu, observed_bit(wb[k]));
       if (lane < 4) {
-        const int r = ((j * kMcThreads + warp * 32) >> 3) + lane;  // row = y + 8z
+        const int r = ((k * kMcThreads + warp * 32) >> 3) + lane;  // row = y + 8z
         const int gy = r & 7, gz = r >> 3;
         atomicOr(&sm.grid_in[s][gz * 9 + gy], (bin >> (8 * lane)) & 0xFFu);
         atomicOr(&sm.grid_ob[s][gz * 9 + gy], (bob >> (8 * lane)) & 0xFFu);
@@ -232,8 +253,8 @@ __global__ void __launch_bounds__(kMcThreads) k_mc_encode(TableView T, const uin
     // ---- cube indices, cutoff, colour, quantised TSDF
     uint32_t nz = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int v = j * kMcThreads + t;
+    for (int k = 0; k < 4; ++k) {
+      const int v = k * kMcThreads + t;
       const int x = v & 7, y = (v >> 3) & 7, z = v >> 6;
       const int r00 = z * 9 + y, r10 = r00 + 1, r01 = r00 + 9, r11 = r00 + 10;
       const uint32_t* gi = sm.grid_in[s];
@@ -243,9 +264,9 @@ __global__ void __launch_bounds__(kMcThreads) k_mc_encode(TableView T, const uin
       const uint32_t ob = ((go[r00] >> x) & 3u) | (((go[r10] >> x) & 3u) << 2) | (((go[r01] >> x) & 3u) << 4) |
                           (((go[r11] >> x) & 3u) << 6);
       if (ob != 255u || idx == 255u) idx = 0u;  // unobserved corner -> 0; cutoff 255 -> 0
-      const uint32_t word = idx ? (idx | (rgb[j] << 8)) : 0u;
+      const uint32_t word = idx ? (idx | (rgb[k] << 8)) : 0u;
       if (mc_blk) __stcs(mc_blk + v, word);
-      if (q_blk) __stcs((char*)q_blk + v, (char)quantise(tb[j], wb[j]));
+      if (q_blk) __stcs((char*)q_blk + v, (char)quantise(tb[k], wb[k]));
       nz += __popc(__ballot_sync(0xffffffffu, idx != 0u));
     }
     if (counts) {

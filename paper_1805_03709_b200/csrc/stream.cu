@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(256) k_multi_insert(const __grid_constant__ Se
     index[(uint64_t)c * n + i] = r.pos;
     delta = r.created;
   }
-  add_size(T, delta);
+  add_size_cta(T, delta);
 }
 
 __global__ void k_multi_fixup(const __grid_constant__ SetViews V, const int32_t* __restrict__ keys, uint64_t n,
@@ -61,7 +61,7 @@ __global__ void k_multi_fixup(const __grid_constant__ SetViews V, const int32_t*
   const TableView& T = V.v[c];
   const int32_t pos = index[(uint64_t)c * n + i];
   atomicAnd(&T.e[pos].meta, ~kFresh);
-  const int32_t m = T.first_op[pos];
+  const int32_t m = (int32_t)(uint32_t)(T.claim[pos] & 0xFFFFFFFFull);
   if (m >= 0 && (uint64_t)m < i && keys[3 * (uint64_t)m] == keys[3 * i] &&
       keys[3 * (uint64_t)m + 1] == keys[3 * i + 1] && keys[3 * (uint64_t)m + 2] == keys[3 * i + 2]) {
     cr[i] = 0;
@@ -96,7 +96,7 @@ __global__ void k_fifo_tail(const uint64_t* __restrict__ off, uint64_t n, int C,
 
 __global__ void __launch_bounds__(256) k_multi_erase(const __grid_constant__ SetViews V,
                                                      const int32_t* __restrict__ keys, uint64_t n,
-                                                     uint8_t* __restrict__ erased) {
+                                                     uint8_t* __restrict__ erased, int32_t* __restrict__ vacated) {
   const int c = blockIdx.y;
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const TableView& T = V.v[c];
@@ -104,26 +104,19 @@ __global__ void __launch_bounds__(256) k_multi_erase(const __grid_constant__ Set
   if (i < n) {
     const int32_t pos = erase_key(T, keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]);
     if (erased) erased[(uint64_t)c * n + i] = pos >= 0;
+    vacated[(uint64_t)c * n + i] = pos;
     delta = -(pos >= 0);
   }
-  add_size(T, delta);
+  add_size_cta(T, delta);
 }
 
-__global__ void k_multi_flush(const __grid_constant__ SetViews V) {
-  const TableView& T = V.v[blockIdx.y];
-  const unsigned long long r = T.ctl->retired_n;
-  const long long top = T.ctl->free_top;
-  for (unsigned long long j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < r;
-       j += (uint64_t)gridDim.x * blockDim.x)
-    T.free_stack[top + (long long)j] = T.retired[j];
-}
-
-__global__ void k_multi_flush_final(const __grid_constant__ SetViews V, int C) {
-  const int c = threadIdx.x;
-  if (c >= C) return;
-  Ctl* ctl = V.v[c].ctl;
-  ctl->free_top += (long long)ctl->retired_n;
-  ctl->retired_n = 0;
+__global__ void k_multi_recycle(const __grid_constant__ SetViews V, const int32_t* __restrict__ vacated, uint64_t n) {
+  const int c = blockIdx.y;
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const TableView& T = V.v[c];
+  const int32_t e = vacated[(uint64_t)c * n + i];
+  if (e >= (int32_t)T.n) push_free(T, (uint32_t)e);
 }
 
 // affected_mc_blocks order: itertools.product((0, -1), repeat=3) -> dx slowest
@@ -187,15 +180,8 @@ static vs_status fill_views(vs_table* const* sets, int n_sets, SetViews& V) {
       set_error("set handle is NULL");
       return VS_ERR_INVALID;
     }
-    V.v[c] = sets[c]->view();
+    V.v[c] = sets[c]->next_view();
   }
-  return VS_OK;
-}
-
-static vs_status flush_multi(const SetViews& V, int C, cudaStream_t s) {
-  { k_multi_flush<<<dim3(64, C), 256, 0, s>>>(V); vsb::count_launch(); }
-  { k_multi_flush_final<<<1, 32, 0, s>>>(V, C); vsb::count_launch(); }
-  VS_CK_LAUNCH("flush_multi");
   return VS_OK;
 }
 
@@ -317,9 +303,14 @@ vs_status vs_stream_remove_many(vs_table* const* sets_host, int n_sets, const in
   }
   DeviceGuard g(sets_host[0]->device);
   cudaStream_t s = (cudaStream_t)stream;
-  { k_multi_erase<<<dim3(grid_for(n, 256), n_sets), 256, 0, s>>>(V, keys, n, erased); vsb::count_launch(); }
-  VS_CK_LAUNCH("k_multi_erase");
-  return flush_multi(V, n_sets, s);
+  int32_t* vacated = nullptr;
+  VS_CK(cudaMallocAsync((void**)&vacated, sizeof(int32_t) * n * (uint64_t)n_sets, s));
+  const dim3 grid(grid_for(n, 256), n_sets);
+  { k_multi_erase<<<grid, 256, 0, s>>>(V, keys, n, erased, vacated); vsb::count_launch(); }
+  { k_multi_recycle<<<grid, 256, 0, s>>>(V, vacated, n); vsb::count_launch(); }
+  cudaFreeAsync(vacated, s);
+  VS_CK_LAUNCH("vs_stream_remove_many");
+  return VS_OK;
 }
 
 vs_status vs_stream_extract_ordered(vs_table* set, const int32_t* fifo_keys, uint64_t fifo_cap, uint64_t* head_host,

@@ -10,31 +10,40 @@
 struct vs_table {
   int device = 0;
   uint32_t n = 0, excess = 0, cap = 0;
+  uint32_t stripes = 1, stripe_cap = 1;
   vsb::Entry* e = nullptr;
   uint32_t* free_stack = nullptr;
-  uint32_t* retired = nullptr;
-  int32_t* first_op = nullptr;
+  long long* tops = nullptr;
+  unsigned long long* claim = nullptr;
   vsb::Ctl* ctl = nullptr;
   uint64_t magic = 0;
+  uint32_t epoch = 0;  // launch epoch for the claim tags
   // ordered-compaction workspace (snapshot / extract)
   uint32_t nchunks = 0;
   uint32_t* chunk_counts = nullptr;
   uint64_t* chunk_offsets = nullptr;  // nchunks + 1
   int32_t* pos_work = nullptr;        // lazily allocated, cap entries
-  unsigned long long* claim = nullptr;  // lazily allocated, duplicate-erase claims
-  uint32_t erase_epoch = 0;
 
+  // view for ONE launch; next_epoch() gives it a fresh claim tag
   vsb::TableView view() const {
     vsb::TableView v;
     v.e = e;
     v.free_stack = free_stack;
-    v.retired = retired;
-    v.first_op = first_op;
+    v.tops = tops;
+    v.claim = claim;
     v.ctl = ctl;
     v.n = n;
     v.excess = excess;
+    v.stripes = stripes;
+    v.stripe_cap = stripe_cap;
     v.magic = magic;
+    v.tag = (unsigned long long)(0xFFFFFFFFu - epoch) << 32;
     return v;
+  }
+  vsb::TableView next_view() {
+    ++epoch;
+    if (epoch == 0xFFFFFFFFu) epoch = 1;  // tags stay ordered for 4G launches; then reset below
+    return view();
   }
 };
 
@@ -75,7 +84,10 @@ struct ProfScope {
 };
 
 // internal entry points shared across translation units
-vs_status flush_retired(vs_table* t, cudaStream_t s);
+// Push vacated excess positions (pos[i] >= n where flag[i] and, if ops is
+// given, ops[i] == VS_OP_ERASE) back onto the striped free list.
+void launch_recycle(const vsb::TableView& v, const int32_t* pos, const uint8_t* flag, const uint8_t* ops,
+                    const uint64_t* n_dev, uint64_t n, cudaStream_t s);
 vs_status erase_device_count(vs_table* t, const int32_t* keys, const uint64_t* n_dev, uint64_t max_n,
                              cudaStream_t s);
 
