@@ -11,7 +11,10 @@ import ctypes
 import pathlib
 import threading
 
-LIB_PATH = pathlib.Path(__file__).resolve().with_name("libvsb200.so")
+import os
+
+# VSB_LIB lets experiments load an alternative build of the same ABI
+LIB_PATH = pathlib.Path(os.environ.get("VSB_LIB") or pathlib.Path(__file__).resolve().with_name("libvsb200.so"))
 HEADER_PATH = pathlib.Path(__file__).resolve().parent.parent / "include" / "vsb200.h"
 
 VS_OK = 0

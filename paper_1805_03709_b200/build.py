@@ -45,34 +45,39 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None = None,
+          defines: tuple = ()) -> pathlib.Path:
+    """Compile to `out` (default: the in-tree libvsb200.so).  `defines` are
+    extra -D flags for experiment variants (e.g. ("VSB_MC_STAGES=3",))."""
+    lib = LIB if out is None else pathlib.Path(out)
+    if out is None and not defines and not force and up_to_date():
         return LIB
-    BUILD.mkdir(parents=True, exist_ok=True)
+    build_dir = BUILD if not defines else BUILD / ("v_" + "_".join(d.replace("=", "") for d in defines))
+    build_dir.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
 
     def compile_one(src: str) -> tuple[str, str]:
-        obj = BUILD / (src.rsplit(".", 1)[0] + ".o")
-        cmd = [cc, *ARCH, *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        obj = build_dir / (src.rsplit(".", 1)[0] + ".o")
+        cmd = [cc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
-        (BUILD / (src + ".ptxas.txt")).write_text(r.stderr)
+        (build_dir / (src + ".ptxas.txt")).write_text(r.stderr)
         return str(obj), r.stderr
 
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         results = list(ex.map(compile_one, SOURCES))
     objs = [o for o, _ in results]
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     if verbose:
         for _, log in results:
             sys.stdout.write(log)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -54,7 +54,9 @@ __device__ __forceinline__ int64_t pop_free(const TableView& T) {
   uint32_t s = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % T.stripes;
 #pragma unroll 1
   for (uint32_t k = 0; k < T.stripes; ++k) {
-    const uint32_t m = __activemask();
+    // lanes that reconverge here may be on different stripes (they entered
+    // at different times): aggregate per stripe
+    const uint32_t m = __match_any_sync(__activemask(), s);
     const int leader = __ffs(m) - 1;
     const int cnt = __popc(m);
     const int rank = __popc(m & lanemask_lt());
@@ -78,7 +80,7 @@ __device__ __forceinline__ void push_free(const TableView& T, uint32_t e) {
   uint32_t s = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % T.stripes;
 #pragma unroll 1
   for (;;) {
-    const uint32_t m = __activemask();
+    const uint32_t m = __match_any_sync(__activemask(), s);
     const int leader = __ffs(m) - 1;
     const int cnt = __popc(m);
     const int rank = __popc(m & lanemask_lt());

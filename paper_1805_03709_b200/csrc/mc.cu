@@ -111,10 +111,23 @@ __device__ __forceinline__ void halo_item(int i, int& c, int& flat, int& row, in
 }
 
 constexpr int kLook = kMcThreads / 8;  // blocks per batched neighbour lookup (16)
+#ifndef VSB_MC_STAGES
+#define VSB_MC_STAGES 2
+#endif
+// Resident CTAs per SM the register allocation must allow (measured best:
+// 10 with in-kernel hash lookups, 8 with a neighbour table; see profiles/).
+#ifndef VSB_MC_MINBLOCKS_KEYS
+#define VSB_MC_MINBLOCKS_KEYS 10
+#endif
+#ifndef VSB_MC_MINBLOCKS_NBR
+#define VSB_MC_MINBLOCKS_NBR 8
+#endif
+constexpr int kStages = VSB_MC_STAGES;  // TMA ring depth (centre blocks in flight + 1)
+constexpr int kAhead = kStages - 1;    // prefetch distance of the centre copy
 
 struct McSmem {
-  alignas(128) uint8_t buf[2][VS_TSDF_BLOCK_BYTES];
-  alignas(8) uint64_t mbar[2];
+  alignas(128) uint8_t buf[kStages][VS_TSDF_BLOCK_BYTES];
+  alignas(8) uint64_t mbar[kStages];
   uint32_t grid_in[2][81];
   uint32_t grid_ob[2][81];
   int32_t nb[2][kLook][8];  // neighbour rows of two lookup batches
@@ -148,8 +161,50 @@ __device__ __forceinline__ void lookup_batch(McSmem& sm, int buf, const TableVie
   sm.nb[buf][slot][c] = blk < n ? load_nbr<kFromKeys>(T, keys, nbr, blk, c) : -1;
 }
 
+// Per-thread halo items (thread t owns items t and t + 128 of 217).
+struct HaloRegs {
+  uint32_t tb[2], wb[2];
+  int row[2];  // grid row, or -1 when the item is absent
+  int bit[2];
+};
+
+__device__ __forceinline__ void halo_prefetch(HaloRegs& h, const int32_t* nbc, const uint8_t* __restrict__ pool) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = threadIdx.x + k * kMcThreads;
+    h.row[k] = -1;
+    if (i < 217) {
+      int c, flat, row, bit;
+      halo_item(i, c, flat, row, bit);
+      const int32_t nrow = nbc[c];
+      if (nrow >= 0) {
+        // voxel records are 12 B: (tsdf, weight) is only 4-byte aligned
+        const uint32_t* src = (const uint32_t*)(pool + (uint64_t)nrow * VS_TSDF_BLOCK_BYTES + 12u * flat);
+        h.tb[k] = __ldg(src);
+        h.wb[k] = __ldg(src + 1);
+        h.row[k] = row;
+        h.bit[k] = bit;
+      }
+    }
+  }
+}
+
+// Neighbour rows of the CTA's j-th block (j counts this CTA's blocks).
+__device__ __forceinline__ const int32_t* nb_of(const McSmem& sm, uint64_t j) {
+  return sm.nb[(j / kLook) & 1][j % kLook];
+}
+
+__device__ __forceinline__ void issue_centre(McSmem& sm, uint64_t j, const uint8_t* __restrict__ pool) {
+  const int32_t row = nb_of(sm, j)[0];
+  if (row < 0) return;
+  const int b = (int)(j % kStages);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_arrive_expect_tx(&sm.mbar[b], VS_TSDF_BLOCK_BYTES);
+  tma_load_1d(sm.buf[b], pool + (uint64_t)row * VS_TSDF_BLOCK_BYTES, VS_TSDF_BLOCK_BYTES, &sm.mbar[b]);
+}
+
 template <bool kFromKeys>
-__global__ void __launch_bounds__(kMcThreads) k_mc_encode(TableView T, const uint8_t* __restrict__ pool,
+__global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS : VSB_MC_MINBLOCKS_NBR) k_mc_encode(TableView T, const uint8_t* __restrict__ pool,
                                                           const int32_t* __restrict__ keys,
                                                           const int32_t* __restrict__ nbr, uint64_t n,
                                                           uint32_t* __restrict__ mc_out, int8_t* __restrict__ q_out,
@@ -158,118 +213,110 @@ __global__ void __launch_bounds__(kMcThreads) k_mc_encode(TableView T, const uin
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const uint64_t G = gridDim.x;
+  // blocks of this CTA: blockIdx.x + j*G for j < nj
+  const uint64_t nj = blockIdx.x < n ? (n - 1 - blockIdx.x) / G + 1 : 0;
 
   if (t == 0) {
-    mbar_init(&sm.mbar[0], 1);
-    mbar_init(&sm.mbar[1], 1);
+    for (int b = 0; b < kStages; ++b) mbar_init(&sm.mbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  uint64_t blk = blockIdx.x;
   lookup_batch<kFromKeys>(sm, 0, T, keys, nbr, n, 0);
   __syncthreads();
-  if (t == 0 && blk < n && sm.nb[0][0][0] >= 0) {
-    mbar_arrive_expect_tx(&sm.mbar[0], VS_TSDF_BLOCK_BYTES);
-    tma_load_1d(sm.buf[0], pool + (uint64_t)sm.nb[0][0][0] * VS_TSDF_BLOCK_BYTES, VS_TSDF_BLOCK_BYTES,
-                &sm.mbar[0]);
-  }
-  uint32_t phases = 0u;  // bit s = parity of mbar[s]
+  if (t == 0)
+    for (uint64_t j = 0; j < kAhead && j < nj; ++j) issue_centre(sm, j, pool);
+  uint32_t phases = 0u;  // bit b = parity of mbar[b]
+  // halo of the block processed next, loaded one iteration ahead
+  HaloRegs hal;
+  if (nj) halo_prefetch(hal, nb_of(sm, 0), pool);
 
-  for (uint64_t j = 0; blk < n; ++j, blk += G) {
+  for (uint64_t j = 0; j < nj; ++j) {
+    const uint64_t blk = blockIdx.x + j * G;
     const int s = (int)(j & 1);
+    const int b = (int)(j % kStages);
     const int slot = (int)(j % kLook);
-    const int bb = (int)((j / kLook) & 1);
-    const uint64_t next = blk + G;
-    const int32_t* nbc = sm.nb[bb][slot];
+    const int32_t* nbc = nb_of(sm, j);
     const int32_t centre = nbc[0];
-    if (slot == kLook - 1 && next < n) lookup_batch<kFromKeys>(sm, bb ^ 1, T, keys, nbr, n, j + 1);
+    // the next lookup batch must be ready before block j + kAhead is issued
+    if (slot == kLook - kAhead && j + kAhead < nj)
+      lookup_batch<kFromKeys>(sm, (int)(((j / kLook) + 1) & 1), T, keys, nbr, n, (j / kLook + 1) * kLook);
     for (int r = t; r < 81; r += kMcThreads) {
       sm.grid_in[s][r] = 0u;
       sm.grid_ob[s][r] = 0u;
     }
-    __syncthreads();  // (A) next lookups ready, grids zeroed, buf[s^1] no longer read
-    if (t == 0 && next < n) {
-      const int32_t nrow = (slot == kLook - 1) ? sm.nb[bb ^ 1][0][0] : sm.nb[bb][slot + 1][0];
-      if (nrow >= 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect_tx(&sm.mbar[s ^ 1], VS_TSDF_BLOCK_BYTES);
-        tma_load_1d(sm.buf[s ^ 1], pool + (uint64_t)nrow * VS_TSDF_BLOCK_BYTES, VS_TSDF_BLOCK_BYTES,
-                    &sm.mbar[s ^ 1]);
-      }
-    }
+    __syncthreads();  // (A) lookups ready, grids zeroed, buf[(j+kAhead)%kStages] no longer read
+    if (t == 0 && j + kAhead < nj) issue_centre(sm, j + kAhead, pool);
     uint32_t* mc_blk = mc_out ? mc_out + blk * VS_BLOCK_VOXELS : nullptr;
     int8_t* q_blk = q_out ? q_out + blk * VS_BLOCK_VOXELS : nullptr;
+    const HaloRegs cur = hal;
+    if (j + 1 < nj) halo_prefetch(hal, nb_of(sm, j + 1), pool);
 
     if (centre < 0) {
       // absent centre: every cube's origin lives here -> all zero (:152-156)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int v = k * kMcThreads + t;
-        if (mc_blk) __stcs(mc_blk + v, 0u);
-        if (q_blk) __stcs((char*)q_blk + v, (char)-128);
-      }
+      if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(0u, 0u, 0u, 0u));
+      if (q_blk) __stcs((uint32_t*)(q_blk + 4 * t), 0x80808080u);
       if (counts && t == 0) counts[blk] = 0u;
       continue;
     }
 
-    // ---- halo: 217 (tsdf, weight) pairs from the 7 positive neighbours
+    // ---- halo: 217 (tsdf, weight) pairs from the 7 positive neighbours,
+    // loaded during the previous iteration
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const int i = t + k * kMcThreads;
-      if (i < 217) {
-        int c, flat, row, bit;
-        halo_item(i, c, flat, row, bit);
-        const int32_t nrow = nbc[c];
-        if (nrow >= 0) {
-          const uint32_t* src = (const uint32_t*)(pool + (uint64_t)nrow * VS_TSDF_BLOCK_BYTES + 12u * flat);
-          const uint32_t tb = __ldg(src), wb = __ldg(src + 1);
-          if (inside_bit(tb)) atomicOr(&sm.grid_in[s][row], 1u << bit);
-          if (observed_bit(wb)) atomicOr(&sm.grid_ob[s][row], 1u << bit);
-        }
+      if (cur.row[k] >= 0) {
+        if (inside_bit(cur.tb[k])) atomicOr(&sm.grid_in[s][cur.row[k]], 1u << cur.bit[k]);
+        if (observed_bit(cur.wb[k])) atomicOr(&sm.grid_ob[s][cur.row[k]], 1u << cur.bit[k]);
       }
     }
 
-    // ---- centre: wait for the TMA copy, ballot the predicates into rows
-    mbar_wait(&sm.mbar[s], (phases >> s) & 1u);
-    phases ^= 1u << s;
-    const uint32_t* b32 = (const uint32_t*)sm.buf[s];
-    uint32_t tb[4], wb[4], rgb[4];
+    // ---- centre: wait for the TMA copy.  Thread t owns voxels 4t .. 4t+3,
+    // i.e. half of row r = t/2 (row = y + 8z), x = 4h .. 4h+3 with h = t&1.
+    mbar_wait(&sm.mbar[b], (phases >> b) & 1u);
+    phases ^= 1u << b;
+    const uint4* b128 = (const uint4*)(sm.buf[b] + 48 * t);  // 4 voxels x 12 B
+    const uint4 p0 = b128[0], p1 = b128[1], p2 = b128[2];
+    const uint32_t tb[4] = {p0.x, p0.w, p1.z, p2.y};
+    const uint32_t wb[4] = {p0.y, p1.x, p1.w, p2.z};
+    const uint32_t rgb[4] = {p0.z & 0xFFFFFFu, p1.y & 0xFFFFFFu, p2.x & 0xFFFFFFu, p2.w & 0xFFFFFFu};
+    const int h = t & 1, r = t >> 1, y = r & 7, z = r >> 3, x0 = 4 * h;
+    uint32_t in4 = 0, ob4 = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int v = k * kMcThreads + t;
-      tb[k] = b32[3 * v];
-      wb[k] = b32[3 * v + 1];
-      rgb[k] = b32[3 * v + 2] & 0x00FFFFFFu;
-      const uint32_t bin = __ballot_sync(0xffffffffu, inside_bit(tb[k]));
-      const uint32_t bob = __ballot_sync(0xffffffffu, observed_bit(wb[k]));
-      if (lane < 4) {
-        const int r = ((k * kMcThreads + warp * 32) >> 3) + lane;  // row = y + 8z
-        const int gy = r & 7, gz = r >> 3;
-        atomicOr(&sm.grid_in[s][gz * 9 + gy], (bin >> (8 * lane)) & 0xFFu);
-        atomicOr(&sm.grid_ob[s][gz * 9 + gy], (bob >> (8 * lane)) & 0xFFu);
-      }
+      in4 |= inside_bit(tb[k]) << k;
+      ob4 |= observed_bit(wb[k]) << k;
+    }
+    // the two halves of a row meet in adjacent lanes
+    uint32_t in_row = in4 << x0, ob_row = ob4 << x0;
+    in_row |= __shfl_xor_sync(0xffffffffu, in_row, 1);
+    ob_row |= __shfl_xor_sync(0xffffffffu, ob_row, 1);
+    if (h == 0) {
+      atomicOr(&sm.grid_in[s][z * 9 + y], in_row);
+      atomicOr(&sm.grid_ob[s][z * 9 + y], ob_row);
     }
     __syncthreads();  // (B) bit grids complete
 
-    // ---- cube indices, cutoff, colour, quantised TSDF
-    uint32_t nz = 0;
+    // ---- cube indices, cutoff, colour, quantised TSDF: 4 voxels per thread
+    const int r00 = z * 9 + y;
+    const uint32_t* gi = sm.grid_in[s];
+    const uint32_t* go = sm.grid_ob[s];
+    const uint32_t i00 = gi[r00] >> x0, i10 = gi[r00 + 1] >> x0, i01 = gi[r00 + 9] >> x0, i11 = gi[r00 + 10] >> x0;
+    const uint32_t o00 = go[r00] >> x0, o10 = go[r00 + 1] >> x0, o01 = go[r00 + 9] >> x0, o11 = go[r00 + 10] >> x0;
+    uint32_t word[4];
+    uint32_t qw = 0, nz = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int v = k * kMcThreads + t;
-      const int x = v & 7, y = (v >> 3) & 7, z = v >> 6;
-      const int r00 = z * 9 + y, r10 = r00 + 1, r01 = r00 + 9, r11 = r00 + 10;
-      const uint32_t* gi = sm.grid_in[s];
-      const uint32_t* go = sm.grid_ob[s];
-      uint32_t idx = ((gi[r00] >> x) & 3u) | (((gi[r10] >> x) & 3u) << 2) | (((gi[r01] >> x) & 3u) << 4) |
-                     (((gi[r11] >> x) & 3u) << 6);
-      const uint32_t ob = ((go[r00] >> x) & 3u) | (((go[r10] >> x) & 3u) << 2) | (((go[r01] >> x) & 3u) << 4) |
-                          (((go[r11] >> x) & 3u) << 6);
+      uint32_t idx = ((i00 >> k) & 3u) | (((i10 >> k) & 3u) << 2) | (((i01 >> k) & 3u) << 4) |
+                     (((i11 >> k) & 3u) << 6);
+      const uint32_t ob = ((o00 >> k) & 3u) | (((o10 >> k) & 3u) << 2) | (((o01 >> k) & 3u) << 4) |
+                          (((o11 >> k) & 3u) << 6);
       if (ob != 255u || idx == 255u) idx = 0u;  // unobserved corner -> 0; cutoff 255 -> 0
-      const uint32_t word = idx ? (idx | (rgb[k] << 8)) : 0u;
-      if (mc_blk) __stcs(mc_blk + v, word);
-      if (q_blk) __stcs((char*)q_blk + v, (char)quantise(tb[k], wb[k]));
-      nz += __popc(__ballot_sync(0xffffffffu, idx != 0u));
+      word[k] = idx ? (idx | (rgb[k] << 8)) : 0u;
+      qw |= ((uint32_t)quantise(tb[k], wb[k]) & 0xFFu) << (8 * k);
+      nz += idx != 0u;
     }
+    if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(word[0], word[1], word[2], word[3]));
+    if (q_blk) __stcs((uint32_t*)(q_blk + 4 * t), qw);
     if (counts) {
+      nz = __reduce_add_sync(0xffffffffu, nz);
       if (lane == 0) sm.cnt[s][warp] = nz;
       __syncthreads();
       if (t == 0) counts[blk] = sm.cnt[s][0] + sm.cnt[s][1] + sm.cnt[s][2] + sm.cnt[s][3];
