@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--batch-log2", type=int, default=22)
     p.add_argument("--mc-steps", type=int, default=10)
     p.add_argument("--no-mc", action="store_true")
+    p.add_argument("--no-stream", action="store_true")
+    p.add_argument("--stream-ticks", type=int, default=60)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
@@ -430,6 +432,109 @@ def run_mc(args, dev):
     return out
 
 
+def run_stream(args, dev):
+    """Config 4: 16 clients' stream sets over the 2.08M-block room scene.
+
+    Fresh fill of every client, then `ticks` ticks of: 512 random updated
+    TSDF keys -> affected dedup -> insert into all 16 sets (one launch) ->
+    every client extract_random(512).  Every 20 ticks one client reconnects
+    fresh (clear + full fill) and a reset of 256 keys is removed from every
+    set.  Unit: stream-set key ops (inserts + removals) per second."""
+    import ctypes
+
+    import torch
+
+    from paper_1805_03709_b200 import BlockHashSet, StreamSet, _lib, fan_out, remove_everywhere, workloads
+
+    keys = torch.from_numpy(workloads.room_block_keys()).to(dev)
+    M = keys.shape[0]
+    C, U, X, K = 16, 512, 512, 256
+    clients = [StreamSet(1 << 21, 1 << 21, device=dev, fifo_capacity=1 << 22) for _ in range(C)]
+    scratch = BlockHashSet(1 << 14, 1 << 14, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(44)
+    aff = torch.empty((8 * U, 3), dtype=torch.int32, device=dev)
+    n_aff = torch.empty(1, dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    ops = {"insert": 0, "remove": 0}
+
+    def tick(t):
+        upd = keys[torch.randint(0, M, (U,), generator=gen, device=dev)]
+        st = torch.cuda.current_stream(dev)
+        _lib.check(lib.vs_affected_dedup(scratch.handle, _lib.ptr(upd), U, _lib.ptr(aff), _lib.ptr(n_aff),
+                                         ctypes.c_void_p(st.cuda_stream)))
+        A = int(n_aff.item())
+        fan_out(clients, aff[:A])
+        ops["insert"] += C * A
+        for c in clients:
+            ops["remove"] += c._set.extract_keys(X).shape[0]
+        if t % 20 == 19:
+            victim = clients[(t // 20) % C]
+            victim.clear()
+            fan_out([victim], keys)
+            ops["insert"] += M
+            reset = keys[torch.randint(0, M, (K,), generator=gen, device=dev)]
+            remove_everywhere(clients, reset)
+            ops["remove"] += C * K
+
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    fan_out(clients, keys)  # fresh fill of all 16 clients: 16 x 2.08M inserts, one launch
+    f1.record()
+    torch.cuda.synchronize()
+    fill_ms = f0.elapsed_time(f1)
+    ok = all(c.size() == M for c in clients)
+    tick(0)
+    ops["insert"] = ops["remove"] = 0
+    ticks = max(args.stream_ticks, 20)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with _lib.Profile() as prof:
+        e0.record()
+        for t in range(1, ticks + 1):
+            tick(t)
+        e1.record()
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    total = ops["insert"] + ops["remove"]
+    ok = ok and all(0 <= c.size() <= M for c in clients)
+    return {"workload": "config 4: 16 clients x 2,080,160-block scene; per tick 512 updated TSDF keys -> "
+                        "affected dedup -> insert into all sets, extract_random(512) per client; every 20 ticks a "
+                        "fresh reconnect (clear + full fill) and a 256-key reset from every set",
+            "value": total / (ms / 1e3) / 1e6, "unit": "M key-ops/s", "ticks": ticks,
+            "ms_per_tick": ms / ticks, "wall_s": wall, "fill_16_clients_ms": fill_ms,
+            "fill_value": C * M / (fill_ms / 1e3) / 1e6, "inserts": ops["insert"], "removes": ops["remove"],
+            "ok": ok, "gpu_launches": prof.launches,
+            "note": "host-synchronous per call (Python StreamSet API); extract_random scans the full 4.2M-entry table"}
+
+
+def cpu_stream_sample(seconds: float = 5.0):
+    """Reference semantics (set + deque StreamSet, server.py:49-95) in Python
+    on a bounded sample: fill one client with the scene, then update ticks."""
+    import numpy as np
+
+    import oracle
+    from paper_1805_03709_b200 import workloads
+
+    keys = [tuple(k) for k in workloads.room_block_keys().tolist()]
+    rng = np.random.default_rng(0)
+    ss = oracle.OracleStreamSet()
+    t0 = time.perf_counter()
+    n = ss.insert_many(keys)
+    ops = len(keys)
+    while time.perf_counter() - t0 < seconds:
+        upd = [keys[i] for i in rng.integers(0, len(keys), 512)]
+        aff = oracle.affected_dedup(upd)
+        ss.insert_many(aff)
+        ops += len(aff)
+        got = ss.extract_ordered(512)
+        ops += len(got)
+    return ops / (time.perf_counter() - t0) / 1e6
+
+
 # ------------------------------------------------------------------ main
 
 def main():
@@ -481,6 +586,9 @@ def main():
     mc = None
     if not args.no_mc and world == 1:
         mc = run_mc(args, dev)
+    stream = None
+    if not args.no_stream and world == 1:
+        stream = run_stream(args, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         times, ok, _ = cpu_hash_sample(spec, threads, batches=1)
@@ -491,6 +599,10 @@ def main():
         if mc_t:
             cpu["mc"] = {"value": mc_n / mc_t, "unit": "blocks/s", "cores": threads, "kind": "port",
                          "sample": f"{mc_n} room blocks (C restatement of recompute_mc_block)"}
+        if not args.no_stream:
+            cpu["stream"] = {"value": cpu_stream_sample(), "unit": "M key-ops/s", "cores": 1, "kind": "port",
+                             "sample": "1 client: fill with the 2.08M-key scene + update ticks for ~5 s "
+                                       "(Python set + deque restatement of StreamSet)"}
     if world > 1:
         import torch.distributed as dist
 
@@ -502,7 +614,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": config,
                 "parity_ok": h["ok"], "roofline": h["roofline"], "gpu_launches": h["gpu_launches"],
-                "clocks": h["clocks"], "cpu_baseline": cpu, "e2e": h.get("e2e"), "mc": mc}
+                "clocks": h["clocks"], "cpu_baseline": cpu, "e2e": h.get("e2e"), "mc": mc, "stream": stream}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -150,3 +150,47 @@ def test_server_core_replays_reference_server(dev, golden):
     assert sorted(list(k) for k in fresh.snapshot()) == g["fresh_pending"]
     # a returning client keeps its set (server.py:225-239)
     assert core.attach(bytes([0]) * 16) is clients[0]
+
+
+def test_config4_tick_loop_vs_oracle(dev):
+    """Config-4 shape at reduced scale: fresh fills, update ticks fanned out to
+    every client, random extraction, fresh reconnect and resets -- each
+    client's pending set and FIFO stay equal to the reference-semantics oracle."""
+    import torch
+
+    from paper_1805_03709_b200 import StreamSet, fan_out, remove_everywhere, workloads
+
+    scene = workloads.room_block_keys()
+    scene = scene[(scene[:, 0] <= -170) & (scene[:, 2] <= -170)]
+    scene_t = [tuple(k) for k in scene.tolist()]
+    rng = np.random.default_rng(8)
+    C = 4
+    gpu = [StreamSet(1 << 14, 1 << 14, fifo_capacity=1 << 12) for _ in range(C)]
+    ref = [oracle.OracleStreamSet() for _ in range(C)]
+    assert fan_out(gpu, scene) == [len(scene)] * C
+    for r in ref:
+        r.insert_many(scene_t)
+    for t in range(30):
+        upd = [scene_t[i] for i in rng.integers(0, len(scene_t), 64)]
+        aff = oracle.affected_dedup(upd)
+        assert fan_out(gpu, aff) == [r.insert_many(aff) for r in ref]
+        for g, r in zip(gpu, ref):
+            got = g.extract_random(50)
+            assert len(got) == len(set(got)) == min(50, r.size())
+            for k in got:
+                assert r.remove(k)  # the GPU's random subset, adopted by the oracle
+        if t % 10 == 9:
+            v = t // 10 % C
+            gpu[v].clear()
+            ref[v] = oracle.OracleStreamSet()
+            fan_out([gpu[v]], scene)
+            ref[v].insert_many(scene_t)
+            reset = [scene_t[i] for i in rng.integers(0, len(scene_t), 32)]
+            remove_everywhere(gpu, reset)
+            for r in ref:
+                for k in reset:
+                    r.remove(k)
+    for g, r in zip(gpu, ref):
+        assert set(g.snapshot()) == r.set
+        assert g.fifo_entries() == list(r.order)  # stale entries included
+        assert g.extract_ordered(10 ** 6) == r.extract_ordered(10 ** 6)
