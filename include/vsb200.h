@@ -208,14 +208,24 @@ vs_status vs_affected_dedup(vs_table *scratch, const int32_t *updated, uint64_t 
  * inserts the same n keys into every set; created[c*n + i] per client; each
  * client's newly created keys are appended, in input order, to its
  * generation-order FIFO ring (server.py:63-64).
- * fifo_keys[c]  : device int32[fifo_cap[c]][3] ring of client c
- * fifo_tail     : device uint64[C] (absolute, monotonically increasing)
- * n_created     : device uint64[C] (may be NULL). */
+ * fifo_keys_host[c] : device int32[fifo_cap_host[c]][3] ring of client c
+ * fifo_tail_host[c] : device uint64 (absolute, monotonically increasing tail)
+ * n_created         : device uint64[C] (may be NULL).
+ * Fully asynchronous; up to 32 sets per call. */
 vs_status vs_stream_insert_many(vs_table *const *sets_host, int n_sets,
                                 const int32_t *keys, uint64_t n, uint8_t *created,
                                 int32_t *const *fifo_keys_host,
-                                const uint64_t *fifo_cap_host, uint64_t *fifo_tail,
+                                const uint64_t *fifo_cap_host, uint64_t *const *fifo_tail_host,
                                 uint64_t *n_created, vs_stream_t stream);
+
+/* extract_batch (concurrent_hash.py:366-402) on up to 32 sets in ONE launch:
+ * set c scans its live entries in position order from a start position
+ * derived from seeds_host[c] (wrapping), removes and returns the first max_n:
+ * keys_out[c][0 .. n_out[c]) (device int32[C][max_n][3], n_out device
+ * uint64[C]).  Asynchronous. */
+vs_status vs_stream_extract_random(vs_table *const *sets_host, int n_sets,
+                                   uint64_t max_n, const uint64_t *seeds_host,
+                                   int32_t *keys_out, uint64_t *n_out, vs_stream_t stream);
 
 /* Bulk remove of n keys from every one of n_sets tables (on_reset_blocks,
  * server.py:425-436).  erased may be NULL or device uint8[n_sets*n]. */

@@ -402,17 +402,30 @@ class BlockHashSet(_HashCore):
         return created
 
     def extract_keys(self, max_n: int, seed: Optional[int] = None):
-        """Device extract_batch -> int32[m,3] tensor of removed keys."""
+        """Device extract_batch -> int32[m,3] tensor of removed keys.
+
+        Small requests use the windowed single-launch scan
+        (vs_stream_extract_random); large ones the full ordered compaction
+        (vs_table_extract).  Both start at a seeded random position and take
+        live entries in position order, like concurrent_hash.py:387-399."""
         torch = self._torch
         with self._mutex:
             if seed is None:
                 seed = random.getrandbits(64)
+            seed &= (1 << 64) - 1
             m = max(0, min(int(max_n), self.capacity))
-            out = torch.empty((max(m, 1), 3), dtype=torch.int32, device=self.device)
+            if m == 0:
+                return torch.empty((0, 3), dtype=torch.int32, device=self.device)
+            out = torch.empty((m, 3), dtype=torch.int32, device=self.device)
             s = self._stream()
-            check(self._lib.vs_table_extract(self._h, max(int(max_n), 0), seed & ((1 << 64) - 1),
-                                             ptr(out), ptr(self._n_dev),
-                                             ctypes.c_void_p(s.cuda_stream)), "extract")
+            if m <= (1 << 16):
+                handles = (ctypes.c_void_p * 1)(self._h.value)
+                seeds = (ctypes.c_uint64 * 1)(seed)
+                check(self._lib.vs_stream_extract_random(handles, 1, m, seeds, ptr(out), ptr(self._n_dev),
+                                                         ctypes.c_void_p(s.cuda_stream)), "extract")
+            else:
+                check(self._lib.vs_table_extract(self._h, m, seed, ptr(out), ptr(self._n_dev),
+                                                 ctypes.c_void_p(s.cuda_stream)), "extract")
             self._done(s)
             s.synchronize()
             n = int(self._n_dev.item())

@@ -33,6 +33,7 @@ struct SetViews {
 struct FifoViews {
   int32_t* keys[kMaxSets];
   uint64_t cap[kMaxSets];
+  uint64_t* tail[kMaxSets];  // device word per client (absolute tail)
 };
 
 __global__ void __launch_bounds__(256) k_multi_insert(const __grid_constant__ SetViews V,
@@ -70,28 +71,95 @@ __global__ void k_multi_fixup(const __grid_constant__ SetViews V, const int32_t*
 }
 
 __global__ void k_fifo_append(const __grid_constant__ FifoViews F, const int32_t* __restrict__ keys, uint64_t n,
-                              const uint8_t* __restrict__ created, const uint64_t* __restrict__ off,
-                              const uint64_t* __restrict__ tails) {
+                              const uint8_t* __restrict__ created, const uint64_t* __restrict__ off) {
   const int c = blockIdx.y;
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint64_t j = (uint64_t)c * n + i;
   if (!created[j]) return;
   const uint64_t rank = off[j] - off[(uint64_t)c * n];
-  const uint64_t p = (tails[c] + rank) % F.cap[c];
+  const uint64_t p = (*F.tail[c] + rank) % F.cap[c];
   int32_t* dst = F.keys[c] + 3 * p;
   dst[0] = keys[3 * i];
   dst[1] = keys[3 * i + 1];
   dst[2] = keys[3 * i + 2];
 }
 
-__global__ void k_fifo_tail(const uint64_t* __restrict__ off, uint64_t n, int C, uint64_t* __restrict__ tails,
-                            uint64_t* __restrict__ n_created) {
+__global__ void k_fifo_tail(const __grid_constant__ FifoViews F, bool fifo, const uint64_t* __restrict__ off,
+                            uint64_t n, int C, uint64_t* __restrict__ n_created) {
   const int c = threadIdx.x;
   if (c >= C) return;
   const uint64_t cnt = off[(uint64_t)(c + 1) * n] - off[(uint64_t)c * n];
-  if (tails) tails[c] += cnt;
+  if (fifo) *F.tail[c] += cnt;
   if (n_created) n_created[c] = cnt;
+}
+
+// extract_batch for several clients in ONE launch (concurrent_hash.py:382-402):
+// one CTA per client scans live entries in position order from a seeded
+// random start (wrapping), keeps the first max_n, and removes them; the
+// vacated excess entries go straight back to the free list (no pops run in
+// this launch, so the push cannot race a pop).
+__global__ void __launch_bounds__(256) k_multi_extract(const __grid_constant__ SetViews V,
+                                                       const __grid_constant__ FifoViews S, uint64_t max_n,
+                                                       int32_t* __restrict__ keys_out, uint64_t* __restrict__ n_out) {
+  const int c = blockIdx.x;
+  const TableView& T = V.v[c];
+  const uint32_t cap = T.n + T.excess;
+  const uint64_t seed = S.cap[c];  // per-client seed rides in the cap slot
+  uint64_t x = seed + 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  const uint32_t start = (uint32_t)(x % cap);
+  int32_t* out = keys_out + (uint64_t)c * max_n * 3;
+  __shared__ uint32_t wcnt[8];
+  __shared__ uint64_t found_s;
+  if (threadIdx.x == 0) found_s = 0;
+  __syncthreads();
+  const uint32_t warp = threadIdx.x >> 5;
+  for (uint64_t scanned = 0; scanned < cap; scanned += 256) {
+    const uint64_t found = found_s;
+    if (found >= max_n) break;
+    uint64_t p = (uint64_t)start + scanned + threadIdx.x;
+    p = p >= cap ? p - cap : p;
+    int4 e = make_int4(0, 0, 0, 0);
+    bool live = false;
+    if (scanned + threadIdx.x < cap) {
+      e = ld_entry(T.e + p);
+      live = ((uint32_t)e.w & kOcc) != 0;
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, live);
+    if (lane_id() == 0) wcnt[warp] = __popc(bal);
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+    for (uint32_t w = 0; w < 8; ++w) {
+      before += (w < warp) ? wcnt[w] : 0;
+      total += wcnt[w];
+    }
+    if (live) {
+      const uint64_t o = found + before + __popc(bal & lanemask_lt());
+      if (o < max_n) {
+        out[3 * o] = e.x;
+        out[3 * o + 1] = e.y;
+        out[3 * o + 2] = e.z;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) found_s = found + total;
+    __syncthreads();
+  }
+  const uint64_t m = found_s < max_n ? found_s : max_n;
+  __syncthreads();  // keys_out complete before the removals read it
+  int delta = 0;
+  for (uint64_t j = threadIdx.x; j < m; j += blockDim.x) {
+    const int32_t pos = erase_key(T, out[3 * j], out[3 * j + 1], out[3 * j + 2]);
+    if (pos >= 0) {
+      --delta;
+      if (pos >= (int32_t)T.n) push_free(T, (uint32_t)pos);
+    }
+  }
+  add_size_cta(T, delta);
+  if (threadIdx.x == 0) n_out[c] = m;
 }
 
 __global__ void __launch_bounds__(256) k_multi_erase(const __grid_constant__ SetViews V,
@@ -238,7 +306,7 @@ vs_status vs_affected_dedup(vs_table* scratch, const int32_t* updated, uint64_t 
 
 vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const int32_t* keys, uint64_t n,
                                 uint8_t* created, int32_t* const* fifo_keys_host, const uint64_t* fifo_cap_host,
-                                uint64_t* fifo_tail, uint64_t* n_created, vs_stream_t stream) {
+                                uint64_t* const* fifo_tail_host, uint64_t* n_created, vs_stream_t stream) {
   SetViews V;
   if (!sets_host) {
     set_error("sets is NULL");
@@ -270,20 +338,41 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
   { ProfScope prof(2, s); k_multi_insert<<<grid, 256, 0, s>>>(V, keys, n, created, index); vsb::count_launch(); }
   { k_multi_fixup<<<grid, 256, 0, s>>>(V, keys, n, created, index); vsb::count_launch(); }
   cudaError_t e = exclusive_scan<uint8_t>(created, total, off, work, s);
-  if (e == cudaSuccess && fifo_keys_host && fifo_cap_host && fifo_tail) {
-    FifoViews F;
+  const bool fifo = fifo_keys_host && fifo_cap_host && fifo_tail_host;
+  FifoViews F{};
+  if (fifo) {
     for (int c = 0; c < n_sets; ++c) {
       F.keys[c] = fifo_keys_host[c];
       F.cap[c] = fifo_cap_host[c] ? fifo_cap_host[c] : 1;
+      F.tail[c] = fifo_tail_host[c];
     }
-    { k_fifo_append<<<grid, 256, 0, s>>>(F, keys, n, created, off, fifo_tail); vsb::count_launch(); }
   }
-  if (e == cudaSuccess) { k_fifo_tail<<<1, 32, 0, s>>>(off, n, n_sets, fifo_tail, n_created); vsb::count_launch(); }
+  if (e == cudaSuccess && fifo) { k_fifo_append<<<grid, 256, 0, s>>>(F, keys, n, created, off); vsb::count_launch(); }
+  if (e == cudaSuccess) { k_fifo_tail<<<1, 32, 0, s>>>(F, fifo, off, n, n_sets, n_created); vsb::count_launch(); }
   cudaFreeAsync(index, s);
   cudaFreeAsync(off, s);
   cudaFreeAsync(work, s);
   if (e != cudaSuccess) return cuda_status(e, "vs_stream_insert_many");
   VS_CK_LAUNCH("vs_stream_insert_many");
+  return VS_OK;
+}
+
+vs_status vs_stream_extract_random(vs_table* const* sets_host, int n_sets, uint64_t max_n,
+                                   const uint64_t* seeds_host, int32_t* keys_out, uint64_t* n_out,
+                                   vs_stream_t stream) {
+  SetViews V;
+  if (!sets_host || !seeds_host || !n_out || (max_n && !keys_out)) {
+    set_error("sets/seeds/keys_out/n_out must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  vs_status st = fill_views(sets_host, n_sets, V);
+  if (st != VS_OK) return st;
+  DeviceGuard g(sets_host[0]->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  FifoViews S{};
+  for (int c = 0; c < n_sets; ++c) S.cap[c] = seeds_host[c];
+  { k_multi_extract<<<n_sets, 256, 0, s>>>(V, S, max_n, keys_out, n_out); vsb::count_launch(); }
+  VS_CK_LAUNCH("vs_stream_extract_random");
   return VS_OK;
 }
 

@@ -31,7 +31,9 @@ class StreamSet:
     """Per-destination pending-update set with a generation-order queue
     (server.py:49-95).  The queue is a device ring of keys that keeps stale
     entries exactly like the reference's deque; ``extract_ordered`` skips
-    them by validating membership."""
+    them by validating membership.  The ring tail lives on the device so
+    fan-outs need no host synchronisation; the host keeps the head and an
+    upper bound of the tail for ring sizing."""
 
     def __init__(self, buckets: int = 1 << 16, excess: int = 1 << 16, *, device=None,
                  fifo_capacity: Optional[int] = None) -> None:
@@ -42,24 +44,36 @@ class StreamSet:
         cap = fifo_capacity or max(1024, min(buckets + excess, 1 << 20))
         self._fifo = torch.empty((cap, 3), dtype=torch.int32, device=self.device)
         self._head = 0
-        self._tail = 0
+        self._tail_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._tail_bound = 0
         self._scratch: Optional[BlockHashSet] = None
 
-    # -- FIFO ring management (host-authoritative head/tail) ---------------
+    # -- FIFO ring management -------------------------------------------------
 
     @property
     def fifo_capacity(self) -> int:
         return self._fifo.shape[0]
 
+    def _tail(self) -> int:
+        """Exact tail (synchronises with the table's stream)."""
+        s = _order_streams([self._set])
+        with self._torch.cuda.stream(s):
+            t = int(self._tail_dev.item())
+        self._tail_bound = t
+        return t
+
     def _ring_view(self):
         """Pending FIFO entries [head, tail) in order (device tensor)."""
         torch = self._torch
         cap = self.fifo_capacity
-        idx = (torch.arange(self._head, self._tail, device=self.device) % cap)
+        idx = torch.arange(self._head, self._tail(), device=self.device) % cap
         return self._fifo[idx]
 
     def _ensure_fifo(self, extra: int) -> None:
-        need = (self._tail - self._head) + extra
+        if self._tail_bound + extra - self._head <= self.fifo_capacity:
+            return
+        tail = self._tail()
+        need = tail - self._head + extra
         if need <= self.fifo_capacity:
             return
         torch = self._torch
@@ -68,7 +82,8 @@ class StreamSet:
         fifo = torch.empty((cap, 3), dtype=torch.int32, device=self.device)
         fifo[: live.shape[0]] = live
         self._fifo = fifo
-        self._tail -= self._head
+        self._tail_dev.fill_(tail - self._head)
+        self._tail_bound = tail - self._head
         self._head = 0
 
     def fifo_entries(self) -> list[BlockKey]:
@@ -109,7 +124,8 @@ class StreamSet:
     def extract_ordered_keys(self, max_n: int):
         """Device version of extract_ordered (server.py:86-95) -> int32[m,3]."""
         torch = self._torch
-        if max_n <= 0 or self._head >= self._tail:
+        tail = self._tail()
+        if max_n <= 0 or self._head >= tail:
             return torch.empty((0, 3), dtype=torch.int32, device=self.device)
         if self._scratch is None:
             self._scratch = BlockHashSet(1 << 12, 1 << 12, device=self.device)
@@ -118,7 +134,7 @@ class StreamSet:
         n_out = ctypes.c_uint64(0)
         s = _order_streams([self._set, self._scratch])
         check(_lib.load().vs_stream_extract_ordered(
-            self._set.handle, ptr(self._fifo), self.fifo_capacity, ctypes.byref(head), self._tail, max_n,
+            self._set.handle, ptr(self._fifo), self.fifo_capacity, ctypes.byref(head), tail, max_n,
             ptr(out), ctypes.byref(n_out), self._scratch.handle, ctypes.c_void_p(s.cuda_stream)),
             "extract_ordered")
         _mark_done([self._set, self._scratch], s)
@@ -128,7 +144,11 @@ class StreamSet:
     def clear(self) -> None:
         """Bulk reset (fresh reconnect of a retained client)."""
         self._set.clear()
-        self._head = self._tail = 0
+        s = _order_streams([self._set])
+        with self._torch.cuda.stream(s):
+            self._tail_dev.zero_()
+        _mark_done([self._set], s)
+        self._head = self._tail_bound = 0
 
 
 def _order_streams(tables):
@@ -153,7 +173,7 @@ def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True):
     For each client the newly created keys (the set difference keys \\
     pending) are appended to its FIFO in input order, exactly like the
     reference's per-key deque.append.  Returns the created count per client
-    (synchronising), or the device counts when sync=False.
+    (synchronising), or the device counts (int64[C]) when sync=False.
     """
     if not sets:
         return []
@@ -175,17 +195,42 @@ def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True):
         handles = (ctypes.c_void_p * C)(*[t.handle.value for t in tables])
         fifos = (ctypes.c_void_p * C)(*[st._fifo.data_ptr() for st in group])
         caps = (ctypes.c_uint64 * C)(*[st.fifo_capacity for st in group])
-        tails = torch.tensor([st._tail for st in group], dtype=torch.int64).to(dev, non_blocking=True)
+        tails = (ctypes.c_void_p * C)(*[st._tail_dev.data_ptr() for st in group])
         s = _order_streams(tables)
-        check(lib.vs_stream_insert_many(handles, C, ptr(k), n, ptr(created), fifos, caps, ptr(tails),
+        check(lib.vs_stream_insert_many(handles, C, ptr(k), n, ptr(created), fifos, caps, tails,
                                         ptr(counts[g0:g0 + C]), ctypes.c_void_p(s.cuda_stream)), "fan_out")
         _mark_done(tables, s)
+        for st in group:
+            st._tail_bound += n
     if not sync:
         return counts
-    host = counts.cpu().tolist()
-    for st, c in zip(sets, host):
-        st._tail += int(c)
-    return [int(c) for c in host]
+    return [int(c) for c in counts.cpu().tolist()]
+
+
+def extract_random_many(sets: Sequence[StreamSet], max_n: int, seeds: Optional[Sequence[int]] = None):
+    """``[s.extract_random(max_n) for s in sets]`` in one launch per 32
+    clients.  Returns (keys int32[C, max_n, 3], n int64[C]) device tensors."""
+    import random
+
+    torch = sets[0]._torch
+    dev = sets[0].device
+    C = len(sets)
+    keys = torch.empty((C, max(max_n, 1), 3), dtype=torch.int32, device=dev)
+    n = torch.zeros(C, dtype=torch.int64, device=dev)
+    if max_n <= 0:
+        return keys[:, :0], n
+    lib = _lib.load()
+    for g0 in range(0, C, _MAX_SETS_PER_LAUNCH):
+        group = list(sets[g0:g0 + _MAX_SETS_PER_LAUNCH])
+        G = len(group)
+        tables = [st._set if isinstance(st, StreamSet) else st for st in group]
+        handles = (ctypes.c_void_p * G)(*[t.handle.value for t in tables])
+        sd = (ctypes.c_uint64 * G)(*[(seeds[g0 + i] if seeds else random.getrandbits(64)) for i in range(G)])
+        s = _order_streams(tables)
+        check(lib.vs_stream_extract_random(handles, G, max_n, sd, ptr(keys[g0:g0 + G]), ptr(n[g0:g0 + G]),
+                                           ctypes.c_void_p(s.cuda_stream)), "extract_random_many")
+        _mark_done(tables, s)
+    return keys, n
 
 
 def remove_everywhere(sets: Sequence[StreamSet], keys) -> None:

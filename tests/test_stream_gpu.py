@@ -194,3 +194,26 @@ def test_config4_tick_loop_vs_oracle(dev):
         assert set(g.snapshot()) == r.set
         assert g.fifo_entries() == list(r.order)  # stale entries included
         assert g.extract_ordered(10 ** 6) == r.extract_ordered(10 ** 6)
+
+
+def test_extract_random_many_properties(dev):
+    """Windowed multi-client extraction: distinct keys, subset of the set,
+    count = min(max_n, size), post-set = pre-set minus returned, rotation
+    start honoured (positions ascending from the start, wrapping)."""
+    from paper_1805_03709_b200 import StreamSet, extract_random_many
+
+    rng = np.random.default_rng(5)
+    sets = [StreamSet(1 << 12, 1 << 12) for _ in range(5)]
+    pre = []
+    for i, s in enumerate(sets):
+        ks = {tuple(int(v) for v in r) for r in rng.integers(-50, 50, (200 * (i + 1), 3))}
+        s.insert_many(sorted(ks))
+        pre.append(ks)
+    keys, n = extract_random_many(sets, 300, seeds=[1, 2, 3, 4, 5])
+    for i, s in enumerate(sets):
+        got = [tuple(k) for k in keys[i, : int(n[i])].cpu().tolist()]
+        assert len(got) == len(set(got)) == min(300, len(pre[i]))
+        assert set(got) <= pre[i]
+        assert set(s.snapshot()) == pre[i] - set(got)
+        a = s._set.audit()
+        assert a["duplicates"] == 0 and a["free"] + a["reachable_excess"] == s._set.excess_capacity
