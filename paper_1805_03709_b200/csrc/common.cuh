@@ -47,6 +47,7 @@ struct TableView {
   uint32_t* free_stack;      // [stripes * stripe_cap] absolute excess positions
   long long* tops;           // [stripes * kTopStride] entries per stripe
   unsigned long long* claim; // [cap] epoch-tagged lowest op index (created / erase dedup)
+  uint32_t* dupbits;         // [cap/32] entry got a duplicate insert in this launch
   Ctl* ctl;
   uint32_t n;                // bucket_count
   uint32_t excess;

@@ -3,13 +3,12 @@
 // Reference: concurrent_hash.py (all of it).  Per-op algorithms live in
 // hash_ops.cuh; this file holds the launches: one thread per op, every op
 // type in one launch if wanted (vs_table_apply), followed by
-//   k_fixup_created  -- gives `created` to the lowest op index among in-batch
-//                       duplicates, i.e. the sequential-replay answer;
-//   k_recycle        -- pushes the excess entries vacated by erases back onto
-//                       the striped free list (FreeListStack.push,
-//                       concurrent_hash.py:72-73), from the ops' vacated
-//                       positions, so the op kernel itself needs no atomics
-//                       for it.
+//   k_post           -- gives `created` to the lowest op index among in-batch
+//                       duplicates (the sequential-replay answer) and pushes
+//                       the excess entries vacated by erases back onto the
+//                       striped free list (FreeListStack.push,
+//                       concurrent_hash.py:72-73), in one pass, so the op
+//                       kernel itself needs no atomics for either.
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -206,22 +205,14 @@ __global__ void __launch_bounds__(kOpBlock) k_apply(TableView T, const int32_t* 
   add_size_cta(T, delta);
 }
 
-// created[i] goes to the lowest op index that inserted the same key in this
-// batch (sequential replay: the first occurrence creates, later ones find).
-__global__ void k_fixup_created(TableView T, const int32_t* __restrict__ keys, const uint8_t* __restrict__ ops,
-                                uint64_t n, uint8_t* __restrict__ created, const int32_t* __restrict__ index) {
+// Post pass after k_insert / k_apply: created flags to the lowest op index
+// among in-batch duplicates (sequential replay), FRESH cleared, and the
+// excess entries vacated by erases recycled -- one launch, one pass.
+__global__ void k_post(TableView T, const int32_t* __restrict__ keys, const uint8_t* __restrict__ ops, uint64_t n,
+                       uint8_t* __restrict__ result, const int32_t* __restrict__ index) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  if (ops && ops[i] != VS_OP_INSERT) return;
-  if (!created[i]) return;
-  const int32_t pos = index[i];
-  atomicAnd(&T.e[pos].meta, ~kFresh);
-  const int32_t m = (int32_t)(uint32_t)(T.claim[pos] & 0xFFFFFFFFull);
-  if (m >= 0 && (uint64_t)m < i && keys[3 * (uint64_t)m] == keys[3 * i] &&
-      keys[3 * (uint64_t)m + 1] == keys[3 * i + 1] && keys[3 * (uint64_t)m + 2] == keys[3 * i + 2]) {
-    created[i] = 0;
-    created[m] = 1;
-  }
+  post_op(T, keys, i, ops ? ops[i] : (uint8_t)VS_OP_INSERT, result, index[i]);
 }
 
 // Push vacated excess positions back onto the striped free list (warp-
@@ -548,6 +539,7 @@ vs_status vs_table_create(uint64_t bucket_count, uint64_t excess_capacity, int d
   A((void**)&t->free_stack, sizeof(uint32_t) * (size_t)t->stripes * t->stripe_cap);
   A((void**)&t->tops, sizeof(long long) * (size_t)t->stripes * kTopStride);
   A((void**)&t->claim, sizeof(unsigned long long) * (size_t)t->cap);
+  A((void**)&t->dupbits, sizeof(uint32_t) * (size_t)(t->cap / 32 + 1));
   A((void**)&t->ctl, sizeof(Ctl));
   A((void**)&t->chunk_counts, sizeof(uint32_t) * (size_t)t->nchunks);
   A((void**)&t->chunk_offsets, sizeof(uint64_t) * ((size_t)t->nchunks + 1));
@@ -575,6 +567,7 @@ vs_status vs_table_destroy(vs_table* t) {
   cudaFree(t->free_stack);
   cudaFree(t->tops);
   cudaFree(t->claim);
+  cudaFree(t->dupbits);
   cudaFree(t->ctl);
   cudaFree(t->chunk_counts);
   cudaFree(t->chunk_offsets);
@@ -621,7 +614,7 @@ vs_status vs_table_insert(vs_table* t, const int32_t* keys, uint64_t n, uint8_t*
     ProfScope prof(0, s);
     { k_insert<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, created, index); vsb::count_launch(); }
   }
-  { k_fixup_created<<<grid_for(n, 256), 256, 0, s>>>(v, keys, nullptr, n, created, index); vsb::count_launch(); }
+  { k_post<<<grid_for(n, 256), 256, 0, s>>>(v, keys, nullptr, n, created, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_insert");
   return VS_OK;
 }
@@ -683,8 +676,7 @@ vs_status vs_table_apply(vs_table* t, const int32_t* keys, const uint8_t* ops, u
     ProfScope prof(0, s);
     { k_apply<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
   }
-  { k_fixup_created<<<grid_for(n, 256), 256, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
-  launch_recycle(v, index, result, ops, nullptr, n, s);
+  { k_post<<<grid_for(n, 256), 256, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_apply");
   return VS_OK;
 }
@@ -750,6 +742,7 @@ vs_status vs_table_clear(vs_table* t, vs_stream_t stream) {
   cudaStream_t s = (cudaStream_t)stream;
   VS_CK(cudaMemsetAsync(t->e, 0, sizeof(Entry) * (size_t)t->cap, s));
   VS_CK(cudaMemsetAsync(t->claim, 0xFF, sizeof(unsigned long long) * (size_t)t->cap, s));
+  VS_CK(cudaMemsetAsync(t->dupbits, 0, sizeof(uint32_t) * (size_t)(t->cap / 32 + 1), s));
   t->epoch = 0;
   const TableView v = t->view();
   const unsigned g_init = grid_for(t->excess, 256) < 4096 ? grid_for(t->excess, 256) : 4096;

@@ -20,8 +20,9 @@
 //   * the free-list stack is striped over kStripes counters (separate L2
 //     sectors) with warp-aggregated pops; a pop fails (CapacityExhausted)
 //     only after every stripe was seen empty, so exhaustion stays exact;
-//   * "created" for in-batch duplicates goes to the lowest op index through
-//     an epoch-tagged 64-bit atomicMin (no ordering, no clearing pass).
+//   * "created" for in-batch duplicates goes to the lowest op index: a
+//     duplicate marks a 1-bit-per-entry bitmap and atomicMins an epoch-tagged
+//     64-bit word (no ordering, no clearing pass); creators touch neither.
 #pragma once
 #include "common.cuh"
 
@@ -116,9 +117,12 @@ __device__ __forceinline__ int32_t find_pos(const TableView& T, int32_t x, int32
   }
 }
 
-// Compete for the "created" flag of an entry created in this launch: lowest
-// op index wins (resolved by the fixup launch).
+// A duplicate insert of an entry created in this launch (FRESH): mark the
+// entry in the L2-resident dup bitmap and compete for the "created" flag by
+// lowest op index (resolved by the post launch).  Creators touch neither, so
+// the common no-duplicate case costs no extra memory traffic.
 __device__ __forceinline__ void claim_min(const TableView& T, int32_t pos, int32_t op) {
+  atomicOr(&T.dupbits[(uint32_t)pos >> 5], 1u << ((uint32_t)pos & 31u));
   atomicMin(&T.claim[pos], T.tag | (unsigned long long)(uint32_t)op);
 }
 
@@ -173,7 +177,6 @@ __device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x
     if (!(old & kOcc)) {
       // claim the free bucket entry: key, OCC and unlock in ONE 16-byte
       // store; its NEXT link is kept (:185-192)
-      claim_min(T, (int32_t)b, op);
       st_entry(T.e + b, x, y, z, (old & kNext) | kOcc | kFresh);
       return {(int32_t)b, 1};
     }
@@ -184,7 +187,6 @@ __device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x
       return {-1, 0};
     }
     const uint32_t e = (uint32_t)ne;
-    claim_min(T, (int32_t)e, op);
     st_entry(T.e + e, x, y, z, kOcc | kFresh);  // NEXT = 0 clears the stale offset (:200)
     const uint32_t link = e - T.n + 1u;
     if (tail == b) {
@@ -240,6 +242,30 @@ __device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int3
     }
     // key vanished between the find and the lock; re-check (:293)
     atom_exch_relaxed(bmeta, old);
+  }
+}
+
+// Post pass for one op of an insert/apply batch: settle the created flag of
+// a creator against in-batch duplicates (lowest op index wins), clear FRESH;
+// recycle the excess entry vacated by an erase.
+__device__ __forceinline__ void post_op(const TableView& T, const int32_t* __restrict__ keys, uint64_t i, uint8_t op,
+                                        uint8_t* __restrict__ result, int32_t pos) {
+  if (op == 0 /*VS_OP_INSERT*/) {
+    if (!result[i]) return;
+    const uint32_t bit = 1u << ((uint32_t)pos & 31u);
+    uint32_t* w = &T.dupbits[(uint32_t)pos >> 5];
+    atomicAnd(&T.e[pos].meta, ~kFresh);
+    if (!(*w & bit)) return;  // no duplicate touched this entry
+    atomicAnd(w, ~bit);
+    const unsigned long long c = T.claim[pos];
+    if ((c & 0xFFFFFFFF00000000ull) != T.tag) return;
+    const uint64_t m = (uint32_t)(c & 0xFFFFFFFFull);
+    if (m < i && keys[3 * m] == keys[3 * i] && keys[3 * m + 1] == keys[3 * i + 1] && keys[3 * m + 2] == keys[3 * i + 2]) {
+      result[i] = 0;
+      result[m] = 1;
+    }
+  } else if (op == 2 /*VS_OP_ERASE*/) {
+    if (result[i] && pos >= (int32_t)T.n) push_free(T, (uint32_t)pos);
   }
 }
 

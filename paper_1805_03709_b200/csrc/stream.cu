@@ -57,17 +57,7 @@ __global__ void k_multi_fixup(const __grid_constant__ SetViews V, const int32_t*
   const int c = blockIdx.y;
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint8_t* cr = created + (uint64_t)c * n;
-  if (!cr[i]) return;
-  const TableView& T = V.v[c];
-  const int32_t pos = index[(uint64_t)c * n + i];
-  atomicAnd(&T.e[pos].meta, ~kFresh);
-  const int32_t m = (int32_t)(uint32_t)(T.claim[pos] & 0xFFFFFFFFull);
-  if (m >= 0 && (uint64_t)m < i && keys[3 * (uint64_t)m] == keys[3 * i] &&
-      keys[3 * (uint64_t)m + 1] == keys[3 * i + 1] && keys[3 * (uint64_t)m + 2] == keys[3 * i + 2]) {
-    cr[i] = 0;
-    cr[m] = 1;
-  }
+  post_op(V.v[c], keys, i, 0, created + (uint64_t)c * n, index[(uint64_t)c * n + i]);
 }
 
 __global__ void k_fifo_append(const __grid_constant__ FifoViews F, const int32_t* __restrict__ keys, uint64_t n,

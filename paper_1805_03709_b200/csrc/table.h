@@ -15,6 +15,7 @@ struct vs_table {
   uint32_t* free_stack = nullptr;
   long long* tops = nullptr;
   unsigned long long* claim = nullptr;
+  uint32_t* dupbits = nullptr;
   vsb::Ctl* ctl = nullptr;
   uint64_t magic = 0;
   uint32_t epoch = 0;  // launch epoch for the claim tags
@@ -31,6 +32,7 @@ struct vs_table {
     v.free_stack = free_stack;
     v.tops = tops;
     v.claim = claim;
+    v.dupbits = dupbits;
     v.ctl = ctl;
     v.n = n;
     v.excess = excess;
