@@ -87,6 +87,42 @@ __device__ __forceinline__ int4 ld_entry(const Entry* p) {
   return v;
 }
 
+// L2 eviction priority for bucket entries: every op starts at its bucket
+// entry, so the bucket region (n x 16 B) is worth keeping in L2 ahead of the
+// excess region and the streamed per-op inputs (VSB_HASH_L2HINT).
+#ifndef VSB_HASH_L2HINT
+#define VSB_HASH_L2HINT 1
+#endif
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ int4 ld_bucket(const Entry* p) {
+#if VSB_HASH_L2HINT
+  int4 v;
+  asm volatile("ld.relaxed.gpu.global.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(policy_evict_last())
+               : "memory");
+  return v;
+#else
+  return ld_entry(p);
+#endif
+}
+
+// streamed per-op inputs: read once, do not displace table lines
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+#if VSB_HASH_L2HINT
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
+
 __device__ __forceinline__ void st_entry(Entry* p, int32_t x, int32_t y, int32_t z, uint32_t meta) {
   asm volatile("st.relaxed.gpu.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(x), "r"(y),
                "r"(z), "r"(meta)

@@ -175,34 +175,71 @@ __global__ void __launch_bounds__(kOpBlock) k_erase_win(TableView T, const int32
   add_size_cta(T, delta);
 }
 
+// One mixed op (insert / find / erase).  Returns the size delta.
+__device__ __forceinline__ int apply_one(const TableView& T, const int32_t* __restrict__ keys,
+                                         const uint8_t* __restrict__ ops, uint64_t i, uint8_t* __restrict__ result,
+                                         int32_t* __restrict__ index) {
+  const int32_t x = ld_stream(keys + 3 * i), y = ld_stream(keys + 3 * i + 1), z = ld_stream(keys + 3 * i + 2);
+  const uint8_t op = ld_stream(ops + i);
+  int32_t pos;
+  uint8_t res;
+  int delta = 0;
+  if (op == VS_OP_INSERT) {
+    const InsertResult r = insert_key(T, x, y, z, (int32_t)i);
+    pos = r.pos;
+    res = r.created;
+    delta = r.created;
+  } else if (op == VS_OP_ERASE) {
+    pos = erase_key(T, x, y, z);
+    res = pos >= 0;
+    delta = -(int)res;
+  } else {
+    uint32_t meta;
+    pos = find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
+    res = pos >= 0;
+  }
+  __stcs(result + i, res);
+  __stcs(index + i, pos);
+  return delta;
+}
+
+// Mixed batch.  VSB_HASH_PERSIST: a persistent grid whose lanes loop over
+// ops, so a lane that finishes a short op (a find) starts the next one
+// instead of idling until the slowest op of its CTA (a contended insert) is done.
+#ifndef VSB_HASH_PERSIST
+#define VSB_HASH_PERSIST 0
+#endif
 __global__ void __launch_bounds__(kOpBlock) k_apply(TableView T, const int32_t* __restrict__ keys,
                                                     const uint8_t* __restrict__ ops, uint64_t n,
                                                     uint8_t* __restrict__ result, int32_t* __restrict__ index) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int delta = 0;
-  if (i < n) {
-    const int32_t x = keys[3 * i], y = keys[3 * i + 1], z = keys[3 * i + 2];
-    const uint8_t op = ops[i];
-    int32_t pos;
-    uint8_t res;
-    if (op == VS_OP_INSERT) {
-      const InsertResult r = insert_key(T, x, y, z, (int32_t)i);
-      pos = r.pos;
-      res = r.created;
-      delta = r.created;
-    } else if (op == VS_OP_ERASE) {
-      pos = erase_key(T, x, y, z);
-      res = pos >= 0;
-      delta = -(int)res;
-    } else {
-      uint32_t meta;
-      pos = find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
-      res = pos >= 0;
-    }
-    result[i] = res;
-    index[i] = pos;
-  }
+#if VSB_HASH_PERSIST
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+#pragma unroll 1
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    delta += apply_one(T, keys, ops, i, result, index);
+#else
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) delta = apply_one(T, keys, ops, i, result, index);
+#endif
   add_size_cta(T, delta);
+}
+
+static unsigned apply_grid(uint64_t n) {
+#if VSB_HASH_PERSIST
+  static int resident = 0;
+  if (resident == 0) {
+    int dev = 0, sms = 148, per_sm = 8;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply, kOpBlock, 0);
+    resident = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const unsigned g = grid_for(n, kOpBlock);
+  return g < (unsigned)resident ? g : (unsigned)resident;
+#else
+  return grid_for(n, kOpBlock);
+#endif
 }
 
 // Post pass after k_insert / k_apply: created flags to the lowest op index
@@ -674,7 +711,7 @@ vs_status vs_table_apply(vs_table* t, const int32_t* keys, const uint8_t* ops, u
   const TableView v = t->next_view();
   {
     ProfScope prof(0, s);
-    { k_apply<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
+    { k_apply<<<apply_grid(n), kOpBlock, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
   }
   { k_post<<<grid_for(n, 256), 256, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_apply");

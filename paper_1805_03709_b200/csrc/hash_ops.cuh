@@ -103,10 +103,10 @@ __device__ __forceinline__ void push_free(const TableView& T, uint32_t e) {
 // Returns the position or -1; *meta_out = meta of the matching entry.
 __device__ __forceinline__ int32_t find_pos(const TableView& T, int32_t x, int32_t y, int32_t z, uint32_t b,
                                            uint32_t* meta_out) {
+  int4 s = ld_bucket(T.e + b);  // first hop: the bucket entry (L2 evict_last)
   uint32_t e = b;
 #pragma unroll 1
   for (;;) {
-    const int4 s = ld_entry(T.e + e);
     const uint32_t meta = (uint32_t)s.w;
     if ((meta & kOcc) && key_eq(s, x, y, z)) {
       *meta_out = meta;
@@ -114,6 +114,7 @@ __device__ __forceinline__ int32_t find_pos(const TableView& T, int32_t x, int32
     }
     if (!(meta & kNext)) return -1;
     e = next_pos(T, meta);
+    s = ld_entry(T.e + e);
   }
 }
 
