@@ -227,6 +227,24 @@ vs_status vs_stream_extract_random(vs_table *const *sets_host, int n_sets,
                                    uint64_t max_n, const uint64_t *seeds_host,
                                    int32_t *keys_out, uint64_t *n_out, vs_stream_t stream);
 
+/* extract_matching with the server's frustum-AABB predicate
+ * (server.py:365-387, geometry.py:121-147) on up to 32 sets in one launch:
+ * like vs_stream_extract_random, but only blocks whose AABB
+ * [key*block_size, key*block_size + block_size] passes every plane
+ * (nx*px + ny*py + nz*pz + d >= -margin at the positive vertex) are taken.
+ * planes_host = double[6][4] (Frustum._planes); evaluated in IEEE double in
+ * the reference's operation order (bit-identical decisions). */
+vs_status vs_stream_extract_visible(vs_table *const *sets_host, int n_sets,
+                                    uint64_t max_n, const uint64_t *seeds_host,
+                                    const double *planes_host, double margin, double block_size,
+                                    int32_t *keys_out, uint64_t *n_out, vs_stream_t stream);
+
+/* MC_BATCH payload (wire.py:292-299, _pack_batch(blocks, 2048)) straight from
+ * the device MC pool: out = u32 n, then n x {<3i key, 2048 MC bytes at
+ * mc_pool + pos[i]*2048}; out holds 4 + 2060*n bytes (4-byte aligned). */
+vs_status vs_mc_pack(const int32_t *keys, const int32_t *pos, uint64_t n,
+                     const uint8_t *mc_pool, uint8_t *out, vs_stream_t stream);
+
 /* Bulk remove of n keys from every one of n_sets tables (on_reset_blocks,
  * server.py:425-436).  erased may be NULL or device uint8[n_sets*n]. */
 vs_status vs_stream_remove_many(vs_table *const *sets_host, int n_sets,

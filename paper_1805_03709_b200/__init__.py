@@ -25,6 +25,7 @@ from .mc_encoding import (
     encode_blocks,
     encode_keys,
     neighbors,
+    pack_mc_batch,
     recompute_mc_block,
     recompute_mc_blocks,
 )
@@ -35,7 +36,7 @@ __all__ = [
     "BLOCK_EDGE", "BlockHashMap", "BlockHashSet", "BlockKey", "CapacityExhausted", "FreeListStack",
     "GpuServerCore", "McBlock", "McVoxel", "NativeUnavailable", "StreamSet", "TsdfBlock",
     "affected_mc_blocks", "apply_cutoff", "compact", "compute_mc_index", "encode_blocks", "encode_keys",
-    "extract_random_many", "fan_out", "hash_key", "hash_keys", "neighbors", "recompute_mc_block", "recompute_mc_blocks",
+    "extract_random_many", "fan_out", "hash_key", "hash_keys", "neighbors", "pack_mc_batch", "recompute_mc_block", "recompute_mc_blocks",
     "remove_everywhere",
 ]
 

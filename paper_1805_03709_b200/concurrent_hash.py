@@ -431,6 +431,35 @@ class BlockHashSet(_HashCore):
             n = int(self._n_dev.item())
             return out[:n]
 
+    def extract_visible_keys(self, max_n: int, planes, margin: float, block_size: float,
+                             seed: Optional[int] = None):
+        """extract_matching with the server's frustum-AABB predicate
+        (server.py:365-387) evaluated on the device -> int32[m,3] tensor.
+        planes: (6,4) float64 (Frustum._planes), margin/block_size: floats."""
+        torch = self._torch
+        with self._mutex:
+            if seed is None:
+                seed = random.getrandbits(64)
+            m = max(0, min(int(max_n), self.capacity))
+            if m == 0:
+                return torch.empty((0, 3), dtype=torch.int32, device=self.device)
+            pl = np.ascontiguousarray(np.asarray(planes, dtype=np.float64).reshape(24))
+            out = torch.empty((m, 3), dtype=torch.int32, device=self.device)
+            s = self._stream()
+            handles = (ctypes.c_void_p * 1)(self._h.value)
+            seeds = (ctypes.c_uint64 * 1)(seed & ((1 << 64) - 1))
+            check(self._lib.vs_stream_extract_visible(handles, 1, m, seeds, (ctypes.c_double * 24)(*pl),
+                                                      float(margin), float(block_size), ptr(out), ptr(self._n_dev),
+                                                      ctypes.c_void_p(s.cuda_stream)), "extract_visible")
+            self._done(s)
+            s.synchronize()
+            return out[: int(self._n_dev.item())]
+
+    def extract_visible(self, max_n: int, planes, margin: float, block_size: float) -> list[BlockKey]:
+        if max_n <= 0:
+            return []
+        return [tuple(k) for k in self.extract_visible_keys(max_n, planes, margin, block_size).cpu().tolist()]
+
     def extract_batch(self, max_n: int) -> list[BlockKey]:
         """Remove and return up to max_n keys from a rotating random start
         (concurrent_hash.py:366-374, 382-402)."""

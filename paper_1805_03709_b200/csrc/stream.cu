@@ -84,13 +84,43 @@ __global__ void k_fifo_tail(const __grid_constant__ FifoViews F, bool fifo, cons
   if (n_created) n_created[c] = cnt;
 }
 
-// extract_batch for several clients in ONE launch (concurrent_hash.py:382-402):
+// Frustum-AABB visibility of a block (server.py:375-387): every plane
+// (nx, ny, nz, d) must satisfy nx*px + ny*py + nz*pz + d >= -margin at the box
+// vertex furthest along the normal.  Evaluated in double with explicitly
+// rounded operations in the reference's (numpy float64) order, no FMA, so
+// the decision is bit-identical to the Python predicate.
+struct Frustum {
+  double p[6][4];
+  double margin;
+  double block;
+  int enabled;
+};
+
+__device__ __forceinline__ bool block_visible(const Frustum& F, int32_t kx, int32_t ky, int32_t kz) {
+  const double x0 = __dmul_rn((double)kx, F.block), y0 = __dmul_rn((double)ky, F.block),
+               z0 = __dmul_rn((double)kz, F.block);
+  const double x1 = __dadd_rn(x0, F.block), y1 = __dadd_rn(y0, F.block), z1 = __dadd_rn(z0, F.block);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const double nx = F.p[k][0], ny = F.p[k][1], nz = F.p[k][2], d = F.p[k][3];
+    const double px = nx >= 0.0 ? x1 : x0, py = ny >= 0.0 ? y1 : y0, pz = nz >= 0.0 ? z1 : z0;
+    double acc = __dadd_rn(__dmul_rn(nx, px), __dmul_rn(ny, py));
+    acc = __dadd_rn(acc, __dmul_rn(nz, pz));
+    acc = __dadd_rn(acc, d);
+    if (acc < -F.margin) return false;
+  }
+  return true;
+}
+
+// extract_batch / extract_matching(frustum) for several clients in ONE
+// launch (concurrent_hash.py:366-402):
 // one CTA per client scans live entries in position order from a seeded
 // random start (wrapping), keeps the first max_n, and removes them; the
 // vacated excess entries go straight back to the free list (no pops run in
 // this launch, so the push cannot race a pop).
 __global__ void __launch_bounds__(256) k_multi_extract(const __grid_constant__ SetViews V,
-                                                       const __grid_constant__ FifoViews S, uint64_t max_n,
+                                                       const __grid_constant__ FifoViews S,
+                                                       const __grid_constant__ Frustum F, uint64_t max_n,
                                                        int32_t* __restrict__ keys_out, uint64_t* __restrict__ n_out) {
   const int c = blockIdx.x;
   const TableView& T = V.v[c];
@@ -117,6 +147,7 @@ __global__ void __launch_bounds__(256) k_multi_extract(const __grid_constant__ S
     if (scanned + threadIdx.x < cap) {
       e = ld_entry(T.e + p);
       live = ((uint32_t)e.w & kOcc) != 0;
+      if (live && F.enabled) live = block_visible(F, e.x, e.y, e.z);
     }
     const uint32_t bal = __ballot_sync(0xffffffffu, live);
     if (lane_id() == 0) wcnt[warp] = __popc(bal);
@@ -347,9 +378,8 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
   return VS_OK;
 }
 
-vs_status vs_stream_extract_random(vs_table* const* sets_host, int n_sets, uint64_t max_n,
-                                   const uint64_t* seeds_host, int32_t* keys_out, uint64_t* n_out,
-                                   vs_stream_t stream) {
+static vs_status multi_extract(vs_table* const* sets_host, int n_sets, uint64_t max_n, const uint64_t* seeds_host,
+                               const Frustum& F, int32_t* keys_out, uint64_t* n_out, vs_stream_t stream) {
   SetViews V;
   if (!sets_host || !seeds_host || !n_out || (max_n && !keys_out)) {
     set_error("sets/seeds/keys_out/n_out must be non-NULL");
@@ -361,8 +391,62 @@ vs_status vs_stream_extract_random(vs_table* const* sets_host, int n_sets, uint6
   cudaStream_t s = (cudaStream_t)stream;
   FifoViews S{};
   for (int c = 0; c < n_sets; ++c) S.cap[c] = seeds_host[c];
-  { k_multi_extract<<<n_sets, 256, 0, s>>>(V, S, max_n, keys_out, n_out); vsb::count_launch(); }
-  VS_CK_LAUNCH("vs_stream_extract_random");
+  { k_multi_extract<<<n_sets, 256, 0, s>>>(V, S, F, max_n, keys_out, n_out); vsb::count_launch(); }
+  VS_CK_LAUNCH("vs_stream_extract");
+  return VS_OK;
+}
+
+// MC_BATCH payload (wire.py:292-299): u32 count, then per block the key as
+// <3i and its 2,048 MC bytes, gathered straight from the device MC pool.
+__global__ void k_mc_pack(const int32_t* __restrict__ keys, const int32_t* __restrict__ pos, uint64_t n,
+                          const uint32_t* __restrict__ pool, uint32_t* __restrict__ out) {
+  const uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r == 0 && lane == 0 && blockIdx.x == 0) out[0] = (uint32_t)n;
+  if (r >= n) return;
+  uint32_t* dst = out + 1 + r * (VS_MC_BLOCK_BYTES + 12) / 4;
+  if (lane < 3) dst[lane] = (uint32_t)keys[3 * r + lane];
+  const uint32_t* src = pool + (uint64_t)pos[r] * (VS_MC_BLOCK_BYTES / 4);
+#pragma unroll 4
+  for (int j = lane; j < VS_MC_BLOCK_BYTES / 4; j += 32) dst[3 + j] = __ldcs(src + j);
+}
+
+
+vs_status vs_stream_extract_random(vs_table* const* sets_host, int n_sets, uint64_t max_n,
+                                   const uint64_t* seeds_host, int32_t* keys_out, uint64_t* n_out,
+                                   vs_stream_t stream) {
+  Frustum F{};
+  return multi_extract(sets_host, n_sets, max_n, seeds_host, F, keys_out, n_out, stream);
+}
+
+vs_status vs_stream_extract_visible(vs_table* const* sets_host, int n_sets, uint64_t max_n,
+                                    const uint64_t* seeds_host, const double* planes_host, double margin,
+                                    double block_size, int32_t* keys_out, uint64_t* n_out, vs_stream_t stream) {
+  if (!planes_host) {
+    set_error("planes must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  Frustum F{};
+  for (int k = 0; k < 24; ++k) F.p[k / 4][k % 4] = planes_host[k];
+  F.margin = margin;
+  F.block = block_size;
+  F.enabled = 1;
+  return multi_extract(sets_host, n_sets, max_n, seeds_host, F, keys_out, n_out, stream);
+}
+
+vs_status vs_mc_pack(const int32_t* keys, const int32_t* pos, uint64_t n, const uint8_t* mc_pool, uint8_t* out,
+                     vs_stream_t stream) {
+  if (!out || (n && (!keys || !pos || !mc_pool))) {
+    set_error("keys/pos/mc_pool/out must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  if (((uintptr_t)out & 3u) || ((uintptr_t)mc_pool & 3u)) {
+    set_error("out and mc_pool must be 4-byte aligned");
+    return VS_ERR_INVALID;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  { k_mc_pack<<<grid_for(32 * (n ? n : 1), 256), 256, 0, s>>>(keys, pos, n, (const uint32_t*)mc_pool, (uint32_t*)out); vsb::count_launch(); }
+  VS_CK_LAUNCH("vs_mc_pack");
   return VS_OK;
 }
 

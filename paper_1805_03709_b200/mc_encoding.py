@@ -171,6 +171,22 @@ def compact(mc, counts, cell_cap: Optional[int] = None):
     return offsets, flat[:total], cells[:total]
 
 
+def pack_mc_batch(keys, pos, mc_pool):
+    """MC_BATCH payload (wire.py:292-299) straight from the device MC pool:
+    u32 count + per block <3i key + 2,048 MC bytes at mc_pool[pos].
+    Returns a device uint8 tensor of 4 + 2060*n bytes."""
+    torch = _lib.require_cuda()
+    dev = mc_pool.device
+    from .concurrent_hash import _as_keys
+
+    k = _as_keys(keys, dev)
+    p = pos.to(dev, torch.int32).contiguous()
+    n = k.shape[0]
+    out = torch.empty(4 + (MC_BLOCK_BYTES + 12) * n, dtype=torch.uint8, device=dev)
+    check(_lib.load().vs_mc_pack(ptr(k), ptr(p), n, ptr(mc_pool), ptr(out), _lib.stream_of(dev)), "mc_pack")
+    return out
+
+
 def _pool_from_blocks(torch, blocks, device):
     rows = np.stack([block_row(b) for b in blocks]) if blocks else np.zeros((1, TSDF_BLOCK_BYTES), np.uint8)
     return torch.from_numpy(rows).to(device)

@@ -21,7 +21,7 @@ from typing import Callable, Optional, Sequence
 from . import _lib
 from ._lib import check, ptr
 from .concurrent_hash import BlockHashSet, BlockKey, _as_keys
-from .mc_encoding import MC_BLOCK_BYTES, Q_BLOCK_BYTES, encode_keys
+from .mc_encoding import MC_BLOCK_BYTES, Q_BLOCK_BYTES, encode_keys, pack_mc_batch
 from .voxel_model import TSDF_BLOCK_BYTES
 
 _MAX_SETS_PER_LAUNCH = 32
@@ -116,6 +116,14 @@ class StreamSet:
 
     def extract_matching(self, max_n: int, predicate: Callable) -> list[BlockKey]:
         return self._set.extract_matching(max_n, predicate)
+
+    def extract_visible_first(self, max_n: int, planes, margin: float, block_size: float) -> list[BlockKey]:
+        """VISIBLE_FIRST (server.py:339-344): frustum-visible keys first, then
+        a random top-up so requests stay full-sized."""
+        keys = self._set.extract_visible(max_n, planes, margin, block_size)
+        if len(keys) < max_n:
+            keys.extend(self.extract_random(max_n - len(keys)))
+        return keys
 
     def extract_ordered(self, max_n: int) -> list[BlockKey]:
         keys = self.extract_ordered_keys(max_n)
@@ -354,6 +362,29 @@ class GpuServerCore:
         _, tpos = self.tsdf_map.erase_keys(k)
         _, mpos = self.mc_map.erase_keys(k)
         remove_everywhere(self.streams(), k)
+
+    def on_block_request(self, client_id: bytes, max_blocks: int, strategy: int, planes=None,
+                         margin: float = 0.0, block_size: float = 0.04) -> tuple[list, bytes]:
+        """server.py:334-363 without the transport: extract by strategy
+        (0 GENERATION_ORDER, 1 VISIBLE_FIRST, 2 RANDOM), drop keys deleted
+        meanwhile, and pack the MC_BATCH payload (wire.py:292-299) from the
+        device MC pool.  Returns (keys, payload bytes)."""
+        torch = self._torch
+        st = self.sessions[client_id]["stream"]
+        if strategy == 1:
+            keys = st.extract_visible_first(max_blocks, planes, margin, block_size)
+        elif strategy == 0:
+            keys = st.extract_ordered(max_blocks)
+        else:
+            keys = st.extract_random(max_blocks)
+        if not keys:
+            return [], (0).to_bytes(4, "little")
+        k = _as_keys(keys, self.device)
+        found, pos = self.mc_map.find_keys(k)
+        keep = found.bool()
+        payload = pack_mc_batch(k[keep], pos[keep], self.mc_pool)
+        kept = [kk for kk, f in zip(keys, found.cpu().tolist()) if f]
+        return kept, bytes(payload.cpu().numpy().tobytes())
 
     def mc_payload(self, key: BlockKey) -> Optional[bytes]:
         found, pos = self.mc_map.find_keys([key])

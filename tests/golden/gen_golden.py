@@ -334,6 +334,42 @@ def gen_server() -> None:
     (OUT / "server_seq.json").write_text(json.dumps(out))
 
 
+def gen_visibility() -> None:
+    """Server._visibility_predicate (server.py:365-387) decisions for block
+    keys around four camera poses, after the wire's float32 round trip."""
+    from voxelstream.geometry import CameraIntrinsics, Frustum, Pose
+
+    s = srv_mod.Server(srv_mod.ServerConfig(buckets=1 << 10, excess=1 << 10, voxel_size=0.01))
+    rng = np.random.default_rng(12)
+    planes, margins, blocks, keys_all, vis_all, poses, intrs = [], [], [], [], [], [], []
+    for trial in range(4):
+        eye = rng.uniform(-1, 1, 3)
+        pose = Pose.look_at(eye, eye + rng.normal(size=3))
+        pose_f = tuple(float(v) for v in np.concatenate([pose.rotation.reshape(-1), pose.translation]))
+        intr = (float(rng.uniform(30, 80)), float(rng.uniform(30, 80)), 40.0, 30.0, 0.05, float(rng.uniform(1, 3)))
+        req = wire.decode_message(wire.encode_message(
+            wire.BlockRequest(64, wire.Strategy.VISIBLE_FIRST, pose_f, intr), 0))
+        pred = s._visibility_predicate(req)
+        block = 8 * 0.01  # BLOCK_EDGE * voxel_size (server.py:366-367)
+        fx, fy, cx, cy, near, far = req.intrinsics
+        fr = Frustum(Pose.from_floats(req.pose), CameraIntrinsics(fx=fx, fy=fy, cx=cx, cy=cy, width=int(2 * cx) or 640,
+                                                                   height=int(2 * cy) or 480),
+                     near=max(near, 1e-3), far=far, margin=block)
+        c = np.floor(eye / block).astype(np.int64)
+        keys = (c + rng.integers(-45, 46, (20000, 3))).astype(np.int32)
+        vis = np.array([pred(tuple(int(v) for v in k)) for k in keys], dtype=bool)
+        planes.append(fr._planes)
+        margins.append(fr.margin)
+        blocks.append(block)
+        keys_all.append(keys)
+        vis_all.append(vis)
+        poses.append(req.pose)
+        intrs.append(req.intrinsics)
+    np.savez_compressed(OUT / "visibility.npz", planes=np.stack(planes), margin=np.array(margins),
+                        block=np.array(blocks), keys=np.stack(keys_all), visible=np.stack(vis_all),
+                        pose=np.array(poses), intrinsics=np.array(intrs))
+
+
 def main() -> None:
     gen_hash_kat()
     gen_hash_seq()
@@ -343,6 +379,7 @@ def main() -> None:
     gen_mc_sphere()
     gen_stream()
     gen_server()
+    gen_visibility()
     for p in sorted(OUT.iterdir()):
         if p.suffix in (".json", ".npz"):
             print(f"{p.name:24s} {p.stat().st_size:>9d} B")

@@ -217,3 +217,56 @@ def test_extract_random_many_properties(dev):
         assert set(s.snapshot()) == pre[i] - set(got)
         a = s._set.audit()
         assert a["duplicates"] == 0 and a["free"] + a["reachable_excess"] == s._set.excess_capacity
+
+
+def test_visible_first_predicate_bit_exact_with_reference(dev, golden):
+    """Device frustum-AABB decisions == Server._visibility_predicate (recorded
+    from the reference after the wire's float32 round trip)."""
+    from paper_1805_03709_b200 import BlockHashSet
+
+    d = np.load(golden / "visibility.npz")
+    for t in range(d["keys"].shape[0]):
+        keys = d["keys"][t]
+        uniq, first = np.unique(keys, axis=0, return_index=True)
+        vis = d["visible"][t][first]
+        s = BlockHashSet(1 << 15, 1 << 15)
+        s.insert_keys(uniq)
+        got = s.extract_visible(len(uniq), d["planes"][t], float(d["margin"][t]), float(d["block"][t]))
+        want = {tuple(k) for k, v in zip(uniq.tolist(), vis) if v}
+        assert set(got) == want and len(got) == len(want), t
+        assert s.approx_size() == len(uniq) - len(want)
+        # bounded request: max_n visible keys, all visible, distinct
+        s2 = BlockHashSet(1 << 15, 1 << 15)
+        s2.insert_keys(uniq)
+        some = s2.extract_visible(7, d["planes"][t], float(d["margin"][t]), float(d["block"][t]))
+        assert len(some) == min(7, len(want)) and set(some) <= want
+
+
+def test_block_request_strategies_and_mc_batch_payload(dev, golden):
+    """Server.on_block_request (server.py:334-363) on the GPU core: strategies
+    and the MC_BATCH payload layout (wire.py:292-299)."""
+    import struct
+
+    from paper_1805_03709_b200 import GpuServerCore
+
+    d = np.load(golden / "server_blocks.npz")
+    core = GpuServerCore(1 << 12, 1 << 12, stream_buckets=1 << 10, stream_excess=1 << 10)
+    cid = b"c" * 16
+    st = core.attach(cid)
+    core.on_tsdf_batch(d["keys"], d["blocks"])
+    pending = set(st.snapshot())
+    fifo = [k for k in st.fifo_entries()]
+    keys, payload = core.on_block_request(cid, 10, 0)  # generation order
+    assert keys == fifo[:10]
+    n = struct.unpack_from("<I", payload, 0)[0]
+    assert n == len(keys) and len(payload) == 4 + 2060 * n
+    for i, k in enumerate(keys):
+        off = 4 + 2060 * i
+        assert struct.unpack_from("<3i", payload, off) == k
+        assert payload[off + 12: off + 2060] == core.mc_payload(k)
+    keys2, _ = core.on_block_request(cid, 25, 2)  # random
+    assert len(keys2) == 25 and set(keys2) <= pending - set(keys)
+    v = np.load(golden / "visibility.npz")
+    keys3, payload3 = core.on_block_request(cid, 30, 1, v["planes"][0], float(v["margin"][0]), float(v["block"][0]))
+    assert len(keys3) == 30 and len(set(keys3)) == 30  # visible first, topped up
+    assert set(st.snapshot()) == pending - set(keys) - set(keys2) - set(keys3)
