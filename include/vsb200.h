@@ -239,6 +239,14 @@ vs_status vs_stream_extract_visible(vs_table *const *sets_host, int n_sets,
                                     const double *planes_host, double margin, double block_size,
                                     int32_t *keys_out, uint64_t *n_out, vs_stream_t stream);
 
+/* TSDF ingest: tsdf_map.put for n wire-layout rows (server.py:300-303,
+ * voxel_model.py:62-72): insert the keys into `t` (VS_ERR_CAPACITY rules of
+ * vs_table_insert), then copy each row into pool + index[i]*6144 with the
+ * LAST op of duplicate keys winning (sequential put order).  index[i] =
+ * position (device int32[n]).  rows / pool 16-byte aligned. */
+vs_status vs_tsdf_put(vs_table *t, const int32_t *keys, const uint8_t *rows, uint64_t n,
+                      uint8_t *pool, int32_t *index, vs_stream_t stream);
+
 /* MC_BATCH payload (wire.py:292-299, _pack_batch(blocks, 2048)) straight from
  * the device MC pool: out = u32 n, then n x {<3i key, 2048 MC bytes at
  * mc_pool + pos[i]*2048}; out holds 4 + 2060*n bytes (4-byte aligned). */

@@ -79,6 +79,7 @@ SIGNATURES: dict[str, tuple] = {
                                          ctypes.POINTER(ctypes.c_double * 24), ctypes.c_double, ctypes.c_double,
                                          _vp, _vp, _vp]),
     "vs_mc_pack": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp]),
+    "vs_tsdf_put": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),
     "vs_stream_remove_many": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _vp, _u64, _vp, _vp]),
     "vs_stream_extract_ordered": (_i32, [_vp, _vp, _u64, _pu64, _u64, _u64, _vp, _pu64, _vp, _vp]),
 }

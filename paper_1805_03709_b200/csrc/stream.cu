@@ -396,6 +396,30 @@ static vs_status multi_extract(vs_table* const* sets_host, int n_sets, uint64_t 
   return VS_OK;
 }
 
+// TSDF ingest (server.py:300-303: tsdf_map.put(key, TsdfBlock.from_bytes(raw))
+// per block, latest write wins): after the batched insert, the LAST op per
+// position wins the claim word (epoch-tagged atomicMin of ~op), then the
+// winners copy their 6,144-byte wire rows into the pool (one warp per row,
+// 16-byte vector copies).
+__global__ void k_put_claim(TableView T, const int32_t* __restrict__ pos, uint64_t n) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || pos[i] < 0) return;
+  atomicMin(&T.claim[pos[i]], T.tag | (unsigned long long)(0xFFFFFFFFu - (uint32_t)i));
+}
+
+__global__ void k_put_rows(TableView T, const int32_t* __restrict__ pos, uint64_t n, const uint4* __restrict__ rows,
+                           uint4* __restrict__ pool) {
+  const uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int32_t p = pos[i];
+  if (p < 0 || T.claim[p] != (T.tag | (unsigned long long)(0xFFFFFFFFu - (uint32_t)i))) return;
+  const uint4* src = rows + i * (VS_TSDF_BLOCK_BYTES / 16);
+  uint4* dst = pool + (uint64_t)p * (VS_TSDF_BLOCK_BYTES / 16);
+#pragma unroll 4
+  for (int j = lane; j < VS_TSDF_BLOCK_BYTES / 16; j += 32) dst[j] = __ldcs(src + j);
+}
+
 // MC_BATCH payload (wire.py:292-299): u32 count, then per block the key as
 // <3i and its 2,048 MC bytes, gathered straight from the device MC pool.
 __global__ void k_mc_pack(const int32_t* __restrict__ keys, const int32_t* __restrict__ pos, uint64_t n,
@@ -432,6 +456,31 @@ vs_status vs_stream_extract_visible(vs_table* const* sets_host, int n_sets, uint
   F.block = block_size;
   F.enabled = 1;
   return multi_extract(sets_host, n_sets, max_n, seeds_host, F, keys_out, n_out, stream);
+}
+
+vs_status vs_tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows, uint64_t n, uint8_t* pool,
+                      int32_t* index, vs_stream_t stream) {
+  if (!t || !index || (n && (!keys || !rows || !pool))) {
+    set_error("table/keys/rows/pool/index must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  if (((uintptr_t)rows & 15u) || ((uintptr_t)pool & 15u)) {
+    set_error("rows and pool must be 16-byte aligned");
+    return VS_ERR_INVALID;
+  }
+  if (n == 0) return VS_OK;
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t* created = nullptr;
+  VS_CK(cudaMallocAsync((void**)&created, n, s));
+  vs_status st = vs_table_insert(t, keys, n, created, index, stream);
+  cudaFreeAsync(created, s);
+  if (st != VS_OK) return st;
+  const TableView v = t->next_view();
+  { k_put_claim<<<grid_for(n, 256), 256, 0, s>>>(v, index, n); vsb::count_launch(); }
+  { k_put_rows<<<grid_for(32 * n, 256), 256, 0, s>>>(v, index, n, (const uint4*)rows, (uint4*)pool); vsb::count_launch(); }
+  VS_CK_LAUNCH("vs_tsdf_put");
+  return VS_OK;
 }
 
 vs_status vs_mc_pack(const int32_t* keys, const int32_t* pos, uint64_t n, const uint8_t* mc_pool, uint8_t* out,

@@ -323,15 +323,17 @@ class GpuServerCore:
         U = k.shape[0]
         if U == 0:
             return k
-        # tsdf_map.put: latest write wins (sequential put order)
+        # tsdf_map.put: exact sequential failure semantics first (the reference
+        # raises at the first block that finds the excess list empty), then the
+        # fused put: latest write wins (sequential put order)
         self.tsdf_map.insert_many_exact(k)
-        _, pos = self.tsdf_map.find_keys(k)
-        pos = pos.to(torch.int64)
-        last = torch.full((self.tsdf_map.capacity,), -1, dtype=torch.int64, device=dev)
-        order = torch.arange(U, device=dev)
-        last.scatter_reduce_(0, pos, order, reduce="amax")
-        win = last[pos] == order
-        self.tsdf_pool[pos[win]] = rows[win]
+        pos = torch.empty(U, dtype=torch.int32, device=dev)
+        rows = rows.contiguous()
+        st = _order_streams([self.tsdf_map])
+        check(_lib.load().vs_tsdf_put(self.tsdf_map.handle, ptr(k), ptr(rows), U, ptr(self.tsdf_pool), ptr(pos),
+                                      ctypes.c_void_p(st.cuda_stream)), "tsdf_put")
+        _mark_done([self.tsdf_map], st)
+        self.tsdf_map.check_capacity()
         # affected = ordered first-occurrence dedup of the 8 affected blocks per key
         if 8 * U > self._dedup.bucket_count:
             self._dedup = BlockHashSet(16 * U, 16 * U, device=dev)

@@ -270,3 +270,21 @@ def test_block_request_strategies_and_mc_batch_payload(dev, golden):
     keys3, payload3 = core.on_block_request(cid, 30, 1, v["planes"][0], float(v["margin"][0]), float(v["block"][0]))
     assert len(keys3) == 30 and len(set(keys3)) == 30  # visible first, topped up
     assert set(st.snapshot()) == pending - set(keys) - set(keys2) - set(keys3)
+
+
+def test_tsdf_ingest_latest_write_wins(dev):
+    """tsdf_map.put semantics (server.py:300-303, tests/test_server.py
+    test_latest_write_wins) incl. duplicate keys inside one batch."""
+    from paper_1805_03709_b200 import GpuServerCore
+
+    rng = np.random.default_rng(1)
+    core = GpuServerCore(1 << 10, 1 << 10, stream_buckets=1 << 9, stream_excess=1 << 9)
+    keys = np.array([[2, 2, 2], [3, 2, 2], [2, 2, 2], [4, 4, 4], [2, 2, 2]], np.int32)
+    rows = rng.integers(0, 256, (5, 6144), dtype=np.uint8)
+    core.on_tsdf_batch(keys, rows)
+    assert core.tsdf_payload((2, 2, 2)) == rows[4].tobytes()
+    assert core.tsdf_payload((3, 2, 2)) == rows[1].tobytes()
+    rows2 = rng.integers(0, 256, (1, 6144), dtype=np.uint8)
+    core.on_tsdf_batch(keys[:1], rows2)
+    assert core.tsdf_payload((2, 2, 2)) == rows2[0].tobytes()
+    assert core.tsdf_map.approx_size() == 3
