@@ -31,11 +31,15 @@ struct __align__(16) Entry {
   uint32_t meta;
 };
 
+constexpr uint32_t kSizeStripes = 32;  // live-key counter stripes
+constexpr uint32_t kSizeStride = 16;   // long longs between counter stripes (128 B)
+
 // Device control block of one table.
 struct Ctl {
-  unsigned long long size;  // live keys (approx_size)
-  unsigned int error;       // sticky: bit 0 = capacity exhausted
+  unsigned int error;  // sticky: bit 0 = capacity exhausted
   unsigned int pad;
+  unsigned long long size_sum;  // scratch for vs_table_size
+  long long size[kSizeStripes * kSizeStride];  // live keys = sum of the stripes (approx_size)
 };
 
 constexpr uint32_t kMaxStripes = 32;  // free-list stripes

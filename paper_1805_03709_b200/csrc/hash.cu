@@ -97,10 +97,8 @@ __global__ void k_reset_ctl(TableView T) {
     if (c > (long long)T.stripe_cap) c = T.stripe_cap;
     T.tops[(size_t)s * kTopStride] = c < 0 ? 0 : c;
   }
-  if (threadIdx.x == 0) {
-    T.ctl->size = 0;
-    T.ctl->error = 0;
-  }
+  for (uint32_t k = threadIdx.x; k < kSizeStripes; k += blockDim.x) T.ctl->size[k * kSizeStride] = 0;
+  if (threadIdx.x == 0) T.ctl->error = 0;
 }
 
 __global__ void __launch_bounds__(kOpBlock) k_insert(TableView T, const int32_t* __restrict__ keys, uint64_t n,
@@ -358,6 +356,12 @@ __global__ void __launch_bounds__(256) k_chunk_write(TableView T, uint32_t cap, 
     running += total;
     __syncthreads();
   }
+}
+
+__global__ void k_sum_size(Ctl* ctl) {
+  long long v = threadIdx.x < kSizeStripes ? ctl->size[threadIdx.x * kSizeStride] : 0;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (threadIdx.x == 0) ctl->size_sum = (unsigned long long)(v < 0 ? 0 : v);
 }
 
 __global__ void k_copy_total(const uint64_t* __restrict__ offsets, uint32_t nchunks, uint64_t* __restrict__ n_dev) {
@@ -743,9 +747,10 @@ vs_status vs_table_size(vs_table* t, uint64_t* size_dev, uint64_t* size_host, vs
   }
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (size_dev) VS_CK(cudaMemcpyAsync(size_dev, &t->ctl->size, 8, cudaMemcpyDeviceToDevice, s));
+  { k_sum_size<<<1, 32, 0, s>>>(t->ctl); vsb::count_launch(); }
+  if (size_dev) VS_CK(cudaMemcpyAsync(size_dev, &t->ctl->size_sum, 8, cudaMemcpyDeviceToDevice, s));
   if (size_host) {
-    VS_CK(cudaMemcpyAsync(size_host, &t->ctl->size, 8, cudaMemcpyDeviceToHost, s));
+    VS_CK(cudaMemcpyAsync(size_host, &t->ctl->size_sum, 8, cudaMemcpyDeviceToHost, s));
     VS_CK(cudaStreamSynchronize(s));
   }
   return VS_OK;

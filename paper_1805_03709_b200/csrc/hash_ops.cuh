@@ -270,20 +270,16 @@ __device__ __forceinline__ void post_op(const TableView& T, const int32_t* __res
   }
 }
 
-// CTA-aggregated update of the live-key counter: one atomic per CTA.  Every
-// thread of the CTA must call it exactly once (out-of-range threads with 0).
+// Warp-aggregated update of the live-key counter into one of kSizeStripes
+// counters (separate 128-B lines): no CTA barrier, so a warp retires as soon
+// as its own ops are done.  Every lane of the warp must call it once.
 __device__ __forceinline__ void add_size_cta(const TableView& T, int delta) {
-  __shared__ int red[32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) delta += __shfl_xor_sync(0xffffffffu, delta, o);
-  const int w = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane_id() == 0) red[w] = delta;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int s = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-    if (s) atomicAdd(&T.ctl->size, (unsigned long long)(long long)s);
+  __syncwarp();
+  delta = __reduce_add_sync(0xffffffffu, delta);
+  if (lane_id() == 0 && delta != 0) {
+    const uint32_t w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    atomicAdd((unsigned long long*)&T.ctl->size[(w % kSizeStripes) * kSizeStride],
+              (unsigned long long)(long long)delta);
   }
 }
 
