@@ -494,6 +494,8 @@ def run_stream(args, dev):
     done_removes.zero_()
     ticks = max(args.stream_ticks, 20)
     torch.cuda.synchronize()
+    clocks = Clocks(dev.index).start()
+    time.sleep(0.12)
     t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with _lib.Profile() as prof:
@@ -503,6 +505,7 @@ def run_stream(args, dev):
         e1.record()
         torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     ops["remove"] += int(done_removes.item())
     total = ops["insert"] + ops["remove"]
@@ -513,7 +516,7 @@ def run_stream(args, dev):
             "value": total / (ms / 1e3) / 1e6, "unit": "M key-ops/s", "ticks": ticks,
             "ms_per_tick": ms / ticks, "wall_s": wall, "fill_16_clients_ms": fill_ms,
             "fill_value": C * M / (fill_ms / 1e3) / 1e6, "inserts": ops["insert"], "removes": ops["remove"],
-            "ok": ok, "gpu_launches": prof.launches,
+            "ok": ok, "gpu_launches": prof.launches, "clocks": clk,
             "note": "inserts count created-or-not key inserts into every set; removes = extracted + reset keys; "
                     "one host sync per tick (affected count)"}
 

@@ -544,6 +544,20 @@ vs_status vs_hash_keys(const int32_t* keys, uint64_t n, uint32_t bucket_count, u
   return VS_OK;
 }
 
+// Scratch buffers of the batched calls come from the stream-ordered
+// allocator; keep freed pool memory mapped (release threshold = max) so a
+// large call does not pay page mapping again after every synchronisation.
+static void keep_pool_resident(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 vs_status vs_table_create(uint64_t bucket_count, uint64_t excess_capacity, int device, vs_table** out) {
   if (!out) {
     set_error("out is NULL");
@@ -563,6 +577,7 @@ vs_status vs_table_create(uint64_t bucket_count, uint64_t excess_capacity, int d
     return VS_ERR_INVALID;
   }
   DeviceGuard g(device);
+  keep_pool_resident(device);
   vs_table* t = new vs_table();
   t->device = device;
   t->n = (uint32_t)bucket_count;
