@@ -30,7 +30,10 @@ vs_status cuda_status(cudaError_t err, const char* what) {
   return VS_ERR_CUDA;
 }
 
-constexpr int kOpBlock = 256;
+#ifndef VSB_HASH_BLOCK
+#define VSB_HASH_BLOCK 128
+#endif
+constexpr int kOpBlock = VSB_HASH_BLOCK;  // threads per CTA of the op kernels
 
 // ------------------------------------------------------- launch accounting
 
@@ -173,27 +176,26 @@ __global__ void __launch_bounds__(kOpBlock) k_erase_win(TableView T, const int32
   add_size_cta(T, delta);
 }
 
-// One mixed op (insert / find / erase).  Returns the size delta.
-__device__ __forceinline__ int apply_one(const TableView& T, const int32_t* __restrict__ keys,
-                                         const uint8_t* __restrict__ ops, uint64_t i, uint8_t* __restrict__ result,
+// One mixed op (insert / find / erase) with its bucket entry already loaded.
+// Returns the size delta.
+__device__ __forceinline__ int apply_one(const TableView& T, int32_t x, int32_t y, int32_t z, uint8_t op, uint64_t i,
+                                         uint32_t b, const int4& pre, uint8_t* __restrict__ result,
                                          int32_t* __restrict__ index) {
-  const int32_t x = ld_stream(keys + 3 * i), y = ld_stream(keys + 3 * i + 1), z = ld_stream(keys + 3 * i + 2);
-  const uint8_t op = ld_stream(ops + i);
   int32_t pos;
   uint8_t res;
   int delta = 0;
   if (op == VS_OP_INSERT) {
-    const InsertResult r = insert_key(T, x, y, z, (int32_t)i);
+    const InsertResult r = insert_key(T, x, y, z, (int32_t)i, &pre);
     pos = r.pos;
     res = r.created;
     delta = r.created;
   } else if (op == VS_OP_ERASE) {
-    pos = erase_key(T, x, y, z);
+    pos = erase_key(T, x, y, z, &pre);
     res = pos >= 0;
     delta = -(int)res;
   } else {
     uint32_t meta;
-    pos = find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
+    pos = find_pos_from(T, x, y, z, b, pre, &meta);
     res = pos >= 0;
   }
   __stcs(result + i, res);
@@ -201,44 +203,44 @@ __device__ __forceinline__ int apply_one(const TableView& T, const int32_t* __re
   return delta;
 }
 
-// Mixed batch.  VSB_HASH_PERSIST: a persistent grid whose lanes loop over
-// ops, so a lane that finishes a short op (a find) starts the next one
-// instead of idling until the slowest op of its CTA (a contended insert) is done.
-#ifndef VSB_HASH_PERSIST
-#define VSB_HASH_PERSIST 0
+// Mixed batch.  Each thread owns kOpsPerThread ops (kOpBlock apart, so loads
+// stay coalesced) and issues all their bucket-entry loads before walking
+// any chain: more independent misses in flight per SM.
+#ifndef VSB_HASH_OPS_PER_THREAD
+#define VSB_HASH_OPS_PER_THREAD 1
 #endif
+constexpr int kOpsPerThread = VSB_HASH_OPS_PER_THREAD;
+
 __global__ void __launch_bounds__(kOpBlock) k_apply(TableView T, const int32_t* __restrict__ keys,
                                                     const uint8_t* __restrict__ ops, uint64_t n,
                                                     uint8_t* __restrict__ result, int32_t* __restrict__ index) {
+  const uint64_t base = (uint64_t)blockIdx.x * (kOpBlock * kOpsPerThread) + threadIdx.x;
+  int32_t x[kOpsPerThread], y[kOpsPerThread], z[kOpsPerThread];
+  uint8_t op[kOpsPerThread];
+  uint32_t b[kOpsPerThread];
+  int4 pre[kOpsPerThread];
+#pragma unroll
+  for (int k = 0; k < kOpsPerThread; ++k) {
+    const uint64_t i = base + (uint64_t)k * kOpBlock;
+    if (i < n) {
+      x[k] = ld_stream(keys + 3 * i);
+      y[k] = ld_stream(keys + 3 * i + 1);
+      z[k] = ld_stream(keys + 3 * i + 2);
+      op[k] = ld_stream(ops + i);
+      b[k] = bucket_of(T, x[k], y[k], z[k]);
+      pre[k] = ld_bucket(T.e + b[k]);
+    }
+  }
   int delta = 0;
-#if VSB_HASH_PERSIST
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-#pragma unroll 1
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    delta += apply_one(T, keys, ops, i, result, index);
-#else
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) delta = apply_one(T, keys, ops, i, result, index);
-#endif
+#pragma unroll
+  for (int k = 0; k < kOpsPerThread; ++k) {
+    const uint64_t i = base + (uint64_t)k * kOpBlock;
+    if (i < n) delta += apply_one(T, x[k], y[k], z[k], op[k], i, b[k], pre[k], result, index);
+  }
   add_size_cta(T, delta);
 }
 
-static unsigned apply_grid(uint64_t n) {
-#if VSB_HASH_PERSIST
-  static int resident = 0;
-  if (resident == 0) {
-    int dev = 0, sms = 148, per_sm = 8;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply, kOpBlock, 0);
-    resident = sms * (per_sm > 0 ? per_sm : 1);
-  }
-  const unsigned g = grid_for(n, kOpBlock);
-  return g < (unsigned)resident ? g : (unsigned)resident;
-#else
-  return grid_for(n, kOpBlock);
-#endif
-}
+static unsigned apply_grid(uint64_t n) { return grid_for(n, kOpBlock * kOpsPerThread); }
 
 // Post pass after k_insert / k_apply: created flags to the lowest op index
 // among in-batch duplicates (sequential replay), FRESH cleared, and the

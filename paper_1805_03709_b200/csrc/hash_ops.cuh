@@ -101,9 +101,10 @@ __device__ __forceinline__ void push_free(const TableView& T, uint32_t e) {
 
 // Lock-free retrieval (_find + _scan_chain, concurrent_hash.py:127-157).
 // Returns the position or -1; *meta_out = meta of the matching entry.
-__device__ __forceinline__ int32_t find_pos(const TableView& T, int32_t x, int32_t y, int32_t z, uint32_t b,
-                                           uint32_t* meta_out) {
-  int4 s = ld_bucket(T.e + b);  // first hop: the bucket entry (L2 evict_last)
+// ... starting from an already loaded bucket entry `s` (lets a thread
+// issue the first loads of several ops before walking any of them).
+__device__ __forceinline__ int32_t find_pos_from(const TableView& T, int32_t x, int32_t y, int32_t z, uint32_t b,
+                                                int4 s, uint32_t* meta_out) {
   uint32_t e = b;
 #pragma unroll 1
   for (;;) {
@@ -116,6 +117,11 @@ __device__ __forceinline__ int32_t find_pos(const TableView& T, int32_t x, int32
     e = next_pos(T, meta);
     s = ld_entry(T.e + e);
   }
+}
+
+__device__ __forceinline__ int32_t find_pos(const TableView& T, int32_t x, int32_t y, int32_t z, uint32_t b,
+                                           uint32_t* meta_out) {
+  return find_pos_from(T, x, y, z, b, ld_bucket(T.e + b), meta_out);  // first hop: L2 evict_last
 }
 
 // A duplicate insert of an entry created in this launch (FRESH): mark the
@@ -134,13 +140,17 @@ struct InsertResult {
 
 // _insert_pos (concurrent_hash.py:159-208): loop of non-blocking attempts;
 // each retry starts with a fresh lock-free retrieval.
-__device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x, int32_t y, int32_t z, int32_t op) {
+// `pre` (optional): the bucket entry loaded ahead of time (first attempt only;
+// a stale snapshot is harmless, every mutation re-validates under the lock).
+__device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x, int32_t y, int32_t z, int32_t op,
+                                                   const int4* pre = nullptr) {
   const uint32_t b = bucket_of(T, x, y, z);
   uint32_t* bmeta = &T.e[b].meta;
 #pragma unroll 1
   for (int attempt = 0;; ++attempt) {
     uint32_t fmeta;
-    const int32_t pos = find_pos(T, x, y, z, b, &fmeta);
+    const int32_t pos = (attempt == 0 && pre) ? find_pos_from(T, x, y, z, b, *pre, &fmeta)
+                                              : find_pos(T, x, y, z, b, &fmeta);
     if (pos >= 0) {
       if (fmeta & kFresh) claim_min(T, pos, op);
       return {pos, 0};
@@ -202,13 +212,16 @@ __device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x
 
 // remove (concurrent_hash.py:251-295).  Returns the vacated position or -1.
 // Vacated EXCESS positions are recycled by the caller's recycle launch.
-__device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int32_t y, int32_t z) {
+__device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int32_t y, int32_t z,
+                                            const int4* pre = nullptr) {
   const uint32_t b = bucket_of(T, x, y, z);
   uint32_t* bmeta = &T.e[b].meta;
 #pragma unroll 1
   for (int attempt = 0;; ++attempt) {
     uint32_t fmeta;
-    if (find_pos(T, x, y, z, b, &fmeta) < 0) return -1;
+    const int32_t fp = (attempt == 0 && pre) ? find_pos_from(T, x, y, z, b, *pre, &fmeta)
+                                             : find_pos(T, x, y, z, b, &fmeta);
+    if (fp < 0) return -1;
     const uint32_t old = atom_or_relaxed(bmeta, kLock);
     if (old & kLock) {
       if (attempt > 4) __nanosleep(64);
