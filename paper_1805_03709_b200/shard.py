@@ -48,26 +48,40 @@ class ShardedBlockHashSet:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.backend = dist.get_backend(group)
+        self._stage = False
+
+    def _a2a(self, out, inp, out_splits=None, in_splits=None):
+        """all_to_all_single; staged through host memory when the backend
+        cannot move device tensors (gloo: multi-rank tests on one GPU)."""
+        import torch.distributed as dist
+
+        if self._stage:
+            o = out.cpu()
+            dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits, group=self.group)
+            out.copy_(o)
+        else:
+            dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
 
     def apply(self, keys, ops, device: Optional[object] = None):
         """Mixed batch (ops 0 insert / 1 find / 2 erase) of THIS rank; returns
         the per-op results in input order.  Collective: every rank calls it."""
         import torch
-        import torch.distributed as dist
 
         dev = keys.device
+        self._stage = dev.type == "cuda" and self.backend == "gloo"
         own = owner_of(keys, self.world)
         order = torch.argsort(own, stable=True)
         send_counts = torch.bincount(own, minlength=self.world)
         recv_counts = torch.empty_like(send_counts)
-        dist.all_to_all_single(recv_counts, send_counts, group=self.group)
+        self._a2a(recv_counts, send_counts)
         sc, rc = send_counts.tolist(), recv_counts.tolist()
         payload = torch.cat([keys[order].to(torch.int32), ops[order].to(torch.int32)[:, None]], dim=1).contiguous()
         recv = torch.empty((sum(rc), 4), dtype=torch.int32, device=dev)
-        dist.all_to_all_single(recv, payload, rc, sc, group=self.group)
+        self._a2a(recv, payload, rc, sc)
         res, _ = self.local.apply(recv[:, :3].contiguous(), recv[:, 3].to(torch.uint8))
         back = torch.empty(keys.shape[0], dtype=torch.uint8, device=dev)
-        dist.all_to_all_single(back, res.to(torch.uint8).contiguous(), sc, rc, group=self.group)
+        self._a2a(back, res.to(torch.uint8).contiguous(), sc, rc)
         out = torch.empty_like(back)
         out[order] = back
         return out
@@ -77,7 +91,7 @@ class ShardedBlockHashSet:
         import torch.distributed as dist
 
         n = torch.tensor([self.local.approx_size()], dtype=torch.int64)
-        if dist.get_backend(self.group) == "nccl":
+        if self.backend == "nccl":
             n = n.cuda()
         dist.all_reduce(n, group=self.group)
         return int(n.item())
