@@ -120,6 +120,14 @@ vs_status vs_table_apply(vs_table *t, const int32_t *keys, const uint8_t *ops,
                          uint64_t n, uint8_t *result, int32_t *index,
                          vs_stream_t stream);
 
+/* SYNCHRONOUS single-key op (the reference's per-key API: insert / remove /
+ * __contains__, concurrent_hash.py:297-298,361-364,251-295) through pinned
+ * staging: key_host[3] in, *result_host (created/found/erased) and
+ * *index_host out.  An insert that finds the excess list empty returns
+ * VS_ERR_CAPACITY with the table unchanged. */
+vs_status vs_table_single(vs_table *t, int op, const int32_t key_host[3],
+                          uint8_t *result_host, int32_t *index_host, vs_stream_t stream);
+
 /* SYNCHRONOUS: returns VS_ERR_CAPACITY (and clears the flag) if any insert
  * since the last check hit an empty free list, else VS_OK. */
 vs_status vs_table_check(vs_table *t, vs_stream_t stream);

@@ -60,6 +60,8 @@ SIGNATURES: dict[str, tuple] = {
     "vs_table_erase": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp]),
     "vs_table_apply": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),
     "vs_table_check": (_i32, [_vp, _vp]),
+    "vs_table_single": (_i32, [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int32 * 3),
+                               ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(ctypes.c_int32), _vp]),
     "vs_table_size": (_i32, [_vp, _vp, _pu64, _vp]),
     "vs_table_free_count": (_i32, [_vp, _pu64, _vp]),
     "vs_table_clear": (_i32, [_vp, _vp]),

@@ -142,13 +142,7 @@ class _HashCore:
         self._h = handle
         self._values: Optional[list[Any]] = [None] * self.capacity if store_values else None
         self._mutex = threading.RLock()
-        self._event = None
-        # pinned staging for the per-key compatibility path
-        self._k_host = torch.empty((1, 3), dtype=torch.int32, pin_memory=True)
-        self._k_dev = torch.empty((1, 3), dtype=torch.int32, device=self.device)
-        self._f_dev = torch.empty(1, dtype=torch.uint8, device=self.device)
-        self._i_dev = torch.empty(1, dtype=torch.int32, device=self.device)
-        self._out_host = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        self._last_stream = None
         self._n_dev = torch.empty(1, dtype=torch.int64, device=self.device)
 
     # -- lifetime ----------------------------------------------------------
@@ -167,17 +161,21 @@ class _HashCore:
         return self._h
 
     # -- stream ordering: all launches on one table are serialised --------
+    # Launches are stream-ordered per table.  When a call comes from a
+    # different stream than the table's last launch, the new stream waits for
+    # an event recorded on the old one; on the same stream nothing is needed.
 
     def _stream(self):
         s = self._torch.cuda.current_stream(self.device)
-        if self._event is not None:
-            s.wait_event(self._event)
+        last = self._last_stream
+        if last is not None and last != s:
+            ev = self._torch.cuda.Event()
+            ev.record(last)
+            s.wait_event(ev)
         return s
 
     def _done(self, s) -> None:
-        ev = self._torch.cuda.Event()
-        ev.record(s)
-        self._event = ev
+        self._last_stream = s
 
     def _keys(self, keys):
         return _as_keys(keys, self.device)
@@ -308,25 +306,26 @@ class _HashCore:
 
     # -- per-key compatibility path ----------------------------------------
 
+    _OPS = {"vs_table_insert": 0, "vs_table_find": 1, "vs_table_erase": 2}
+
     def _one(self, fn_name: str, key: BlockKey) -> tuple[int, int]:
+        """One key through vs_table_single (pinned staging inside the
+        library, one launch, synchronous) -> (flag, position)."""
         with self._mutex:
-            self._k_host[0, 0], self._k_host[0, 1], self._k_host[0, 2] = key
             s = self._stream()
-            with self._torch.cuda.stream(s):
-                self._k_dev.copy_(self._k_host, non_blocking=True)
-            fn = getattr(self._lib, fn_name)
-            check(fn(self._h, ptr(self._k_dev), 1, ptr(self._f_dev), ptr(self._i_dev),
-                     ctypes.c_void_p(s.cuda_stream)), fn_name)
-            with self._torch.cuda.stream(s):
-                self._out_host[0:1].copy_(self._f_dev.to(self._torch.int32), non_blocking=True)
-                self._out_host[1:2].copy_(self._i_dev, non_blocking=True)
-            s.synchronize()
-            return int(self._out_host[0]), int(self._out_host[1])
+            k = (ctypes.c_int32 * 3)(*key)
+            res = ctypes.c_uint8(0)
+            idx = ctypes.c_int32(-1)
+            st = self._lib.vs_table_single(self._h, self._OPS[fn_name], ctypes.byref(k), ctypes.byref(res),
+                                           ctypes.byref(idx), ctypes.c_void_p(s.cuda_stream))
+            if st == _lib.VS_ERR_CAPACITY:
+                return 0, -1
+            check(st, fn_name)
+            return int(res.value), int(idx.value)
 
     def _insert_pos(self, key: BlockKey) -> tuple[int, bool]:
         created, pos = self._one("vs_table_insert", key)
         if pos < 0:
-            self.check_capacity()
             raise CapacityExhausted(f"excess list exhausted ({self.excess_capacity} entries)")
         return pos, bool(created)
 
@@ -339,13 +338,7 @@ class _HashCore:
         failure mode (every attempt loops to completion), so this returns the
         entry position, or None only when the free list is exhausted."""
         created, pos = self._one("vs_table_insert", key)
-        if pos < 0:
-            try:
-                self.check_capacity()
-            except CapacityExhausted:
-                pass
-            return None
-        return pos
+        return None if pos < 0 else pos
 
     def remove(self, key: BlockKey) -> bool:
         erased, pos = self._one("vs_table_erase", key)

@@ -242,6 +242,33 @@ __global__ void __launch_bounds__(kOpBlock) k_apply(TableView T, const int32_t* 
 
 static unsigned apply_grid(uint64_t n) { return grid_for(n, kOpBlock * kOpsPerThread); }
 
+// One op of any kind on one key, then its post pass, in a single thread
+// (the per-key compatibility path: BlockHashSet.insert/remove/__contains__).
+__global__ void k_single(TableView T, const int32_t* __restrict__ kio, uint8_t op, uint8_t* __restrict__ res,
+                         int32_t* __restrict__ idx) {
+  const int32_t x = kio[0], y = kio[1], z = kio[2];
+  int delta = 0;
+  if (op == VS_OP_INSERT) {
+    const InsertResult r = insert_key(T, x, y, z, 0);
+    *res = r.created;
+    *idx = r.pos;
+    delta = r.created;
+    if (r.created) atomicAnd(&T.e[r.pos].meta, ~kFresh);
+  } else if (op == VS_OP_ERASE) {
+    const int32_t pos = erase_key(T, x, y, z);
+    *res = pos >= 0;
+    *idx = pos;
+    delta = -(pos >= 0);
+    if (pos >= (int32_t)T.n) push_free(T, (uint32_t)pos);  // no pops in this launch
+  } else {
+    uint32_t meta;
+    const int32_t pos = find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
+    *res = pos >= 0;
+    *idx = pos;
+  }
+  if (delta) atomicAdd((unsigned long long*)&T.ctl->size[0], (unsigned long long)(long long)delta);
+}
+
 // Post pass after k_insert / k_apply: created flags to the lowest op index
 // among in-batch duplicates (sequential replay), FRESH cleared, and the
 // excess entries vacated by erases recycled -- one launch, one pass.
@@ -736,6 +763,38 @@ vs_status vs_table_apply(vs_table* t, const int32_t* keys, const uint8_t* ops, u
   }
   { k_post<<<grid_for(n, 256), 256, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_apply");
+  return VS_OK;
+}
+
+vs_status vs_table_single(vs_table* t, int op, const int32_t key_host[3], uint8_t* result_host,
+                           int32_t* index_host, vs_stream_t stream) {
+  if (!t || !key_host || !result_host || !index_host || op < 0 || op > 2) {
+    set_error("table/key/result/index must be non-NULL and op in {0,1,2}");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!t->stage_host) {
+    // mapped pinned staging: the kernel reads the key and writes the result
+    // straight in host memory, so a per-key call is one launch + one sync
+    VS_CK(cudaHostAlloc((void**)&t->stage_host, 32, cudaHostAllocMapped));
+    VS_CK(cudaHostGetDevicePointer((void**)&t->stage_dev, t->stage_host, 0));
+  }
+  volatile int32_t* hk = (volatile int32_t*)t->stage_host;
+  hk[0] = key_host[0];
+  hk[1] = key_host[1];
+  hk[2] = key_host[2];
+  int32_t* dk = (int32_t*)t->stage_dev;
+  { k_single<<<1, 1, 0, s>>>(t->next_view(), dk, (uint8_t)op, (uint8_t*)(t->stage_dev + 20), dk + 4); vsb::count_launch(); }
+  VS_CK(cudaStreamSynchronize(s));
+  *index_host = ((volatile int32_t*)t->stage_host)[4];
+  *result_host = ((volatile uint8_t*)t->stage_host)[20];
+  if (op == VS_OP_INSERT && *index_host < 0) {
+    unsigned int zero = 0;
+    VS_CK(cudaMemcpy(&t->ctl->error, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+    set_error("excess list exhausted (" + std::to_string(t->excess) + " entries)");
+    return VS_ERR_CAPACITY;
+  }
   return VS_OK;
 }
 

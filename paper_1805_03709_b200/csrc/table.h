@@ -24,6 +24,8 @@ struct vs_table {
   uint32_t* chunk_counts = nullptr;
   uint64_t* chunk_offsets = nullptr;  // nchunks + 1
   int32_t* pos_work = nullptr;        // lazily allocated, cap entries
+  uint8_t* stage_host = nullptr;      // pinned staging of the single-key path (32 B)
+  uint8_t* stage_dev = nullptr;
 
   // view for ONE launch; next_epoch() gives it a fresh claim tag
   vsb::TableView view() const {

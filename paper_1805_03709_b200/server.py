@@ -160,19 +160,21 @@ class StreamSet:
 
 
 def _order_streams(tables):
-    """Current stream, made to wait for the last launch on every table."""
-    s = tables[0]._torch.cuda.current_stream(tables[0].device)
+    """Current stream, ordered after the last launch on every table."""
+    torch = tables[0]._torch
+    s = torch.cuda.current_stream(tables[0].device)
     for t in tables:
-        if t._event is not None:
-            s.wait_event(t._event)
+        last = t._last_stream
+        if last is not None and last != s:
+            ev = torch.cuda.Event()
+            ev.record(last)
+            s.wait_event(ev)
     return s
 
 
 def _mark_done(tables, s) -> None:
-    ev = tables[0]._torch.cuda.Event()
-    ev.record(s)
     for t in tables:
-        t._event = ev
+        t._last_stream = s
 
 
 def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True):
