@@ -242,6 +242,44 @@ __global__ void __launch_bounds__(kOpBlock) k_apply(TableView T, const int32_t* 
 
 static unsigned apply_grid(uint64_t n) { return grid_for(n, kOpBlock * kOpsPerThread); }
 
+// Optional L2 persistence of the bucket region (VSB_HASH_PERSIST_L2): every
+// op starts with a random bucket-entry access, so a persisting carve-out over
+// the n x 16 B bucket array turns most first hops into L2 hits.
+#ifndef VSB_HASH_PERSIST_L2
+#define VSB_HASH_PERSIST_L2 0
+#endif
+static cudaError_t launch_apply(const TableView& v, const int32_t* keys, const uint8_t* ops, uint64_t n,
+                                uint8_t* result, int32_t* index, cudaStream_t s) {
+#if VSB_HASH_PERSIST_L2
+  static size_t carve = 0;
+  if (carve == 0) {
+    int dev = 0, maxp = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    carve = (size_t)maxp;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(apply_grid(n));
+  cfg.blockDim = dim3(kOpBlock);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  attr[0].val.accessPolicyWindow.base_ptr = (void*)v.e;
+  const size_t bytes = (size_t)v.n * sizeof(Entry);
+  attr[0].val.accessPolicyWindow.num_bytes = bytes;
+  attr[0].val.accessPolicyWindow.hitRatio = bytes > carve ? (float)carve / (float)bytes : 1.0f;
+  attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_apply, v, keys, ops, n, result, index);
+#else
+  k_apply<<<apply_grid(n), kOpBlock, 0, s>>>(v, keys, ops, n, result, index);
+  return cudaGetLastError();
+#endif
+}
+
 // One op of any kind on one key, then its post pass, in a single thread
 // (the per-key compatibility path: BlockHashSet.insert/remove/__contains__).
 __global__ void k_single(TableView T, const int32_t* __restrict__ kio, uint8_t op, uint8_t* __restrict__ res,
@@ -759,7 +797,7 @@ vs_status vs_table_apply(vs_table* t, const int32_t* keys, const uint8_t* ops, u
   const TableView v = t->next_view();
   {
     ProfScope prof(0, s);
-    { k_apply<<<apply_grid(n), kOpBlock, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
+    { VS_CK(launch_apply(v, keys, ops, n, result, index, s)); vsb::count_launch(); }
   }
   { k_post<<<grid_for(n, 256), 256, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_apply");
