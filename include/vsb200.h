@@ -277,6 +277,31 @@ vs_status vs_stream_extract_ordered(vs_table *set, const int32_t *fifo_keys,
                                     int32_t *keys_out, uint64_t *n_out_host,
                                     vs_table *scratch, vs_stream_t stream);
 
+/* ------------------------------------------------- RC-side voxel hashing --- */
+
+/* VoxelModel.allocate_blocks / integrate_frame (voxel_model.py:105-141,
+ * 165-299) on the device, bit-exact with the reference (IEEE ops in numpy's
+ * order and precision; OpenBLAS FMA order for the 3x3 products).
+ * params_host points to a vs_rc_params block (layout: see fusion.cu RcParams;
+ * size vs_rc_params_bytes()) holding pose, intrinsics, fusion config, the
+ * depth-step fractions and the sensor frustum planes.
+ *   vs_rc_candidates: candidate block keys of the frame's truncation bands
+ *     (_segment_block_keys, boundary-inclusive), warp-deduplicated, unordered;
+ *     *n_dev = count (may exceed cap: then call again with a larger buffer).
+ *   vs_rc_zero_rows: zero the pool rows of created blocks (TsdfBlock()).
+ *   vs_rc_integrate: for n live blocks (keys, pool rows): frustum culling,
+ *     coarse rejection, per-voxel projection and weighted update of the wire
+ *     rows in place; touched[i] = 1 if any voxel of block i was updated.
+ * depth: device float32[h][w]; color: device uint8[h][w][3]. */
+uint64_t vs_rc_params_bytes(void);
+vs_status vs_rc_candidates(const float *depth, const void *params_host, int32_t *keys_out,
+                           uint64_t cap, uint64_t *n_dev, vs_stream_t stream);
+vs_status vs_rc_zero_rows(const int32_t *pos, const uint8_t *created, uint64_t n,
+                          uint8_t *pool, vs_stream_t stream);
+vs_status vs_rc_integrate(const int32_t *keys, const int32_t *pos, uint64_t n,
+                          const float *depth, const uint8_t *color, const void *params_host,
+                          uint8_t *pool, uint8_t *touched, vs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

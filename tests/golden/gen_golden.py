@@ -287,6 +287,7 @@ class _Conn:
 
 def gen_server() -> None:
     """Server.on_tsdf_batch fan-out + reset + fresh attach, recorded per client."""
+    random.seed(0)  # extract_batch draws its start with random.randrange
     s = srv_mod.Server(srv_mod.ServerConfig(buckets=1 << 12, excess=1 << 12, voxel_size=0.01))
     sessions = []
     for i in range(3):
@@ -370,6 +371,36 @@ def gen_visibility() -> None:
                         pose=np.array(poses), intrinsics=np.array(intrs))
 
 
+def gen_fusion() -> None:
+    """The RC-side fusion behind the sphere fixture (fixtures.py:28-41):
+    the 8 frames, intrinsics and config, and per frame the keys
+    allocate_blocks created and integrate_frame touched (voxel_model.py:165-299).
+    The final TSDF blocks are mc_sphere.npz."""
+    from voxelstream.dataset import SphereScene, default_intrinsics, synthetic_frames
+    from voxelstream.voxel_model import FusionConfig, VoxelModel
+
+    scene = SphereScene(radius=0.4, orbit_radius=1.4)
+    intr = default_intrinsics(80, 60)
+    cfg = FusionConfig(voxel_size=0.01, truncation=0.06)
+    model = VoxelModel(cfg, bucket_count=1 << 13, excess_capacity=1 << 13)
+    depth, color, pose, created, touched = [], [], [], [], []
+    for frame in synthetic_frames(scene, intr, 8):
+        new = model.allocate_blocks(frame.depth, frame.pose, intr)
+        tch = model.integrate_frame(frame.depth, frame.color, frame.pose, intr)
+        depth.append(frame.depth)
+        color.append(frame.color)
+        pose.append(np.concatenate([frame.pose.rotation.reshape(-1), frame.pose.translation]))
+        created.append(np.asarray(new, np.int32).reshape(-1, 3))
+        touched.append(np.asarray(sorted(tch), np.int32).reshape(-1, 3))
+    np.savez_compressed(
+        OUT / "fusion_sphere.npz", depth=np.stack(depth).astype(np.float32), color=np.stack(color).astype(np.uint8),
+        pose=np.stack(pose).astype(np.float64),
+        intr=np.array([intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height], np.float64),
+        cfg=np.array([cfg.voxel_size, cfg.truncation, cfg.max_weight, cfg.alloc_stride], np.float64),
+        created_counts=np.array([len(c) for c in created]), created=np.concatenate(created),
+        touched_counts=np.array([len(t) for t in touched]), touched=np.concatenate(touched))
+
+
 def main() -> None:
     gen_hash_kat()
     gen_hash_seq()
@@ -380,6 +411,7 @@ def main() -> None:
     gen_stream()
     gen_server()
     gen_visibility()
+    gen_fusion()
     for p in sorted(OUT.iterdir()):
         if p.suffix in (".json", ".npz"):
             print(f"{p.name:24s} {p.stat().st_size:>9d} B")
