@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--mc-steps", type=int, default=10)
     p.add_argument("--no-mc", action="store_true")
     p.add_argument("--no-stream", action="store_true")
+    p.add_argument("--no-rc", action="store_true")
+    p.add_argument("--rc-frames", type=int, default=20)
     p.add_argument("--stream-ticks", type=int, default=60)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -545,6 +547,60 @@ def cpu_stream_sample(seconds: float = 5.0):
     return ops / (time.perf_counter() - t0) / 1e6
 
 
+def run_rc(args, dev):
+    """RC-side voxel hashing: allocate_blocks +
+    integrate_frame of 640x480 RGB-D frames from inside the synthetic room at
+    5 mm voxels (mu 0.06 m), frames resident on the device."""
+    import torch
+
+    from paper_1805_03709_b200 import _lib, workloads
+    from paper_1805_03709_b200.voxel_model import GpuVoxelModel
+
+    import types
+
+    n = args.rc_frames
+    depth, color, Rs, ts, (fx, fy, cx, cy, w, h) = workloads.room_frames(n + 2, 640, 480)
+    intr = types.SimpleNamespace(fx=fx, fy=fy, cx=cx, cy=cy, width=w, height=h)
+    cfg = types.SimpleNamespace(voxel_size=0.005, truncation=0.06, max_weight=128.0, alloc_stride=1)
+    model = GpuVoxelModel(cfg, bucket_count=1 << 21, excess_capacity=1 << 21, device=dev)
+    dd = torch.from_numpy(depth).to(dev)
+    cc = torch.from_numpy(color).to(dev)
+    for f in range(2):  # warm-up frames
+        model.allocate_blocks_tensor(dd[f], (Rs[f], ts[f]), intr)
+        model.integrate_frame_tensor(dd[f], cc[f], (Rs[f], ts[f]), intr)
+    torch.cuda.synchronize()
+    created = touched = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    with _lib.Profile() as prof:
+        e0.record()
+        for f in range(2, n + 2):
+            created += model.allocate_blocks_tensor(dd[f], (Rs[f], ts[f]), intr).shape[0]
+            touched += model.integrate_frame_tensor(dd[f], cc[f], (Rs[f], ts[f]), intr).shape[0]
+        e1.record()
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    return {"workload": f"RC fusion: {n} frames 640x480 inside the 16x3x16 m room, 5 mm voxels, mu 0.06 m",
+            "value": n / (ms / 1e3), "unit": "frames/s", "ms_per_frame": ms / n, "wall_s": wall,
+            "blocks": model.blocks.approx_size(), "created": created, "touched": touched,
+            "integrate_kernel_ms_per_frame": prof.ms["other"] / max(1, prof.count["other"]),
+            "gpu_launches": prof.launches}
+
+
+def cpu_rc_sample():
+    """Reference fusion (numpy restatement, 1 thread) on 1 frame of the same workload."""
+    from oracle.fusion_oracle import OracleVoxelModel
+    from paper_1805_03709_b200 import workloads
+
+    depth, color, Rs, ts, (fx, fy, cx, cy, w, h) = workloads.room_frames(1, 640, 480)
+    m = OracleVoxelModel(0.005, 0.06)
+    t0 = time.perf_counter()
+    m.allocate(depth[0], Rs[0], ts[0], float(fx), float(fy), float(cx), float(cy))
+    m.integrate(depth[0], color[0], Rs[0], ts[0], float(fx), float(fy), float(cx), float(cy))
+    return 1.0 / (time.perf_counter() - t0)
+
+
 # ------------------------------------------------------------------ main
 
 def main():
@@ -599,6 +655,9 @@ def main():
     stream = None
     if not args.no_stream and world == 1:
         stream = run_stream(args, dev)
+    rc = None
+    if not args.no_rc and world == 1:
+        rc = run_rc(args, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         times, ok, _ = cpu_hash_sample(spec, threads, batches=1)
@@ -609,6 +668,10 @@ def main():
         if mc_t:
             cpu["mc"] = {"value": mc_n / mc_t, "unit": "blocks/s", "cores": threads, "kind": "port",
                          "sample": f"{mc_n} room blocks (C restatement of recompute_mc_block)"}
+        if not args.no_rc:
+            cpu["rc"] = {"value": cpu_rc_sample(), "unit": "frames/s", "cores": 1, "kind": "port",
+                         "sample": "1 frame 640x480 of the RC workload (numpy restatement of allocate_blocks + "
+                                   "integrate_frame)"}
         if not args.no_stream:
             cpu["stream"] = {"value": cpu_stream_sample(), "unit": "M key-ops/s", "cores": 1, "kind": "port",
                              "sample": "1 client: fill with the 2.08M-key scene + update ticks for ~5 s "
@@ -624,7 +687,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": config,
                 "parity_ok": h["ok"], "roofline": h["roofline"], "gpu_launches": h["gpu_launches"],
-                "clocks": h["clocks"], "cpu_baseline": cpu, "e2e": h.get("e2e"), "mc": mc, "stream": stream}
+                "clocks": h["clocks"], "cpu_baseline": cpu, "e2e": h.get("e2e"), "mc": mc, "stream": stream, "rc": rc}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

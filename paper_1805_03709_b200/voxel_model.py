@@ -192,6 +192,11 @@ class GpuVoxelModel:
     def allocate_blocks(self, depth, pose, intrinsics) -> list:
         """Ensure blocks along every valid ray segment [d-mu, d+mu]; returns the
         newly created keys in sorted order, like the reference."""
+        new = self.allocate_blocks_tensor(depth, pose, intrinsics, sort=True)
+        return [tuple(r) for r in new.cpu().tolist()]
+
+    def allocate_blocks_tensor(self, depth, pose, intrinsics, sort: bool = False):
+        """Device fast path of allocate_blocks -> int32[m,3] created keys."""
         torch = self._torch
         lib = self._lib
         d = self._img(depth, torch.float32)
@@ -213,23 +218,28 @@ class GpuVoxelModel:
         s = self.blocks._stream()
         lib.check(lib.load().vs_rc_zero_rows(lib.ptr(pos), lib.ptr(created), n, lib.ptr(self.pool),
                                              _ct.c_void_p(s.cuda_stream)), "rc_zero_rows")
+        self.blocks._done(s)
         new = cand[created.bool()]
-        if new.shape[0] == 0:
-            return []
+        if not sort or new.shape[0] == 0:
+            return new
         k = new.to(torch.int64)
         off = 1 << 20
         enc = ((k[:, 0] + off) << 42) | ((k[:, 1] + off) << 21) | (k[:, 2] + off)
-        return [tuple(r) for r in new[torch.argsort(enc)].cpu().tolist()]
+        return new[torch.argsort(enc)]
 
     def integrate_frame(self, depth, color, pose, intrinsics) -> list:
         """Fuse one registered RGB-D frame into all allocated in-view blocks;
         returns the keys that received at least one voxel update."""
+        return [tuple(r) for r in self.integrate_frame_tensor(depth, color, pose, intrinsics).cpu().tolist()]
+
+    def integrate_frame_tensor(self, depth, color, pose, intrinsics):
+        """Device fast path of integrate_frame -> int32[m,3] touched keys."""
         torch = self._torch
         lib = self._lib
         keys, pos = self.blocks.snapshot_tensor()
         n = keys.shape[0]
         if n == 0:
-            return []
+            return keys
         d = self._img(depth, torch.float32)
         c = self._img(color, torch.uint8)
         P = self._params(pose, intrinsics, planes=True)
@@ -239,7 +249,7 @@ class GpuVoxelModel:
                                              lib.ptr(self.pool), lib.ptr(touched), _ct.c_void_p(s.cuda_stream)),
                   "rc_integrate")
         self.blocks._done(s)
-        return [tuple(r) for r in keys[touched.bool()].cpu().tolist()]
+        return keys[touched.bool()]
 
     def keys(self) -> list:
         return self.blocks.snapshot_keys()

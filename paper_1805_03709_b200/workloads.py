@@ -269,3 +269,52 @@ def room_tsdf_rows(keys, spec: RoomSpec = RoomSpec()):
     rows[..., 1] = weight.view(torch.int32)
     rows[..., 2] = rgb.to(torch.int32)
     return rows.view(torch.uint8).reshape(N, 6144)
+
+
+# ------------------------------------------------------- RC frames (room)
+
+def look_at(eye, target, up=(0.0, -1.0, 0.0)):
+    """Camera-to-world rotation whose +z looks from eye to target, +y image-down
+    (the convention of geometry.Pose.look_at)."""
+    eye = np.asarray(eye, np.float64)
+    fwd = np.asarray(target, np.float64) - eye
+    fwd /= np.linalg.norm(fwd)
+    right = np.cross(np.asarray(up, np.float64), fwd)
+    right /= np.linalg.norm(right)
+    down = np.cross(fwd, right)
+    return np.stack([right, down, fwd], axis=1)
+
+
+def room_frames(n: int, width: int = 640, height: int = 480, spec: RoomSpec = RoomSpec(), seed: int = 0):
+    """n RGB-D frames rendered analytically from inside the box room: the
+    camera orbits the centre at 3 m and looks at the walls; depth = distance
+    along the camera z axis to the first wall hit (float32, metres), colour a
+    procedural pattern of the hit point.  Returns (depth [n,h,w] f32,
+    color [n,h,w,3] u8, R [n,3,3] f64, t [n,3] f64, (fx, fy, cx, cy, w, h))."""
+    rng = np.random.default_rng(seed)
+    f = float(width)  # ~53 degree horizontal FOV (dataset.default_intrinsics)
+    intr = (f, f, width / 2, height / 2, width, height)
+    half = np.asarray(spec.half, np.float64)
+    uu, vv = np.meshgrid(np.arange(width, dtype=np.float64), np.arange(height, dtype=np.float64))
+    cam_rays = np.stack([(uu - intr[2]) / f, (vv - intr[3]) / f, np.ones_like(uu)], axis=-1).reshape(-1, 3)
+    depth = np.zeros((n, height, width), np.float32)
+    color = np.zeros((n, height, width, 3), np.uint8)
+    Rs = np.zeros((n, 3, 3))
+    ts = np.zeros((n, 3))
+    for i in range(n):
+        a = 2 * np.pi * i / max(n, 1) + rng.uniform(-0.05, 0.05)
+        eye = np.array([3.0 * np.cos(a), rng.uniform(-0.5, 0.5), 3.0 * np.sin(a)])
+        target = np.array([8.0 * np.cos(a + 0.6), rng.uniform(-1.0, 1.0), 8.0 * np.sin(a + 0.6)])
+        R = look_at(eye, target)
+        d = cam_rays @ R.T
+        with np.errstate(divide="ignore", invalid="ignore"):
+            tt = np.where(d > 0, (half - eye) / d, np.where(d < 0, (-half - eye) / d, np.inf))
+        hit_t = tt.min(axis=1)
+        p = eye + d * hit_t[:, None]
+        depth[i] = hit_t.reshape(height, width).astype(np.float32)
+        chk = ((np.floor(p[:, 0] * 2) + np.floor(p[:, 1] * 2) + np.floor(p[:, 2] * 2)) % 2).reshape(height, width)
+        color[i, ..., 0] = (80 + 120 * chk).astype(np.uint8)
+        color[i, ..., 1] = (np.abs(p[:, 1]).reshape(height, width) * 60 + 40).astype(np.uint8)
+        color[i, ..., 2] = (np.abs(p[:, 0] + p[:, 2]).reshape(height, width) * 10 % 255).astype(np.uint8)
+        Rs[i], ts[i] = R, eye
+    return depth, color, Rs, ts, intr

@@ -62,3 +62,29 @@ def test_reallocation_is_idempotent_and_get_block(dev, golden):
     blk = model.get_block(first[0])
     assert blk is not None and not blk.weight.any()  # fresh TsdfBlock(): zeros
     assert model.get_block((10 ** 6, 0, 0)) is None
+
+
+def test_room_frames_gpu_vs_oracle(dev):
+    """Synthetic room RGB-D frames (analytic ray-box depth): GPU fusion ==
+    the numpy restatement, created keys / touched keys / every voxel."""
+    from oracle.fusion_oracle import OracleVoxelModel
+    from paper_1805_03709_b200 import workloads
+    from paper_1805_03709_b200.voxel_model import GpuVoxelModel, rows_from_soa
+
+    depth, color, Rs, ts, (fx, fy, cx, cy, w, h) = workloads.room_frames(4, 160, 120)
+    intr = types.SimpleNamespace(fx=fx, fy=fy, cx=cx, cy=cy, width=w, height=h)
+    cfg = types.SimpleNamespace(voxel_size=0.02, truncation=0.08, max_weight=128.0, alloc_stride=1)
+    gpu = GpuVoxelModel(cfg, bucket_count=1 << 15, excess_capacity=1 << 15)
+    ref = OracleVoxelModel(0.02, 0.08)
+    for f in range(4):
+        a = gpu.allocate_blocks(depth[f], (Rs[f], ts[f]), intr)
+        b = ref.allocate(depth[f], Rs[f], ts[f], float(fx), float(fy), float(cx), float(cy))
+        assert a == b, f
+        ta = gpu.integrate_frame(depth[f], color[f], (Rs[f], ts[f]), intr)
+        tb = ref.integrate(depth[f], color[f], Rs[f], ts[f], float(fx), float(fy), float(cx), float(cy))
+        assert set(ta) == set(tb), f
+    keys = sorted(ref.blocks)
+    assert sorted(gpu.keys()) == keys
+    want = rows_from_soa(np.stack([ref.blocks[k][0] for k in keys]), np.stack([ref.blocks[k][1] for k in keys]),
+                         np.stack([ref.blocks[k][2] for k in keys]))
+    assert np.array_equal(gpu.rows(np.asarray(keys, np.int32)).cpu().numpy(), want)

@@ -236,3 +236,29 @@ def test_server_fanout_oracle(golden):
                 assert sorted(list(k) for k in ss.set) == entry["pending_after_reset"][c]
     assert sorted(list(k) for k in mc_keys) == g["mc_keys"]
     assert g["fresh_pending"] == g["mc_keys"]
+
+
+def test_fusion_oracle_matches_reference_sequence(golden):
+    """The numpy RC-fusion restatement reproduces the recorded reference run
+    (per-frame created / touched keys, final blocks) bit for bit."""
+    from oracle.fusion_oracle import OracleVoxelModel
+
+    d = np.load(golden / "fusion_sphere.npz")
+    fx, fy, cx, cy, w, h = (float(v) for v in d["intr"])
+    voxel, mu, maxw, stride = d["cfg"].tolist()
+    m = OracleVoxelModel(voxel, mu, maxw, int(stride))
+    c_off = np.concatenate([[0], np.cumsum(d["created_counts"])])
+    t_off = np.concatenate([[0], np.cumsum(d["touched_counts"])])
+    for f in range(8):
+        R, t = d["pose"][f][:9].reshape(3, 3), d["pose"][f][9:]
+        new = m.allocate(d["depth"][f], R, t, fx, fy, cx, cy)
+        assert new == [tuple(k) for k in d["created"][c_off[f]:c_off[f + 1]].tolist()]
+        got = m.integrate(d["depth"][f], d["color"][f], R, t, fx, fy, cx, cy)
+        assert set(got) == {tuple(k) for k in d["touched"][t_off[f]:t_off[f + 1]].tolist()}
+    s = np.load(golden / "mc_sphere.npz")
+    keys = [tuple(k) for k in s["keys"].tolist()]
+    assert sorted(m.blocks) == keys
+    for i, k in enumerate(keys):
+        tsdf, wt, col = m.blocks[k]
+        assert np.array_equal(tsdf, s["tsdf"][i]) and np.array_equal(wt, s["weight"][i])
+        assert np.array_equal(col, s["color"][i])
