@@ -292,6 +292,11 @@ vs_status vs_stream_extract_ordered(vs_table *set, const int32_t *fifo_keys,
  *   vs_rc_integrate: for n live blocks (keys, pool rows): frustum culling,
  *     coarse rejection, per-voxel projection and weighted update of the wire
  *     rows in place; touched[i] = 1 if any voxel of block i was updated.
+ *   vs_rc_integrate_table: the same over every live block of the TSDF map
+ *     `t` whose pool rows are indexed by entry slot (pool has t's capacity
+ *     rows); no snapshot needed.  touched_keys_out (capacity x 3 int32)
+ *     receives the touched keys in ascending slot order, *n_touched_dev
+ *     their count.
  * depth: device float32[h][w]; color: device uint8[h][w][3]. */
 uint64_t vs_rc_params_bytes(void);
 vs_status vs_rc_candidates(const float *depth, const void *params_host, int32_t *keys_out,
@@ -301,6 +306,9 @@ vs_status vs_rc_zero_rows(const int32_t *pos, const uint8_t *created, uint64_t n
 vs_status vs_rc_integrate(const int32_t *keys, const int32_t *pos, uint64_t n,
                           const float *depth, const uint8_t *color, const void *params_host,
                           uint8_t *pool, uint8_t *touched, vs_stream_t stream);
+vs_status vs_rc_integrate_table(const vs_table *t, const float *depth, const uint8_t *color,
+                                const void *params_host, uint8_t *pool, int32_t *touched_keys_out,
+                                uint64_t *n_touched_dev, vs_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -86,6 +86,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_rc_candidates": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp]),
     "vs_rc_zero_rows": (_i32, [_vp, _vp, _u64, _vp, _vp]),
     "vs_rc_integrate": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "vs_rc_integrate_table": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "vs_stream_remove_many": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _vp, _u64, _vp, _vp]),
     "vs_stream_extract_ordered": (_i32, [_vp, _vp, _u64, _pu64, _u64, _u64, _vp, _pu64, _vp, _vp]),
 }

@@ -91,6 +91,9 @@ __device__ __forceinline__ int4 ld_entry(const Entry* p) {
   return v;
 }
 
+// read-only pass over a table no kernel is mutating (stream-ordered scans)
+__device__ __forceinline__ int4 ld_entry_ro(const Entry* p) { return __ldg((const int4*)p); }
+
 // L2 eviction priority for bucket entries: every op starts at its bucket
 // entry, so the bucket region (n x 16 B) is worth keeping in L2 ahead of the
 // excess region and the streamed per-op inputs (VSB_HASH_L2HINT).

@@ -15,14 +15,38 @@ constexpr int kScanTile = 4096;  // elements per CTA (256 threads x 16)
 
 inline uint64_t scan_tiles(uint64_t n) { return (n + kScanTile - 1) / kScanTile; }
 
+// v[0..16) = in[base .. base+16) (0 past n); one or four 16-B loads when the
+// run is whole and aligned, element loads otherwise
+template <typename T>
+__device__ __forceinline__ void load16(const T* __restrict__ in, uint64_t base, uint64_t n, uint32_t v[16]) {
+  const T* p = in + base;
+  if (base + 16 <= n && ((uintptr_t)p & 15) == 0) {
+    if constexpr (sizeof(T) == 1) {
+      const uint4 q = __ldg((const uint4*)p);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = (w[k >> 2] >> (8 * (k & 3))) & 0xffu;
+      return;
+    } else if constexpr (sizeof(T) == 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 r = __ldg((const uint4*)p + q);
+        v[4 * q] = r.x, v[4 * q + 1] = r.y, v[4 * q + 2] = r.z, v[4 * q + 3] = r.w;
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = base + k < n ? (uint32_t)p[k] : 0u;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_tile_sums(const T* __restrict__ in, uint64_t n, uint64_t* __restrict__ sums) {
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
+  uint32_t v[16];
+  load16(in, (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * 16, n, v);
   uint64_t s = 0;
-  for (int j = threadIdx.x; j < kScanTile; j += 256) {
-    const uint64_t i = base + j;
-    if (i < n) s += (uint64_t)in[i];
-  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s += v[k];
   __shared__ uint64_t red[8];
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -70,37 +94,44 @@ static __global__ void __launch_bounds__(1024) k_scan_tiles(uint64_t* __restrict
   if (threadIdx.x == 0) sums[ntiles] = carry_s;
 }
 
-// out[i] = exclusive prefix of in[0..i); out[n] = total
+// out[i] = exclusive prefix of in[0..i); out[n] = total (a tile's own sum
+// must fit in u32: byte flags and per-block counts do).  Each thread scans
+// 16 consecutive inputs; the tile-local results are staged in shared memory
+// (row pitch 17 words: conflict-free) so the u64 stores leave coalesced.
 template <typename T>
 __global__ void __launch_bounds__(256) k_tile_scan(const T* __restrict__ in, uint64_t n,
                                                    const uint64_t* __restrict__ tile_off, uint64_t ntiles,
                                                    uint64_t* __restrict__ out) {
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * 16;
+  __shared__ uint32_t stage[256 * 17];
+  __shared__ uint32_t ws[8];
+  const uint64_t tile = (uint64_t)blockIdx.x * kScanTile;
+  const uint64_t base = tile + (uint64_t)threadIdx.x * 16;
   uint32_t v[16];
-  uint64_t local = 0;
+  load16(in, base, n, v);
+  uint32_t local = 0;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const uint64_t i = base + k;
-    v[k] = i < n ? (uint32_t)in[i] : 0u;
-    local += v[k];
-  }
-  __shared__ uint64_t ws[8];
+  for (int k = 0; k < 16; ++k) local += v[k];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t x = local;
+  uint32_t x = local;
   for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) ws[warp] = x;
   __syncthreads();
-  uint64_t pre = tile_off[blockIdx.x];
-  for (int w = 0; w < warp; ++w) pre += ws[w];
-  uint64_t run = pre + x - local;
+  uint32_t run = x - local;
+  for (int w = 0; w < warp; ++w) run += ws[w];
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
-    const uint64_t i = base + k;
-    if (i < n) out[i] = run;
+    stage[threadIdx.x * 17 + k] = run;
     run += v[k];
+  }
+  __syncthreads();
+  const uint64_t t0 = tile_off[blockIdx.x];
+#pragma unroll 4
+  for (int j = threadIdx.x; j < kScanTile; j += 256) {
+    const uint64_t i = tile + j;
+    if (i < n) out[i] = t0 + stage[(j >> 4) * 17 + (j & 15)];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = tile_off[ntiles];
 }

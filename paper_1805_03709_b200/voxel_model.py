@@ -202,7 +202,8 @@ class GpuVoxelModel:
         d = self._img(depth, torch.float32)
         P = self._params(pose, intrinsics, planes=False)
         s = self.blocks._stream()
-        cap = max(1 << 16, 2 * d.numel())
+        # candidate buffer sized by the largest count seen so far (one pass per frame)
+        cap = max(getattr(self, "_cand_cap", 0), 1 << 16, 2 * d.numel())
         n_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
         while True:
             cand = torch.empty((cap, 3), dtype=torch.int32, device=self.device)
@@ -211,7 +212,8 @@ class GpuVoxelModel:
             n = int(n_dev.item())
             if n <= cap:
                 break
-            cap = n
+            cap = n + n // 4
+        self._cand_cap = cap
         cand = cand[:n]
         self.blocks._done(s)
         created, pos = self.blocks.insert_many_exact(cand)
@@ -233,23 +235,26 @@ class GpuVoxelModel:
         return [tuple(r) for r in self.integrate_frame_tensor(depth, color, pose, intrinsics).cpu().tolist()]
 
     def integrate_frame_tensor(self, depth, color, pose, intrinsics):
-        """Device fast path of integrate_frame -> int32[m,3] touched keys."""
+        """Device fast path of integrate_frame -> int32[m,3] touched keys
+        (ascending pool row).  Walks the map's entry slots directly (pool
+        row = slot), so no snapshot is taken; one host sync for the count."""
         torch = self._torch
         lib = self._lib
-        keys, pos = self.blocks.snapshot_tensor()
-        n = keys.shape[0]
-        if n == 0:
-            return keys
         d = self._img(depth, torch.float32)
         c = self._img(color, torch.uint8)
         P = self._params(pose, intrinsics, planes=True)
-        touched = torch.empty(n, dtype=torch.uint8, device=self.device)
+        if getattr(self, "_touched_buf", None) is None:
+            self._touched_buf = torch.empty((self.blocks.capacity, 3), dtype=torch.int32, device=self.device)
+            self._touched_n = torch.zeros(1, dtype=torch.int64, device=self.device)
         s = self.blocks._stream()
-        lib.check(lib.load().vs_rc_integrate(lib.ptr(keys), lib.ptr(pos), n, lib.ptr(d), lib.ptr(c), _ct.byref(P),
-                                             lib.ptr(self.pool), lib.ptr(touched), _ct.c_void_p(s.cuda_stream)),
+        lib.check(lib.load().vs_rc_integrate_table(self.blocks._h, lib.ptr(d), lib.ptr(c), _ct.byref(P),
+                                                   lib.ptr(self.pool), lib.ptr(self._touched_buf),
+                                                   lib.ptr(self._touched_n), _ct.c_void_p(s.cuda_stream)),
                   "rc_integrate")
+        n = int(self._touched_n.item())
+        out = self._touched_buf[:n].clone()
         self.blocks._done(s)
-        return keys[touched.bool()]
+        return out
 
     def keys(self) -> list:
         return self.blocks.snapshot_keys()

@@ -88,3 +88,43 @@ def test_room_frames_gpu_vs_oracle(dev):
     want = rows_from_soa(np.stack([ref.blocks[k][0] for k in keys]), np.stack([ref.blocks[k][1] for k in keys]),
                          np.stack([ref.blocks[k][2] for k in keys]))
     assert np.array_equal(gpu.rows(np.asarray(keys, np.int32)).cpu().numpy(), want)
+
+
+def test_integrate_keys_abi_matches_table_walk(dev):
+    """vs_rc_integrate (explicit keys + pool rows, e.g. a snapshot) and
+    vs_rc_integrate_table (walks the map's slots) give the same rows and
+    flag the same blocks; the table walk returns ascending slots."""
+    import ctypes
+
+    import torch
+
+    from paper_1805_03709_b200 import _lib, workloads
+    from paper_1805_03709_b200.voxel_model import GpuVoxelModel
+
+    depth, color, Rs, ts, (fx, fy, cx, cy, w, h) = workloads.room_frames(3, 160, 120)
+    intr = types.SimpleNamespace(fx=fx, fy=fy, cx=cx, cy=cy, width=w, height=h)
+    cfg = types.SimpleNamespace(voxel_size=0.02, truncation=0.08, max_weight=128.0, alloc_stride=1)
+    a = GpuVoxelModel(cfg, bucket_count=1 << 15, excess_capacity=1 << 15)
+    b = GpuVoxelModel(cfg, bucket_count=1 << 15, excess_capacity=1 << 15)
+    lib = _lib.load()
+    for f in range(3):
+        a.allocate_blocks(depth[f], (Rs[f], ts[f]), intr)
+        b.allocate_blocks(depth[f], (Rs[f], ts[f]), intr)
+        ta = a.integrate_frame_tensor(torch.from_numpy(depth[f]).to(dev), torch.from_numpy(color[f]).to(dev),
+                                      (Rs[f], ts[f]), intr)
+        keys, pos = b.blocks.snapshot_tensor()
+        touched = torch.empty(keys.shape[0], dtype=torch.uint8, device=dev)
+        P = b._params((Rs[f], ts[f]), intr, planes=True)
+        d = torch.from_numpy(depth[f]).to(dev)
+        c = torch.from_numpy(color[f]).contiguous().to(dev)
+        _lib.check(lib.vs_rc_integrate(_lib.ptr(keys), _lib.ptr(pos), keys.shape[0], _lib.ptr(d), _lib.ptr(c),
+                                       ctypes.byref(P), _lib.ptr(b.pool), _lib.ptr(touched),
+                                       ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "rc_integrate")
+        tb = keys[touched.bool()]
+        assert ta.shape[0] > 0
+        slot = a.blocks.find_keys(ta)[1]
+        assert bool((slot[1:] > slot[:-1]).all())
+        # same set (slot assignment of the two maps may differ)
+        assert sorted(map(tuple, ta.tolist())) == sorted(map(tuple, tb.tolist())), f
+    keys, _ = a.blocks.snapshot_tensor()
+    assert torch.equal(a.rows(keys), b.rows(keys))
