@@ -277,6 +277,36 @@ vs_status vs_stream_extract_ordered(vs_table *set, const int32_t *fifo_keys,
                                     int32_t *keys_out, uint64_t *n_out_host,
                                     vs_table *scratch, vs_stream_t stream);
 
+/* ------------------------------------------- key-hash sharded hash set --- */
+
+/* One partition of a block hash set sharded over the `world` GPUs of a node
+ * (BASELINE config 5; the reference is a single in-process
+ * table, concurrent_hash.py:348-402 -- sharding is new).  owner(k) =
+ * fmix32(hash_key pre-modulo, concurrent_hash.py:58) mod world.  Every rank
+ * creates its shard over its local table, exports its window handle (CUDA
+ * IPC, 64 bytes), gathers all ranks' handles (any out-of-band channel, e.g.
+ * torch.distributed all_gather_object) and connects.  vs_shard_apply is then
+ * COLLECTIVE: every rank calls it once per batch, in the same order; each
+ * op is routed to its owner and the result comes back, by peer stores over
+ * NVLink/NVSwitch from the kernels themselves (no host synchronisation, no
+ * NCCL).  Per-op results equal a sequential replay of rank 0's batch, then
+ * rank 1's, ... (A18 batches: of any order).  max_batch bounds n per call
+ * (<= 2^30; world*max_batch < 2^31). */
+typedef struct vs_shard vs_shard;
+vs_status vs_shard_create(vs_table *local, int rank, int world, uint64_t max_batch, vs_shard **out);
+void vs_shard_destroy(vs_shard *s);
+vs_status vs_shard_export(vs_shard *s, uint8_t handle_out[64]);
+/* handles: world x 64 bytes, rank-major (own entry ignored). */
+vs_status vs_shard_connect(vs_shard *s, const uint8_t *handles);
+/* keys device int32[n][3], ops device uint8[n] (VS_OP_*), result device
+ * uint8[n] (created / found / erased).  Asynchronous on `stream`. */
+vs_status vs_shard_apply(vs_shard *s, const int32_t *keys, const uint8_t *ops, uint64_t n,
+                         uint8_t *result, vs_stream_t stream);
+/* SYNCHRONOUS: VS_ERR_CUDA if a wait for a peer timed out since creation. */
+vs_status vs_shard_check(vs_shard *s);
+/* Host helper: owner rank of n HOST keys (the routing function). */
+vs_status vs_shard_owner(const int32_t *keys, uint64_t n, int world, int32_t *owner_out);
+
 /* ------------------------------------------------- RC-side voxel hashing --- */
 
 /* VoxelModel.allocate_blocks / integrate_frame (voxel_model.py:105-141,

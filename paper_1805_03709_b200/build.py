@@ -21,7 +21,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "vsb200"
 LIB = PKG / "libvsb200.so"
-SOURCES = ["hash.cu", "mc.cu", "stream.cu", "fusion.cu"]
+SOURCES = ["hash.cu", "mc.cu", "stream.cu", "fusion.cu", "shard.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
               "-Xptxas", "-v", f"-I{ROOT / 'include'}"]

@@ -176,33 +176,6 @@ __global__ void __launch_bounds__(kOpBlock) k_erase_win(TableView T, const int32
   add_size_cta(T, delta);
 }
 
-// One mixed op (insert / find / erase) with its bucket entry already loaded.
-// Returns the size delta.
-__device__ __forceinline__ int apply_one(const TableView& T, int32_t x, int32_t y, int32_t z, uint8_t op, uint64_t i,
-                                         uint32_t b, const int4& pre, uint8_t* __restrict__ result,
-                                         int32_t* __restrict__ index) {
-  int32_t pos;
-  uint8_t res;
-  int delta = 0;
-  if (op == VS_OP_INSERT) {
-    const InsertResult r = insert_key(T, x, y, z, (int32_t)i, &pre);
-    pos = r.pos;
-    res = r.created;
-    delta = r.created;
-  } else if (op == VS_OP_ERASE) {
-    pos = erase_key(T, x, y, z, &pre);
-    res = pos >= 0;
-    delta = -(int)res;
-  } else {
-    uint32_t meta;
-    pos = find_pos_from(T, x, y, z, b, pre, &meta);
-    res = pos >= 0;
-  }
-  __stcs(result + i, res);
-  __stcs(index + i, pos);
-  return delta;
-}
-
 // Mixed batch.  Each thread owns kOpsPerThread ops (kOpBlock apart, so loads
 // stay coalesced) and issues all their bucket-entry loads before walking
 // any chain: more independent misses in flight per SM.

@@ -261,9 +261,12 @@ __device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int3
 
 // Post pass for one op of an insert/apply batch: settle the created flag of
 // a creator against in-batch duplicates (lowest op index wins), clear FRESH;
-// recycle the excess entry vacated by an erase.
-__device__ __forceinline__ void post_op(const TableView& T, const int32_t* __restrict__ keys, uint64_t i, uint8_t op,
-                                        uint8_t* __restrict__ result, int32_t pos) {
+// recycle the excess entry vacated by an erase.  `same_key(m)` tells whether
+// op m names the same key as op i (ops live in a flat int3 array, or in the
+// routed records of a sharded batch).
+template <class SameKey>
+__device__ __forceinline__ void post_op_t(const TableView& T, SameKey same_key, uint64_t i, uint8_t op,
+                                          uint8_t* __restrict__ result, int32_t pos) {
   if (op == 0 /*VS_OP_INSERT*/) {
     if (!result[i]) return;
     const uint32_t bit = 1u << ((uint32_t)pos & 31u);
@@ -274,13 +277,50 @@ __device__ __forceinline__ void post_op(const TableView& T, const int32_t* __res
     const unsigned long long c = T.claim[pos];
     if ((c & 0xFFFFFFFF00000000ull) != T.tag) return;
     const uint64_t m = (uint32_t)(c & 0xFFFFFFFFull);
-    if (m < i && keys[3 * m] == keys[3 * i] && keys[3 * m + 1] == keys[3 * i + 1] && keys[3 * m + 2] == keys[3 * i + 2]) {
+    if (m < i && same_key(m)) {
       result[i] = 0;
       result[m] = 1;
     }
   } else if (op == 2 /*VS_OP_ERASE*/) {
     if (result[i] && pos >= (int32_t)T.n) push_free(T, (uint32_t)pos);
   }
+}
+
+__device__ __forceinline__ void post_op(const TableView& T, const int32_t* __restrict__ keys, uint64_t i, uint8_t op,
+                                        uint8_t* __restrict__ result, int32_t pos) {
+  post_op_t(
+      T,
+      [&](uint64_t m) {
+        return keys[3 * m] == keys[3 * i] && keys[3 * m + 1] == keys[3 * i + 1] && keys[3 * m + 2] == keys[3 * i + 2];
+      },
+      i, op, result, pos);
+}
+
+// One mixed op (insert / find / erase) with its bucket entry already loaded.
+// Returns the size delta.
+__device__ __forceinline__ int apply_one(const TableView& T, int32_t x, int32_t y, int32_t z, uint8_t op, uint64_t i,
+                                         uint32_t b, const int4& pre, uint8_t* __restrict__ result,
+                                         int32_t* __restrict__ index) {
+  int32_t pos;
+  uint8_t res;
+  int delta = 0;
+  if (op == 0 /*VS_OP_INSERT*/) {
+    const InsertResult r = insert_key(T, x, y, z, (int32_t)i, &pre);
+    pos = r.pos;
+    res = r.created;
+    delta = r.created;
+  } else if (op == 2 /*VS_OP_ERASE*/) {
+    pos = erase_key(T, x, y, z, &pre);
+    res = pos >= 0;
+    delta = -(int)res;
+  } else {
+    uint32_t meta;
+    pos = find_pos_from(T, x, y, z, b, pre, &meta);
+    res = pos >= 0;
+  }
+  __stcs(result + i, res);
+  __stcs(index + i, pos);
+  return delta;
 }
 
 // Warp-aggregated update of the live-key counter into one of kSizeStripes

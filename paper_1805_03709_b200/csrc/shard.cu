@@ -1,0 +1,580 @@
+// shard.cu -- the block hash set sharded by key hash over the GPUs of one
+// node, with the exchange done by the kernels themselves over peer memory
+// (BASELINE config 5).
+//
+// The reference never shards (concurrent_hash.py is one in-process table);
+// the owner function is free: owner(k) = fmix32(hash_key pre-modulo) mod G,
+// bits independent of the local bucket hash_key(k) mod n.  Instead of the
+// collective route (partition -> all-to-all counts -> all-to-all records ->
+// apply -> all-to-all results -> scatter, shard.py's NCCL path), every rank
+// maps every other rank's receive window (CUDA IPC over NVLink/NVSwitch) and
+// one batch is six stream-ordered kernels with no host synchronisation:
+//
+//   k_part_push    single-pass stable partition by owner (decoupled look-back
+//                  over 2,048-op tiles); each op's 16-B record {x, y, z,
+//                  op<<30 | input index} is STORED STRAIGHT INTO THE OWNER'S
+//                  WINDOW (region of this source rank, input order kept);
+//                  the last CTA publishes the per-owner counts and a release
+//                  flag to every owner
+//   k_wait         owner: acquire the G push flags of this epoch
+//   k_shard_apply  owner: the mixed op over the concatenation of the G
+//                  regions (source-major, input order inside a source) --
+//                  exactly the order the collective route delivers, so the
+//                  lowest-index-creates rule of duplicate inserts resolves
+//                  the same way: per-op results equal a sequential replay of
+//                  rank 0's batch, then rank 1's, ...
+//   k_shard_post   created-flag fixup + free-list recycling (hash_ops.cuh)
+//   k_shard_return owner: each result byte is stored straight back into the
+//                  source's window at the op's input index; last CTA flags
+//   k_wait         source: acquire the G return flags, then copy out
+//
+// Window reuse is safe without double buffering: a source pushes batch e+1
+// only after every owner flagged the return of batch e, which each owner
+// does after its last read of batch e's records.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "hash_ops.cuh"
+#include "table.h"
+
+namespace vsb {
+
+constexpr int kMaxWorld = 32;
+constexpr int kPartThreads = 256;
+constexpr int kPartRounds = 8;
+constexpr uint32_t kPartTile = kPartThreads * kPartRounds;  // ops per partition tile
+static_assert(kPartThreads / 32 == kPartRounds, "k_part_push maps (round, owner) onto (warp, lane)");
+constexpr int kShardOpBlock = 128;
+constexpr unsigned kReturnCtas = 148 * 4;
+constexpr unsigned kPushCtas = 148 * 3;  // persistent partition CTAs (3 resident per SM)
+constexpr uint32_t kOrigMask = (1u << 30) - 1u;
+
+// Start of every rank's IPC window: flags and counts written by the peers.
+struct ShardHdr {
+  unsigned long long push_flag[kMaxWorld];  // [src] epoch of src's last completed push into this window
+  unsigned long long ret_flag[kMaxWorld];   // [owner] epoch of owner's last completed return into this window
+  unsigned long long cnt[kMaxWorld];        // [src] records src pushed in its last push
+  unsigned long long pad[kMaxWorld];
+};
+constexpr size_t kHdrBytes = 4096;
+static_assert(sizeof(ShardHdr) <= kHdrBytes, "header");
+
+// By-value view of the G windows for one launch.
+struct ShardView {
+  char* win[kMaxWorld];  // mapped base of every rank's window (own included)
+  int world, rank;
+  uint32_t bmax;        // per-source region capacity (records)
+  uint64_t rec_off;     // byte offset of the records in a window
+  uint64_t out_off;     // byte offset of the result bytes in a window
+};
+
+__device__ __forceinline__ ShardHdr* hdr_of(const ShardView& V, int r) { return (ShardHdr*)V.win[r]; }
+__device__ __forceinline__ int4* rec_of(const ShardView& V, int r) { return (int4*)(V.win[r] + V.rec_off); }
+__device__ __forceinline__ uint8_t* out_of(const ShardView& V, int r) { return (uint8_t*)(V.win[r] + V.out_off); }
+
+// fmix32 (MurmurHash3 finaliser) of the reference's pre-modulo hash.
+__host__ __device__ __forceinline__ uint32_t owner_of(int32_t x, int32_t y, int32_t z, uint32_t world) {
+  uint32_t h = hash_raw(x, y, z);
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h % world;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Last CTA of a grid to arrive (threadFenceReduction pattern at system
+// scope): every CTA fences its peer stores, then counts itself in.
+__device__ __forceinline__ bool last_cta(unsigned int* ctr) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    last = atomicInc(ctr, gridDim.x - 1) == gridDim.x - 1;  // wraps to 0: self-resetting
+  }
+  __syncthreads();
+  return last;
+}
+
+// ---- partition + push in ONE pass (stable, single-pass decoupled look-back)
+//
+// Tile t (2,048 ops, ids taken in launch order so every predecessor is
+// running or done) counts its ops per owner, publishes the counts, and lane
+// o of warp 0 walks back over the predecessors' per-owner status words until
+// it meets an inclusive prefix.  Status word (tile, owner) = tag(30) |
+// kind(2) | value(32); the tag is the launch epoch, so stale words of earlier
+// launches read as "not ready" and nothing is ever cleared.  Every op then
+// knows its slot in the owner's region: the tile's exclusive prefix + the
+// ops of the same owner before it inside the tile (input order kept).
+constexpr unsigned long long kAggregate = 1ull << 32, kInclusive = 2ull << 32;
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_push(ShardView V, const int32_t* __restrict__ keys,
+                                                            const uint8_t* __restrict__ ops, uint64_t n,
+                                                            unsigned long long* __restrict__ status,
+                                                            unsigned long long epoch, unsigned int* ctr) {
+  constexpr int kWarps = kPartThreads / 32;
+  __shared__ uint32_t wc[kPartRounds][kWarps][kMaxWorld];  // ops per (round, warp, owner) -> exclusive offsets
+  __shared__ uint32_t rt[kPartRounds][kMaxWorld];          // ops per (round, owner)
+  __shared__ uint32_t excl[kMaxWorld];                     // tile's exclusive prefix per owner
+  __shared__ uint32_t tile_s;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const int G = V.world;
+  const unsigned long long tag = (epoch & 0x3FFFFFFFull) << 34;
+  const uint32_t ntiles = (uint32_t)((n + kPartTile - 1) / kPartTile);
+  const size_t region = (size_t)V.rank * V.bmax;
+  // persistent CTAs take tiles in order from a counter (reset by the last CTA)
+#pragma unroll 1
+  for (;;) {
+    if (threadIdx.x == 0) tile_s = atomicAdd(ctr + 1, 1u);
+    for (uint32_t k = threadIdx.x; k < kPartRounds * kWarps * kMaxWorld; k += kPartThreads) (&wc[0][0][0])[k] = 0;
+    __syncthreads();
+    const uint32_t tile = tile_s;
+    if (tile >= ntiles) break;
+    const uint64_t t0 = (uint64_t)tile * kPartTile;
+
+    // all loads of the tile first (8 ops per thread in flight)
+    int32_t x[kPartRounds], y[kPartRounds], z[kPartRounds];
+    uint32_t op[kPartRounds], o[kPartRounds], lr[kPartRounds];
+#pragma unroll
+    for (int r = 0; r < kPartRounds; ++r) {
+      const uint64_t i = t0 + (uint64_t)r * kPartThreads + threadIdx.x;
+      o[r] = 0xFFFFFFFFu;
+      x[r] = y[r] = z[r] = 0;
+      op[r] = 0;
+      if (i < n) {
+        x[r] = ld_stream(keys + 3 * i);
+        y[r] = ld_stream(keys + 3 * i + 1);
+        z[r] = ld_stream(keys + 3 * i + 2);
+        op[r] = ld_stream(ops + i);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kPartRounds; ++r) {
+      const uint64_t i = t0 + (uint64_t)r * kPartThreads + threadIdx.x;
+      if (i < n) o[r] = owner_of(x[r], y[r], z[r], (uint32_t)G);
+      const uint32_t m = __match_any_sync(0xFFFFFFFFu, o[r]);
+      lr[r] = __popc(m & lanemask_lt());
+      if (o[r] != 0xFFFFFFFFu && (int)lane == __ffs(m) - 1) wc[r][warp][o[r]] = __popc(m);
+    }
+    __syncthreads();
+    // exclusive offsets over (round, warp) per owner: thread (round = warp id,
+    // owner = lane) scans its round's 8 warps, then rounds are combined
+    {
+      const uint32_t r = warp, ow = lane;
+      uint32_t a = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t c = wc[r][w][ow];
+        wc[r][w][ow] = a;
+        a += c;
+      }
+      rt[r][ow] = a;
+    }
+    __syncthreads();
+    {
+      const uint32_t r = warp, ow = lane;
+      uint32_t before = 0;
+      for (uint32_t q = 0; q < r; ++q) before += rt[q][ow];
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) wc[r][w][ow] += before;
+    }
+    // publish this tile's counts (aggregates first, so successors never wait
+    // on a look-back), then look back for the exclusive prefix: warp w serves
+    // owners w, w + 8, ...; its 32 lanes read a window of 32 predecessors at
+    // once and stop at the nearest inclusive prefix
+    if (warp == 0 && (int)lane < G) {
+      uint32_t agg = 0;
+#pragma unroll
+      for (int r = 0; r < kPartRounds; ++r) agg += rt[r][lane];
+      st_relaxed_u64(status + (size_t)tile * kMaxWorld + lane, tag | (tile == 0 ? kInclusive : kAggregate) | agg);
+    }
+    for (int ow = warp; ow < G; ow += kWarps) {
+      uint32_t agg = 0;
+#pragma unroll
+      for (int r = 0; r < kPartRounds; ++r) agg += rt[r][ow];
+      uint32_t pre = 0;
+      if (tile > 0) {
+        int64_t hi = (int64_t)tile - 1;  // window [hi - 31, hi]; lane l reads hi - l
+        for (;;) {
+          const int64_t j = hi - (int64_t)lane;
+          unsigned long long w = kInclusive;  // before tile 0: inclusive 0
+          if (j >= 0) {
+            const unsigned long long* pj = status + (size_t)j * kMaxWorld + ow;
+            w = ld_relaxed_u64(pj);
+            while ((w & ~0x3FFFFFFFFull) != tag) {
+              __nanosleep(20);
+              w = ld_relaxed_u64(pj);
+            }
+          }
+          const uint32_t inc = __ballot_sync(0xFFFFFFFFu, (w & kInclusive) != 0);
+          const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive (or the whole window)
+          uint32_t v = (int)lane <= stop ? (uint32_t)w : 0u;
+          v = __reduce_add_sync(0xFFFFFFFFu, v);
+          pre += v;
+          if (inc) break;
+          hi -= 32;
+        }
+        if (lane == 0) st_relaxed_u64(status + (size_t)tile * kMaxWorld + ow, tag | kInclusive | (uint32_t)(pre + agg));
+      }
+      if (lane == 0) excl[ow] = pre;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kPartRounds; ++r) {
+      if (o[r] == 0xFFFFFFFFu) continue;
+      const uint64_t i = t0 + (uint64_t)r * kPartThreads + threadIdx.x;
+      const uint32_t off = excl[o[r]] + wc[r][warp][o[r]] + lr[r];
+      int4 rec;
+      rec.x = x[r];
+      rec.y = y[r];
+      rec.z = z[r];
+      rec.w = (int)((op[r] << 30) | (uint32_t)i);
+      rec_of(V, o[r])[region + off] = rec;  // peer store over NVLink (local for o == rank)
+    }
+    __syncthreads();  // wc / excl are rewritten by the next tile
+  }
+  if (last_cta(ctr) && (int)threadIdx.x < G) {
+    // every tile is done: the last tile's inclusive prefix is the total
+    const int ow = threadIdx.x;
+    if (ow == 0) ctr[1] = 0;  // every CTA took its last ticket before arriving
+    const uint32_t total = ntiles ? (uint32_t)ld_relaxed_u64(status + (size_t)(ntiles - 1) * kMaxWorld + ow) : 0u;
+    __threadfence_system();
+    ShardHdr* h = hdr_of(V, ow);
+    st_relaxed_sys(&h->cnt[V.rank], total);
+    st_release_sys(&h->push_flag[V.rank], epoch);
+  }
+}
+
+// Acquire flags[0..world) >= epoch.  Bounded: after `timeout_ns` the error
+// word gets bit 1 and the kernel returns (a peer that never arrives must not
+// hang the GPU).
+__global__ void k_wait(const unsigned long long* flags, int world, unsigned long long epoch, unsigned int* err,
+                       uint64_t timeout_ns) {
+  const int r = threadIdx.x;
+  if (r >= world) return;
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire_sys(flags + r) < epoch) {
+    __nanosleep(200);
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicOr(err, 2u);
+      return;
+    }
+  }
+}
+
+// Routed op v (the concatenation of the G source regions, source-major):
+// region r and record position p of v from the per-source counts, whose
+// prefix sums every CTA keeps in shared memory.
+struct Routed {
+  const uint32_t* pre;  // shared [world + 1]
+  int world;
+  uint32_t bmax;
+  __device__ __forceinline__ uint32_t total() const { return pre[world]; }
+  __device__ __forceinline__ size_t pos(uint32_t v, int* region) const {
+    int r = 0;
+    while (r + 1 < world && pre[r + 1] <= v) ++r;
+    *region = r;
+    return (size_t)r * bmax + (v - pre[r]);
+  }
+};
+
+// Every thread of the CTA must call it (barrier inside).
+__device__ __forceinline__ Routed load_routed(const ShardView& V, uint32_t* spre) {
+  if (threadIdx.x == 0) {
+    const ShardHdr* h = hdr_of(V, V.rank);
+    uint32_t a = 0;
+    spre[0] = 0;
+    for (int r = 0; r < V.world; ++r) spre[r + 1] = a += (uint32_t)h->cnt[r];
+  }
+  __syncthreads();
+  Routed R;
+  R.pre = spre;
+  R.world = V.world;
+  R.bmax = V.bmax;
+  return R;
+}
+
+__global__ void __launch_bounds__(kShardOpBlock) k_shard_apply(TableView T, ShardView V, uint8_t* __restrict__ res,
+                                                               int32_t* __restrict__ idx) {
+  __shared__ uint32_t spre[kMaxWorld + 1];
+  const Routed R = load_routed(V, spre);
+  const int4* rec = rec_of(V, V.rank);
+  const uint32_t total = R.total();
+  int delta = 0;
+#pragma unroll 1
+  for (uint32_t v = blockIdx.x * kShardOpBlock + threadIdx.x; v < total; v += gridDim.x * kShardOpBlock) {
+    int r;
+    const int4 q = __ldcs(rec + R.pos(v, &r));
+    const uint32_t b = bucket_of(T, q.x, q.y, q.z);
+    const int4 pre = ld_bucket(T.e + b);
+    delta += apply_one(T, q.x, q.y, q.z, (uint8_t)((uint32_t)q.w >> 30), v, b, pre, res, idx);
+  }
+  add_size_cta(T, delta);
+}
+
+__global__ void __launch_bounds__(256) k_shard_post(TableView T, ShardView V, uint8_t* __restrict__ res,
+                                                    const int32_t* __restrict__ idx) {
+  __shared__ uint32_t spre[kMaxWorld + 1];
+  const Routed R = load_routed(V, spre);
+  const int4* rec = rec_of(V, V.rank);
+  const uint32_t total = R.total();
+#pragma unroll 1
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < total; v += gridDim.x * blockDim.x) {
+    int r;
+    const int4 q = rec[R.pos(v, &r)];
+    post_op_t(
+        T,
+        [&](uint64_t m) {
+          int rm;
+          const int4 p = rec[R.pos((uint32_t)m, &rm)];
+          return p.x == q.x && p.y == q.y && p.z == q.z;
+        },
+        v, (uint8_t)((uint32_t)q.w >> 30), res, idx[v]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_shard_return(ShardView V, const uint8_t* __restrict__ res,
+                                                      unsigned long long epoch, unsigned int* ctr) {
+  __shared__ uint32_t spre[kMaxWorld + 1];
+  const Routed R = load_routed(V, spre);
+  const int4* rec = rec_of(V, V.rank);
+  const uint32_t total = R.total();
+  const uint32_t stride = gridDim.x * blockDim.x;
+#pragma unroll 1
+  for (uint32_t v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < total; v0 += 4 * stride) {
+    // four independent record loads in flight before the stores
+    uint32_t w[4];
+    uint8_t b[4];
+    int r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t v = v0 + k * stride;
+      if (v < total) {
+        w[k] = (uint32_t)__ldcs(&rec[R.pos(v, &r[k])].w);
+        b[k] = res[v];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (v0 + k * stride < total) out_of(V, r[k])[w[k] & kOrigMask] = b[k];  // peer store into the source's window
+  }
+  if (last_cta(ctr) && threadIdx.x < V.world) {
+    __threadfence_system();
+    st_release_sys(&hdr_of(V, threadIdx.x)->ret_flag[V.rank], epoch);
+  }
+}
+
+}  // namespace vsb
+
+using namespace vsb;
+
+struct vs_shard {
+  vs_table* table = nullptr;
+  int device = 0, rank = 0, world = 1;
+  uint32_t bmax = 0, ntiles_max = 0;
+  char* win = nullptr;  // own window (cudaMalloc, exported over CUDA IPC)
+  size_t win_bytes = 0, rec_off = 0, out_off = 0;
+  char* peer[kMaxWorld] = {};
+  bool opened[kMaxWorld] = {};
+  bool connected = false;
+  // local workspace
+  unsigned long long* status = nullptr;  // [ntiles_max][kMaxWorld] look-back words
+  unsigned int* ctl = nullptr;  // [0] push CTA counter, [32] return CTA counter, [64] error word
+  uint8_t* res = nullptr;
+  int32_t* idx = nullptr;
+  unsigned long long epoch = 0;
+  uint64_t timeout_ns = 20ull * 1000000000ull;
+
+  ShardView view() const {
+    ShardView v;
+    memset(&v, 0, sizeof(v));
+    for (int r = 0; r < world; ++r) v.win[r] = peer[r];
+    v.world = world;
+    v.rank = rank;
+    v.bmax = bmax;
+    v.rec_off = rec_off;
+    v.out_off = out_off;
+    return v;
+  }
+};
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+extern "C" {
+
+vs_status vs_shard_create(vs_table* local, int rank, int world, uint64_t max_batch, vs_shard** out) {
+  if (!local || !out || world < 1 || world > kMaxWorld || rank < 0 || rank >= world || max_batch < 1 ||
+      max_batch > kOrigMask + 1ull || (uint64_t)world * max_batch > 0x7FFFFFFFull) {
+    set_error("vs_shard_create: need 1 <= world <= 32, 0 <= rank < world, 1 <= max_batch <= 2^30, world*max_batch < 2^31");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(local->device);
+  vs_shard* s = new vs_shard();
+  s->table = local;
+  s->device = local->device;
+  s->rank = rank;
+  s->world = world;
+  s->bmax = (uint32_t)max_batch;
+  s->ntiles_max = (uint32_t)((max_batch + kPartTile - 1) / kPartTile);
+  s->rec_off = kHdrBytes;
+  s->out_off = align_up(s->rec_off + (size_t)world * max_batch * sizeof(int4), 256);
+  s->win_bytes = align_up(s->out_off + max_batch, 4096);
+  cudaError_t e = cudaMalloc(&s->win, s->win_bytes);
+  if (e == cudaSuccess) e = cudaMemset(s->win, 0, kHdrBytes);
+  if (e == cudaSuccess) e = cudaMalloc(&s->status, (size_t)s->ntiles_max * kMaxWorld * 8);
+  if (e == cudaSuccess) e = cudaMemset(s->status, 0, (size_t)s->ntiles_max * kMaxWorld * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&s->ctl, 128 * 4);
+  if (e == cudaSuccess) e = cudaMemset(s->ctl, 0, 128 * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->res, (size_t)world * max_batch);
+  if (e == cudaSuccess) e = cudaMalloc(&s->idx, (size_t)world * max_batch * 4);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    vs_shard_destroy(s);
+    return cuda_status(e, "vs_shard_create");
+  }
+  s->peer[rank] = s->win;
+  if (world == 1) s->connected = true;
+  *out = s;
+  return VS_OK;
+}
+
+vs_status vs_shard_export(vs_shard* s, uint8_t handle_out[64]) {
+  if (!s || !handle_out) {
+    set_error("vs_shard_export: NULL argument");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(s->device);
+  cudaIpcMemHandle_t h;
+  VS_CK(cudaIpcGetMemHandle(&h, s->win));
+  static_assert(sizeof(h) == 64, "ipc handle size");
+  memcpy(handle_out, &h, 64);
+  return VS_OK;
+}
+
+vs_status vs_shard_connect(vs_shard* s, const uint8_t* handles) {
+  if (!s || !handles) {
+    set_error("vs_shard_connect: NULL argument");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(s->device);
+  for (int r = 0; r < s->world; ++r) {
+    if (r == s->rank || s->opened[r]) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + 64 * (size_t)r, 64);
+    void* p = nullptr;
+    VS_CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    s->peer[r] = (char*)p;
+    s->opened[r] = true;
+  }
+  s->connected = true;
+  return VS_OK;
+}
+
+vs_status vs_shard_apply(vs_shard* s, const int32_t* keys, const uint8_t* ops, uint64_t n, uint8_t* result,
+                         vs_stream_t stream) {
+  if (!s || !s->connected) {
+    set_error("vs_shard_apply: shard not connected (vs_shard_connect)");
+    return VS_ERR_INVALID;
+  }
+  if (n > s->bmax || (n && (!keys || !ops || !result))) {
+    set_error("vs_shard_apply: n > max_batch or NULL buffer");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(s->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned long long ep = ++s->epoch;
+  const ShardView V = s->view();
+  const uint32_t ntiles = n ? (uint32_t)((n + kPartTile - 1) / kPartTile) : 1u;
+  ShardHdr* own = (ShardHdr*)s->win;
+  k_part_push<<<ntiles < kPushCtas ? ntiles : kPushCtas, kPartThreads, 0, st>>>(V, keys, ops, n, s->status, ep,
+                                                                               s->ctl);
+  count_launch();
+  k_wait<<<1, 32, 0, st>>>(own->push_flag, s->world, ep, s->ctl + 64, s->timeout_ns);
+  count_launch();
+  // incoming ~ n per rank when the keys hash evenly; the grid-stride loops
+  // cover any skew
+  const uint64_t hint = n + n / 8 + 4096;
+  const TableView T = s->table->next_view();
+  {
+    ProfScope prof(0, st);
+    k_shard_apply<<<grid_for(hint, kShardOpBlock), kShardOpBlock, 0, st>>>(T, V, s->res, s->idx);
+    count_launch();
+  }
+  k_shard_post<<<grid_for(hint, 256), 256, 0, st>>>(T, V, s->res, s->idx);
+  count_launch();
+  // bounded grid: the last-CTA signal costs one same-address atomic per CTA
+  k_shard_return<<<kReturnCtas, 256, 0, st>>>(V, s->res, ep, s->ctl + 32);
+  count_launch();
+  k_wait<<<1, 32, 0, st>>>(own->ret_flag, s->world, ep, s->ctl + 64, s->timeout_ns);
+  count_launch();
+  if (n) VS_CK(cudaMemcpyAsync(result, s->win + s->out_off, n, cudaMemcpyDeviceToDevice, st));
+  VS_CK_LAUNCH("vs_shard_apply");
+  return VS_OK;
+}
+
+vs_status vs_shard_check(vs_shard* s) {
+  if (!s) {
+    set_error("vs_shard_check: NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(s->device);
+  unsigned int err = 0;
+  VS_CK(cudaMemcpy(&err, s->ctl + 64, 4, cudaMemcpyDeviceToHost));
+  if (err & 2u) {
+    set_error("vs_shard: a peer did not arrive within the timeout (collective call mismatch?)");
+    return VS_ERR_CUDA;
+  }
+  return VS_OK;
+}
+
+vs_status vs_shard_owner(const int32_t* keys, uint64_t n, int world, int32_t* owner_out) {
+  if (world < 1 || (n && (!keys || !owner_out))) {
+    set_error("vs_shard_owner: bad arguments");
+    return VS_ERR_INVALID;
+  }
+  for (uint64_t i = 0; i < n; ++i)
+    owner_out[i] = (int32_t)owner_of(keys[3 * i], keys[3 * i + 1], keys[3 * i + 2], (uint32_t)world);
+  return VS_OK;
+}
+
+void vs_shard_destroy(vs_shard* s) {
+  if (!s) return;
+  DeviceGuard g(s->device);
+  for (int r = 0; r < kMaxWorld; ++r)
+    if (s->opened[r]) cudaIpcCloseMemHandle(s->peer[r]);
+  cudaFree(s->win);
+  cudaFree(s->status);
+  cudaFree(s->ctl);
+  cudaFree(s->res);
+  cudaFree(s->idx);
+  delete s;
+}
+
+}  // extern "C"

@@ -3,7 +3,20 @@
 Every rank owns one partition of the key space: owner(k) = fmix32(h(k)) mod
 G, where h is the reference's pre-modulo spatial hash (concurrent_hash.py:58)
 and fmix32 (MurmurHash3 finaliser) decorrelates the owner from the local
-bucket h mod n.  A batch is routed to the owners and back:
+bucket h mod n.
+
+Two exchanges route a batch to the owners and back.
+
+``exchange="peer"`` (the product path on GPUs; csrc/shard.cu): every rank
+maps every other rank's receive window over CUDA IPC (NVLink/NVSwitch), and
+the kernels themselves store each op's 16-byte record into its owner's
+window, apply the owner's ops, and store each result byte back into the
+source's window -- one stream-ordered call per batch, no host
+synchronisation, no NCCL.  The windows are exchanged once, at construction,
+over the process group.
+
+``exchange="collective"`` (the parity reference for the peer path, and the
+CPU/gloo path of the multi-process tests):
 
   1. owner of every op, stable partition of the batch by owner
   2. all-to-all of the per-owner counts
@@ -38,18 +51,96 @@ class ShardedBlockHashSet:
     """A block hash set partitioned over the ranks of a process group.
 
     ``local`` is the rank's own table (a BlockHashSet on its GPU; tests may
-    pass any object with the same ``apply`` signature).
+    pass any object with the same ``apply`` signature).  ``exchange``:
+    "peer" (kernel peer stores over CUDA IPC windows; needs a BlockHashSet
+    on a CUDA device), "collective" (all-to-all over the process group), or
+    "auto" (peer when the local table is a device table, else collective).
+    ``max_batch`` bounds the ops per ``apply`` call on the peer path (it
+    sizes the windows: world x max_batch x 16 B per rank).
     """
 
-    def __init__(self, local, group=None) -> None:
+    def __init__(self, local, group=None, exchange: str = "auto", max_batch: int = 1 << 22) -> None:
         import torch.distributed as dist
 
+        if exchange not in ("auto", "peer", "collective"):
+            raise ValueError(f"unknown exchange {exchange!r}")
         self.local = local
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.backend = dist.get_backend(group)
         self._stage = False
+        self._shard = None
+        self.max_batch = int(max_batch)
+        device_table = getattr(local, "handle", None) is not None and getattr(local, "device", None) is not None \
+            and getattr(local.device, "type", None) == "cuda"
+        if exchange == "peer" and not device_table:
+            raise ValueError("exchange='peer' needs a BlockHashSet on a CUDA device")
+        self.exchange = "peer" if (exchange == "peer" or (exchange == "auto" and device_table)) else "collective"
+        if self.exchange == "peer":
+            self._connect()
+
+    # -- peer-window exchange (csrc/shard.cu) ------------------------------
+
+    def _connect(self) -> None:
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+
+        lib = _lib.load()
+        h = ctypes.c_void_p()
+        _lib.check(lib.vs_shard_create(self.local.handle, self.rank, self.world, self.max_batch, ctypes.byref(h)),
+                   "vs_shard_create")
+        self._lib = lib
+        self._shard = h
+        mine = (ctypes.c_uint8 * 64)()
+        _lib.check(lib.vs_shard_export(h, ctypes.byref(mine)), "vs_shard_export")
+        handles: list = [None] * self.world
+        dist.all_gather_object(handles, bytes(mine), group=self.group)
+        _lib.check(lib.vs_shard_connect(h, b"".join(handles)), "vs_shard_connect")
+        # every rank mapped every window before anyone stores into one
+        dist.barrier(group=self.group)
+
+    def __del__(self) -> None:
+        h = getattr(self, "_shard", None)
+        if h is not None and h.value:
+            try:
+                self._lib.vs_shard_destroy(h)
+            except Exception:
+                pass
+            self._shard = None
+
+    def check(self) -> None:
+        """Raise if a peer wait timed out (mismatched collective calls)."""
+        if self._shard is not None:
+            from . import _lib
+
+            _lib.check(self._lib.vs_shard_check(self._shard), "vs_shard")
+
+    def _apply_peer(self, keys, ops):
+        import ctypes
+
+        import torch
+
+        from . import _lib
+
+        loc = self.local
+        n = keys.shape[0]
+        if n > self.max_batch:
+            raise ValueError(f"batch of {n} ops exceeds max_batch={self.max_batch} of the shard windows")
+        with loc._mutex:
+            k = loc._keys(keys)
+            o = ops.to(loc.device, torch.uint8).contiguous()
+            if o.shape[0] != n:
+                raise ValueError("ops and keys differ in length")
+            out = torch.empty(n, dtype=torch.uint8, device=loc.device)
+            s = loc._stream()
+            _lib.check(self._lib.vs_shard_apply(self._shard, _lib.ptr(k), _lib.ptr(o), n, _lib.ptr(out),
+                                                ctypes.c_void_p(s.cuda_stream)), "vs_shard_apply")
+            loc._done(s)
+        return out
 
     def _a2a(self, out, inp, out_splits=None, in_splits=None):
         """all_to_all_single; staged through host memory when the backend
@@ -68,6 +159,8 @@ class ShardedBlockHashSet:
         the per-op results in input order.  Collective: every rank calls it."""
         import torch
 
+        if self.exchange == "peer":
+            return self._apply_peer(keys, ops)
         dev = keys.device
         self._stage = dev.type == "cuda" and self.backend == "gloo"
         own = owner_of(keys, self.world)

@@ -1,7 +1,12 @@
-"""Two ranks sharing one B200: the sharded router with the real GPU tables
-(exchanges over gloo, staged through host memory -- NCCL needs one GPU per
-rank).  Per-op results must equal the analytic expectation of the A18
-workload, every key must live on its owner, the global size must add up."""
+"""Two ranks sharing one B200: the sharded hash set with the real GPU tables,
+through both exchanges -- "peer" (csrc/shard.cu: the kernels store records
+and results straight into CUDA-IPC-mapped windows of the other rank) and
+"collective" (all-to-all over the process group; gloo here, staged through
+host memory, because NCCL needs one GPU per rank).  Per-op results must
+equal the analytic expectation of the A18 workload, every key must live on
+its owner, the global size must add up, and duplicate fresh inserts across
+ranks must resolve like a sequential replay of rank 0's batch, then rank
+1's (the lowest routed index creates)."""
 
 from __future__ import annotations
 
@@ -24,9 +29,12 @@ from paper_1805_03709_b200.shard import ShardedBlockHashSet, owner_of
 
 dist.init_process_group("gloo")
 rank, world = dist.get_rank(), dist.get_world_size()
+exch = os.environ["EXCH"]
 dev = torch.device("cuda", 0)
 spec = workloads.MixSpec(live=50_000, load_factor=0.7, batch=1 << 14)
-shard = ShardedBlockHashSet(BlockHashSet(spec.bucket_count, spec.excess, device=dev))
+shard = ShardedBlockHashSet(BlockHashSet(spec.bucket_count, spec.excess, device=dev), exchange=exch,
+                            max_batch=1 << 16)
+assert shard.exchange == exch
 base = rank << 40
 init = workloads.id_to_key_torch(torch.arange(base, base + spec.live, device=dev))
 r = shard.apply(init, torch.zeros(spec.live, dtype=torch.uint8, device=dev))
@@ -39,9 +47,29 @@ for step in range(4):
     ids, ops, expect = workloads.mix_batch_ids(spec, step, lo, hi, gen, dev)
     ids = torch.where(ids >= workloads.MISS_BASE, ids + (rank << 50), ids)
     res = shard.apply(workloads.id_to_key_torch(ids), ops)
-    assert torch.equal(res, expect), (rank, step)
+    assert torch.equal(res, expect), (rank, step, int((res != expect).sum()))
     lo += spec.counts["erase"]; hi += spec.counts["fresh"]
 assert shard.size() == world * spec.live
+
+# duplicate fresh inserts across and within ranks: the same 300 new keys on
+# both ranks, each twice on a rank (positions i and i + 300); finds of them
+# in the same batch would break A18, so only inserts
+shared = workloads.id_to_key_torch(torch.arange(7 << 45, (7 << 45) + 300, device=dev))
+keys = torch.cat([shared, shared])
+r = shard.apply(keys, torch.zeros(600, dtype=torch.uint8, device=dev))
+want = torch.zeros(600, dtype=torch.uint8, device=dev)
+if rank == 0:
+    want[:300] = 1
+assert torch.equal(r, want), (rank, r.sum().item())
+# empty batch on one rank, a batch on the other: still collective-safe
+if rank == 0:
+    r = shard.apply(shared[:0], torch.zeros(0, dtype=torch.uint8, device=dev))
+    assert r.numel() == 0
+else:
+    r = shard.apply(shared, torch.full((300,), 2, dtype=torch.uint8, device=dev))
+    assert int(r.sum()) == 300
+assert shard.size() == world * spec.live
+shard.check()
 a = shard.local.audit()
 assert a["duplicates"] == 0 and a["unreachable_live"] == 0
 print("RANK_OK", rank, flush=True)
@@ -49,13 +77,58 @@ dist.destroy_process_group()
 '''
 
 
-def test_two_ranks_one_gpu_routing(tmp_path, dev):
+@pytest.mark.parametrize("exch,port", [("peer", 29546), ("collective", 29544)])
+def test_two_ranks_one_gpu_routing(tmp_path, dev, exch, port):
     w = tmp_path / "worker.py"
     w.write_text(WORKER)
-    env = dict(os.environ, ROOT=str(ROOT), OMP_NUM_THREADS="1")
+    env = dict(os.environ, ROOT=str(ROOT), OMP_NUM_THREADS="1", EXCH=exch)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", "--master-port=29544", str(w)]
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(w)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-3000:]
     assert out.count("RANK_OK") == 2, out[-3000:]
+
+
+def test_peer_single_rank_equals_table(tmp_path, dev):
+    """world 1: the peer path (partition, self-window, routed apply, return)
+    gives exactly the plain table's per-op results on the config-2 mix."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1805_03709_b200 import BlockHashSet, workloads
+    from paper_1805_03709_b200.shard import ShardedBlockHashSet
+
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1)
+    try:
+        spec = workloads.MixSpec(live=200_000, load_factor=0.7, batch=1 << 16)
+        a = BlockHashSet(spec.bucket_count, spec.excess, device=dev)
+        b = BlockHashSet(spec.bucket_count, spec.excess, device=dev)
+        sh = ShardedBlockHashSet(b, exchange="peer", max_batch=spec.live)
+        init = workloads.id_to_key_torch(torch.arange(spec.live, device=dev))
+        a.insert_keys(init)
+        assert int(sh.apply(init, torch.zeros(spec.live, dtype=torch.uint8, device=dev)).sum()) == spec.live
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(5)
+        lo, hi = 0, spec.live
+        for step in range(3):
+            ids, ops, expect = workloads.mix_batch_ids(spec, step, lo, hi, gen, dev)
+            k = workloads.id_to_key_torch(ids)
+            ra = a.apply(k, ops)[0]
+            rb = sh.apply(k, ops)
+            assert torch.equal(ra, expect) and torch.equal(rb, expect)
+            lo += spec.counts["erase"]
+            hi += spec.counts["fresh"]
+        # duplicates inside one batch: lowest index creates, as the table
+        k = workloads.id_to_key_torch(torch.arange(1 << 44, (1 << 44) + 1000, device=dev))
+        k = torch.cat([k, k.flip(0), k])
+        z = torch.zeros(k.shape[0], dtype=torch.uint8, device=dev)
+        assert torch.equal(a.apply(k, z)[0], sh.apply(k, z))
+        ka, _ = a.snapshot_tensor()
+        kb, _ = b.snapshot_tensor()
+        assert a.approx_size() == b.approx_size()
+        assert set(map(tuple, ka.tolist())) == set(map(tuple, kb.tolist()))
+        sh.check()
+    finally:
+        dist.destroy_process_group()
