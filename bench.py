@@ -41,6 +41,8 @@ BYTES_PER_BLOCK = 8704  # 6144 TSDF read + 2048 MC write + 512 quantised write
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--exchange", default="auto", choices=["auto", "peer", "collective"],
+                   help="sharded routing at N>1: kernel peer stores (auto/peer) or NCCL all-to-all")
     p.add_argument("--steps", type=int, default=300)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
@@ -199,7 +201,7 @@ def sync_max(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -228,7 +230,7 @@ def run_hash(args, dev, rank, world):
     if world > 1:
         from paper_1805_03709_b200.shard import ShardedBlockHashSet
 
-        router = ShardedBlockHashSet(s)
+        router = ShardedBlockHashSet(s, exchange=args.exchange, max_batch=B)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + rank)
     # initial fill: `live` keys (routed when sharded)
@@ -264,7 +266,7 @@ def run_hash(args, dev, rank, world):
         r = step_fn(i)
         ok &= bool(torch.equal(r, batches[i][2]))
     s.check_capacity()
-    clocks = Clocks(dev.index if world == 1 else int(os.environ.get("LOCAL_RANK", 0)))
+    clocks = Clocks(dev.index)
     barrier(world)
     clocks.start()
     time.sleep(0.12)  # let the sampler attach before the region starts
@@ -291,6 +293,7 @@ def run_hash(args, dev, rank, world):
     peak, peak_src = peaks()
     out = {
         "value": value, "ms_per_step": ms / args.steps, "ok": ok and size_ok, "clocks": clk,
+        "exchange": router.exchange if router else None,
         "gpu_launches": prof.launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic("k_apply"), "kernel": "vsb::k_apply",
@@ -300,7 +303,7 @@ def run_hash(args, dev, rank, world):
     # ---- e2e through the public API with pinned host buffers: H2D of keys +
     # ops, the apply launch and the D2H of the per-op result flags overlap
     # across steps on three streams (copy-in, compute, copy-out)
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
         extra = batches[n_total:]
         E = len(extra)
         hk = [b[0].cpu().pin_memory() for b in extra]
@@ -311,7 +314,7 @@ def run_hash(args, dev, rank, world):
         comp = torch.cuda.current_stream(dev)
         cin, cout = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         free = [torch.cuda.Event() for _ in range(2)]
-        torch.cuda.synchronize()
+        barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         e0.record(comp)
@@ -327,7 +330,7 @@ def run_hash(args, dev, rank, world):
                 ready = torch.cuda.Event()
                 ready.record(cin)
             comp.wait_event(ready)
-            res, _ = s.apply(dk[slot], do[slot])
+            res = router.apply(dk[slot], do[slot]) if router else s.apply(dk[slot], do[slot])[0]
             free[slot].record(comp)
             done = torch.cuda.Event()
             done.record(comp)
@@ -341,12 +344,13 @@ def run_hash(args, dev, rank, world):
         e1.record(comp)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        e_ms = e0.elapsed_time(e1)
+        e_ms = sync_max(e0.elapsed_time(e1), world)
         e2e_ok = all(torch.equal(hr[j], extra[j][2].cpu()) for j in range(E))
-        out["e2e"] = {"value": E * B / (e_ms / 1e3) / 1e6, "unit": "M ops/s",
+        out["e2e"] = {"value": E * B * world / (e_ms / 1e3) / 1e6, "unit": "M ops/s",
                       "h2d_bytes_per_step": B * 13, "d2h_bytes_per_step": B * 1, "steps": E,
                       "wall_s": wall, "ok": e2e_ok,
-                      "note": "BlockHashSet.apply on pinned host keys+ops; per-op result flags read back; "
+                      "note": ("ShardedBlockHashSet.apply" if router else "BlockHashSet.apply") +
+                              " on pinned host keys+ops; per-op result flags read back; "
                               "copy-in / compute / copy-out overlapped on three streams"}
     del batches, results
     return out
@@ -618,6 +622,9 @@ def main():
               "mix": spec.counts, "key_space": "int3 in [-2^20, 2^20)^3 (injective id map)",
               "l2": "inputs larger than L2: 229 MB table + fresh 55 MB batch per step",
               "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU"}
+    if world > 1:
+        config["exchange"] = ("peer stores into CUDA-IPC windows over NVLink (csrc/shard.cu)" if args.exchange != "collective"
+                              else "NCCL all-to-all (shard.py collective path)")
 
     if args.impl == "reference":
         # reference arm: the C oracle port of the reference algorithm on host cores
@@ -641,11 +648,19 @@ def main():
 
     import torch
 
+    # VSB_BENCH_ONE_GPU=1: every rank on cuda:0 over gloo -- a functional
+    # check of the multi-rank path on a one-GPU box (numbers not meaningful)
+    one_gpu = os.environ.get("VSB_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     h = run_hash(args, dev, rank, world)
@@ -679,7 +694,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        oks = torch.tensor([1.0 if h["ok"] else 0.0], device=dev)
+        oks = torch.tensor([1.0 if h["ok"] else 0.0], device=dev if not one_gpu else "cpu")
         dist.all_reduce(oks, op=dist.ReduceOp.MIN)
         h["ok"] = bool(oks.item() > 0)
     if rank == 0:

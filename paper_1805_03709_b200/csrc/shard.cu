@@ -8,10 +8,11 @@
 // collective route (partition -> all-to-all counts -> all-to-all records ->
 // apply -> all-to-all results -> scatter, shard.py's NCCL path), every rank
 // maps every other rank's receive window (CUDA IPC over NVLink/NVSwitch) and
-// one batch is six stream-ordered kernels with no host synchronisation:
+// one batch is eight stream-ordered kernels with no host synchronisation:
 //
-//   k_part_push    single-pass stable partition by owner (decoupled look-back
-//                  over 2,048-op tiles); each op's 16-B record {x, y, z,
+//   k_wpart_count  ops per owner in every warp tile (256 ops)
+//   k_wpart_scan   one CTA per owner: exclusive scan over the warp tiles
+//   k_wpart_push   stable placement: each op's 16-B record {x, y, z,
 //                  op<<30 | input index} is STORED STRAIGHT INTO THE OWNER'S
 //                  WINDOW (region of this source rank, input order kept);
 //                  the last CTA publishes the per-owner counts and a release
@@ -43,11 +44,8 @@ namespace vsb {
 constexpr int kMaxWorld = 32;
 constexpr int kPartThreads = 256;
 constexpr int kPartRounds = 8;
-constexpr uint32_t kPartTile = kPartThreads * kPartRounds;  // ops per partition tile
-static_assert(kPartThreads / 32 == kPartRounds, "k_part_push maps (round, owner) onto (warp, lane)");
 constexpr int kShardOpBlock = 128;
 constexpr unsigned kReturnCtas = 148 * 4;
-constexpr unsigned kPushCtas = 148 * 3;  // persistent partition CTAs (3 resident per SM)
 constexpr uint32_t kOrigMask = (1u << 30) - 1u;
 
 // Start of every rank's IPC window: flags and counts written by the peers.
@@ -67,6 +65,7 @@ struct ShardView {
   uint32_t bmax;        // per-source region capacity (records)
   uint64_t rec_off;     // byte offset of the records in a window
   uint64_t out_off;     // byte offset of the result bytes in a window
+  uint64_t wmagic;      // fastmod_magic(world)
 };
 
 __device__ __forceinline__ ShardHdr* hdr_of(const ShardView& V, int r) { return (ShardHdr*)V.win[r]; }
@@ -74,14 +73,21 @@ __device__ __forceinline__ int4* rec_of(const ShardView& V, int r) { return (int
 __device__ __forceinline__ uint8_t* out_of(const ShardView& V, int r) { return (uint8_t*)(V.win[r] + V.out_off); }
 
 // fmix32 (MurmurHash3 finaliser) of the reference's pre-modulo hash.
-__host__ __device__ __forceinline__ uint32_t owner_of(int32_t x, int32_t y, int32_t z, uint32_t world) {
+__host__ __device__ __forceinline__ uint32_t owner_mix(int32_t x, int32_t y, int32_t z) {
   uint32_t h = hash_raw(x, y, z);
   h ^= h >> 16;
   h *= 0x85EBCA6Bu;
   h ^= h >> 13;
   h *= 0xC2B2AE35u;
   h ^= h >> 16;
-  return h % world;
+  return h;
+}
+__host__ __device__ __forceinline__ uint32_t owner_of(int32_t x, int32_t y, int32_t z, uint32_t world) {
+  return owner_mix(x, y, z) % world;
+}
+// same, with the modulo by Lemire fastmod (M = fastmod_magic(world))
+__device__ __forceinline__ uint32_t owner_fast(int32_t x, int32_t y, int32_t z, uint64_t M, uint32_t world) {
+  return fastmod(owner_mix(x, y, z), M, world);
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -114,160 +120,182 @@ __device__ __forceinline__ bool last_cta(unsigned int* ctr) {
   return last;
 }
 
-// ---- partition + push in ONE pass (stable, single-pass decoupled look-back)
-//
-// Tile t (2,048 ops, ids taken in launch order so every predecessor is
-// running or done) counts its ops per owner, publishes the counts, and lane
-// o of warp 0 walks back over the predecessors' per-owner status words until
-// it meets an inclusive prefix.  Status word (tile, owner) = tag(30) |
-// kind(2) | value(32); the tag is the launch epoch, so stale words of earlier
-// launches read as "not ready" and nothing is ever cleared.  Every op then
-// knows its slot in the owner's region: the tile's exclusive prefix + the
-// ops of the same owner before it inside the tile (input order kept).
-constexpr unsigned long long kAggregate = 1ull << 32, kInclusive = 2ull << 32;
+// ---- stable partition by owner (measured at world 1, 2^22 ops: count 14 us,
+// scan 10 us, push 44 us; a single-pass decoupled look-back variant took
+// 72 us and a CTA-tile count/scan/push 77 us -- the barrier-free warp tiles
+// win).  Every warp owns a tile of
+// 32 x kPartRounds ops and works without CTA barriers -- per-owner counts
+// per warp tile, one CTA per owner scans them, and the push places every op
+// at (tile offset + same-owner ops before it in the tile), input order kept.
+constexpr uint32_t kWTile = 32 * kPartRounds;
 
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// The warp's tile of keys (and op codes) is staged through warp-private
+// shared memory with 16-byte coalesced loads when the tile is whole and the
+// buffers 16-B aligned; lane l then takes op r*32+l of round r (stride-3
+// words: bank-conflict free).
+struct WarpStage {
+  int32_t k[3 * kWTile];
+  uint8_t op[kWTile];
+};
+
+__device__ __forceinline__ void load_rounds(const int32_t* __restrict__ keys, const uint8_t* __restrict__ ops,
+                                            uint64_t n, uint64_t t0, WarpStage& S, int32_t* x, int32_t* y, int32_t* z,
+                                            uint32_t* op) {
+  const uint32_t lane = lane_id();
+  const bool whole = t0 + kWTile <= n && ((uintptr_t)keys & 15) == 0 && (!ops || ((uintptr_t)ops & 15) == 0);
+  if (whole) {
+    const int4* kv = (const int4*)(keys + 3 * t0);
+#pragma unroll
+    for (int q = 0; q < 3 * kWTile / 4 / 32; ++q) ((int4*)S.k)[q * 32 + lane] = __ldcs(kv + q * 32 + lane);
+    if (ops && lane < kWTile / 16) ((int4*)S.op)[lane] = __ldcs((const int4*)(ops + t0) + lane);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kPartRounds; ++r) {
+      const uint32_t j = r * 32 + lane;
+      x[r] = S.k[3 * j];
+      y[r] = S.k[3 * j + 1];
+      z[r] = S.k[3 * j + 2];
+      if (op) op[r] = S.op[j];
+    }
+    __syncwarp();
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < kPartRounds; ++r) {
+    const uint64_t i = t0 + (uint64_t)r * 32 + lane;
+    x[r] = y[r] = z[r] = 0;
+    if (op) op[r] = 0;
+    if (i < n) {
+      x[r] = ld_stream(keys + 3 * i);
+      y[r] = ld_stream(keys + 3 * i + 1);
+      z[r] = ld_stream(keys + 3 * i + 2);
+      if (op) op[r] = ld_stream(ops + i);
+    }
+  }
 }
 
-__global__ void __launch_bounds__(kPartThreads) k_part_push(ShardView V, const int32_t* __restrict__ keys,
-                                                            const uint8_t* __restrict__ ops, uint64_t n,
-                                                            unsigned long long* __restrict__ status,
-                                                            unsigned long long epoch, unsigned int* ctr) {
-  constexpr int kWarps = kPartThreads / 32;
-  __shared__ uint32_t wc[kPartRounds][kWarps][kMaxWorld];  // ops per (round, warp, owner) -> exclusive offsets
-  __shared__ uint32_t rt[kPartRounds][kMaxWorld];          // ops per (round, owner)
-  __shared__ uint32_t excl[kMaxWorld];                     // tile's exclusive prefix per owner
-  __shared__ uint32_t tile_s;
+__global__ void __launch_bounds__(kPartThreads) k_wpart_count(const int32_t* __restrict__ keys, uint64_t n, int world,
+                                                              uint64_t wmagic, uint32_t nwt,
+                                                              uint32_t* __restrict__ tile_cnt) {
+  __shared__ uint32_t c[kPartThreads / 32][kMaxWorld];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  const int G = V.world;
-  const unsigned long long tag = (epoch & 0x3FFFFFFFull) << 34;
-  const uint32_t ntiles = (uint32_t)((n + kPartTile - 1) / kPartTile);
-  const size_t region = (size_t)V.rank * V.bmax;
-  // persistent CTAs take tiles in order from a counter (reset by the last CTA)
-#pragma unroll 1
-  for (;;) {
-    if (threadIdx.x == 0) tile_s = atomicAdd(ctr + 1, 1u);
-    for (uint32_t k = threadIdx.x; k < kPartRounds * kWarps * kMaxWorld; k += kPartThreads) (&wc[0][0][0])[k] = 0;
-    __syncthreads();
-    const uint32_t tile = tile_s;
-    if (tile >= ntiles) break;
-    const uint64_t t0 = (uint64_t)tile * kPartTile;
+  const uint32_t wt = blockIdx.x * (kPartThreads / 32) + warp;
+  if (wt >= nwt) return;
+  c[warp][lane] = 0;
+  __syncwarp();
+  int32_t x[kPartRounds], y[kPartRounds], z[kPartRounds];
+  __shared__ WarpStage stage[kPartThreads / 32];
+  load_rounds(keys, nullptr, n, (uint64_t)wt * kWTile, stage[warp], x, y, z, nullptr);
+#pragma unroll
+  for (int r = 0; r < kPartRounds; ++r) {
+    const uint64_t i = (uint64_t)wt * kWTile + (uint64_t)r * 32 + lane;
+    const uint32_t o = i < n ? owner_fast(x[r], y[r], z[r], wmagic, (uint32_t)world) : 0xFFFFFFFFu;
+    const uint32_t m = __match_any_sync(0xFFFFFFFFu, o);
+    if (o != 0xFFFFFFFFu && (int)lane == __ffs(m) - 1) c[warp][o] += __popc(m);
+    __syncwarp();
+  }
+  if ((int)lane < world) tile_cnt[(size_t)lane * nwt + wt] = c[warp][lane];
+}
 
-    // all loads of the tile first (8 ops per thread in flight)
+// CTA o: exclusive scan of owner o's warp-tile counts; chunks of 8,192 are
+// loaded coalesced into shared memory, each thread scans 8 consecutive
+__global__ void __launch_bounds__(1024) k_wpart_scan(const uint32_t* __restrict__ tile_cnt, uint32_t nwt,
+                                                     uint32_t* __restrict__ tile_off, uint32_t* __restrict__ totals) {
+  constexpr int kPer = 8;
+  constexpr uint32_t kChunk = 1024 * kPer;
+  __shared__ uint32_t buf[kChunk];
+  __shared__ uint32_t ws[32];
+  const uint32_t o = blockIdx.x, lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t* in = tile_cnt + (size_t)o * nwt;
+  uint32_t* out = tile_off + (size_t)o * nwt;
+  uint32_t carry = 0;
+  for (uint32_t b = 0; b < nwt; b += kChunk) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const uint32_t t = b + k * 1024 + threadIdx.x;
+      buf[k * 1024 + threadIdx.x] = t < nwt ? in[t] : 0u;
+    }
+    __syncthreads();
+    uint32_t v[kPer], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) sum += (v[k] = buf[threadIdx.x * kPer + k]);
+    uint32_t xs = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, xs, d);
+      if ((int)lane >= d) xs += y;
+    }
+    if (lane == 31) ws[warp] = xs;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t q = ws[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, q, d);
+        if ((int)lane >= d) q += y;
+      }
+      ws[lane] = q;
+    }
+    __syncthreads();
+    uint32_t run = carry + (warp ? ws[warp - 1] : 0u) + xs - sum;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      buf[threadIdx.x * kPer + k] = run;
+      run += v[k];
+    }
+    carry += ws[31];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const uint32_t t = b + k * 1024 + threadIdx.x;
+      if (t < nwt) out[t] = buf[k * 1024 + threadIdx.x];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) totals[o] = carry;
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_wpart_push(ShardView V, const int32_t* __restrict__ keys,
+                                                             const uint8_t* __restrict__ ops, uint64_t n, uint32_t nwt,
+                                                             const uint32_t* __restrict__ tile_off,
+                                                             const uint32_t* __restrict__ totals,
+                                                             unsigned long long epoch, unsigned int* ctr) {
+  __shared__ uint32_t run[kPartThreads / 32][kMaxWorld];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t wt = blockIdx.x * (kPartThreads / 32) + warp;
+  const int G = V.world;
+  if (wt < nwt) {
+    run[warp][lane] = (int)lane < G ? tile_off[(size_t)lane * nwt + wt] : 0u;
+    __syncwarp();
     int32_t x[kPartRounds], y[kPartRounds], z[kPartRounds];
-    uint32_t op[kPartRounds], o[kPartRounds], lr[kPartRounds];
+    uint32_t op[kPartRounds];
+    const uint64_t t0 = (uint64_t)wt * kWTile;
+    __shared__ WarpStage stage[kPartThreads / 32];
+    load_rounds(keys, ops, n, t0, stage[warp], x, y, z, op);
+    const size_t region = (size_t)V.rank * V.bmax;
 #pragma unroll
     for (int r = 0; r < kPartRounds; ++r) {
-      const uint64_t i = t0 + (uint64_t)r * kPartThreads + threadIdx.x;
-      o[r] = 0xFFFFFFFFu;
-      x[r] = y[r] = z[r] = 0;
-      op[r] = 0;
-      if (i < n) {
-        x[r] = ld_stream(keys + 3 * i);
-        y[r] = ld_stream(keys + 3 * i + 1);
-        z[r] = ld_stream(keys + 3 * i + 2);
-        op[r] = ld_stream(ops + i);
+      const uint64_t i = t0 + (uint64_t)r * 32 + lane;
+      const uint32_t o = i < n ? owner_fast(x[r], y[r], z[r], V.wmagic, (uint32_t)G) : 0xFFFFFFFFu;
+      const uint32_t m = __match_any_sync(0xFFFFFFFFu, o);
+      if (o != 0xFFFFFFFFu) {
+        const uint32_t off = run[warp][o] + __popc(m & lanemask_lt());
+        int4 rec;
+        rec.x = x[r];
+        rec.y = y[r];
+        rec.z = z[r];
+        rec.w = (int)((op[r] << 30) | (uint32_t)i);
+        rec_of(V, o)[region + off] = rec;  // peer store over NVLink (local for o == rank)
       }
+      __syncwarp();
+      if (o != 0xFFFFFFFFu && (int)lane == __ffs(m) - 1) run[warp][o] += __popc(m);
+      __syncwarp();
     }
-#pragma unroll
-    for (int r = 0; r < kPartRounds; ++r) {
-      const uint64_t i = t0 + (uint64_t)r * kPartThreads + threadIdx.x;
-      if (i < n) o[r] = owner_of(x[r], y[r], z[r], (uint32_t)G);
-      const uint32_t m = __match_any_sync(0xFFFFFFFFu, o[r]);
-      lr[r] = __popc(m & lanemask_lt());
-      if (o[r] != 0xFFFFFFFFu && (int)lane == __ffs(m) - 1) wc[r][warp][o[r]] = __popc(m);
-    }
-    __syncthreads();
-    // exclusive offsets over (round, warp) per owner: thread (round = warp id,
-    // owner = lane) scans its round's 8 warps, then rounds are combined
-    {
-      const uint32_t r = warp, ow = lane;
-      uint32_t a = 0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = wc[r][w][ow];
-        wc[r][w][ow] = a;
-        a += c;
-      }
-      rt[r][ow] = a;
-    }
-    __syncthreads();
-    {
-      const uint32_t r = warp, ow = lane;
-      uint32_t before = 0;
-      for (uint32_t q = 0; q < r; ++q) before += rt[q][ow];
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) wc[r][w][ow] += before;
-    }
-    // publish this tile's counts (aggregates first, so successors never wait
-    // on a look-back), then look back for the exclusive prefix: warp w serves
-    // owners w, w + 8, ...; its 32 lanes read a window of 32 predecessors at
-    // once and stop at the nearest inclusive prefix
-    if (warp == 0 && (int)lane < G) {
-      uint32_t agg = 0;
-#pragma unroll
-      for (int r = 0; r < kPartRounds; ++r) agg += rt[r][lane];
-      st_relaxed_u64(status + (size_t)tile * kMaxWorld + lane, tag | (tile == 0 ? kInclusive : kAggregate) | agg);
-    }
-    for (int ow = warp; ow < G; ow += kWarps) {
-      uint32_t agg = 0;
-#pragma unroll
-      for (int r = 0; r < kPartRounds; ++r) agg += rt[r][ow];
-      uint32_t pre = 0;
-      if (tile > 0) {
-        int64_t hi = (int64_t)tile - 1;  // window [hi - 31, hi]; lane l reads hi - l
-        for (;;) {
-          const int64_t j = hi - (int64_t)lane;
-          unsigned long long w = kInclusive;  // before tile 0: inclusive 0
-          if (j >= 0) {
-            const unsigned long long* pj = status + (size_t)j * kMaxWorld + ow;
-            w = ld_relaxed_u64(pj);
-            while ((w & ~0x3FFFFFFFFull) != tag) {
-              __nanosleep(20);
-              w = ld_relaxed_u64(pj);
-            }
-          }
-          const uint32_t inc = __ballot_sync(0xFFFFFFFFu, (w & kInclusive) != 0);
-          const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive (or the whole window)
-          uint32_t v = (int)lane <= stop ? (uint32_t)w : 0u;
-          v = __reduce_add_sync(0xFFFFFFFFu, v);
-          pre += v;
-          if (inc) break;
-          hi -= 32;
-        }
-        if (lane == 0) st_relaxed_u64(status + (size_t)tile * kMaxWorld + ow, tag | kInclusive | (uint32_t)(pre + agg));
-      }
-      if (lane == 0) excl[ow] = pre;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kPartRounds; ++r) {
-      if (o[r] == 0xFFFFFFFFu) continue;
-      const uint64_t i = t0 + (uint64_t)r * kPartThreads + threadIdx.x;
-      const uint32_t off = excl[o[r]] + wc[r][warp][o[r]] + lr[r];
-      int4 rec;
-      rec.x = x[r];
-      rec.y = y[r];
-      rec.z = z[r];
-      rec.w = (int)((op[r] << 30) | (uint32_t)i);
-      rec_of(V, o[r])[region + off] = rec;  // peer store over NVLink (local for o == rank)
-    }
-    __syncthreads();  // wc / excl are rewritten by the next tile
   }
   if (last_cta(ctr) && (int)threadIdx.x < G) {
-    // every tile is done: the last tile's inclusive prefix is the total
-    const int ow = threadIdx.x;
-    if (ow == 0) ctr[1] = 0;  // every CTA took its last ticket before arriving
-    const uint32_t total = ntiles ? (uint32_t)ld_relaxed_u64(status + (size_t)(ntiles - 1) * kMaxWorld + ow) : 0u;
     __threadfence_system();
-    ShardHdr* h = hdr_of(V, ow);
-    st_relaxed_sys(&h->cnt[V.rank], total);
+    ShardHdr* h = hdr_of(V, threadIdx.x);
+    st_relaxed_sys(&h->cnt[V.rank], totals[threadIdx.x]);
     st_release_sys(&h->push_flag[V.rank], epoch);
   }
 }
@@ -398,14 +426,16 @@ using namespace vsb;
 struct vs_shard {
   vs_table* table = nullptr;
   int device = 0, rank = 0, world = 1;
-  uint32_t bmax = 0, ntiles_max = 0;
+  uint32_t bmax = 0;
   char* win = nullptr;  // own window (cudaMalloc, exported over CUDA IPC)
   size_t win_bytes = 0, rec_off = 0, out_off = 0;
   char* peer[kMaxWorld] = {};
   bool opened[kMaxWorld] = {};
   bool connected = false;
   // local workspace
-  unsigned long long* status = nullptr;  // [ntiles_max][kMaxWorld] look-back words
+  uint32_t* tile_cnt = nullptr;  // [world][warp tiles] ops per owner per warp tile
+  uint32_t* tile_off = nullptr;
+  uint32_t* totals = nullptr;
   unsigned int* ctl = nullptr;  // [0] push CTA counter, [32] return CTA counter, [64] error word
   uint8_t* res = nullptr;
   int32_t* idx = nullptr;
@@ -421,6 +451,7 @@ struct vs_shard {
     v.bmax = bmax;
     v.rec_off = rec_off;
     v.out_off = out_off;
+    v.wmagic = fastmod_magic((uint32_t)world);
     return v;
   }
 };
@@ -442,14 +473,16 @@ vs_status vs_shard_create(vs_table* local, int rank, int world, uint64_t max_bat
   s->rank = rank;
   s->world = world;
   s->bmax = (uint32_t)max_batch;
-  s->ntiles_max = (uint32_t)((max_batch + kPartTile - 1) / kPartTile);
   s->rec_off = kHdrBytes;
   s->out_off = align_up(s->rec_off + (size_t)world * max_batch * sizeof(int4), 256);
   s->win_bytes = align_up(s->out_off + max_batch, 4096);
   cudaError_t e = cudaMalloc(&s->win, s->win_bytes);
   if (e == cudaSuccess) e = cudaMemset(s->win, 0, kHdrBytes);
-  if (e == cudaSuccess) e = cudaMalloc(&s->status, (size_t)s->ntiles_max * kMaxWorld * 8);
-  if (e == cudaSuccess) e = cudaMemset(s->status, 0, (size_t)s->ntiles_max * kMaxWorld * 8);
+  // warp tiles (kWTile ops) are the finest partition granularity
+  const size_t nwt_max = (max_batch + kWTile - 1) / kWTile;
+  if (e == cudaSuccess) e = cudaMalloc(&s->tile_cnt, (size_t)world * nwt_max * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->tile_off, (size_t)world * nwt_max * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->totals, kMaxWorld * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->ctl, 128 * 4);
   if (e == cudaSuccess) e = cudaMemset(s->ctl, 0, 128 * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->res, (size_t)world * max_batch);
@@ -511,11 +544,21 @@ vs_status vs_shard_apply(vs_shard* s, const int32_t* keys, const uint8_t* ops, u
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned long long ep = ++s->epoch;
   const ShardView V = s->view();
-  const uint32_t ntiles = n ? (uint32_t)((n + kPartTile - 1) / kPartTile) : 1u;
   ShardHdr* own = (ShardHdr*)s->win;
-  k_part_push<<<ntiles < kPushCtas ? ntiles : kPushCtas, kPartThreads, 0, st>>>(V, keys, ops, n, s->status, ep,
-                                                                               s->ctl);
-  count_launch();
+  {
+    const uint32_t nwt = (uint32_t)((n + kWTile - 1) / kWTile);
+    const unsigned ctas = nwt ? (nwt + kPartThreads / 32 - 1) / (kPartThreads / 32) : 1u;
+    if (nwt) {
+      k_wpart_count<<<ctas, kPartThreads, 0, st>>>(keys, n, s->world, V.wmagic, nwt, s->tile_cnt);
+      count_launch();
+      k_wpart_scan<<<s->world, 1024, 0, st>>>(s->tile_cnt, nwt, s->tile_off, s->totals);
+      count_launch();
+    } else {
+      VS_CK(cudaMemsetAsync(s->totals, 0, kMaxWorld * 4, st));
+    }
+    k_wpart_push<<<ctas, kPartThreads, 0, st>>>(V, keys, ops, n, nwt, s->tile_off, s->totals, ep, s->ctl);
+    count_launch();
+  }
   k_wait<<<1, 32, 0, st>>>(own->push_flag, s->world, ep, s->ctl + 64, s->timeout_ns);
   count_launch();
   // incoming ~ n per rank when the keys hash evenly; the grid-stride loops
@@ -570,7 +613,9 @@ void vs_shard_destroy(vs_shard* s) {
   for (int r = 0; r < kMaxWorld; ++r)
     if (s->opened[r]) cudaIpcCloseMemHandle(s->peer[r]);
   cudaFree(s->win);
-  cudaFree(s->status);
+  cudaFree(s->tile_cnt);
+  cudaFree(s->tile_off);
+  cudaFree(s->totals);
   cudaFree(s->ctl);
   cudaFree(s->res);
   cudaFree(s->idx);
