@@ -165,6 +165,13 @@ vs_status vs_table_extract(vs_table *t, uint64_t max_n, uint64_t seed,
  * out_host[5] = free-list entries that are also reachable (must be 0)  */
 vs_status vs_table_audit(vs_table *t, uint64_t out_host[6], vs_stream_t stream);
 
+/* Diagnostics (bench.py only): the speed of light of the op kernels' memory
+ * pattern on THIS table's storage -- n threads in k_apply's launch shape,
+ * each doing `hops` DEPENDENT random 16-byte entry loads (same load flavour
+ * as a chain walk) and one result byte; no logic, no atomics.  out: device
+ * uint8[n]. */
+vs_status vs_table_probe_sol(vs_table *t, uint64_t n, int hops, uint8_t *out, vs_stream_t stream);
+
 /* ------------------------------------------------------------ MC encode --- */
 
 /* TSDF pool: caller-owned rows of VS_TSDF_BLOCK_BYTES in the wire layout

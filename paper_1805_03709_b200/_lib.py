@@ -89,6 +89,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_rc_integrate_table": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "vs_stream_remove_many": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _vp, _u64, _vp, _vp]),
     "vs_stream_extract_ordered": (_i32, [_vp, _vp, _u64, _pu64, _u64, _u64, _vp, _pu64, _vp, _vp]),
+    "vs_table_probe_sol": (_i32, [_vp, _u64, ctypes.c_int, _vp, _vp]),
     "vs_shard_create": (_i32, [_vp, ctypes.c_int, ctypes.c_int, _u64, ctypes.POINTER(_vp)]),
     "vs_shard_destroy": (None, [_vp]),
     "vs_shard_export": (_i32, [_vp, ctypes.POINTER(ctypes.c_uint8 * 64)]),

@@ -11,6 +11,7 @@
 //                       kernel itself needs no atomics for either.
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -251,6 +252,28 @@ static cudaError_t launch_apply(const TableView& v, const int32_t* keys, const u
   k_apply<<<apply_grid(n), kOpBlock, 0, s>>>(v, keys, ops, n, result, index);
   return cudaGetLastError();
 #endif
+}
+
+// Speed-of-light probe (diagnostics): `hops` dependent random entry loads per
+// thread over the whole table, k_apply's launch shape, one result byte.
+__global__ void __launch_bounds__(kOpBlock) k_probe_sol(TableView T, uint64_t n, int hops, uint8_t* __restrict__ out) {
+  const uint64_t i = (uint64_t)blockIdx.x * kOpBlock + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t cap = T.n + T.excess;
+  uint32_t h = (uint32_t)i * 0x9E3779B1u + 0x7F4A7C15u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  uint32_t e = h % cap;
+  uint32_t acc = 0;
+#pragma unroll 1
+  for (int k = 0; k < hops; ++k) {
+    const int4 v = k == 0 ? ld_bucket(T.e + e) : ld_entry(T.e + e);
+    acc ^= (uint32_t)v.x ^ (uint32_t)v.w;
+    h = h * 0x85EBCA6Bu + acc + 0x165667B1u;  // next address depends on the loaded entry
+    e = h % cap;
+  }
+  __stcs(out + i, (uint8_t)(acc & 1u));
 }
 
 // One op of any kind on one key, then its post pass, in a single thread
@@ -595,6 +618,11 @@ static void keep_pool_resident(int device) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
+  // experiment knob: L2 fetch granularity hint for random entry accesses
+  if (const char* g = getenv("VSB_L2_FETCH")) {
+    DeviceGuard dg(device);
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(g));
+  }
   done[device] = true;
 }
 
@@ -918,6 +946,24 @@ vs_status vs_table_extract(vs_table* t, uint64_t max_n, uint64_t seed, int32_t* 
                                         keys_out, n_dev); vsb::count_launch(); }
   VS_CK_LAUNCH("k_extract_select");
   return erase_device_count(t, keys_out, n_dev, m, s);
+}
+
+vs_status vs_table_probe_sol(vs_table* t, uint64_t n, int hops, uint8_t* out, vs_stream_t stream) {
+  if (!t || (n && !out) || hops < 1 || hops > 16) {
+    set_error("vs_table_probe_sol: bad arguments");
+    return VS_ERR_INVALID;
+  }
+  if (n == 0) return VS_OK;
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const TableView v = t->view();
+  {
+    ProfScope prof(3, s);
+    k_probe_sol<<<apply_grid(n), kOpBlock, 0, s>>>(v, n, hops, out);
+    vsb::count_launch();
+  }
+  VS_CK_LAUNCH("vs_table_probe_sol");
+  return VS_OK;
 }
 
 vs_status vs_table_audit(vs_table* t, uint64_t out_host[6], vs_stream_t stream) {
