@@ -42,7 +42,10 @@ struct Ctl {
   long long size[kSizeStripes * kSizeStride];  // live keys = sum of the stripes (approx_size)
 };
 
-constexpr uint32_t kMaxStripes = 32;  // free-list stripes
+#ifndef VSB_HASH_STRIPES
+#define VSB_HASH_STRIPES 128
+#endif
+constexpr uint32_t kMaxStripes = VSB_HASH_STRIPES;  // free-list stripes
 constexpr uint32_t kTopStride = 32;   // long longs between stripe tops (256 B)
 
 // By-value view passed to kernels.

@@ -305,12 +305,39 @@ __global__ void k_single(TableView T, const int32_t* __restrict__ kio, uint8_t o
 
 // Post pass after k_insert / k_apply: created flags to the lowest op index
 // among in-batch duplicates (sequential replay), FRESH cleared, and the
-// excess entries vacated by erases recycled -- one launch, one pass.
-__global__ void k_post(TableView T, const int32_t* __restrict__ keys, const uint8_t* __restrict__ ops, uint64_t n,
-                       uint8_t* __restrict__ result, const int32_t* __restrict__ index) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  post_op(T, keys, i, ops ? ops[i] : (uint8_t)VS_OP_INSERT, result, index[i]);
+// excess entries vacated by erases recycled -- one launch, one pass.  Each
+// thread takes kPostOps ops (loads of all of them in flight first) and the
+// vacated positions of a whole warp go back with one reservation.
+constexpr int kPostOps = 4;
+constexpr int kPostBlock = 256;
+__global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t* __restrict__ keys,
+                                                     const uint8_t* __restrict__ ops, uint64_t n,
+                                                     uint8_t* __restrict__ result, const int32_t* __restrict__ index) {
+  const uint64_t base = (uint64_t)blockIdx.x * (kPostBlock * kPostOps) + threadIdx.x;
+  uint8_t op[kPostOps], res[kPostOps];
+  int32_t pos[kPostOps];
+#pragma unroll
+  for (int k = 0; k < kPostOps; ++k) {
+    const uint64_t i = base + (uint64_t)k * kPostBlock;
+    op[k] = 0xFF;
+    if (i < n) {
+      op[k] = ops ? ops[i] : (uint8_t)VS_OP_INSERT;
+      res[k] = result[i];
+      pos[k] = index[i];
+    }
+  }
+  uint32_t vac[kPostOps];
+  int nv = 0;
+#pragma unroll
+  for (int k = 0; k < kPostOps; ++k) {
+    const uint64_t i = base + (uint64_t)k * kPostBlock;
+    if (op[k] == VS_OP_INSERT && res[k]) {
+      post_op(T, keys, i, VS_OP_INSERT, result, pos[k]);
+    } else if (op[k] == VS_OP_ERASE && res[k] && pos[k] >= (int32_t)T.n) {
+      vac[nv++] = (uint32_t)pos[k];
+    }
+  }
+  push_free_many<kPostOps>(T, vac, nv);
 }
 
 // Push vacated excess positions back onto the striped free list (warp-
@@ -738,7 +765,7 @@ vs_status vs_table_insert(vs_table* t, const int32_t* keys, uint64_t n, uint8_t*
     ProfScope prof(0, s);
     { k_insert<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, created, index); vsb::count_launch(); }
   }
-  { k_post<<<grid_for(n, 256), 256, 0, s>>>(v, keys, nullptr, n, created, index); vsb::count_launch(); }
+  { k_post<<<grid_for(n, kPostBlock * kPostOps), kPostBlock, 0, s>>>(v, keys, nullptr, n, created, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_insert");
   return VS_OK;
 }
@@ -800,7 +827,7 @@ vs_status vs_table_apply(vs_table* t, const int32_t* keys, const uint8_t* ops, u
     ProfScope prof(0, s);
     { VS_CK(launch_apply(v, keys, ops, n, result, index, s)); vsb::count_launch(); }
   }
-  { k_post<<<grid_for(n, 256), 256, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
+  { k_post<<<grid_for(n, kPostBlock * kPostOps), kPostBlock, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_apply");
   return VS_OK;
 }

@@ -105,6 +105,39 @@ __device__ __forceinline__ void push_free(const TableView& T, uint32_t e) {
   }
 }
 
+// Push up to kMaxPush vacated positions per lane with ONE warp-wide
+// reservation (post passes).  Every lane of the warp must call it.  A stripe
+// that would overflow is given back and the lane's items go one by one
+// through push_free (which moves on to the next stripe).
+template <int kMaxPush>
+__device__ __forceinline__ void push_free_many(const TableView& T, const uint32_t (&v)[kMaxPush], int nv) {
+  const uint32_t lane = lane_id();
+  uint32_t incl = (uint32_t)nv;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if ((int)lane >= d) incl += y;
+  }
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  if (total == 0) return;
+  const uint32_t s = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % T.stripes;
+  long long* top = T.tops + (size_t)s * kTopStride;
+  long long old = 0;
+  if (lane == 0) old = (long long)atomicAdd((unsigned long long*)top, (unsigned long long)total);
+  old = __shfl_sync(0xFFFFFFFFu, old, 0);
+  if (old + (long long)total <= (long long)T.stripe_cap) {
+    uint32_t* dst = T.free_stack + (size_t)s * T.stripe_cap + (size_t)old + (incl - (uint32_t)nv);
+#pragma unroll
+    for (int j = 0; j < kMaxPush; ++j)
+      if (j < nv) dst[j] = v[j];
+    return;
+  }
+  if (lane == 0) atomicAdd((unsigned long long*)top, (unsigned long long)(-(long long)total));
+#pragma unroll
+  for (int j = 0; j < kMaxPush; ++j)
+    if (j < nv) push_free(T, v[j]);
+}
+
 // Lock-free retrieval (_find + _scan_chain, concurrent_hash.py:127-157).
 // Returns the position or -1; *meta_out = meta of the matching entry.
 // ... starting from an already loaded bucket entry `s` (lets a thread
