@@ -439,8 +439,8 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
         return {-1, 0};
       }
       const uint32_t e = (uint32_t)ne;
-      st_entry(T.e + e, x, y, z, kOcc | kFresh);  // NEXT = 0 clears the stale offset (:200)
       const uint32_t link = e - T.n + 1u;
+      st_entry(T.e + e, x, y, z, kOcc | kFresh);  // NEXT = 0 clears the stale offset (:200)
       if (prev == b) {
         atom_exch_release(bmeta, (old & ~kNext) | link);  // publish + unlock
       } else {
