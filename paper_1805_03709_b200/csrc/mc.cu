@@ -56,6 +56,44 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
+// L2 policies (experiment knobs): in the forward sweep a TSDF
+// row is first read as the halo of its -x/-y/-z neighbours and LAST as a
+// centre, so centre copies may be evict-first and halo reads evict-last.
+#ifndef VSB_MC_CENTRE_HINT
+#define VSB_MC_CENTRE_HINT 0
+#endif
+#ifndef VSB_MC_HALO_HINT
+#define VSB_MC_HALO_HINT 0
+#endif
+#ifndef VSB_MC_PROBE_HINT
+#define VSB_MC_PROBE_HINT 1
+#endif
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_halo(const uint32_t* p) {
+#if VSB_MC_HALO_HINT
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t ok = 0;
   do {
@@ -143,7 +181,12 @@ __device__ __forceinline__ int32_t load_nbr(const TableView& T, const int32_t* _
     const int32_t y = keys[3 * blk + 1] + ((c >> 1) & 1);
     const int32_t z = keys[3 * blk + 2] + ((c >> 2) & 1);
     uint32_t meta;
-    return find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
+    const uint32_t b = bucket_of(T, x, y, z);
+#if VSB_MC_PROBE_HINT
+    return find_pos(T, x, y, z, b, &meta);
+#else
+    return find_pos_from(T, x, y, z, b, ld_entry(T.e + b), &meta);
+#endif
   } else {
     return __ldg(&nbr[8 * blk + c]);
   }
@@ -180,8 +223,8 @@ __device__ __forceinline__ void halo_prefetch(HaloRegs& h, const int32_t* nbc, c
       if (nrow >= 0) {
         // voxel records are 12 B: (tsdf, weight) is only 4-byte aligned
         const uint32_t* src = (const uint32_t*)(pool + (uint64_t)nrow * VS_TSDF_BLOCK_BYTES + 12u * flat);
-        h.tb[k] = __ldg(src);
-        h.wb[k] = __ldg(src + 1);
+        h.tb[k] = ld_halo(src);
+        h.wb[k] = ld_halo(src + 1);
         h.row[k] = row;
         h.bit[k] = bit;
       }
@@ -200,7 +243,12 @@ __device__ __forceinline__ void issue_centre(McSmem& sm, uint64_t j, const uint8
   const int b = (int)(j % kStages);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   mbar_arrive_expect_tx(&sm.mbar[b], VS_TSDF_BLOCK_BYTES);
+#if VSB_MC_CENTRE_HINT
+  tma_load_1d_hint(sm.buf[b], pool + (uint64_t)row * VS_TSDF_BLOCK_BYTES, VS_TSDF_BLOCK_BYTES, &sm.mbar[b],
+                   policy_evict_first());
+#else
   tma_load_1d(sm.buf[b], pool + (uint64_t)row * VS_TSDF_BLOCK_BYTES, VS_TSDF_BLOCK_BYTES, &sm.mbar[b]);
+#endif
 }
 
 template <bool kFromKeys>

@@ -367,24 +367,57 @@ __global__ void __launch_bounds__(kShardOpBlock) k_shard_apply(TableView T, Shar
   add_size_cta(T, delta);
 }
 
+// Post pass over the routed ops: 4 ops per thread per round (loads in
+// flight first), created-flag fixup via the records, vacated excess entries
+// back onto the free list with one warp-wide reservation per round.
 __global__ void __launch_bounds__(256) k_shard_post(TableView T, ShardView V, uint8_t* __restrict__ res,
                                                     const int32_t* __restrict__ idx) {
+  constexpr int kOps = 4;
   __shared__ uint32_t spre[kMaxWorld + 1];
   const Routed R = load_routed(V, spre);
   const int4* rec = rec_of(V, V.rank);
   const uint32_t total = R.total();
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t rounds = (total + kOps * stride - 1) / (kOps * stride);  // uniform: warps stay converged
 #pragma unroll 1
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < total; v += gridDim.x * blockDim.x) {
-    int r;
-    const int4 q = rec[R.pos(v, &r)];
-    post_op_t(
-        T,
-        [&](uint64_t m) {
-          int rm;
-          const int4 p = rec[R.pos((uint32_t)m, &rm)];
-          return p.x == q.x && p.y == q.y && p.z == q.z;
-        },
-        v, (uint8_t)((uint32_t)q.w >> 30), res, idx[v]);
+  for (uint32_t it = 0; it < rounds; ++it) {
+    const uint32_t v0 = it * kOps * stride + blockIdx.x * blockDim.x + threadIdx.x;
+    int4 q[kOps];
+    uint8_t rs[kOps];
+    int32_t ps[kOps];
+#pragma unroll
+    for (int k = 0; k < kOps; ++k) {
+      const uint32_t v = v0 + k * stride;
+      q[k].w = -1;
+      if (v < total) {
+        int r;
+        q[k] = rec[R.pos(v, &r)];
+        rs[k] = res[v];
+        ps[k] = idx[v];
+      }
+    }
+    uint32_t vac[kOps];
+    int nv = 0;
+#pragma unroll
+    for (int k = 0; k < kOps; ++k) {
+      const uint32_t v = v0 + k * stride;
+      if (v >= total) continue;
+      const uint32_t op = (uint32_t)q[k].w >> 30;
+      if (op == 0u /*VS_OP_INSERT*/ && rs[k]) {
+        const int4 qk = q[k];
+        post_op_t(
+            T,
+            [&](uint64_t m) {
+              int rm;
+              const int4 p = rec[R.pos((uint32_t)m, &rm)];
+              return p.x == qk.x && p.y == qk.y && p.z == qk.z;
+            },
+            v, 0, res, ps[k]);
+      } else if (op == 2u /*VS_OP_ERASE*/ && rs[k] && ps[k] >= (int32_t)T.n) {
+        vac[nv++] = (uint32_t)ps[k];
+      }
+    }
+    push_free_many<kOps>(T, vac, nv);
   }
 }
 
