@@ -349,7 +349,7 @@ __device__ __forceinline__ Routed load_routed(const ShardView& V, uint32_t* spre
   return R;
 }
 
-__global__ void __launch_bounds__(kShardOpBlock) k_shard_apply(TableView T, ShardView V, uint8_t* __restrict__ res,
+__global__ void __launch_bounds__(kShardOpBlock, 2048 / kShardOpBlock) k_shard_apply(TableView T, ShardView V, uint8_t* __restrict__ res,
                                                                int32_t* __restrict__ idx) {
   __shared__ uint32_t spre[kMaxWorld + 1];
   const Routed R = load_routed(V, spre);
@@ -603,7 +603,7 @@ vs_status vs_shard_apply(vs_shard* s, const int32_t* keys, const uint8_t* ops, u
     k_shard_apply<<<grid_for(hint, kShardOpBlock), kShardOpBlock, 0, st>>>(T, V, s->res, s->idx);
     count_launch();
   }
-  k_shard_post<<<grid_for(hint, 256), 256, 0, st>>>(T, V, s->res, s->idx);
+  k_shard_post<<<grid_for(hint, 256 * 4), 256, 0, st>>>(T, V, s->res, s->idx);
   count_launch();
   // bounded grid: the last-CTA signal costs one same-address atomic per CTA
   k_shard_return<<<kReturnCtas, 256, 0, st>>>(V, s->res, ep, s->ctl + 32);
