@@ -172,6 +172,12 @@ struct McSmem {
   uint32_t cnt[2][4];
 };
 
+// Sweep order (experiment knob VSB_MC_REVERSE): block of sweep index i.
+#ifndef VSB_MC_REVERSE
+#define VSB_MC_REVERSE 0
+#endif
+__device__ __forceinline__ uint64_t sweep_block(uint64_t i, uint64_t n) { return VSB_MC_REVERSE ? n - 1 - i : i; }
+
 // Neighbour row of block `blk` for corner-block c.
 template <bool kFromKeys>
 __device__ __forceinline__ int32_t load_nbr(const TableView& T, const int32_t* __restrict__ keys,
@@ -200,8 +206,8 @@ __device__ __forceinline__ void lookup_batch(McSmem& sm, int buf, const TableVie
                                              const int32_t* nbr, uint64_t n, uint64_t j0) {
   const int t = threadIdx.x;
   const int slot = t >> 3, c = t & 7;
-  const uint64_t blk = blockIdx.x + (j0 + slot) * (uint64_t)gridDim.x;
-  sm.nb[buf][slot][c] = blk < n ? load_nbr<kFromKeys>(T, keys, nbr, blk, c) : -1;
+  const uint64_t sblk = blockIdx.x + (j0 + slot) * (uint64_t)gridDim.x;  // sweep index
+  sm.nb[buf][slot][c] = sblk < n ? load_nbr<kFromKeys>(T, keys, nbr, sweep_block(sblk, n), c) : -1;
 }
 
 // Per-thread halo items (thread t owns items t and t + 128 of 217).
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
   if (nj) halo_prefetch(hal, nb_of(sm, 0), pool);
 
   for (uint64_t j = 0; j < nj; ++j) {
-    const uint64_t blk = blockIdx.x + j * G;
+    const uint64_t blk = sweep_block(blockIdx.x + j * G, n);
     const int s = (int)(j & 1);
     const int b = (int)(j % kStages);
     const int slot = (int)(j % kLook);
