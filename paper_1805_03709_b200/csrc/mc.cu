@@ -122,6 +122,14 @@ __device__ __forceinline__ int32_t quantise(uint32_t tb, uint32_t wb) {
   return __float2int_rn(s);
 }
 
+// byte k (k < 4) = bits (k, k+1) of v: the corner pair of voxel x0 + k
+#ifndef VSB_MC_SIMD_INDEX
+#define VSB_MC_SIMD_INDEX 1
+#endif
+__device__ __forceinline__ uint32_t pair4(uint32_t v) {
+  return (v & 3u) | ((v & 6u) << 7) | ((v & 12u) << 14) | ((v & 24u) << 21);
+}
+
 // Halo item -> (neighbour c, source flat index, grid row, grid bit).
 // grid rows are indexed gz*9 + gy, bit gx, with g in [0, 8].
 __device__ __forceinline__ void halo_item(int i, int& c, int& flat, int& row, int& bit) {
@@ -356,6 +364,23 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     const uint32_t o00 = go[r00] >> x0, o10 = go[r00 + 1] >> x0, o01 = go[r00 + 9] >> x0, o11 = go[r00 + 10] >> x0;
     uint32_t word[4];
     uint32_t qw = 0, nz = 0;
+#if VSB_MC_SIMD_INDEX
+    // all 4 cube indices at once, one per byte: byte k of pair(v) holds bits
+    // (k, k+1) of row v, so the 8 corner bits of voxel k are the 4 rows'
+    // pairs stacked at bit offsets 0/2/4/6 (corner c = (c&1, c>>1&1, c>>2&1))
+    const uint32_t I = pair4(i00) | (pair4(i10) << 2) | (pair4(i01) << 4) | (pair4(i11) << 6);
+    const uint32_t O = pair4(o00) | (pair4(o10) << 2) | (pair4(o01) << 4) | (pair4(o11) << 6);
+    // keep a byte only where all 8 corners are observed and it is not 255
+    const uint32_t keep = __vcmpeq4(O, 0xFFFFFFFFu) & ~__vcmpeq4(I, 0xFFFFFFFFu);
+    const uint32_t idx4 = I & keep;
+    const uint32_t nzm = __vcmpne4(idx4, 0u);
+    nz = __popc(nzm) >> 3;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      word[k] = ((nzm >> (8 * k)) & 1u) ? ((idx4 >> (8 * k)) & 0xFFu) | (rgb[k] << 8) : 0u;
+      qw |= ((uint32_t)quantise(tb[k], wb[k]) & 0xFFu) << (8 * k);
+    }
+#else
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       uint32_t idx = ((i00 >> k) & 3u) | (((i10 >> k) & 3u) << 2) | (((i01 >> k) & 3u) << 4) |
@@ -367,6 +392,7 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
       qw |= ((uint32_t)quantise(tb[k], wb[k]) & 0xFFu) << (8 * k);
       nz += idx != 0u;
     }
+#endif
     if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(word[0], word[1], word[2], word[3]));
     if (q_blk) __stcs((uint32_t*)(q_blk + 4 * t), qw);
     if (counts) {
