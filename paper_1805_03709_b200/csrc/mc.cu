@@ -225,22 +225,47 @@ struct HaloRegs {
   int bit[2];
 };
 
-__device__ __forceinline__ void halo_prefetch(HaloRegs& h, const int32_t* nbc, const uint8_t* __restrict__ pool) {
+// A thread's two halo items decoded once per kernel (they do not depend on
+// the block): neighbour c (-1: no item), byte offset in the row, grid row/bit.
+struct HaloDesc {
+  int c[2];
+  uint32_t off[2];
+  int row[2], bit[2];
+};
+
+__device__ __forceinline__ HaloDesc halo_desc() {
+  HaloDesc d;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int i = threadIdx.x + k * kMcThreads;
-    h.row[k] = -1;
+    d.c[k] = -1;
+    d.off[k] = 0;
+    d.row[k] = d.bit[k] = 0;
     if (i < 217) {
       int c, flat, row, bit;
       halo_item(i, c, flat, row, bit);
-      const int32_t nrow = nbc[c];
+      d.c[k] = c;
+      d.off[k] = 12u * (uint32_t)flat;  // voxel records are 12 B: (tsdf, weight) is only 4-byte aligned
+      d.row[k] = row;
+      d.bit[k] = bit;
+    }
+  }
+  return d;
+}
+
+__device__ __forceinline__ void halo_prefetch(HaloRegs& h, const HaloDesc& d, const int32_t* nbc,
+                                              const uint8_t* __restrict__ pool) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    h.row[k] = -1;
+    if (d.c[k] >= 0) {
+      const int32_t nrow = nbc[d.c[k]];
       if (nrow >= 0) {
-        // voxel records are 12 B: (tsdf, weight) is only 4-byte aligned
-        const uint32_t* src = (const uint32_t*)(pool + (uint64_t)nrow * VS_TSDF_BLOCK_BYTES + 12u * flat);
+        const uint32_t* src = (const uint32_t*)(pool + (uint64_t)nrow * VS_TSDF_BLOCK_BYTES + d.off[k]);
         h.tb[k] = ld_halo(src);
         h.wb[k] = ld_halo(src + 1);
-        h.row[k] = row;
-        h.bit[k] = bit;
+        h.row[k] = d.row[k];
+        h.bit[k] = d.bit[k];
       }
     }
   }
@@ -288,8 +313,9 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     for (uint64_t j = 0; j < kAhead && j < nj; ++j) issue_centre(sm, j, pool);
   uint32_t phases = 0u;  // bit b = parity of mbar[b]
   // halo of the block processed next, loaded one iteration ahead
+  const HaloDesc hd = halo_desc();
   HaloRegs hal;
-  if (nj) halo_prefetch(hal, nb_of(sm, 0), pool);
+  if (nj) halo_prefetch(hal, hd, nb_of(sm, 0), pool);
 
   for (uint64_t j = 0; j < nj; ++j) {
     const uint64_t blk = sweep_block(blockIdx.x + j * G, n);
@@ -310,7 +336,7 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     uint32_t* mc_blk = mc_out ? mc_out + blk * VS_BLOCK_VOXELS : nullptr;
     int8_t* q_blk = q_out ? q_out + blk * VS_BLOCK_VOXELS : nullptr;
     const HaloRegs cur = hal;
-    if (j + 1 < nj) halo_prefetch(hal, nb_of(sm, j + 1), pool);
+    if (j + 1 < nj) halo_prefetch(hal, hd, nb_of(sm, j + 1), pool);
 
     if (centre < 0) {
       // absent centre: every cube's origin lives here -> all zero (:152-156)
