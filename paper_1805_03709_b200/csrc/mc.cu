@@ -180,6 +180,12 @@ struct McSmem {
   uint32_t cnt[2][4];
 };
 
+// Per-block non-empty counts summed after the next iteration's first barrier
+// instead of behind an extra barrier (VSB_MC_DEFER_COUNT; measured slower: off).
+#ifndef VSB_MC_DEFER_COUNT
+#define VSB_MC_DEFER_COUNT 0
+#endif
+
 // Sweep order (experiment knob VSB_MC_REVERSE): block of sweep index i.
 #ifndef VSB_MC_REVERSE
 #define VSB_MC_REVERSE 0
@@ -317,6 +323,7 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
   HaloRegs hal;
   if (nj) halo_prefetch(hal, hd, nb_of(sm, 0), pool);
 
+  bool pend = false;  // the previous block's per-warp counts await summing
   for (uint64_t j = 0; j < nj; ++j) {
     const uint64_t blk = sweep_block(blockIdx.x + j * G, n);
     const int s = (int)(j & 1);
@@ -332,6 +339,10 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
       sm.grid_ob[s][r] = 0u;
     }
     __syncthreads();  // (A) lookups ready, grids zeroed, buf[(j+kAhead)%kStages] no longer read
+    // count of the previous block, deferred past this barrier (no extra sync)
+    if (VSB_MC_DEFER_COUNT && counts && t == 0 && pend)
+      counts[sweep_block(blockIdx.x + (j - 1) * G, n)] = sm.cnt[s ^ 1][0] + sm.cnt[s ^ 1][1] + sm.cnt[s ^ 1][2] + sm.cnt[s ^ 1][3];
+    pend = false;
     if (t == 0 && j + kAhead < nj) issue_centre(sm, j + kAhead, pool);
     uint32_t* mc_blk = mc_out ? mc_out + blk * VS_BLOCK_VOXELS : nullptr;
     int8_t* q_blk = q_out ? q_out + blk * VS_BLOCK_VOXELS : nullptr;
@@ -424,8 +435,19 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     if (counts) {
       nz = __reduce_add_sync(0xffffffffu, nz);
       if (lane == 0) sm.cnt[s][warp] = nz;
+#if VSB_MC_DEFER_COUNT
+      pend = true;  // summed by thread 0 after the next barrier
+#else
       __syncthreads();
       if (t == 0) counts[blk] = sm.cnt[s][0] + sm.cnt[s][1] + sm.cnt[s][2] + sm.cnt[s][3];
+#endif
+    }
+  }
+  if (counts) {
+    __syncthreads();
+    if (t == 0 && pend) {
+      const int s = (int)((nj - 1) & 1);
+      counts[sweep_block(blockIdx.x + (nj - 1) * G, n)] = sm.cnt[s][0] + sm.cnt[s][1] + sm.cnt[s][2] + sm.cnt[s][3];
     }
   }
 }
