@@ -161,35 +161,6 @@ __device__ __forceinline__ uint32_t atom_exch_release(uint32_t* p, uint32_t v) {
   return old;
 }
 
-// 16-byte compare-and-swap of a whole entry (ATOMG.CAS.128); returns the old
-// entry (equal to `e` iff the swap happened).
-__device__ __forceinline__ int4 cas_entry(Entry* p, int4 e, int4 d) {
-  const unsigned long long el = ((unsigned long long)(uint32_t)e.y << 32) | (uint32_t)e.x;
-  const unsigned long long eh = ((unsigned long long)(uint32_t)e.w << 32) | (uint32_t)e.z;
-  const unsigned long long dl = ((unsigned long long)(uint32_t)d.y << 32) | (uint32_t)d.x;
-  const unsigned long long dh = ((unsigned long long)(uint32_t)d.w << 32) | (uint32_t)d.z;
-  unsigned long long rl, rh;
-  asm volatile(
-      "{\n\t.reg .b128 rd, rb, rc;\n\t"
-      "mov.b128 rb, {%2, %3};\n\t"
-      "mov.b128 rc, {%4, %5};\n\t"
-      "atom.relaxed.gpu.global.cas.b128 rd, [%6], rb, rc;\n\t"
-      "mov.b128 {%0, %1}, rd;\n\t}"
-      : "=l"(rl), "=l"(rh)
-      : "l"(el), "l"(eh), "l"(dl), "l"(dh), "l"(p)
-      : "memory");
-  int4 r;
-  r.x = (int)(uint32_t)rl;
-  r.y = (int)(rl >> 32);
-  r.z = (int)(uint32_t)rh;
-  r.w = (int)(rh >> 32);
-  return r;
-}
-
-__device__ __forceinline__ bool same_entry(const int4& a, const int4& b) {
-  return a.x == b.x && a.y == b.y && a.z == b.z && a.w == b.w;
-}
-
 __device__ __forceinline__ bool key_eq(const int4& s, int32_t x, int32_t y, int32_t z) {
   return s.x == x && s.y == y && s.z == z;
 }

@@ -26,11 +26,6 @@
 #pragma once
 #include "common.cuh"
 
-// 16-byte-CAS fast paths for empty-bucket claims and bucket-case removes
-// (measured slower than the locked path on B200: 14.15 vs 14.42 G ops/s)
-#ifndef VSB_HASH_CAS_FAST
-#define VSB_HASH_CAS_FAST 0
-#endif
 
 namespace vsb {
 
@@ -172,174 +167,10 @@ __device__ __forceinline__ void claim_min(const TableView& T, int32_t pos, int32
   atomicMin(&T.claim[pos], T.tag | (unsigned long long)(uint32_t)op);
 }
 
-// Result of a lock-free lookup already done by the caller (apply_one does the
-// lookup of every op kind in one convergent phase, then branches).
-struct FindHint {
-  int4 s0;       // the bucket entry the walk started from
-  int32_t pos;   // found position or -1
-  uint32_t meta; // meta of the found entry
-};
-
 struct InsertResult {
   int32_t pos;  // -1 on capacity failure
   uint8_t created;
 };
-
-// _insert_pos (concurrent_hash.py:159-208): loop of non-blocking attempts;
-// each retry starts with a fresh lock-free retrieval.
-// `pre` (optional): the bucket entry loaded ahead of time (first attempt only;
-// a stale snapshot is harmless, every mutation re-validates under the lock).
-__device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x, int32_t y, int32_t z, int32_t op,
-                                                   const int4* pre = nullptr, const FindHint* hint = nullptr) {
-  const uint32_t b = bucket_of(T, x, y, z);
-  uint32_t* bmeta = &T.e[b].meta;
-#pragma unroll 1
-  for (int attempt = 0;; ++attempt) {
-    uint32_t fmeta;
-    int4 s0;
-    int32_t pos;
-    if (attempt == 0 && hint) {
-      s0 = hint->s0;
-      pos = hint->pos;
-      fmeta = hint->meta;
-    } else {
-      s0 = (attempt == 0 && pre) ? *pre : ld_bucket(T.e + b);
-      pos = find_pos_from(T, x, y, z, b, s0, &fmeta);
-    }
-    if (pos >= 0) {
-      if (fmeta & kFresh) claim_min(T, pos, op);
-      return {pos, 0};
-    }
-#if VSB_HASH_CAS_FAST
-    // Lock-free claim of an empty bucket with an empty chain: if the bucket
-    // entry still holds exactly this snapshot (unlocked, unoccupied, no
-    // chain), the key is absent from the table, so ONE 16-byte CAS claims
-    // it.  Any interleaved change (a lock, a claim, a link) fails the CAS.
-    if (attempt == 0 && ((uint32_t)s0.w & (kLock | kOcc | kNext)) == 0u) {
-      const int4 want = make_int4(x, y, z, (int)(kOcc | kFresh));
-      if (same_entry(cas_entry(T.e + b, s0, want), s0)) return {(int32_t)b, 1};
-    }
-#endif
-    const uint32_t old = atom_or_relaxed(bmeta, kLock);
-    if (old & kLock) {
-      if (attempt > 4) __nanosleep(64);
-      continue;
-    }
-    // --- chain lock held.  The re-scan's first load depends on `old`, so it
-    // is issued only after the lock word came back (acquire by dependency).
-    const uint32_t dep = (old >> 31) & 1u;  // always 0 here
-    uint32_t tail = b, tail_meta = old;
-    {
-      const int4 s = ld_entry(T.e + b + dep);
-      if ((old & kOcc) && key_eq(s, x, y, z)) {
-        atom_exch_relaxed(bmeta, old);  // unlock; nothing was modified
-        if (old & kFresh) claim_min(T, (int32_t)b, op);
-        return {(int32_t)b, 0};
-      }
-      uint32_t meta = old;
-      while (meta & kNext) {
-        const uint32_t e = next_pos(T, meta);
-        const int4 t = ld_entry(T.e + e);
-        meta = (uint32_t)t.w;
-        if ((meta & kOcc) && key_eq(t, x, y, z)) {
-          atom_exch_relaxed(bmeta, old);
-          if (meta & kFresh) claim_min(T, (int32_t)e, op);
-          return {(int32_t)e, 0};
-        }
-        tail = e;
-        tail_meta = meta;
-      }
-    }
-    if (!(old & kOcc)) {
-      // claim the free bucket entry: key, OCC and unlock in ONE 16-byte
-      // store; its NEXT link is kept (:185-192)
-      st_entry(T.e + b, x, y, z, (old & kNext) | kOcc | kFresh);
-      return {(int32_t)b, 1};
-    }
-    const int64_t ne = pop_free(T);
-    if (ne < 0) {
-      atom_exch_relaxed(bmeta, old);
-      atomicOr(&T.ctl->error, 1u);
-      return {-1, 0};
-    }
-    const uint32_t e = (uint32_t)ne;
-    st_entry(T.e + e, x, y, z, kOcc | kFresh);  // NEXT = 0 clears the stale offset (:200)
-    const uint32_t link = e - T.n + 1u;
-    if (tail == b) {
-      atom_exch_release(bmeta, (old & ~kNext) | link);  // publish + unlock
-    } else {
-      st_release_u32(&T.e[tail].meta, (tail_meta & ~kNext) | link);  // publish last (:204)
-      atom_exch_release(bmeta, old);                                   // unlock after the link
-    }
-    return {(int32_t)e, 1};
-  }
-}
-
-// remove (concurrent_hash.py:251-295).  Returns the vacated position or -1.
-// Vacated EXCESS positions are recycled by the caller's recycle launch.
-__device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int32_t y, int32_t z,
-                                            const int4* pre = nullptr, const FindHint* hint = nullptr) {
-  const uint32_t b = bucket_of(T, x, y, z);
-  uint32_t* bmeta = &T.e[b].meta;
-#pragma unroll 1
-  for (int attempt = 0;; ++attempt) {
-    uint32_t fmeta;
-    int4 s0;
-    int32_t fp;
-    if (attempt == 0 && hint) {
-      s0 = hint->s0;
-      fp = hint->pos;
-    } else {
-      s0 = (attempt == 0 && pre) ? *pre : ld_bucket(T.e + b);
-      fp = find_pos_from(T, x, y, z, b, s0, &fmeta);
-    }
-    if (fp < 0) return -1;
-#if VSB_HASH_CAS_FAST
-    // Bucket case without the lock: if the bucket entry still holds exactly
-    // the snapshot that matched (this key, occupied, unlocked), clearing its
-    // occupancy with ONE 16-byte CAS is the reference's bucket-case remove
-    // (NEXT kept, :266-275).
-    if (attempt == 0 && fp == (int32_t)b && !((uint32_t)s0.w & kLock)) {
-      const int4 want = make_int4(s0.x, s0.y, s0.z, (int)((uint32_t)s0.w & ~(kOcc | kFresh)));
-      if (same_entry(cas_entry(T.e + b, s0, want), s0)) return (int32_t)b;
-    }
-#endif
-    const uint32_t old = atom_or_relaxed(bmeta, kLock);
-    if (old & kLock) {
-      if (attempt > 4) __nanosleep(64);
-      continue;
-    }
-    const uint32_t dep = (old >> 31) & 1u;
-    const int4 s = ld_entry(T.e + b + dep);
-    if ((old & kOcc) && key_eq(s, x, y, z)) {
-      // bucket case: clear occupancy only; NEXT and the chain stay (:266-275)
-      atom_exch_relaxed(bmeta, old & ~(kOcc | kFresh));
-      return (int32_t)b;
-    }
-    uint32_t prev = b, prev_meta = old, meta = old;
-    while (meta & kNext) {
-      const uint32_t e = next_pos(T, meta);
-      const int4 t = ld_entry(T.e + e);
-      meta = (uint32_t)t.w;
-      if ((meta & kOcc) && key_eq(t, x, y, z)) {
-        // excess case: clear the victim but keep its stale NEXT (:280-289)
-        st_relaxed_u32(&T.e[e].meta, meta & ~(kOcc | kFresh));
-        const uint32_t vnext = meta & kNext;
-        if (prev == b) {
-          atom_exch_relaxed(bmeta, (old & ~kNext) | vnext);  // relink + unlock, one word
-        } else {
-          st_relaxed_u32(&T.e[prev].meta, (prev_meta & ~kNext) | vnext);
-          atom_exch_release(bmeta, old);  // unlock only after the relink
-        }
-        return (int32_t)e;
-      }
-      prev = e;
-      prev_meta = meta;
-    }
-    // key vanished between the find and the lock; re-check (:293)
-    atom_exch_relaxed(bmeta, old);
-  }
-}
 
 // Post pass for one op of an insert/apply batch: settle the created flag of
 // a creator against in-batch duplicates (lowest op index wins), clear FRESH;
@@ -471,50 +302,55 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
   }
 }
 
+// _insert_pos (concurrent_hash.py:159-208): a lock-free retrieval, then, if
+// the key is absent, the locked claim (mutate_locked).  `pre` (optional):
+// the bucket entry loaded ahead of time (a stale snapshot is harmless: every
+// mutation re-validates under the lock).
+__device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x, int32_t y, int32_t z, int32_t op,
+                                                   const int4* pre = nullptr) {
+  const uint32_t b = bucket_of(T, x, y, z);
+  uint32_t fmeta;
+  const int32_t pos = find_pos_from(T, x, y, z, b, pre ? *pre : ld_bucket(T.e + b), &fmeta);
+  if (pos >= 0) {
+    if (fmeta & kFresh) claim_min(T, pos, op);
+    return {pos, 0};
+  }
+  return mutate_locked(T, x, y, z, true, op, b);
+}
+
+// remove (concurrent_hash.py:251-295).  Returns the vacated position or -1.
+// Vacated EXCESS positions are recycled by the caller's recycle launch.
+__device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int32_t y, int32_t z,
+                                            const int4* pre = nullptr) {
+  const uint32_t b = bucket_of(T, x, y, z);
+  uint32_t fmeta;
+  if (find_pos_from(T, x, y, z, b, pre ? *pre : ld_bucket(T.e + b), &fmeta) < 0) return -1;
+  return mutate_locked(T, x, y, z, false, 0, b).pos;
+}
+
 // One mixed op (insert / find / erase) with its bucket entry already loaded.
 // The lock-free lookup is the same walk for every kind, so it runs first for
 // all lanes together (a warp with mixed kinds would otherwise walk its
 // chains once per kind, one branch after the other); only inserts of absent
 // keys and erases of present keys go on to mutate.  Returns the size delta.
-#ifndef VSB_HASH_CONVERGENT_LOOKUP
-#define VSB_HASH_CONVERGENT_LOOKUP 1
-#endif
 __device__ __forceinline__ int apply_one(const TableView& T, int32_t x, int32_t y, int32_t z, uint8_t op, uint64_t i,
                                          uint32_t b, const int4& pre, uint8_t* __restrict__ result,
                                          int32_t* __restrict__ index) {
   int32_t pos;
   uint8_t res;
   int delta = 0;
-#if VSB_HASH_CONVERGENT_LOOKUP
-  FindHint h;
-  h.s0 = pre;
-  h.pos = find_pos_from(T, x, y, z, b, pre, &h.meta);
+  uint32_t fmeta;
+  const int32_t fpos = find_pos_from(T, x, y, z, b, pre, &fmeta);
   const bool ins = op == 0 /*VS_OP_INSERT*/, era = op == 2 /*VS_OP_ERASE*/;
-  pos = h.pos;
-  res = !ins && h.pos >= 0;  // find: found; erase: provisional
-  if (ins && h.pos >= 0 && (h.meta & kFresh)) claim_min(T, h.pos, (int32_t)i);
-  if ((ins && h.pos < 0) || (era && h.pos >= 0)) {
+  pos = fpos;
+  res = !ins && fpos >= 0;  // find: found; erase: provisional
+  if (ins && fpos >= 0 && (fmeta & kFresh)) claim_min(T, fpos, (int32_t)i);
+  if ((ins && fpos < 0) || (era && fpos >= 0)) {
     const InsertResult r = mutate_locked(T, x, y, z, ins, (int32_t)i, b);
     pos = r.pos;
     res = ins ? r.created : (uint8_t)(r.pos >= 0);
     delta = ins ? (int)r.created : -(int)(r.pos >= 0);
   }
-#else
-  if (op == 0 /*VS_OP_INSERT*/) {
-    const InsertResult r = insert_key(T, x, y, z, (int32_t)i, &pre);
-    pos = r.pos;
-    res = r.created;
-    delta = r.created;
-  } else if (op == 2 /*VS_OP_ERASE*/) {
-    pos = erase_key(T, x, y, z, &pre);
-    res = pos >= 0;
-    delta = -(int)res;
-  } else {
-    uint32_t meta;
-    pos = find_pos_from(T, x, y, z, b, pre, &meta);
-    res = pos >= 0;
-  }
-#endif
   __stcs(result + i, res);
   __stcs(index + i, pos);
   return delta;
