@@ -305,6 +305,10 @@ void vs_shard_destroy(vs_shard *s);
 vs_status vs_shard_export(vs_shard *s, uint8_t handle_out[64]);
 /* handles: world x 64 bytes, rank-major (own entry ignored). */
 vs_status vs_shard_connect(vs_shard *s, const uint8_t *handles);
+/* All ranks of a world in ONE process on ONE device (tests and diagnostics:
+ * an 8-rank node simulated on one GPU, each rank's vs_shard_apply on its own
+ * stream): connects the windows directly, no IPC. */
+vs_status vs_shard_connect_local(vs_shard *const *shards, int n);
 /* keys device int32[n][3], ops device uint8[n] (VS_OP_*), result device
  * uint8[n] (created / found / erased).  Asynchronous on `stream`. */
 vs_status vs_shard_apply(vs_shard *s, const int32_t *keys, const uint8_t *ops, uint64_t n,

@@ -95,6 +95,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_shard_export": (_i32, [_vp, ctypes.POINTER(ctypes.c_uint8 * 64)]),
     "vs_shard_connect": (_i32, [_vp, ctypes.c_char_p]),
     "vs_shard_apply": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp]),
+    "vs_shard_connect_local": (_i32, [ctypes.POINTER(_vp), ctypes.c_int]),
     "vs_shard_check": (_i32, [_vp]),
     "vs_shard_owner": (_i32, [_vp, _u64, ctypes.c_int, _vp]),
 }

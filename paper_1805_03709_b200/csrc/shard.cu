@@ -525,6 +525,21 @@ vs_status vs_shard_create(vs_table* local, int rank, int world, uint64_t max_bat
     vs_shard_destroy(s);
     return cuda_status(e, "vs_shard_create");
   }
+  // load every kernel of the route now: with lazy module loading, a first
+  // launch inside vs_shard_apply could wait for the device while this rank's
+  // k_wait spins on peers whose launches sit behind it (one-process groups)
+  {
+    cudaFuncAttributes fa;
+    const void* fns[] = {(const void*)k_wpart_count, (const void*)k_wpart_scan, (const void*)k_wpart_push,
+                         (const void*)k_wait,        (const void*)k_shard_apply, (const void*)k_shard_post,
+                         (const void*)k_shard_return};
+    for (const void* f : fns)
+      if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) {
+      vs_shard_destroy(s);
+      return cuda_status(e, "vs_shard_create (kernel load)");
+    }
+  }
   s->peer[rank] = s->win;
   if (world == 1) s->connected = true;
   *out = s;
@@ -560,6 +575,25 @@ vs_status vs_shard_connect(vs_shard* s, const uint8_t* handles) {
     s->opened[r] = true;
   }
   s->connected = true;
+  return VS_OK;
+}
+
+vs_status vs_shard_connect_local(vs_shard* const* shards, int n) {
+  if (!shards || n < 1) {
+    set_error("vs_shard_connect_local: bad arguments");
+    return VS_ERR_INVALID;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (!shards[i] || shards[i]->world != n || shards[i]->rank != i || shards[i]->device != shards[0]->device ||
+        shards[i]->bmax != shards[0]->bmax) {
+      set_error("vs_shard_connect_local: shards must be ranks 0..n-1 of one world on one device, same max_batch");
+      return VS_ERR_INVALID;
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    for (int r = 0; r < n; ++r) shards[i]->peer[r] = shards[r]->win;
+    shards[i]->connected = true;
+  }
   return VS_OK;
 }
 

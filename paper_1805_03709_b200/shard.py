@@ -188,3 +188,79 @@ class ShardedBlockHashSet:
             n = n.cuda()
         dist.all_reduce(n, group=self.group)
         return int(n.item())
+
+
+class OneGpuShardGroup:
+    """All `world` ranks of a sharded set on ONE GPU in ONE process (tests and
+    diagnostics): rank r owns `tables[r]`; ``apply`` queues every rank's
+    batch on the rank's own stream, exactly as G processes would, and the
+    kernels route through the same windows and flags as across GPUs
+    (csrc/shard.cu, vs_shard_connect_local).  The process must give every
+    rank stream its own hardware queue (CUDA_DEVICE_MAX_CONNECTIONS >= world
+    + 1, set before CUDA initialises), or a rank's push can queue behind
+    another rank's spin-wait; such a wait times out and check() raises."""
+
+    def __init__(self, tables, max_batch: int) -> None:
+        import ctypes
+
+        import torch
+
+        from . import _lib
+
+        self._lib = _lib.load()
+        self.tables = list(tables)
+        self.world = len(self.tables)
+        self.max_batch = int(max_batch)
+        self.device = self.tables[0].device
+        self.shards = []
+        for r, t in enumerate(self.tables):
+            h = ctypes.c_void_p()
+            _lib.check(self._lib.vs_shard_create(t.handle, r, self.world, self.max_batch, ctypes.byref(h)),
+                       "vs_shard_create")
+            self.shards.append(h)
+        arr = (ctypes.c_void_p * self.world)(*[h.value for h in self.shards])
+        _lib.check(self._lib.vs_shard_connect_local(arr, self.world), "vs_shard_connect_local")
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(self.world)]
+
+    def apply(self, keys_list, ops_list):
+        """One collective batch: keys_list[r] / ops_list[r] are rank r's ops;
+        returns the per-rank results (device uint8), ordered after the call."""
+        import ctypes
+
+        import torch
+
+        from . import _lib
+
+        cur = torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        outs = []
+        for r in range(self.world):
+            k = keys_list[r].to(self.device, torch.int32).contiguous()
+            o = ops_list[r].to(self.device, torch.uint8).contiguous()
+            out = torch.empty(k.shape[0], dtype=torch.uint8, device=self.device)
+            st = self.streams[r]
+            st.wait_event(ev)
+            k.record_stream(st)
+            o.record_stream(st)
+            out.record_stream(st)
+            _lib.check(self._lib.vs_shard_apply(self.shards[r], _lib.ptr(k), _lib.ptr(o), k.shape[0], _lib.ptr(out),
+                                                ctypes.c_void_p(st.cuda_stream)), "vs_shard_apply")
+            outs.append(out)
+        for st in self.streams:
+            cur.wait_stream(st)
+        return outs
+
+    def check(self) -> None:
+        from . import _lib
+
+        for h in self.shards:
+            _lib.check(self._lib.vs_shard_check(h), "vs_shard")
+
+    def __del__(self) -> None:
+        for h in getattr(self, "shards", []):
+            try:
+                self._lib.vs_shard_destroy(h)
+            except Exception:
+                pass
+        self.shards = []

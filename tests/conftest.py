@@ -2,8 +2,15 @@
 
 from __future__ import annotations
 
+import os
 import pathlib
 import sys
+
+# One-GPU simulations of multi-rank nodes (OneGpuShardGroup) run every rank's
+# kernels on its own stream and spin-wait across streams: each stream needs
+# its own hardware queue, or a rank's push can sit behind another rank's wait
+# (CUDA's default is 8 queues).  Read at CUDA context creation.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import pytest
 

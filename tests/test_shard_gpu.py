@@ -132,3 +132,67 @@ def test_peer_single_rank_equals_table(tmp_path, dev):
         sh.check()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [3, 8])
+def test_peer_route_world_on_one_gpu(dev, world):
+    """An 8-rank (and a 3-rank) node simulated in one process on one GPU:
+    every rank's batch on its own stream through the real windows, flags and
+    kernels (OneGpuShardGroup).  Per-op results equal the A18 expectation,
+    every key lives on its owner, sizes add up, cross-rank duplicate fresh
+    inserts resolve to the lowest rank, and every table audits clean."""
+    import torch
+
+    from paper_1805_03709_b200 import BlockHashSet, workloads
+    from paper_1805_03709_b200.shard import OneGpuShardGroup, owner_of
+
+    spec = workloads.MixSpec(live=40_000, load_factor=0.7, batch=1 << 13)
+    tabs = [BlockHashSet(spec.bucket_count, spec.excess, device=dev) for _ in range(world)]
+    g = OneGpuShardGroup(tabs, max_batch=spec.live)
+    z = lambda n: torch.zeros(n, dtype=torch.uint8, device=dev)  # noqa: E731
+    init = [workloads.id_to_key_torch(torch.arange(r << 40, (r << 40) + spec.live, device=dev)) for r in range(world)]
+    res = g.apply(init, [z(spec.live)] * world)
+    torch.cuda.synchronize()
+    assert all(int(x.sum()) == spec.live for x in res)
+    for r, t in enumerate(tabs):
+        mine, _ = t.snapshot_tensor()
+        assert bool((owner_of(mine, world) == r).all()), r
+    gens = [torch.Generator(device=dev) for _ in range(world)]
+    for r, gg in enumerate(gens):
+        gg.manual_seed(100 + r)
+    lo = [r << 40 for r in range(world)]
+    hi = [(r << 40) + spec.live for r in range(world)]
+    for step in range(3):
+        ks, os_, ex = [], [], []
+        for r in range(world):
+            ids, ops, expect = workloads.mix_batch_ids(spec, step, lo[r], hi[r], gens[r], dev)
+            ids = torch.where(ids >= workloads.MISS_BASE, ids + (r << 50), ids)
+            ks.append(workloads.id_to_key_torch(ids))
+            os_.append(ops)
+            ex.append(expect)
+            lo[r] += spec.counts["erase"]
+            hi[r] += spec.counts["fresh"]
+        out = g.apply(ks, os_)
+        torch.cuda.synchronize()
+        for r in range(world):
+            assert torch.equal(out[r], ex[r]), (world, step, r, int((out[r] != ex[r]).sum()))
+    assert sum(t.approx_size() for t in tabs) == world * spec.live
+    # the same 500 new keys on every rank (twice each): rank 0's first copy creates
+    shared = workloads.id_to_key_torch(torch.arange(9 << 45, (9 << 45) + 500, device=dev))
+    both = torch.cat([shared, shared])
+    out = g.apply([both] * world, [z(1000)] * world)
+    torch.cuda.synchronize()
+    want0 = torch.cat([torch.ones(500, dtype=torch.uint8, device=dev), z(500)])
+    assert torch.equal(out[0], want0)
+    for r in range(1, world):
+        assert int(out[r].sum()) == 0
+    # ragged: empty batch on some ranks
+    ks = [shared[: (r % 3) * 100] for r in range(world)]
+    out = g.apply(ks, [torch.ones(k.shape[0], dtype=torch.uint8, device=dev) for k in ks])
+    torch.cuda.synchronize()
+    for r in range(world):
+        assert int(out[r].sum()) == ks[r].shape[0]
+    g.check()
+    for t in tabs:
+        a = t.audit()
+        assert a["duplicates"] == 0 and a["unreachable_live"] == 0
