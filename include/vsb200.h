@@ -313,6 +313,10 @@ vs_status vs_shard_connect_local(vs_shard *const *shards, int n);
  * uint8[n] (created / found / erased).  Asynchronous on `stream`. */
 vs_status vs_shard_apply(vs_shard *s, const int32_t *keys, const uint8_t *ops, uint64_t n,
                          uint8_t *result, vs_stream_t stream);
+/* Bound on every device-side wait for a peer (default 20 s): a rank whose
+ * peers never arrive (mismatched collective calls) gives up instead of
+ * hanging the GPU, raises the shard's error flag and returns garbage. */
+vs_status vs_shard_set_timeout_ms(vs_shard *s, uint64_t ms);
 /* SYNCHRONOUS: VS_ERR_CUDA if a wait for a peer timed out since creation. */
 vs_status vs_shard_check(vs_shard *s);
 /* Host helper: owner rank of n HOST keys (the routing function). */

@@ -97,6 +97,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_shard_apply": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp]),
     "vs_shard_connect_local": (_i32, [ctypes.POINTER(_vp), ctypes.c_int]),
     "vs_shard_check": (_i32, [_vp]),
+    "vs_shard_set_timeout_ms": (_i32, [_vp, _u64]),
     "vs_shard_owner": (_i32, [_vp, _u64, ctypes.c_int, _vp]),
 }
 

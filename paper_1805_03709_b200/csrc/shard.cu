@@ -649,6 +649,15 @@ vs_status vs_shard_apply(vs_shard* s, const int32_t* keys, const uint8_t* ops, u
   return VS_OK;
 }
 
+vs_status vs_shard_set_timeout_ms(vs_shard* s, uint64_t ms) {
+  if (!s || ms < 1) {
+    set_error("vs_shard_set_timeout_ms: bad arguments");
+    return VS_ERR_INVALID;
+  }
+  s->timeout_ns = ms * 1000000ull;
+  return VS_OK;
+}
+
 vs_status vs_shard_check(vs_shard* s) {
   if (!s) {
     set_error("vs_shard_check: NULL");

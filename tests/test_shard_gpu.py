@@ -196,3 +196,29 @@ def test_peer_route_world_on_one_gpu(dev, world):
     for t in tabs:
         a = t.audit()
         assert a["duplicates"] == 0 and a["unreachable_live"] == 0
+
+
+def test_peer_route_timeout_is_loud(dev):
+    """A collective call only one rank makes: that rank's device-side wait
+    gives up after the (shortened) timeout instead of hanging the GPU, and
+    check() raises."""
+    import ctypes
+
+    import torch
+
+    from paper_1805_03709_b200 import BlockHashSet, _lib, workloads
+    from paper_1805_03709_b200.shard import OneGpuShardGroup
+
+    tabs = [BlockHashSet(1 << 12, 1 << 12, device=dev) for _ in range(2)]
+    g = OneGpuShardGroup(tabs, max_batch=1024)
+    lib = _lib.load()
+    for h in g.shards:
+        _lib.check(lib.vs_shard_set_timeout_ms(h, 200))
+    k = workloads.id_to_key_torch(torch.arange(100, device=dev))
+    o = torch.zeros(100, dtype=torch.uint8, device=dev)
+    out = torch.empty(100, dtype=torch.uint8, device=dev)
+    st = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    _lib.check(lib.vs_shard_apply(g.shards[0], _lib.ptr(k), _lib.ptr(o), 100, _lib.ptr(out), st))  # rank 1 never calls
+    torch.cuda.synchronize()
+    with pytest.raises(RuntimeError, match="timeout"):
+        _lib.check(lib.vs_shard_check(g.shards[0]), "vs_shard")
