@@ -226,10 +226,14 @@ vs_status vs_affected_dedup(vs_table *scratch, const int32_t *updated, uint64_t 
  * fifo_keys_host[c] : device int32[fifo_cap_host[c]][3] ring of client c
  * fifo_tail_host[c] : device uint64 (absolute, monotonically increasing tail)
  * n_created         : device uint64[C] (may be NULL).
+ * n_dev             : device uint64 (may be NULL): only the first
+ *                     min(*n_dev, n) keys are inserted (n is then a bound),
+ *                     so a count produced on the device (vs_affected_dedup)
+ *                     needs no host synchronisation.
  * Fully asynchronous; up to 32 sets per call. */
 vs_status vs_stream_insert_many(vs_table *const *sets_host, int n_sets,
-                                const int32_t *keys, uint64_t n, uint8_t *created,
-                                int32_t *const *fifo_keys_host,
+                                const int32_t *keys, uint64_t n, const uint64_t *n_dev,
+                                uint8_t *created, int32_t *const *fifo_keys_host,
                                 const uint64_t *fifo_cap_host, uint64_t *const *fifo_tail_host,
                                 uint64_t *n_created, vs_stream_t stream);
 

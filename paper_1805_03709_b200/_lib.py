@@ -74,7 +74,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_mc_compact": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp, _u64, _vp, _vp]),
     "vs_scan_workspace_bytes": (_u64, [_u64]),
     "vs_affected_dedup": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp]),
-    "vs_stream_insert_many": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _vp, _u64, _vp,
+    "vs_stream_insert_many": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _vp, _u64, _vp, _vp,
                                      ctypes.POINTER(_vp), _pu64, ctypes.POINTER(_vp), _vp, _vp]),
     "vs_stream_extract_random": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _u64, _pu64, _vp, _vp, _vp]),
     "vs_stream_extract_visible": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _u64, _pu64,

@@ -38,12 +38,18 @@ struct FifoViews {
 
 __global__ void __launch_bounds__(256) k_multi_insert(const __grid_constant__ SetViews V,
                                                       const int32_t* __restrict__ keys, uint64_t n,
+                                                      const uint64_t* __restrict__ n_dev,
                                                       uint8_t* __restrict__ created, int32_t* __restrict__ index) {
   const int c = blockIdx.y;
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const TableView& T = V.v[c];
+  const uint64_t nv = n_dev && *n_dev < n ? *n_dev : n;  // keys past the device count: not inserted
   int delta = 0;
-  if (i < n) {
+  if (i >= nv && i < n) {
+    created[(uint64_t)c * n + i] = 0;
+    index[(uint64_t)c * n + i] = -1;
+  }
+  if (i < nv) {
     const InsertResult r = insert_key(T, keys[3 * i], keys[3 * i + 1], keys[3 * i + 2], (int32_t)i);
     created[(uint64_t)c * n + i] = r.created;
     index[(uint64_t)c * n + i] = r.pos;
@@ -137,37 +143,48 @@ __global__ void __launch_bounds__(256) k_multi_extract(const __grid_constant__ S
   if (threadIdx.x == 0) found_s = 0;
   __syncthreads();
   const uint32_t warp = threadIdx.x >> 5;
-  for (uint64_t scanned = 0; scanned < cap; scanned += 256) {
-    const uint64_t found = found_s;
-    if (found >= max_n) break;
-    uint64_t p = (uint64_t)start + scanned + threadIdx.x;
-    p = p >= cap ? p - cap : p;
-    int4 e = make_int4(0, 0, 0, 0);
-    bool live = false;
-    if (scanned + threadIdx.x < cap) {
-      e = ld_entry(T.e + p);
-      live = ((uint32_t)e.w & kOcc) != 0;
-      if (live && F.enabled) live = block_visible(F, e.x, e.y, e.z);
-    }
-    const uint32_t bal = __ballot_sync(0xffffffffu, live);
-    if (lane_id() == 0) wcnt[warp] = __popc(bal);
-    __syncthreads();
-    uint32_t before = 0, total = 0;
-    for (uint32_t w = 0; w < 8; ++w) {
-      before += (w < warp) ? wcnt[w] : 0;
-      total += wcnt[w];
-    }
-    if (live) {
-      const uint64_t o = found + before + __popc(bal & lanemask_lt());
-      if (o < max_n) {
-        out[3 * o] = e.x;
-        out[3 * o + 1] = e.y;
-        out[3 * o + 2] = e.z;
+  // chunks of kExtractK x 256 positions: all loads of a chunk in flight
+  // first, then the ordered selection round by round (position order)
+  constexpr int kExtractK = 8;
+  for (uint64_t scanned = 0; scanned < cap; scanned += 256 * kExtractK) {
+    if (found_s >= max_n) break;
+    int4 e[kExtractK];
+    bool live[kExtractK];
+#pragma unroll
+    for (int k = 0; k < kExtractK; ++k) {
+      const uint64_t q = scanned + (uint64_t)k * 256 + threadIdx.x;
+      uint64_t p = (uint64_t)start + q;
+      p = p >= cap ? p - cap : p;
+      live[k] = false;
+      if (q < cap) {
+        e[k] = ld_entry(T.e + p);
+        live[k] = ((uint32_t)e[k].w & kOcc) != 0;
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) found_s = found + total;
-    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kExtractK; ++k) {
+      if (live[k] && F.enabled) live[k] = block_visible(F, e[k].x, e[k].y, e[k].z);
+      const uint64_t found = found_s;
+      const uint32_t bal = __ballot_sync(0xffffffffu, live[k]);
+      if (lane_id() == 0) wcnt[warp] = __popc(bal);
+      __syncthreads();
+      uint32_t before = 0, total = 0;
+      for (uint32_t w = 0; w < 8; ++w) {
+        before += (w < warp) ? wcnt[w] : 0;
+        total += wcnt[w];
+      }
+      if (live[k]) {
+        const uint64_t o = found + before + __popc(bal & lanemask_lt());
+        if (o < max_n) {
+          out[3 * o] = e[k].x;
+          out[3 * o + 1] = e[k].y;
+          out[3 * o + 2] = e[k].z;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) found_s = found + total;
+      __syncthreads();
+    }
   }
   const uint64_t m = found_s < max_n ? found_s : max_n;
   __syncthreads();  // keys_out complete before the removals read it
@@ -326,7 +343,8 @@ vs_status vs_affected_dedup(vs_table* scratch, const int32_t* updated, uint64_t 
 }
 
 vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const int32_t* keys, uint64_t n,
-                                uint8_t* created, int32_t* const* fifo_keys_host, const uint64_t* fifo_cap_host,
+                                const uint64_t* n_dev, uint8_t* created, int32_t* const* fifo_keys_host,
+                                const uint64_t* fifo_cap_host,
                                 uint64_t* const* fifo_tail_host, uint64_t* n_created, vs_stream_t stream) {
   SetViews V;
   if (!sets_host) {
@@ -356,7 +374,7 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
   VS_CK(cudaMallocAsync((void**)&off, 8 * (total + 1), s));
   VS_CK(cudaMallocAsync((void**)&work, 8 * (scan_tiles(total) + 1), s));
   const dim3 grid(grid_for(n, 256), n_sets);
-  { ProfScope prof(2, s); k_multi_insert<<<grid, 256, 0, s>>>(V, keys, n, created, index); vsb::count_launch(); }
+  { ProfScope prof(2, s); k_multi_insert<<<grid, 256, 0, s>>>(V, keys, n, n_dev, created, index); vsb::count_launch(); }
   { k_multi_fixup<<<grid, 256, 0, s>>>(V, keys, n, created, index); vsb::count_launch(); }
   cudaError_t e = exclusive_scan<uint8_t>(created, total, off, work, s);
   const bool fifo = fifo_keys_host && fifo_cap_host && fifo_tail_host;

@@ -177,13 +177,16 @@ def _mark_done(tables, s) -> None:
         t._last_stream = s
 
 
-def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True):
+def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True, n_dev=None):
     """``for s in sets: s.insert_many(keys)`` in one launch per 32 clients.
 
     For each client the newly created keys (the set difference keys \\
     pending) are appended to its FIFO in input order, exactly like the
     reference's per-key deque.append.  Returns the created count per client
     (synchronising), or the device counts (int64[C]) when sync=False.
+    ``n_dev`` (device int64[1], optional): only the first min(n_dev, len(keys))
+    keys count -- a device-produced count (vs_affected_dedup) needs no host
+    synchronisation.
     """
     if not sets:
         return []
@@ -207,7 +210,7 @@ def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True):
         caps = (ctypes.c_uint64 * C)(*[st.fifo_capacity for st in group])
         tails = (ctypes.c_void_p * C)(*[st._tail_dev.data_ptr() for st in group])
         s = _order_streams(tables)
-        check(lib.vs_stream_insert_many(handles, C, ptr(k), n, ptr(created), fifos, caps, tails,
+        check(lib.vs_stream_insert_many(handles, C, ptr(k), n, ptr(n_dev), ptr(created), fifos, caps, tails,
                                         ptr(counts[g0:g0 + C]), ctypes.c_void_p(s.cuda_stream)), "fan_out")
         _mark_done(tables, s)
         for st in group:

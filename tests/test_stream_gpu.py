@@ -95,6 +95,28 @@ def test_fan_out_40_clients_vs_oracle(dev):
         assert set(s.snapshot()) == o.set
 
 
+def test_fan_out_device_count_bound(dev):
+    """fan_out(keys, n_dev=k): only the first k keys count (sets, FIFO order,
+    created counts), the rest of the buffer is ignored -- the sync-free tick."""
+    import torch
+
+    from paper_1805_03709_b200 import StreamSet, fan_out
+
+    rng = np.random.default_rng(11)
+    a = [StreamSet(1 << 10, 1 << 10) for _ in range(5)]
+    b = [StreamSet(1 << 10, 1 << 10) for _ in range(5)]
+    for step in range(4):
+        keys = torch.from_numpy(rng.integers(0, 16, (300, 3)).astype(np.int32)).to(dev)
+        k = int(rng.integers(0, 301))
+        n_dev = torch.tensor([k], dtype=torch.int64, device=dev)
+        got = fan_out(a, keys, n_dev=n_dev)
+        want = fan_out(b, keys[:k])
+        assert got == want, (step, k)
+        for x, y in zip(a, b):
+            assert x.fifo_entries() == y.fifo_entries()
+            assert set(x.snapshot()) == set(y.snapshot())
+
+
 def test_affected_dedup_order(dev):
     import ctypes
 
