@@ -7,7 +7,7 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 tail -3 gpurun_out/bench.err
 if [ "${NCU:-1}" = "1" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ --csv \
-  --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --mc-steps 2 \
+  --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --mc-steps 2 --stream-ticks 20 \
   > gpurun_out/ncu_launch_bench.log 2>&1; echo ncu_launch=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_apply -s 3 -c 1 \
   -o gpurun_out/prof_apply python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-mc \

@@ -38,7 +38,7 @@ for r in rows[start:]:
     agg[name][1] += float(r[iv].replace(",", ""))
 tot = sum(v[1] for v in agg.values())
 lines = [f"# ncu launch list ({tag}): ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_",
-         "#   python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --mc-steps 2   (cold-cache, serialised)",
+         "#   python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --mc-steps 2 --stream-ticks 20   (cold-cache, serialised)",
          f"{'kernel':40s} {'launches':>8s} {'total_ms':>10s} {'avg_us':>10s} {'share':>7s}"]
 for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
     lines.append(f"{k:40s} {c:8d} {v / 1e6:10.3f} {v / c / 1e3:10.1f} {100 * v / tot:6.1f}%")
