@@ -138,9 +138,12 @@ struct WarpStage {
   uint8_t op[kWTile];
 };
 
-__device__ __forceinline__ void load_rounds(const int32_t* __restrict__ keys, const uint8_t* __restrict__ ops,
-                                            uint64_t n, uint64_t t0, WarpStage& S, int32_t* x, int32_t* y, int32_t* z,
-                                            uint32_t* op) {
+// Stage the warp's tile into its shared buffer: 16-byte coalesced loads
+// when the tile is whole and the buffers 16-B aligned, element loads (zero
+// past n) otherwise.  Rounds then read their keys from shared memory, which
+// keeps the kernels at 8 resident CTAs per SM.
+__device__ __forceinline__ void stage_tile(const int32_t* __restrict__ keys, const uint8_t* __restrict__ ops,
+                                           uint64_t n, uint64_t t0, WarpStage& S) {
   const uint32_t lane = lane_id();
   const bool whole = t0 + kWTile <= n && ((uintptr_t)keys & 15) == 0 && (!ops || ((uintptr_t)ops & 15) == 0);
   if (whole) {
@@ -148,30 +151,12 @@ __device__ __forceinline__ void load_rounds(const int32_t* __restrict__ keys, co
 #pragma unroll
     for (int q = 0; q < 3 * kWTile / 4 / 32; ++q) ((int4*)S.k)[q * 32 + lane] = __ldcs(kv + q * 32 + lane);
     if (ops && lane < kWTile / 16) ((int4*)S.op)[lane] = __ldcs((const int4*)(ops + t0) + lane);
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < kPartRounds; ++r) {
-      const uint32_t j = r * 32 + lane;
-      x[r] = S.k[3 * j];
-      y[r] = S.k[3 * j + 1];
-      z[r] = S.k[3 * j + 2];
-      if (op) op[r] = S.op[j];
-    }
-    __syncwarp();
-    return;
+  } else {
+    for (uint32_t j = lane; j < 3 * kWTile; j += 32) S.k[j] = t0 * 3 + j < 3 * n ? ld_stream(keys + 3 * t0 + j) : 0;
+    if (ops)
+      for (uint32_t j = lane; j < kWTile; j += 32) S.op[j] = t0 + j < n ? ld_stream(ops + t0 + j) : (uint8_t)0;
   }
-#pragma unroll
-  for (int r = 0; r < kPartRounds; ++r) {
-    const uint64_t i = t0 + (uint64_t)r * 32 + lane;
-    x[r] = y[r] = z[r] = 0;
-    if (op) op[r] = 0;
-    if (i < n) {
-      x[r] = ld_stream(keys + 3 * i);
-      y[r] = ld_stream(keys + 3 * i + 1);
-      z[r] = ld_stream(keys + 3 * i + 2);
-      if (op) op[r] = ld_stream(ops + i);
-    }
-  }
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(kPartThreads) k_wpart_count(const int32_t* __restrict__ keys, uint64_t n, int world,
@@ -183,13 +168,15 @@ __global__ void __launch_bounds__(kPartThreads) k_wpart_count(const int32_t* __r
   if (wt >= nwt) return;
   c[warp][lane] = 0;
   __syncwarp();
-  int32_t x[kPartRounds], y[kPartRounds], z[kPartRounds];
   __shared__ WarpStage stage[kPartThreads / 32];
-  load_rounds(keys, nullptr, n, (uint64_t)wt * kWTile, stage[warp], x, y, z, nullptr);
+  WarpStage& S = stage[warp];
+  stage_tile(keys, nullptr, n, (uint64_t)wt * kWTile, S);
 #pragma unroll
   for (int r = 0; r < kPartRounds; ++r) {
-    const uint64_t i = (uint64_t)wt * kWTile + (uint64_t)r * 32 + lane;
-    const uint32_t o = i < n ? owner_fast(x[r], y[r], z[r], wmagic, (uint32_t)world) : 0xFFFFFFFFu;
+    const uint32_t j = r * 32 + lane;
+    const uint64_t i = (uint64_t)wt * kWTile + j;
+    const uint32_t o = i < n ? owner_fast(S.k[3 * j], S.k[3 * j + 1], S.k[3 * j + 2], wmagic, (uint32_t)world)
+                             : 0xFFFFFFFFu;
     const uint32_t m = __match_any_sync(0xFFFFFFFFu, o);
     if (o != 0xFFFFFFFFu && (int)lane == __ffs(m) - 1) c[warp][o] += __popc(m);
     __syncwarp();
@@ -197,28 +184,39 @@ __global__ void __launch_bounds__(kPartThreads) k_wpart_count(const int32_t* __r
   if ((int)lane < world) tile_cnt[(size_t)lane * nwt + wt] = c[warp][lane];
 }
 
-// CTA o: exclusive scan of owner o's warp-tile counts; chunks of 8,192 are
-// loaded coalesced into shared memory, each thread scans 8 consecutive
+// CTA o: exclusive scan of owner o's counts per GROUP of kTilesPerCta warp
+// tiles (= one push CTA); the push CTA adds its warps' in-group prefix
+// itself, so the scan is kTilesPerCta x shorter than a per-tile scan.
+// Per chunk of 4,096 groups: coalesced loads of the tile counts, 8-lane
+// shuffle sums into shared memory, then a block scan of 4 groups per thread.
+constexpr uint32_t kTilesPerCta = kPartThreads / 32;
+static_assert(kTilesPerCta == 8, "k_wpart_scan sums groups with 8-lane shuffles");
 __global__ void __launch_bounds__(1024) k_wpart_scan(const uint32_t* __restrict__ tile_cnt, uint32_t nwt,
-                                                     uint32_t* __restrict__ tile_off, uint32_t* __restrict__ totals) {
-  constexpr int kPer = 8;
-  constexpr uint32_t kChunk = 1024 * kPer;
-  __shared__ uint32_t buf[kChunk];
+                                                     uint32_t* __restrict__ grp_off, uint32_t* __restrict__ totals) {
+  constexpr int kPer = 4;
+  constexpr uint32_t kChunk = 1024 * kPer;  // groups per chunk
+  __shared__ uint32_t gsum[kChunk];
   __shared__ uint32_t ws[32];
   const uint32_t o = blockIdx.x, lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t ngrp = (nwt + kTilesPerCta - 1) / kTilesPerCta;
   const uint32_t* in = tile_cnt + (size_t)o * nwt;
-  uint32_t* out = tile_off + (size_t)o * nwt;
+  uint32_t* out = grp_off + (size_t)o * ngrp;
   uint32_t carry = 0;
-  for (uint32_t b = 0; b < nwt; b += kChunk) {
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const uint32_t t = b + k * 1024 + threadIdx.x;
-      buf[k * 1024 + threadIdx.x] = t < nwt ? in[t] : 0u;
+  for (uint32_t b = 0; b < ngrp; b += kChunk) {
+    const uint64_t t0 = (uint64_t)b * kTilesPerCta;
+#pragma unroll 8
+    for (uint32_t it = 0; it < kChunk * kTilesPerCta / 1024; ++it) {
+      const uint64_t t = t0 + (uint64_t)it * 1024 + threadIdx.x;
+      uint32_t v = t < nwt ? in[t] : 0u;
+      v += __shfl_xor_sync(0xFFFFFFFFu, v, 4);
+      v += __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+      v += __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+      if ((lane & 7) == 0) gsum[(it * 1024 + threadIdx.x) >> 3] = v;
     }
     __syncthreads();
     uint32_t v[kPer], sum = 0;
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) sum += (v[k] = buf[threadIdx.x * kPer + k]);
+    for (int k = 0; k < kPer; ++k) sum += (v[k] = gsum[threadIdx.x * kPer + k]);
     uint32_t xs = sum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -240,15 +238,15 @@ __global__ void __launch_bounds__(1024) k_wpart_scan(const uint32_t* __restrict_
     uint32_t run = carry + (warp ? ws[warp - 1] : 0u) + xs - sum;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
-      buf[threadIdx.x * kPer + k] = run;
+      gsum[threadIdx.x * kPer + k] = run;
       run += v[k];
     }
     carry += ws[31];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
-      const uint32_t t = b + k * 1024 + threadIdx.x;
-      if (t < nwt) out[t] = buf[k * 1024 + threadIdx.x];
+      const uint32_t g = b + k * 1024 + threadIdx.x;
+      if (g < ngrp) out[g] = gsum[k * 1024 + threadIdx.x];
     }
     __syncthreads();
   }
@@ -257,7 +255,8 @@ __global__ void __launch_bounds__(1024) k_wpart_scan(const uint32_t* __restrict_
 
 __global__ void __launch_bounds__(kPartThreads) k_wpart_push(ShardView V, const int32_t* __restrict__ keys,
                                                              const uint8_t* __restrict__ ops, uint64_t n, uint32_t nwt,
-                                                             const uint32_t* __restrict__ tile_off,
+                                                             const uint32_t* __restrict__ tile_cnt,
+                                                             const uint32_t* __restrict__ grp_off,
                                                              const uint32_t* __restrict__ totals,
                                                              unsigned long long epoch, unsigned int* ctr) {
   __shared__ uint32_t run[kPartThreads / 32][kMaxWorld];
@@ -265,26 +264,34 @@ __global__ void __launch_bounds__(kPartThreads) k_wpart_push(ShardView V, const 
   const uint32_t wt = blockIdx.x * (kPartThreads / 32) + warp;
   const int G = V.world;
   if (wt < nwt) {
-    run[warp][lane] = (int)lane < G ? tile_off[(size_t)lane * nwt + wt] : 0u;
+    // tile offset = the group's offset + the tiles of earlier warps in the group
+    uint32_t off0 = 0;
+    if ((int)lane < G) {
+      const uint32_t ngrp = (nwt + kTilesPerCta - 1) / kTilesPerCta;
+      off0 = grp_off[(size_t)lane * ngrp + blockIdx.x];
+      for (uint32_t w = 0; w < warp; ++w) off0 += tile_cnt[(size_t)lane * nwt + blockIdx.x * kTilesPerCta + w];
+    }
+    run[warp][lane] = off0;
     __syncwarp();
-    int32_t x[kPartRounds], y[kPartRounds], z[kPartRounds];
-    uint32_t op[kPartRounds];
     const uint64_t t0 = (uint64_t)wt * kWTile;
     __shared__ WarpStage stage[kPartThreads / 32];
-    load_rounds(keys, ops, n, t0, stage[warp], x, y, z, op);
+    WarpStage& S = stage[warp];
+    stage_tile(keys, ops, n, t0, S);
     const size_t region = (size_t)V.rank * V.bmax;
 #pragma unroll
     for (int r = 0; r < kPartRounds; ++r) {
-      const uint64_t i = t0 + (uint64_t)r * 32 + lane;
-      const uint32_t o = i < n ? owner_fast(x[r], y[r], z[r], V.wmagic, (uint32_t)G) : 0xFFFFFFFFu;
+      const uint32_t j = r * 32 + lane;
+      const uint64_t i = t0 + j;
+      const int32_t x = S.k[3 * j], y = S.k[3 * j + 1], z = S.k[3 * j + 2];
+      const uint32_t o = i < n ? owner_fast(x, y, z, V.wmagic, (uint32_t)G) : 0xFFFFFFFFu;
       const uint32_t m = __match_any_sync(0xFFFFFFFFu, o);
       if (o != 0xFFFFFFFFu) {
         const uint32_t off = run[warp][o] + __popc(m & lanemask_lt());
         int4 rec;
-        rec.x = x[r];
-        rec.y = y[r];
-        rec.z = z[r];
-        rec.w = (int)((op[r] << 30) | (uint32_t)i);
+        rec.x = x;
+        rec.y = y;
+        rec.z = z;
+        rec.w = (int)(((uint32_t)S.op[j] << 30) | (uint32_t)i);
         rec_of(V, o)[region + off] = rec;  // peer store over NVLink (local for o == rank)
       }
       __syncwarp();
@@ -350,7 +357,7 @@ __device__ __forceinline__ Routed load_routed(const ShardView& V, uint32_t* spre
 }
 
 __global__ void __launch_bounds__(kShardOpBlock, 2048 / kShardOpBlock) k_shard_apply(TableView T, ShardView V, uint8_t* __restrict__ res,
-                                                               int32_t* __restrict__ idx) {
+                                                               int32_t* __restrict__ idx, uint32_t* __restrict__ wv) {
   __shared__ uint32_t spre[kMaxWorld + 1];
   const Routed R = load_routed(V, spre);
   const int4* rec = rec_of(V, V.rank);
@@ -362,6 +369,7 @@ __global__ void __launch_bounds__(kShardOpBlock, 2048 / kShardOpBlock) k_shard_a
     const int4 q = __ldcs(rec + R.pos(v, &r));
     const uint32_t b = bucket_of(T, q.x, q.y, q.z);
     const int4 pre = ld_bucket(T.e + b);
+    __stcs(wv + v, (uint32_t)q.w);  // op | input index, for the post and return passes (4 B, not the record)
     delta += apply_one(T, q.x, q.y, q.z, (uint8_t)((uint32_t)q.w >> 30), v, b, pre, res, idx);
   }
   add_size_cta(T, delta);
@@ -371,7 +379,7 @@ __global__ void __launch_bounds__(kShardOpBlock, 2048 / kShardOpBlock) k_shard_a
 // flight first), created-flag fixup via the records, vacated excess entries
 // back onto the free list with one warp-wide reservation per round.
 __global__ void __launch_bounds__(256) k_shard_post(TableView T, ShardView V, uint8_t* __restrict__ res,
-                                                    const int32_t* __restrict__ idx) {
+                                                    const int32_t* __restrict__ idx, const uint32_t* __restrict__ wv) {
   constexpr int kOps = 4;
   __shared__ uint32_t spre[kMaxWorld + 1];
   const Routed R = load_routed(V, spre);
@@ -382,16 +390,15 @@ __global__ void __launch_bounds__(256) k_shard_post(TableView T, ShardView V, ui
 #pragma unroll 1
   for (uint32_t it = 0; it < rounds; ++it) {
     const uint32_t v0 = it * kOps * stride + blockIdx.x * blockDim.x + threadIdx.x;
-    int4 q[kOps];
+    uint32_t w[kOps];
     uint8_t rs[kOps];
     int32_t ps[kOps];
 #pragma unroll
     for (int k = 0; k < kOps; ++k) {
       const uint32_t v = v0 + k * stride;
-      q[k].w = -1;
+      w[k] = 0xFFFFFFFFu;
       if (v < total) {
-        int r;
-        q[k] = rec[R.pos(v, &r)];
+        w[k] = wv[v];
         rs[k] = res[v];
         ps[k] = idx[v];
       }
@@ -402,15 +409,15 @@ __global__ void __launch_bounds__(256) k_shard_post(TableView T, ShardView V, ui
     for (int k = 0; k < kOps; ++k) {
       const uint32_t v = v0 + k * stride;
       if (v >= total) continue;
-      const uint32_t op = (uint32_t)q[k].w >> 30;
+      const uint32_t op = w[k] >> 30;
       if (op == 0u /*VS_OP_INSERT*/ && rs[k]) {
-        const int4 qk = q[k];
         post_op_t(
             T,
-            [&](uint64_t m) {
-              int rm;
+            [&](uint64_t m) {  // records are read only for a duplicate claim
+              int rm, rv;
               const int4 p = rec[R.pos((uint32_t)m, &rm)];
-              return p.x == qk.x && p.y == qk.y && p.z == qk.z;
+              const int4 qv = rec[R.pos(v, &rv)];
+              return p.x == qv.x && p.y == qv.y && p.z == qv.z;
             },
             v, 0, res, ps[k]);
       } else if (op == 2u /*VS_OP_ERASE*/ && rs[k] && ps[k] >= (int32_t)T.n) {
@@ -422,15 +429,15 @@ __global__ void __launch_bounds__(256) k_shard_post(TableView T, ShardView V, ui
 }
 
 __global__ void __launch_bounds__(256) k_shard_return(ShardView V, const uint8_t* __restrict__ res,
-                                                      unsigned long long epoch, unsigned int* ctr) {
+                                                      const uint32_t* __restrict__ wv, unsigned long long epoch,
+                                                      unsigned int* ctr) {
   __shared__ uint32_t spre[kMaxWorld + 1];
   const Routed R = load_routed(V, spre);
-  const int4* rec = rec_of(V, V.rank);
   const uint32_t total = R.total();
   const uint32_t stride = gridDim.x * blockDim.x;
 #pragma unroll 1
   for (uint32_t v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < total; v0 += 4 * stride) {
-    // four independent record loads in flight before the stores
+    // four independent loads in flight before the stores
     uint32_t w[4];
     uint8_t b[4];
     int r[4];
@@ -438,7 +445,8 @@ __global__ void __launch_bounds__(256) k_shard_return(ShardView V, const uint8_t
     for (int k = 0; k < 4; ++k) {
       const uint32_t v = v0 + k * stride;
       if (v < total) {
-        w[k] = (uint32_t)__ldcs(&rec[R.pos(v, &r[k])].w);
+        R.pos(v, &r[k]);
+        w[k] = __ldcs(wv + v);
         b[k] = res[v];
       }
     }
@@ -467,11 +475,12 @@ struct vs_shard {
   bool connected = false;
   // local workspace
   uint32_t* tile_cnt = nullptr;  // [world][warp tiles] ops per owner per warp tile
-  uint32_t* tile_off = nullptr;
+  uint32_t* grp_off = nullptr;   // [world][groups of kTilesPerCta tiles] exclusive offsets
   uint32_t* totals = nullptr;
   unsigned int* ctl = nullptr;  // [0] push CTA counter, [32] return CTA counter, [64] error word
   uint8_t* res = nullptr;
   int32_t* idx = nullptr;
+  uint32_t* wv = nullptr;  // [world * bmax] op | input index of every routed op (written by the apply)
   unsigned long long epoch = 0;
   uint64_t timeout_ns = 20ull * 1000000000ull;
 
@@ -514,12 +523,13 @@ vs_status vs_shard_create(vs_table* local, int rank, int world, uint64_t max_bat
   // warp tiles (kWTile ops) are the finest partition granularity
   const size_t nwt_max = (max_batch + kWTile - 1) / kWTile;
   if (e == cudaSuccess) e = cudaMalloc(&s->tile_cnt, (size_t)world * nwt_max * 4);
-  if (e == cudaSuccess) e = cudaMalloc(&s->tile_off, (size_t)world * nwt_max * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->grp_off, (size_t)world * nwt_max * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->totals, kMaxWorld * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->ctl, 128 * 4);
   if (e == cudaSuccess) e = cudaMemset(s->ctl, 0, 128 * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->res, (size_t)world * max_batch);
   if (e == cudaSuccess) e = cudaMalloc(&s->idx, (size_t)world * max_batch * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->wv, (size_t)world * max_batch * 4);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     vs_shard_destroy(s);
@@ -535,6 +545,11 @@ vs_status vs_shard_create(vs_table* local, int rank, int world, uint64_t max_bat
                          (const void*)k_shard_return};
     for (const void* f : fns)
       if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, f);
+    // the staged partition kernels want 8 CTAs x 27 KB of shared memory per SM
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute((const void*)k_wpart_count, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute((const void*)k_wpart_push, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) {
       vs_shard_destroy(s);
       return cuda_status(e, "vs_shard_create (kernel load)");
@@ -618,12 +633,13 @@ vs_status vs_shard_apply(vs_shard* s, const int32_t* keys, const uint8_t* ops, u
     if (nwt) {
       k_wpart_count<<<ctas, kPartThreads, 0, st>>>(keys, n, s->world, V.wmagic, nwt, s->tile_cnt);
       count_launch();
-      k_wpart_scan<<<s->world, 1024, 0, st>>>(s->tile_cnt, nwt, s->tile_off, s->totals);
+      k_wpart_scan<<<s->world, 1024, 0, st>>>(s->tile_cnt, nwt, s->grp_off, s->totals);
       count_launch();
     } else {
       VS_CK(cudaMemsetAsync(s->totals, 0, kMaxWorld * 4, st));
     }
-    k_wpart_push<<<ctas, kPartThreads, 0, st>>>(V, keys, ops, n, nwt, s->tile_off, s->totals, ep, s->ctl);
+    k_wpart_push<<<ctas, kPartThreads, 0, st>>>(V, keys, ops, n, nwt, s->tile_cnt, s->grp_off, s->totals, ep,
+                                                  s->ctl);
     count_launch();
   }
   k_wait<<<1, 32, 0, st>>>(own->push_flag, s->world, ep, s->ctl + 64, s->timeout_ns);
@@ -634,13 +650,13 @@ vs_status vs_shard_apply(vs_shard* s, const int32_t* keys, const uint8_t* ops, u
   const TableView T = s->table->next_view();
   {
     ProfScope prof(0, st);
-    k_shard_apply<<<grid_for(hint, kShardOpBlock), kShardOpBlock, 0, st>>>(T, V, s->res, s->idx);
+    k_shard_apply<<<grid_for(hint, kShardOpBlock), kShardOpBlock, 0, st>>>(T, V, s->res, s->idx, s->wv);
     count_launch();
   }
-  k_shard_post<<<grid_for(hint, 256 * 4), 256, 0, st>>>(T, V, s->res, s->idx);
+  k_shard_post<<<grid_for(hint, 256 * 4), 256, 0, st>>>(T, V, s->res, s->idx, s->wv);
   count_launch();
   // bounded grid: the last-CTA signal costs one same-address atomic per CTA
-  k_shard_return<<<kReturnCtas, 256, 0, st>>>(V, s->res, ep, s->ctl + 32);
+  k_shard_return<<<kReturnCtas, 256, 0, st>>>(V, s->res, s->wv, ep, s->ctl + 32);
   count_launch();
   k_wait<<<1, 32, 0, st>>>(own->ret_flag, s->world, ep, s->ctl + 64, s->timeout_ns);
   count_launch();
@@ -690,11 +706,12 @@ void vs_shard_destroy(vs_shard* s) {
     if (s->opened[r]) cudaIpcCloseMemHandle(s->peer[r]);
   cudaFree(s->win);
   cudaFree(s->tile_cnt);
-  cudaFree(s->tile_off);
+  cudaFree(s->grp_off);
   cudaFree(s->totals);
   cudaFree(s->ctl);
   cudaFree(s->res);
   cudaFree(s->idx);
+  cudaFree(s->wv);
   delete s;
 }
 
