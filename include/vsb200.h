@@ -183,17 +183,31 @@ vs_status vs_table_probe_sol(vs_table *t, uint64_t n, int hops, uint8_t *out, vs
  *   mc_out[i]  : 2048 B McBlock.to_bytes() (interleaved {index, r, g, b})
  *   q_out[i]   : 512 int8 quantised TSDF of block i (A17; NEW)
  *   counts[i]  : number of voxels with index != 0
- * Any of mc_out / q_out / counts may be NULL to skip that output. */
-vs_status vs_mc_encode(const uint8_t *pool, const int32_t *nbr, uint64_t n,
-                       uint8_t *mc_out, int8_t *q_out, uint32_t *counts,
+ * Any of mc_out / q_out / counts may be NULL to skip that output.
+ * faces (may be NULL): the pool's face bit-packs (vs_mc_faces), 48 B per
+ * row, 16-byte aligned, current for every row a neighbour lookup can hit;
+ * with them the halo of a block is seven 16-B reads instead of 217
+ * scattered voxels.  Output is identical with or without. */
+vs_status vs_mc_encode(const uint8_t *pool, const uint8_t *faces, const int32_t *nbr,
+                       uint64_t n, uint8_t *mc_out, int8_t *q_out, uint32_t *counts,
                        vs_stream_t stream);
 
 /* Same, but the neighbour rows come from hash lookups of keys[i] + delta in
  * `tsdf_table`, whose entry positions index `pool` (the TSDF map's parallel
  * payload array).  This is where the hash feeds the encoder. */
 vs_status vs_mc_encode_keys(const vs_table *tsdf_table, const uint8_t *pool,
-                            const int32_t *keys, uint64_t n, uint8_t *mc_out,
-                            int8_t *q_out, uint32_t *counts, vs_stream_t stream);
+                            const uint8_t *faces, const int32_t *keys, uint64_t n,
+                            uint8_t *mc_out, int8_t *q_out, uint32_t *counts,
+                            vs_stream_t stream);
+
+/* Face bit-packs of pool rows (the halo side table of the encoder; NEW):
+ * for rows[i] (or row i when rows is NULL), faces + 48*row receives the
+ * inside/observed bits (the encoder's IEEE-bit predicates) of the row's
+ * x = 0, y = 0 and z = 0 faces, each {inside lo, inside hi, observed lo,
+ * observed hi} with bit y+8z / x+8z / x+8y.  Call it wherever rows change
+ * (ingest, integration); rows < 0 are skipped. */
+vs_status vs_mc_faces(const uint8_t *pool, const int32_t *rows, uint64_t n,
+                      uint8_t *faces, vs_stream_t stream);
 
 /* Neighbour table only: nbr_out[i][c] as defined above (8 batched finds). */
 vs_status vs_mc_neighbors(const vs_table *tsdf_table, const int32_t *keys,

@@ -68,8 +68,9 @@ SIGNATURES: dict[str, tuple] = {
     "vs_table_snapshot": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp]),
     "vs_table_extract": (_i32, [_vp, _u64, _u64, _vp, _vp, _vp]),
     "vs_table_audit": (_i32, [_vp, ctypes.POINTER(ctypes.c_uint64 * 6), _vp]),
-    "vs_mc_encode": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp, _vp]),
-    "vs_mc_encode_keys": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
+    "vs_mc_encode": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
+    "vs_mc_encode_keys": (_i32, [_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
+    "vs_mc_faces": (_i32, [_vp, _vp, _u64, _vp, _vp]),
     "vs_mc_neighbors": (_i32, [_vp, _vp, _u64, _vp, _vp]),
     "vs_mc_compact": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp, _u64, _vp, _vp]),
     "vs_scan_workspace_bytes": (_u64, [_u64]),

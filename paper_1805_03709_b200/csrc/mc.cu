@@ -123,9 +123,6 @@ __device__ __forceinline__ int32_t quantise(uint32_t tb, uint32_t wb) {
 }
 
 // byte k (k < 4) = bits (k, k+1) of v: the corner pair of voxel x0 + k
-#ifndef VSB_MC_SIMD_INDEX
-#define VSB_MC_SIMD_INDEX 1
-#endif
 __device__ __forceinline__ uint32_t pair4(uint32_t v) {
   return (v & 3u) | ((v & 6u) << 7) | ((v & 12u) << 14) | ((v & 24u) << 21);
 }
@@ -174,17 +171,12 @@ constexpr int kAhead = kStages - 1;    // prefetch distance of the centre copy
 struct McSmem {
   alignas(128) uint8_t buf[kStages][VS_TSDF_BLOCK_BYTES];
   alignas(8) uint64_t mbar[kStages];
+  uint4 pk[2][8];  // face packs of the block's neighbours c = 1..7 (kFaces)
   uint32_t grid_in[2][81];
   uint32_t grid_ob[2][81];
   int32_t nb[2][kLook][8];  // neighbour rows of two lookup batches
   uint32_t cnt[2][4];
 };
-
-// Per-block non-empty counts summed after the next iteration's first barrier
-// instead of behind an extra barrier (VSB_MC_DEFER_COUNT; measured slower: off).
-#ifndef VSB_MC_DEFER_COUNT
-#define VSB_MC_DEFER_COUNT 0
-#endif
 
 // Sweep order (experiment knob VSB_MC_REVERSE): block of sweep index i.
 #ifndef VSB_MC_REVERSE
@@ -296,8 +288,65 @@ __device__ __forceinline__ void issue_centre(McSmem& sm, uint64_t j, const uint8
 #endif
 }
 
-template <bool kFromKeys>
+
+// ---- face bit-packs (halo side table).  For every TSDF pool row, the
+// inside/observed predicate bits of its three LOW faces: the x = 0 face
+// (bit y + 8z), the y = 0 face (bit x + 8z) and the z = 0 face (bit x + 8y),
+// each as {inside lo, inside hi, observed lo, observed hi} (16 B), 48 B per
+// row.  They are exactly the halo a block needs from its 7 positive
+// neighbours, so an encode with packs reads seven 16-B words per block
+// instead of 217 scattered 8-B voxels (~117 DRAM bursts when they miss L2).
+// Packs are maintained where rows change (ingest, integration) with
+// vs_mc_faces.
+constexpr int kFaceBytes = 48;
+
+__device__ __forceinline__ int face_kind(int c) { return (c & 1) ? 0 : (c == 4 ? 2 : 1); }  // c: 1..7
+
+__device__ __forceinline__ uint4 load_face(const uint8_t* __restrict__ faces, int32_t row, int c) {
+  if (row < 0) return make_uint4(0u, 0u, 0u, 0u);
+  return __ldg((const uint4*)(faces + (uint64_t)row * kFaceBytes) + face_kind(c));
+}
+
+__device__ __forceinline__ uint32_t bit64(uint32_t lo, uint32_t hi, int i) {
+  return ((i < 32 ? lo >> i : hi >> (i - 32)) & 1u);
+}
+__device__ __forceinline__ uint32_t byte64(uint32_t lo, uint32_t hi, int k) {
+  return ((k < 4 ? lo >> (8 * k) : hi >> (8 * (k - 4))) & 0xFFu);
+}
+
+// One warp per row: lane l takes bits l and l + 32 of each face.
+__global__ void __launch_bounds__(256) k_mc_faces(const uint8_t* __restrict__ pool, const int32_t* __restrict__ rows,
+                                                  uint64_t n, uint8_t* __restrict__ faces) {
+  const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31u;
+  if (w >= n) return;
+  const int32_t row = rows ? rows[w] : (int32_t)w;
+  if (row < 0) return;
+  const uint8_t* src = pool + (uint64_t)row * VS_TSDF_BLOCK_BYTES;
+  uint32_t word[3][4];
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int i = (int)lane + 32 * half;
+      const int a = i & 7, b = i >> 3;
+      const int flat = f == 0 ? 8 * a + 64 * b : (f == 1 ? a + 64 * b : a + 8 * b);
+      const uint32_t* v = (const uint32_t*)(src + 12 * flat);
+      const uint32_t in = __ballot_sync(0xFFFFFFFFu, inside_bit(__ldg(v)));
+      const uint32_t ob = __ballot_sync(0xFFFFFFFFu, observed_bit(__ldg(v + 1)));
+      word[f][half] = in;
+      word[f][2 + half] = ob;
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < 3; ++f)
+    if (lane == (uint32_t)f)
+      ((uint4*)(faces + (uint64_t)row * kFaceBytes))[f] = make_uint4(word[f][0], word[f][1], word[f][2], word[f][3]);
+}
+
+template <bool kFromKeys, bool kFaces>
 __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS : VSB_MC_MINBLOCKS_NBR) k_mc_encode(TableView T, const uint8_t* __restrict__ pool,
+                                                          const uint8_t* __restrict__ faces,
                                                           const int32_t* __restrict__ keys,
                                                           const int32_t* __restrict__ nbr, uint64_t n,
                                                           uint32_t* __restrict__ mc_out, int8_t* __restrict__ q_out,
@@ -321,9 +370,15 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
   // halo of the block processed next, loaded one iteration ahead
   const HaloDesc hd = halo_desc();
   HaloRegs hal;
-  if (nj) halo_prefetch(hal, hd, nb_of(sm, 0), pool);
+  uint4 fpk = make_uint4(0u, 0u, 0u, 0u);  // kFaces: thread t < 7 holds neighbour t+1's pack, one block ahead
+  if (nj) {
+    if (kFaces) {
+      if (t < 7) fpk = load_face(faces, nb_of(sm, 0)[t + 1], t + 1);
+    } else {
+      halo_prefetch(hal, hd, nb_of(sm, 0), pool);
+    }
+  }
 
-  bool pend = false;  // the previous block's per-warp counts await summing
   for (uint64_t j = 0; j < nj; ++j) {
     const uint64_t blk = sweep_block(blockIdx.x + j * G, n);
     const int s = (int)(j & 1);
@@ -334,21 +389,26 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     // the next lookup batch must be ready before block j + kAhead is issued
     if (slot == kLook - kAhead && j + kAhead < nj)
       lookup_batch<kFromKeys>(sm, (int)(((j / kLook) + 1) & 1), T, keys, nbr, n, (j / kLook + 1) * kLook);
-    for (int r = t; r < 81; r += kMcThreads) {
-      sm.grid_in[s][r] = 0u;
-      sm.grid_ob[s][r] = 0u;
+    if (kFaces) {
+      if (t < 7) sm.pk[s][t] = fpk;  // every grid row is then written whole: no zeroing, no atomics
+    } else {
+      for (int r = t; r < 81; r += kMcThreads) {
+        sm.grid_in[s][r] = 0u;
+        sm.grid_ob[s][r] = 0u;
+      }
     }
-    __syncthreads();  // (A) lookups ready, grids zeroed, buf[(j+kAhead)%kStages] no longer read
-    // count of the previous block, deferred past this barrier (no extra sync)
-    if (VSB_MC_DEFER_COUNT && counts && t == 0 && pend)
-      counts[sweep_block(blockIdx.x + (j - 1) * G, n)] = sm.cnt[s ^ 1][0] + sm.cnt[s ^ 1][1] + sm.cnt[s ^ 1][2] + sm.cnt[s ^ 1][3];
-    pend = false;
+    __syncthreads();  // (A) lookups + packs ready, grids zeroed, buf[(j+kAhead)%kStages] no longer read
     if (t == 0 && j + kAhead < nj) issue_centre(sm, j + kAhead, pool);
     uint32_t* mc_blk = mc_out ? mc_out + blk * VS_BLOCK_VOXELS : nullptr;
     int8_t* q_blk = q_out ? q_out + blk * VS_BLOCK_VOXELS : nullptr;
     const HaloRegs cur = hal;
-    if (j + 1 < nj) halo_prefetch(hal, hd, nb_of(sm, j + 1), pool);
-
+    if (j + 1 < nj) {
+      if (kFaces) {
+        if (t < 7) fpk = load_face(faces, nb_of(sm, j + 1)[t + 1], t + 1);
+      } else {
+        halo_prefetch(hal, hd, nb_of(sm, j + 1), pool);
+      }
+    }
     if (centre < 0) {
       // absent centre: every cube's origin lives here -> all zero (:152-156)
       if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(0u, 0u, 0u, 0u));
@@ -361,7 +421,7 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     // loaded during the previous iteration
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      if (cur.row[k] >= 0) {
+      if (!kFaces && cur.row[k] >= 0) {
         if (inside_bit(cur.tb[k])) atomicOr(&sm.grid_in[s][cur.row[k]], 1u << cur.bit[k]);
         if (observed_bit(cur.wb[k])) atomicOr(&sm.grid_ob[s][cur.row[k]], 1u << cur.bit[k]);
       }
@@ -387,7 +447,29 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     uint32_t in_row = in4 << x0, ob_row = ob4 << x0;
     in_row |= __shfl_xor_sync(0xffffffffu, in_row, 1);
     ob_row |= __shfl_xor_sync(0xffffffffu, ob_row, 1);
-    if (h == 0) {
+    if (kFaces) {
+      // whole rows: centre bits 0..7 + the +x neighbour's x-face bit as bit 8
+      if (h == 0) {
+        const uint4 c1 = sm.pk[s][0];
+        const int i = y + 8 * z;
+        sm.grid_in[s][z * 9 + y] = in_row | (bit64(c1.x, c1.y, i) << 8);
+        sm.grid_ob[s][z * 9 + y] = ob_row | (bit64(c1.z, c1.w, i) << 8);
+      }
+      // the 17 rows on the +y / +z faces (grid rows gz*9 + 8, 72 + gy, 80)
+      if (t >= 64 && t < 81) {
+        uint4 lo, hi;  // the byte-source face (bits 0..7) and the bit-8 source face
+        int kb, ib, row;
+        if (t < 72) {  // gy = 8, gz = t - 64: y-face of (0,1,0), x-face bit (0,0,gz) of (1,1,0)
+          lo = sm.pk[s][1], hi = sm.pk[s][2], kb = t - 64, ib = 8 * (t - 64), row = (t - 64) * 9 + 8;
+        } else if (t < 80) {  // gz = 8, gy = t - 72: z-face of (0,0,1), x-face bit (0,gy,0) of (1,0,1)
+          lo = sm.pk[s][3], hi = sm.pk[s][4], kb = t - 72, ib = t - 72, row = 72 + (t - 72);
+        } else {  // gy = gz = 8: y-face byte 0 of (0,1,1), x-face bit 0 of (1,1,1)
+          lo = sm.pk[s][5], hi = sm.pk[s][6], kb = 0, ib = 0, row = 80;
+        }
+        sm.grid_in[s][row] = byte64(lo.x, lo.y, kb) | (bit64(hi.x, hi.y, ib) << 8);
+        sm.grid_ob[s][row] = byte64(lo.z, lo.w, kb) | (bit64(hi.z, hi.w, ib) << 8);
+      }
+    } else if (h == 0) {
       atomicOr(&sm.grid_in[s][z * 9 + y], in_row);
       atomicOr(&sm.grid_ob[s][z * 9 + y], ob_row);
     }
@@ -401,7 +483,6 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     const uint32_t o00 = go[r00] >> x0, o10 = go[r00 + 1] >> x0, o01 = go[r00 + 9] >> x0, o11 = go[r00 + 10] >> x0;
     uint32_t word[4];
     uint32_t qw = 0, nz = 0;
-#if VSB_MC_SIMD_INDEX
     // all 4 cube indices at once, one per byte: byte k of pair(v) holds bits
     // (k, k+1) of row v, so the 8 corner bits of voxel k are the 4 rows'
     // pairs stacked at bit offsets 0/2/4/6 (corner c = (c&1, c>>1&1, c>>2&1))
@@ -417,37 +498,13 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
       word[k] = ((nzm >> (8 * k)) & 1u) ? ((idx4 >> (8 * k)) & 0xFFu) | (rgb[k] << 8) : 0u;
       qw |= ((uint32_t)quantise(tb[k], wb[k]) & 0xFFu) << (8 * k);
     }
-#else
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t idx = ((i00 >> k) & 3u) | (((i10 >> k) & 3u) << 2) | (((i01 >> k) & 3u) << 4) |
-                     (((i11 >> k) & 3u) << 6);
-      const uint32_t ob = ((o00 >> k) & 3u) | (((o10 >> k) & 3u) << 2) | (((o01 >> k) & 3u) << 4) |
-                          (((o11 >> k) & 3u) << 6);
-      if (ob != 255u || idx == 255u) idx = 0u;  // unobserved corner -> 0; cutoff 255 -> 0
-      word[k] = idx ? (idx | (rgb[k] << 8)) : 0u;
-      qw |= ((uint32_t)quantise(tb[k], wb[k]) & 0xFFu) << (8 * k);
-      nz += idx != 0u;
-    }
-#endif
     if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(word[0], word[1], word[2], word[3]));
     if (q_blk) __stcs((uint32_t*)(q_blk + 4 * t), qw);
     if (counts) {
       nz = __reduce_add_sync(0xffffffffu, nz);
       if (lane == 0) sm.cnt[s][warp] = nz;
-#if VSB_MC_DEFER_COUNT
-      pend = true;  // summed by thread 0 after the next barrier
-#else
       __syncthreads();
       if (t == 0) counts[blk] = sm.cnt[s][0] + sm.cnt[s][1] + sm.cnt[s][2] + sm.cnt[s][3];
-#endif
-    }
-  }
-  if (counts) {
-    __syncthreads();
-    if (t == 0 && pend) {
-      const int s = (int)((nj - 1) & 1);
-      counts[sweep_block(blockIdx.x + (nj - 1) * G, n)] = sm.cnt[s][0] + sm.cnt[s][1] + sm.cnt[s][2] + sm.cnt[s][3];
     }
   }
 }
@@ -487,26 +544,39 @@ __global__ void __launch_bounds__(256) k_mc_compact(const uint32_t* __restrict__
   }
 }
 
-static int g_mc_grid[2] = {0, 0};
+static int g_mc_grid[4] = {0, 0, 0, 0};
 
-template <bool kFromKeys>
-static vs_status launch_mc(const TableView& T, const uint8_t* pool, const int32_t* keys, const int32_t* nbr,
-                           uint64_t n, uint8_t* mc_out, int8_t* q_out, uint32_t* counts, cudaStream_t s) {
-  if (n == 0) return VS_OK;
-  int& grid = g_mc_grid[kFromKeys ? 1 : 0];
+template <bool kFromKeys, bool kFaces>
+static vs_status launch_mc_t(const TableView& T, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
+                             const int32_t* nbr, uint64_t n, uint8_t* mc_out, int8_t* q_out, uint32_t* counts,
+                             cudaStream_t s) {
+  int& grid = g_mc_grid[(kFromKeys ? 1 : 0) + (kFaces ? 2 : 0)];
   if (grid == 0) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mc_encode<kFromKeys>, kMcThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mc_encode<kFromKeys, kFaces>, kMcThreads, 0);
     if (per_sm < 1) per_sm = 1;
     grid = sms * per_sm;
   }
   const uint64_t g = n < (uint64_t)grid ? n : (uint64_t)grid;
-  { ProfScope prof(1, s); k_mc_encode<kFromKeys><<<(unsigned)g, kMcThreads, 0, s>>>(T, pool, keys, nbr, n, (uint32_t*)mc_out, q_out,
-                                                            counts); vsb::count_launch(); }
+  {
+    ProfScope prof(1, s);
+    k_mc_encode<kFromKeys, kFaces><<<(unsigned)g, kMcThreads, 0, s>>>(T, pool, faces, keys, nbr, n,
+                                                                        (uint32_t*)mc_out, q_out, counts);
+    vsb::count_launch();
+  }
   VS_CK_LAUNCH("k_mc_encode");
   return VS_OK;
+}
+
+template <bool kFromKeys>
+static vs_status launch_mc(const TableView& T, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
+                           const int32_t* nbr, uint64_t n, uint8_t* mc_out, int8_t* q_out, uint32_t* counts,
+                           cudaStream_t s) {
+  if (n == 0) return VS_OK;
+  return faces ? launch_mc_t<kFromKeys, true>(T, pool, faces, keys, nbr, n, mc_out, q_out, counts, s)
+               : launch_mc_t<kFromKeys, false>(T, pool, faces, keys, nbr, n, mc_out, q_out, counts, s);
 }
 
 }  // namespace vsb
@@ -515,8 +585,8 @@ using namespace vsb;
 
 extern "C" {
 
-vs_status vs_mc_encode(const uint8_t* pool, const int32_t* nbr, uint64_t n, uint8_t* mc_out, int8_t* q_out,
-                       uint32_t* counts, vs_stream_t stream) {
+vs_status vs_mc_encode(const uint8_t* pool, const uint8_t* faces, const int32_t* nbr, uint64_t n, uint8_t* mc_out,
+                       int8_t* q_out, uint32_t* counts, vs_stream_t stream) {
   if (n && (!pool || !nbr)) {
     set_error("pool/nbr must be non-NULL");
     return VS_ERR_INVALID;
@@ -526,11 +596,15 @@ vs_status vs_mc_encode(const uint8_t* pool, const int32_t* nbr, uint64_t n, uint
     return VS_ERR_INVALID;
   }
   TableView none{};
-  return launch_mc<false>(none, pool, nullptr, nbr, n, mc_out, q_out, counts, (cudaStream_t)stream);
+  if (((uintptr_t)faces & 15u) != 0) {
+    set_error("faces must be 16-byte aligned");
+    return VS_ERR_INVALID;
+  }
+  return launch_mc<false>(none, pool, faces, nullptr, nbr, n, mc_out, q_out, counts, (cudaStream_t)stream);
 }
 
-vs_status vs_mc_encode_keys(const vs_table* t, const uint8_t* pool, const int32_t* keys, uint64_t n,
-                            uint8_t* mc_out, int8_t* q_out, uint32_t* counts, vs_stream_t stream) {
+vs_status vs_mc_encode_keys(const vs_table* t, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
+                            uint64_t n, uint8_t* mc_out, int8_t* q_out, uint32_t* counts, vs_stream_t stream) {
   if (!t || (n && (!pool || !keys))) {
     set_error("table/pool/keys must be non-NULL");
     return VS_ERR_INVALID;
@@ -539,8 +613,12 @@ vs_status vs_mc_encode_keys(const vs_table* t, const uint8_t* pool, const int32_
     set_error("pool must be 16-byte aligned (TMA bulk copy)");
     return VS_ERR_INVALID;
   }
+  if (((uintptr_t)faces & 15u) != 0) {
+    set_error("faces must be 16-byte aligned");
+    return VS_ERR_INVALID;
+  }
   DeviceGuard g(t->device);
-  return launch_mc<true>(t->view(), pool, keys, nullptr, n, mc_out, q_out, counts, (cudaStream_t)stream);
+  return launch_mc<true>(t->view(), pool, faces, keys, nullptr, n, mc_out, q_out, counts, (cudaStream_t)stream);
 }
 
 vs_status vs_mc_neighbors(const vs_table* t, const int32_t* keys, uint64_t n, int32_t* nbr_out,
@@ -557,6 +635,21 @@ vs_status vs_mc_neighbors(const vs_table* t, const int32_t* keys, uint64_t n, in
 }
 
 uint64_t vs_scan_workspace_bytes(uint64_t n) { return 8 * (scan_tiles(n) + 1); }
+
+vs_status vs_mc_faces(const uint8_t* pool, const int32_t* rows, uint64_t n, uint8_t* faces, vs_stream_t stream) {
+  if (n && (!pool || !faces)) {
+    set_error("pool/faces must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  if (((uintptr_t)faces & 15u) != 0) {
+    set_error("faces must be 16-byte aligned");
+    return VS_ERR_INVALID;
+  }
+  if (n == 0) return VS_OK;
+  { k_mc_faces<<<grid_for(32 * n, 256), 256, 0, (cudaStream_t)stream>>>(pool, rows, n, faces); vsb::count_launch(); }
+  VS_CK_LAUNCH("k_mc_faces");
+  return VS_OK;
+}
 
 vs_status vs_mc_compact(const uint8_t* mc, const uint32_t* counts, uint64_t n, uint64_t* offsets,
                         uint16_t* cell_flat, uint32_t* cell_mc, uint64_t cell_cap, void* work_dev,

@@ -98,10 +98,41 @@ def _out(torch, n, device, want, shape, dtype):
     return torch.empty((n,) + shape, dtype=dtype, device=device) if want else None
 
 
-def encode_blocks(pool, nbr, *, mc: bool = True, q: bool = True, counts: bool = True):
+FACE_BYTES = 48  # face bit-pack per pool row (vs_mc_faces)
+
+
+def _faces_arg(faces, pool):
+    torch = _lib.require_cuda()
+    if faces is None:
+        return None
+    if faces.dtype != torch.uint8 or faces.dim() != 2 or faces.shape[1] != FACE_BYTES or \
+            faces.shape[0] < pool.shape[0] or faces.device != pool.device or not faces.is_contiguous():
+        raise ValueError("faces must be a contiguous uint8[>= P, 48] tensor on the pool's device")
+    return faces
+
+
+def face_packs(pool, rows=None, faces=None):
+    """Face bit-packs of pool rows (the encoder's halo side table): computes
+    faces[r] for r in `rows` (int32 tensor; all rows when None) into `faces`
+    (allocated uint8[P, 48] when None, zero for rows never computed).
+    Returns `faces`.  Call it wherever pool rows change."""
+    torch = _lib.require_cuda()
+    dev = pool.device
+    if faces is None:
+        faces = torch.zeros((pool.shape[0], FACE_BYTES), dtype=torch.uint8, device=dev)
+    _faces_arg(faces, pool)
+    r = None if rows is None else rows.to(dev, torch.int32).contiguous()
+    n = pool.shape[0] if r is None else r.shape[0]
+    check(_lib.load().vs_mc_faces(ptr(pool.contiguous()), ptr(r), n, ptr(faces), _lib.stream_of(dev)), "mc_faces")
+    return faces
+
+
+def encode_blocks(pool, nbr, *, mc: bool = True, q: bool = True, counts: bool = True, faces=None):
     """Dense encode of N blocks given neighbour rows nbr int32[N,8] into the
     wire-layout TSDF pool uint8[P,6144].  Returns (mc uint8[N,2048] | None,
-    q int8[N,512] | None, counts int32[N] | None)."""
+    q int8[N,512] | None, counts int32[N] | None).  `faces`: the pool's face
+    bit-packs (face_packs), current for every neighbour row -- same output,
+    less halo traffic."""
     torch = _lib.require_cuda()
     if pool.dtype != torch.uint8 or pool.dim() != 2 or pool.shape[1] != TSDF_BLOCK_BYTES:
         raise ValueError("pool must be uint8[P, 6144]")
@@ -113,14 +144,15 @@ def encode_blocks(pool, nbr, *, mc: bool = True, q: bool = True, counts: bool = 
     q_t = _out(torch, n, dev, q, (Q_BLOCK_BYTES,), torch.int8)
     c_t = _out(torch, n, dev, counts, (), torch.int32)
     s = _lib.stream_of(dev)
-    check(_lib.load().vs_mc_encode(ptr(pool), ptr(nbr), n, ptr(mc_t), ptr(q_t), ptr(c_t), s), "mc_encode")
+    f = _faces_arg(faces, pool)
+    check(_lib.load().vs_mc_encode(ptr(pool), ptr(f), ptr(nbr), n, ptr(mc_t), ptr(q_t), ptr(c_t), s), "mc_encode")
     return mc_t, q_t, c_t
 
 
-def encode_keys(tsdf_table, pool, keys, *, mc: bool = True, q: bool = True, counts: bool = True):
+def encode_keys(tsdf_table, pool, keys, *, mc: bool = True, q: bool = True, counts: bool = True, faces=None):
     """Encode MC blocks `keys` (int32[N,3]); neighbour rows are looked up in
     `tsdf_table` (a BlockHashMap whose positions index `pool`) inside the
-    kernel."""
+    kernel.  `faces`: as for encode_blocks."""
     torch = _lib.require_cuda()
     dev = pool.device
     from .concurrent_hash import _as_keys
@@ -131,8 +163,9 @@ def encode_keys(tsdf_table, pool, keys, *, mc: bool = True, q: bool = True, coun
     q_t = _out(torch, n, dev, q, (Q_BLOCK_BYTES,), torch.int8)
     c_t = _out(torch, n, dev, counts, (), torch.int32)
     s = tsdf_table._stream()
-    check(_lib.load().vs_mc_encode_keys(tsdf_table.handle, ptr(pool), ptr(k), n, ptr(mc_t), ptr(q_t), ptr(c_t),
-                                        ctypes.c_void_p(s.cuda_stream)), "mc_encode_keys")
+    f = _faces_arg(faces, pool)
+    check(_lib.load().vs_mc_encode_keys(tsdf_table.handle, ptr(pool), ptr(f), ptr(k), n, ptr(mc_t), ptr(q_t),
+                                        ptr(c_t), ctypes.c_void_p(s.cuda_stream)), "mc_encode_keys")
     tsdf_table._done(s)
     return mc_t, q_t, c_t
 

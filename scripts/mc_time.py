@@ -3,7 +3,7 @@ import json, os, sys, time
 sys.path.insert(0, os.getcwd())
 import numpy as np
 import torch
-from paper_1805_03709_b200 import BlockHashSet, _lib, encode_keys, encode_blocks, neighbors, workloads
+from paper_1805_03709_b200 import BlockHashSet, _lib, encode_keys, encode_blocks, face_packs, neighbors, workloads
 
 dev = torch.device("cuda", 0)
 keys_np = workloads.room_block_keys()
@@ -16,9 +16,18 @@ pool = torch.empty((t.capacity, 6144), dtype=torch.uint8, device=dev)
 for a in range(0, N, 1 << 15):
     pool[pos[a:a + (1 << 15)].long()] = workloads.room_tsdf_rows(keys[a:a + (1 << 15)])
 nbr = neighbors(t, keys)
+faces = face_packs(pool, rows=pos)
+torch.cuda.synchronize()
+f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+f0.record()
+face_packs(pool, rows=pos, faces=faces)
+f1.record()
+torch.cuda.synchronize()
 ref = None
-out = {"lib": os.environ.get("VSB_LIB", "default")}
-for name, fn in [("keys", lambda: encode_keys(t, pool, keys)), ("nbr", lambda: encode_blocks(pool, nbr))]:
+out = {"lib": os.environ.get("VSB_LIB", "default"), "face_packs_all_rows_ms": round(f0.elapsed_time(f1), 3)}
+for name, fn in [("keys", lambda: encode_keys(t, pool, keys)), ("nbr", lambda: encode_blocks(pool, nbr)),
+                 ("keys+faces", lambda: encode_keys(t, pool, keys, faces=faces)),
+                 ("nbr+faces", lambda: encode_blocks(pool, nbr, faces=faces))]:
     for _ in range(3):
         mc, q, c = fn()
     if ref is None:

@@ -98,6 +98,10 @@ def test_misaligned_pool_is_rejected(dev):
 
     buf = torch.zeros(6144 * 2 + 16, dtype=torch.uint8, device=dev)
     nbr = torch.full((1, 8), -1, dtype=torch.int32, device=dev)
-    st = _lib.load().vs_mc_encode(_lib.ctypes.c_void_p(buf.data_ptr() + 4), _lib.ptr(nbr), 1, None, None, None,
-                                  _lib.stream_of(dev))
+    st = _lib.load().vs_mc_encode(_lib.ctypes.c_void_p(buf.data_ptr() + 4), None, _lib.ptr(nbr), 1, None, None,
+                                  None, _lib.stream_of(dev))
+    assert st == _lib.VS_ERR_INVALID
+    # misaligned face packs likewise
+    st = _lib.load().vs_mc_encode(_lib.ptr(buf), _lib.ctypes.c_void_p(buf.data_ptr() + 4), _lib.ptr(nbr), 1, None,
+                                  None, None, _lib.stream_of(dev))
     assert st == _lib.VS_ERR_INVALID

@@ -26,9 +26,16 @@ def _t(a, dev):
 
 
 def gpu_encode(pool, nbr, dev):
-    from paper_1805_03709_b200 import encode_blocks
+    """Encode through both halo paths -- scattered voxel reads and the face
+    bit-packs -- which must agree byte for byte; returns the first."""
+    import torch
 
-    mc, q, c = encode_blocks(_t(pool, dev), _t(nbr, dev))
+    from paper_1805_03709_b200 import encode_blocks, face_packs
+
+    p, nb = _t(pool, dev), _t(nbr, dev)
+    mc, q, c = encode_blocks(p, nb)
+    mc2, q2, c2 = encode_blocks(p, nb, faces=face_packs(p))
+    assert torch.equal(mc, mc2) and torch.equal(q, q2) and torch.equal(c, c2), "face-pack halo path differs"
     return mc.cpu().numpy(), q.cpu().numpy(), c.cpu().numpy().astype(np.uint32)
 
 
@@ -96,6 +103,10 @@ def test_fused_sphere_reproduces_manifest_model_sha256(dev, golden):
     t, pool = table_with_pool(d["keys"], rows, dev)
     mc, _, _ = encode_keys(t, pool, d["keys"])
     assert hashlib.sha256(mc.cpu().numpy().tobytes()).hexdigest() == meta["model_sha256"]
+    from paper_1805_03709_b200 import face_packs
+
+    mc2, _, _ = encode_keys(t, pool, d["keys"], faces=face_packs(pool))
+    assert hashlib.sha256(mc2.cpu().numpy().tobytes()).hexdigest() == meta["model_sha256"]
 
 
 @pytest.mark.parametrize("field", ["random", "smooth"])
@@ -168,6 +179,13 @@ def test_room_sample_vs_oracle(dev):
     rows = workloads.room_tsdf_rows(kt)
     t, pool = table_with_pool(keys, rows.cpu().numpy(), dev, n=1 << 16, excess=1 << 16)
     mc, q, c = encode_keys(t, pool, keys)
+    from paper_1805_03709_b200 import face_packs
+
+    # face packs maintained for the written rows only (the rest stay zero and
+    # are never looked up): same bytes
+    _, pos = t.find_keys(keys)
+    mc2, q2, c2 = encode_keys(t, pool, keys, faces=face_packs(pool, rows=pos))
+    assert torch.equal(mc, mc2) and torch.equal(q, q2) and torch.equal(c, c2)
     rows_np = rows.cpu().numpy()
     nbr = oracle.neighbor_table(keys, keys)
     omc, oq, oc = oracle.mc_encode(rows_np, nbr, threads=8)
@@ -175,3 +193,26 @@ def test_room_sample_vs_oracle(dev):
     assert np.array_equal(q.cpu().numpy(), oq)
     assert np.array_equal(c.cpu().numpy().astype(np.uint32), oc)
     assert oc.sum() > 0
+
+
+def test_face_packs_track_row_updates(dev):
+    """Packs recomputed for changed rows only keep the face-pack encode equal
+    to the scattered-halo encode (the ingest contract of vs_mc_faces)."""
+    import torch
+
+    from paper_1805_03709_b200 import encode_blocks, face_packs
+
+    keys = workloads.config1_mc_keys()[:2000]
+    tsdf, weight, color = workloads.random_field(len(keys), seed=9)
+    pool = _t(oracle.make_pool(tsdf, weight, color), dev)
+    nbr = _t(oracle.neighbor_table(keys, keys), dev)
+    faces = face_packs(pool)
+    rng = np.random.default_rng(4)
+    for step in range(3):
+        rows = torch.from_numpy(rng.choice(len(keys), 300, replace=False).astype(np.int32)).to(dev)
+        t2, w2, c2 = workloads.random_field(300, seed=100 + step)
+        pool[rows.long()] = _t(oracle.make_pool(t2, w2, c2), dev)
+        face_packs(pool, rows=rows, faces=faces)
+        a = encode_blocks(pool, nbr)
+        b = encode_blocks(pool, nbr, faces=faces)
+        assert all(torch.equal(x, y) for x, y in zip(a, b)), step
