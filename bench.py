@@ -707,6 +707,9 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     h = run_hash(args, dev, rank, world)
+    if world > 1:  # the route actually used (auto falls back when peer access is unavailable)
+        config["exchange"] = ("peer stores into CUDA-IPC windows over NVLink (csrc/shard.cu)"
+                              if h.get("exchange") == "peer" else "collective all-to-all (shard.py)")
     mc = None
     if not args.no_mc:
         mc = run_mc(args, dev, world)

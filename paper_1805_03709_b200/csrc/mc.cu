@@ -175,7 +175,6 @@ struct McSmem {
   uint32_t grid_in[2][81];
   uint32_t grid_ob[2][81];
   int32_t nb[2][kLook][8];  // neighbour rows of two lookup batches
-  uint32_t cnt[2][4];
 };
 
 // Sweep order (experiment knob VSB_MC_REVERSE): block of sweep index i.
@@ -413,8 +412,24 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
       // absent centre: every cube's origin lives here -> all zero (:152-156)
       if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(0u, 0u, 0u, 0u));
       if (q_blk) __stcs((uint32_t*)(q_blk + 4 * t), 0x80808080u);
-      if (counts && t == 0) counts[blk] = 0u;
-      continue;
+      continue;  // counts[blk] stays 0
+    }
+
+    if (kFaces) {
+      // the 17 rows on the +y / +z faces (grid rows gz*9 + 8, 72 + gy, 80)
+      if (t >= 64 && t < 81) {
+        uint4 lo, hi;  // the byte-source face (bits 0..7) and the bit-8 source face
+        int kb, ib, row;
+        if (t < 72) {  // gy = 8, gz = t - 64: y-face of (0,1,0), x-face bit (0,0,gz) of (1,1,0)
+          lo = sm.pk[s][1], hi = sm.pk[s][2], kb = t - 64, ib = 8 * (t - 64), row = (t - 64) * 9 + 8;
+        } else if (t < 80) {  // gz = 8, gy = t - 72: z-face of (0,0,1), x-face bit (0,gy,0) of (1,0,1)
+          lo = sm.pk[s][3], hi = sm.pk[s][4], kb = t - 72, ib = t - 72, row = 72 + (t - 72);
+        } else {  // gy = gz = 8: y-face byte 0 of (0,1,1), x-face bit 0 of (1,1,1)
+          lo = sm.pk[s][5], hi = sm.pk[s][6], kb = 0, ib = 0, row = 80;
+        }
+        sm.grid_in[s][row] = byte64(lo.x, lo.y, kb) | (bit64(hi.x, hi.y, ib) << 8);
+        sm.grid_ob[s][row] = byte64(lo.z, lo.w, kb) | (bit64(hi.z, hi.w, ib) << 8);
+      }
     }
 
     // ---- halo: 217 (tsdf, weight) pairs from the 7 positive neighbours,
@@ -455,20 +470,6 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
         sm.grid_in[s][z * 9 + y] = in_row | (bit64(c1.x, c1.y, i) << 8);
         sm.grid_ob[s][z * 9 + y] = ob_row | (bit64(c1.z, c1.w, i) << 8);
       }
-      // the 17 rows on the +y / +z faces (grid rows gz*9 + 8, 72 + gy, 80)
-      if (t >= 64 && t < 81) {
-        uint4 lo, hi;  // the byte-source face (bits 0..7) and the bit-8 source face
-        int kb, ib, row;
-        if (t < 72) {  // gy = 8, gz = t - 64: y-face of (0,1,0), x-face bit (0,0,gz) of (1,1,0)
-          lo = sm.pk[s][1], hi = sm.pk[s][2], kb = t - 64, ib = 8 * (t - 64), row = (t - 64) * 9 + 8;
-        } else if (t < 80) {  // gz = 8, gy = t - 72: z-face of (0,0,1), x-face bit (0,gy,0) of (1,0,1)
-          lo = sm.pk[s][3], hi = sm.pk[s][4], kb = t - 72, ib = t - 72, row = 72 + (t - 72);
-        } else {  // gy = gz = 8: y-face byte 0 of (0,1,1), x-face bit 0 of (1,1,1)
-          lo = sm.pk[s][5], hi = sm.pk[s][6], kb = 0, ib = 0, row = 80;
-        }
-        sm.grid_in[s][row] = byte64(lo.x, lo.y, kb) | (bit64(hi.x, hi.y, ib) << 8);
-        sm.grid_ob[s][row] = byte64(lo.z, lo.w, kb) | (bit64(hi.z, hi.w, ib) << 8);
-      }
     } else if (h == 0) {
       atomicOr(&sm.grid_in[s][z * 9 + y], in_row);
       atomicOr(&sm.grid_ob[s][z * 9 + y], ob_row);
@@ -500,11 +501,9 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     }
     if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(word[0], word[1], word[2], word[3]));
     if (q_blk) __stcs((uint32_t*)(q_blk + 4 * t), qw);
-    if (counts) {
+    if (counts) {  // counts are zeroed by the launch: one reduction per warp, no barrier
       nz = __reduce_add_sync(0xffffffffu, nz);
-      if (lane == 0) sm.cnt[s][warp] = nz;
-      __syncthreads();
-      if (t == 0) counts[blk] = sm.cnt[s][0] + sm.cnt[s][1] + sm.cnt[s][2] + sm.cnt[s][3];
+      if (lane == 0 && nz) atomicAdd(counts + blk, nz);
     }
   }
 }
@@ -560,6 +559,7 @@ static vs_status launch_mc_t(const TableView& T, const uint8_t* pool, const uint
     grid = sms * per_sm;
   }
   const uint64_t g = n < (uint64_t)grid ? n : (uint64_t)grid;
+  if (counts) VS_CK(cudaMemsetAsync(counts, 0, 4 * n, s));
   {
     ProfScope prof(1, s);
     k_mc_encode<kFromKeys, kFaces><<<(unsigned)g, kMcThreads, 0, s>>>(T, pool, faces, keys, nbr, n,

@@ -77,31 +77,60 @@ class ShardedBlockHashSet:
         if exchange == "peer" and not device_table:
             raise ValueError("exchange='peer' needs a BlockHashSet on a CUDA device")
         self.exchange = "peer" if (exchange == "peer" or (exchange == "auto" and device_table)) else "collective"
-        if self.exchange == "peer":
-            self._connect()
+        if self.exchange == "peer" and not self._connect(required=exchange == "peer"):
+            self.exchange = "collective"
 
     # -- peer-window exchange (csrc/shard.cu) ------------------------------
 
-    def _connect(self) -> None:
+    def _connect(self, required: bool) -> bool:
+        """Create this rank's window, exchange the IPC handles, map the peers.
+        Collective.  Every rank learns whether ALL ranks succeeded; when one
+        did not (e.g. no peer access between two GPUs) and the peer route was
+        not required, every rank falls back to the collective route together."""
         import ctypes
+        import warnings
 
+        import torch
         import torch.distributed as dist
 
         from . import _lib
 
         lib = _lib.load()
-        h = ctypes.c_void_p()
-        _lib.check(lib.vs_shard_create(self.local.handle, self.rank, self.world, self.max_batch, ctypes.byref(h)),
-                   "vs_shard_create")
         self._lib = lib
-        self._shard = h
         mine = (ctypes.c_uint8 * 64)()
-        _lib.check(lib.vs_shard_export(h, ctypes.byref(mine)), "vs_shard_export")
+        err = ""
+        try:
+            h = ctypes.c_void_p()
+            _lib.check(lib.vs_shard_create(self.local.handle, self.rank, self.world, self.max_batch,
+                                           ctypes.byref(h)), "vs_shard_create")
+            self._shard = h
+            _lib.check(lib.vs_shard_export(h, ctypes.byref(mine)), "vs_shard_export")
+        except Exception as exc:  # noqa: BLE001 - reported below, decided collectively
+            err = str(exc)
         handles: list = [None] * self.world
-        dist.all_gather_object(handles, bytes(mine), group=self.group)
-        _lib.check(lib.vs_shard_connect(h, b"".join(handles)), "vs_shard_connect")
+        dist.all_gather_object(handles, None if err else bytes(mine), group=self.group)
+        if not err and all(x is not None for x in handles):
+            try:
+                _lib.check(lib.vs_shard_connect(self._shard, b"".join(handles)), "vs_shard_connect")
+            except Exception as exc:  # noqa: BLE001
+                err = str(exc)
+        elif not err:
+            err = "a peer could not create its window"
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32)
+        if self.backend == "nccl":
+            ok = ok.to(self.local.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if int(ok.item()) == 0:
+            if self._shard is not None:
+                lib.vs_shard_destroy(self._shard)
+                self._shard = None
+            if required:
+                raise RuntimeError(f"peer route unavailable: {err or 'failed on another rank'}")
+            warnings.warn(f"peer route unavailable ({err or 'failed on another rank'}); using the collective route")
+            return False
         # every rank mapped every window before anyone stores into one
         dist.barrier(group=self.group)
+        return True
 
     def __del__(self) -> None:
         h = getattr(self, "_shard", None)
