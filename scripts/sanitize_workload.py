@@ -38,5 +38,34 @@ sets[0].extract_ordered(100); sets[0].fifo_entries(); sets[1].clear()
 core = GpuServerCore(1 << 10, 1 << 10, stream_buckets=1 << 9, stream_excess=1 << 9)
 cl = core.attach(b"a" * 16)
 core.on_tsdf_batch(keys[:20], rows[:20]); core.on_reset_blocks(keys[:5])
+# face packs + both encoder halo paths
+from paper_1805_03709_b200 import face_packs
+fp = face_packs(pool, rows=pos)
+mc3, q3, c3 = encode_keys(tt, pool, keys, faces=fp)
+mc4, q4, c4 = encode_blocks(pool, nb, faces=fp)
+assert torch.equal(mc, mc3) and torch.equal(mc, mc4)
+# fan-out bounded by a device count
+fan_out(sets, keys[:300], n_dev=torch.tensor([123], dtype=torch.int64, device=dev))
+# peer-sharded route at world 1 (partition, push, waits, routed apply/post/return)
+import tempfile
+import torch.distributed as dist
+from paper_1805_03709_b200.shard import ShardedBlockHashSet
+dist.init_process_group("gloo", init_method=f"file://{tempfile.mkdtemp()}/pg", rank=0, world_size=1)
+sh = ShardedBlockHashSet(BlockHashSet(spec.bucket_count, spec.excess), exchange="peer", max_batch=spec.batch)
+sh.apply(workloads.id_to_key_torch(torch.arange(spec.live, device=dev)[:spec.batch]),
+         torch.zeros(spec.batch, dtype=torch.uint8, device=dev))
+r2 = sh.apply(workloads.id_to_key_torch(ids), ops)
+sh.check()
+dist.destroy_process_group()
+# RC fusion kernels on a small frame
+import types
+from paper_1805_03709_b200.voxel_model import GpuVoxelModel
+depth, color, Rs, ts, (fx, fy, cx, cy, w, h) = workloads.room_frames(1, 64, 48)
+intr = types.SimpleNamespace(fx=fx, fy=fy, cx=cx, cy=cy, width=w, height=h)
+cfg = types.SimpleNamespace(voxel_size=0.005, truncation=0.06, max_weight=128.0, alloc_stride=1)
+model = GpuVoxelModel(cfg, bucket_count=1 << 14, excess_capacity=1 << 14, device=dev)
+d0, c0 = torch.from_numpy(depth[0]).to(dev), torch.from_numpy(color[0]).to(dev)
+model.allocate_blocks_tensor(d0, (Rs[0], ts[0]), intr)
+model.integrate_frame_tensor(d0, c0, (Rs[0], ts[0]), intr)
 torch.cuda.synchronize()
 print("SANITIZE_WORKLOAD_OK", flush=True)
