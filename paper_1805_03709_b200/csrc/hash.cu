@@ -585,7 +585,7 @@ using namespace vsb;
 extern "C" {
 
 const char* vs_last_error(void) { return g_last_error.c_str(); }
-int32_t vs_abi_version(void) { return 1; }
+int32_t vs_abi_version(void) { return 2; }  // 2: faces argument of the MC encoders, n_dev of vs_stream_insert_many
 
 vs_status vs_profile_begin(void) {
   std::lock_guard<std::mutex> g(g_prof_mu);

@@ -22,7 +22,7 @@ def test_library_builds_and_loads():
     path = build.build()
     assert path.exists()
     lib = _lib.load()
-    assert lib.vs_abi_version() == 1
+    assert lib.vs_abi_version() == 2
 
 
 def test_every_header_symbol_is_exported_and_bound():
