@@ -124,7 +124,17 @@ __device__ __forceinline__ bool block_visible(const Frustum& F, int32_t kx, int3
 // random start (wrapping), keeps the first max_n, and removes them; the
 // vacated excess entries go straight back to the free list (no pops run in
 // this launch, so the push cannot race a pop).
-__global__ void __launch_bounds__(256) k_multi_extract(const __grid_constant__ SetViews V,
+// extraction CTA shape (one CTA per client set; measured: see DESIGN §4)
+#ifndef VSB_EXTRACT_THREADS
+#define VSB_EXTRACT_THREADS 256
+#endif
+#ifndef VSB_EXTRACT_K
+#define VSB_EXTRACT_K 8
+#endif
+constexpr int kExtractThreads = VSB_EXTRACT_THREADS;
+constexpr int kExtractK = VSB_EXTRACT_K;
+
+__global__ void __launch_bounds__(kExtractThreads) k_multi_extract(const __grid_constant__ SetViews V,
                                                        const __grid_constant__ FifoViews S,
                                                        const __grid_constant__ Frustum F, uint64_t max_n,
                                                        int32_t* __restrict__ keys_out, uint64_t* __restrict__ n_out) {
@@ -138,21 +148,21 @@ __global__ void __launch_bounds__(256) k_multi_extract(const __grid_constant__ S
   x ^= x >> 31;
   const uint32_t start = (uint32_t)(x % cap);
   int32_t* out = keys_out + (uint64_t)c * max_n * 3;
-  __shared__ uint32_t wcnt[8];
+  constexpr uint32_t kWarps = kExtractThreads / 32;
+  __shared__ uint32_t wcnt[kWarps];
   __shared__ uint64_t found_s;
   if (threadIdx.x == 0) found_s = 0;
   __syncthreads();
   const uint32_t warp = threadIdx.x >> 5;
-  // chunks of kExtractK x 256 positions: all loads of a chunk in flight
-  // first, then the ordered selection round by round (position order)
-  constexpr int kExtractK = 8;
-  for (uint64_t scanned = 0; scanned < cap; scanned += 256 * kExtractK) {
+  // chunks of kExtractK x kExtractThreads positions: all loads of a chunk in
+  // flight first, then the ordered selection round by round (position order)
+  for (uint64_t scanned = 0; scanned < cap; scanned += (uint64_t)kExtractThreads * kExtractK) {
     if (found_s >= max_n) break;
     int4 e[kExtractK];
     bool live[kExtractK];
 #pragma unroll
     for (int k = 0; k < kExtractK; ++k) {
-      const uint64_t q = scanned + (uint64_t)k * 256 + threadIdx.x;
+      const uint64_t q = scanned + (uint64_t)k * kExtractThreads + threadIdx.x;
       uint64_t p = (uint64_t)start + q;
       p = p >= cap ? p - cap : p;
       live[k] = false;
@@ -169,7 +179,7 @@ __global__ void __launch_bounds__(256) k_multi_extract(const __grid_constant__ S
       if (lane_id() == 0) wcnt[warp] = __popc(bal);
       __syncthreads();
       uint32_t before = 0, total = 0;
-      for (uint32_t w = 0; w < 8; ++w) {
+      for (uint32_t w = 0; w < kWarps; ++w) {
         before += (w < warp) ? wcnt[w] : 0;
         total += wcnt[w];
       }
@@ -409,7 +419,7 @@ static vs_status multi_extract(vs_table* const* sets_host, int n_sets, uint64_t 
   cudaStream_t s = (cudaStream_t)stream;
   FifoViews S{};
   for (int c = 0; c < n_sets; ++c) S.cap[c] = seeds_host[c];
-  { k_multi_extract<<<n_sets, 256, 0, s>>>(V, S, F, max_n, keys_out, n_out); vsb::count_launch(); }
+  { k_multi_extract<<<n_sets, kExtractThreads, 0, s>>>(V, S, F, max_n, keys_out, n_out); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_stream_extract");
   return VS_OK;
 }
