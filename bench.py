@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--live", type=int, default=10_000_000, help="live keys per GPU (config 2: 10M)")
     p.add_argument("--batch-log2", type=int, default=22)
+    p.add_argument("--bucket-frac", type=float, default=0.5,
+                   help="share of the 0.7-load-factor slots in the bucket region (rest: excess)")
     p.add_argument("--mc-steps", type=int, default=10)
     p.add_argument("--no-mc", action="store_true")
     p.add_argument("--no-stream", action="store_true")
@@ -221,7 +223,7 @@ def run_hash(args, dev, rank, world):
 
     from paper_1805_03709_b200 import BlockHashSet, _lib, workloads
 
-    spec = workloads.MixSpec(live=args.live, load_factor=0.7, batch=1 << args.batch_log2)
+    spec = workloads.MixSpec(live=args.live, load_factor=0.7, batch=1 << args.batch_log2, bucket_frac=args.bucket_frac)
     B = spec.batch
     s = BlockHashSet(spec.bucket_count, spec.excess, device=dev)
     # rank r owns its own id space; with world > 1 keys are routed to owners
@@ -657,7 +659,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     from paper_1805_03709_b200 import workloads
 
-    spec = workloads.MixSpec(live=args.live, load_factor=0.7, batch=1 << args.batch_log2)
+    spec = workloads.MixSpec(live=args.live, load_factor=0.7, batch=1 << args.batch_log2, bucket_frac=args.bucket_frac)
     threads = args.cpu_threads or cpu_cores()
     config = {"workload": "config 2: 10M-key block hash set, 50/30/20 insert/find/erase mix, load factor 0.7, "
                           f"batches of 2^{args.batch_log2} ops (one launch per batch)",

@@ -123,6 +123,7 @@ class MixSpec:
     live: int = 10_000_000
     load_factor: float = 0.7
     batch: int = 1 << 22
+    bucket_frac: float = 0.5  # share of the slots in the bucket region (the reference's defaults: equal halves)
 
     @property
     def slots(self) -> int:
@@ -130,7 +131,9 @@ class MixSpec:
 
     @property
     def bucket_count(self) -> int:
-        return (self.slots + 1) // 2
+        if self.bucket_frac == 0.5:
+            return (self.slots + 1) // 2
+        return max(1, int(round(self.slots * self.bucket_frac)))
 
     @property
     def excess(self) -> int:
