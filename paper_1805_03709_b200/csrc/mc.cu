@@ -174,6 +174,10 @@ struct McSmem {
   uint4 pk[2][8];  // face packs of the block's neighbours c = 1..7 (kFaces)
   uint32_t grid_in[2][81];
   uint32_t grid_ob[2][81];
+  // kFaces: rows stored pre-expanded per half h: pair4(row >> 4h) (the
+  // corner pairs of voxels 4h..4h+3), written once by the row's writers
+  uint32_t ex_in[2][162];
+  uint32_t ex_ob[2][162];
   int32_t nb[2][kLook][8];  // neighbour rows of two lookup batches
 };
 
@@ -427,8 +431,12 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
         } else {  // gy = gz = 8: y-face byte 0 of (0,1,1), x-face bit 0 of (1,1,1)
           lo = sm.pk[s][5], hi = sm.pk[s][6], kb = 0, ib = 0, row = 80;
         }
-        sm.grid_in[s][row] = byte64(lo.x, lo.y, kb) | (bit64(hi.x, hi.y, ib) << 8);
-        sm.grid_ob[s][row] = byte64(lo.z, lo.w, kb) | (bit64(hi.z, hi.w, ib) << 8);
+        const uint32_t vi = byte64(lo.x, lo.y, kb) | (bit64(hi.x, hi.y, ib) << 8);
+        const uint32_t vo = byte64(lo.z, lo.w, kb) | (bit64(hi.z, hi.w, ib) << 8);
+        sm.ex_in[s][2 * row] = pair4(vi);
+        sm.ex_in[s][2 * row + 1] = pair4(vi >> 4);
+        sm.ex_ob[s][2 * row] = pair4(vo);
+        sm.ex_ob[s][2 * row + 1] = pair4(vo >> 4);
       }
     }
 
@@ -463,13 +471,14 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     in_row |= __shfl_xor_sync(0xffffffffu, in_row, 1);
     ob_row |= __shfl_xor_sync(0xffffffffu, ob_row, 1);
     if (kFaces) {
-      // whole rows: centre bits 0..7 + the +x neighbour's x-face bit as bit 8
-      if (h == 0) {
-        const uint4 c1 = sm.pk[s][0];
-        const int i = y + 8 * z;
-        sm.grid_in[s][z * 9 + y] = in_row | (bit64(c1.x, c1.y, i) << 8);
-        sm.grid_ob[s][z * 9 + y] = ob_row | (bit64(c1.z, c1.w, i) << 8);
-      }
+      // whole rows: centre bits 0..7 + the +x neighbour's x-face bit as bit 8;
+      // each lane of the pair stores its own half, pre-expanded
+      const uint4 c1 = sm.pk[s][0];
+      const int i = y + 8 * z;
+      const uint32_t vi = in_row | (bit64(c1.x, c1.y, i) << 8);
+      const uint32_t vo = ob_row | (bit64(c1.z, c1.w, i) << 8);
+      sm.ex_in[s][2 * (z * 9 + y) + h] = pair4(vi >> x0);
+      sm.ex_ob[s][2 * (z * 9 + y) + h] = pair4(vo >> x0);
     } else if (h == 0) {
       atomicOr(&sm.grid_in[s][z * 9 + y], in_row);
       atomicOr(&sm.grid_ob[s][z * 9 + y], ob_row);
@@ -478,17 +487,25 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
 
     // ---- cube indices, cutoff, colour, quantised TSDF: 4 voxels per thread
     const int r00 = z * 9 + y;
-    const uint32_t* gi = sm.grid_in[s];
-    const uint32_t* go = sm.grid_ob[s];
-    const uint32_t i00 = gi[r00] >> x0, i10 = gi[r00 + 1] >> x0, i01 = gi[r00 + 9] >> x0, i11 = gi[r00 + 10] >> x0;
-    const uint32_t o00 = go[r00] >> x0, o10 = go[r00 + 1] >> x0, o01 = go[r00 + 9] >> x0, o11 = go[r00 + 10] >> x0;
     uint32_t word[4];
     uint32_t qw = 0, nz = 0;
     // all 4 cube indices at once, one per byte: byte k of pair(v) holds bits
     // (k, k+1) of row v, so the 8 corner bits of voxel k are the 4 rows'
     // pairs stacked at bit offsets 0/2/4/6 (corner c = (c&1, c>>1&1, c>>2&1))
-    const uint32_t I = pair4(i00) | (pair4(i10) << 2) | (pair4(i01) << 4) | (pair4(i11) << 6);
-    const uint32_t O = pair4(o00) | (pair4(o10) << 2) | (pair4(o01) << 4) | (pair4(o11) << 6);
+    uint32_t I, O;
+    if (kFaces) {
+      const uint32_t* ei = sm.ex_in[s] + h;
+      const uint32_t* eo = sm.ex_ob[s] + h;
+      I = ei[2 * r00] | (ei[2 * (r00 + 1)] << 2) | (ei[2 * (r00 + 9)] << 4) | (ei[2 * (r00 + 10)] << 6);
+      O = eo[2 * r00] | (eo[2 * (r00 + 1)] << 2) | (eo[2 * (r00 + 9)] << 4) | (eo[2 * (r00 + 10)] << 6);
+    } else {
+      const uint32_t* gi = sm.grid_in[s];
+      const uint32_t* go = sm.grid_ob[s];
+      I = pair4(gi[r00] >> x0) | (pair4(gi[r00 + 1] >> x0) << 2) | (pair4(gi[r00 + 9] >> x0) << 4) |
+          (pair4(gi[r00 + 10] >> x0) << 6);
+      O = pair4(go[r00] >> x0) | (pair4(go[r00 + 1] >> x0) << 2) | (pair4(go[r00 + 9] >> x0) << 4) |
+          (pair4(go[r00 + 10] >> x0) << 6);
+    }
     // keep a byte only where all 8 corners are observed and it is not 255
     const uint32_t keep = __vcmpeq4(O, 0xFFFFFFFFu) & ~__vcmpeq4(I, 0xFFFFFFFFu);
     const uint32_t idx4 = I & keep;
