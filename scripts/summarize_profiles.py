@@ -12,7 +12,9 @@ for name, rep, kern in [("apply", "gpurun_out/prof_apply.ncu-rep", "k_apply"),
     d = raw(rep)
     lines = [f"# ncu --set full summary: vsb::{kern} ({tag}), from {rep.split('/')[-1]}",
              f"# command: scripts/gpu_bench.sh (ncu --set full --clock-control none --import-source on -k regex:{kern} -s N -c 1)"]
-    for k in KEYS + ["l1tex__t_sector_hit_rate.pct", "smsp__inst_executed.sum"]:
+    for k in KEYS + ["l1tex__t_sector_hit_rate.pct", "smsp__inst_executed.sum",
+                     "lts__t_requests_srcunit_tex_op_atom.sum", "lts__t_sectors_srcunit_tex_op_atom.sum",
+                     "lts__t_sectors_srcunit_tex_op_red.sum", "lts__t_sectors_op_atom.sum", "lts__t_sectors_op_red.sum"]:
         if k in d:
             lines.append(f"{k:60s} {d[k][0]} {d[k][1]}")
     lines.append("# top stall-sampled source lines (share of warp stall samples)")
