@@ -645,11 +645,6 @@ static void keep_pool_resident(int device) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  // experiment knob: L2 fetch granularity hint for random entry accesses
-  if (const char* g = getenv("VSB_L2_FETCH")) {
-    DeviceGuard dg(device);
-    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(g));
-  }
   done[device] = true;
 }
 
