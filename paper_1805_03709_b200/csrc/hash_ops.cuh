@@ -27,6 +27,13 @@
 #include "common.cuh"
 
 
+// New excess entries are linked at the chain head (1), which also lets an
+// insert skip the locked re-scan when its bucket word is unchanged; 0 = the
+// reference's tail append with a re-scan under every lock.
+#ifndef VSB_HASH_HEAD_INSERT
+#define VSB_HASH_HEAD_INSERT 1
+#endif
+
 namespace vsb {
 
 __device__ __forceinline__ uint32_t next_pos(const TableView& T, uint32_t meta) {
@@ -217,7 +224,7 @@ __device__ __forceinline__ void post_op(const TableView& T, const int32_t* __res
 // Returns {position, created} for an insert, {vacated position or -1, 0}
 // for an erase.
 __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_t x, int32_t y, int32_t z, bool ins,
-                                                      int32_t op, uint32_t b) {
+                                                      int32_t op, uint32_t b, uint32_t snap) {
   uint32_t* bmeta = &T.e[b].meta;
 #pragma unroll 1
   for (int attempt = 0;; ++attempt) {
@@ -230,7 +237,13 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
     const uint32_t dep = (old >> 31) & 1u;  // always 0 here
     int32_t found = -1;
     uint32_t fmeta = 0, prev = b, prev_meta = old;  // prev: predecessor of `found`, else the tail
-    {
+    // An insert whose bucket word is still exactly the one its lock-free
+    // lookup started from needs no re-scan: inserts only claim the bucket
+    // (OCC changes) or link at the head (NEXT changes), and an unlinked
+    // position is not reused inside a launch, so an unchanged word means
+    // no key entered this chain since the lookup found the key absent.
+    const bool rescan = !(VSB_HASH_HEAD_INSERT && ins && old == snap);
+    if (rescan) {
       const int4 s = ld_entry(T.e + b + dep);
       if ((old & kOcc) && key_eq(s, x, y, z)) {
         found = (int32_t)b;
@@ -271,6 +284,15 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
       }
       const uint32_t e = (uint32_t)ne;
       const uint32_t link = e - T.n + 1u;
+#if VSB_HASH_HEAD_INSERT
+      // link at the chain HEAD (right after the bucket): the new entry takes
+      // the bucket's NEXT and ONE release exchange of the bucket word
+      // publishes it and unlocks (the reference appends at the tail, :204;
+      // lock-free readers see either the old chain or the new one)
+      (void)prev_meta;
+      st_entry(T.e + e, x, y, z, kOcc | kFresh | (old & kNext));
+      atom_exch_release(bmeta, (old & ~kNext) | link);
+#else
       st_entry(T.e + e, x, y, z, kOcc | kFresh);  // NEXT = 0 clears the stale offset (:200)
       if (prev == b) {
         atom_exch_release(bmeta, (old & ~kNext) | link);  // publish + unlock
@@ -278,6 +300,7 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
         st_release_u32(&T.e[prev].meta, (prev_meta & ~kNext) | link);  // publish last (:204)
         atom_exch_release(bmeta, old);                                  // unlock after the link
       }
+#endif
       return {(int32_t)e, 1};
     }
     if (found < 0) {  // erased by another op since the lookup
@@ -310,12 +333,13 @@ __device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x
                                                    const int4* pre = nullptr) {
   const uint32_t b = bucket_of(T, x, y, z);
   uint32_t fmeta;
-  const int32_t pos = find_pos_from(T, x, y, z, b, pre ? *pre : ld_bucket(T.e + b), &fmeta);
+  const int4 s0 = pre ? *pre : ld_bucket(T.e + b);
+  const int32_t pos = find_pos_from(T, x, y, z, b, s0, &fmeta);
   if (pos >= 0) {
     if (fmeta & kFresh) claim_min(T, pos, op);
     return {pos, 0};
   }
-  return mutate_locked(T, x, y, z, true, op, b);
+  return mutate_locked(T, x, y, z, true, op, b, (uint32_t)s0.w);
 }
 
 // remove (concurrent_hash.py:251-295).  Returns the vacated position or -1.
@@ -325,7 +349,7 @@ __device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int3
   const uint32_t b = bucket_of(T, x, y, z);
   uint32_t fmeta;
   if (find_pos_from(T, x, y, z, b, pre ? *pre : ld_bucket(T.e + b), &fmeta) < 0) return -1;
-  return mutate_locked(T, x, y, z, false, 0, b).pos;
+  return mutate_locked(T, x, y, z, false, 0, b, 0u).pos;
 }
 
 // One mixed op (insert / find / erase) with its bucket entry already loaded.
@@ -346,7 +370,7 @@ __device__ __forceinline__ int apply_one(const TableView& T, int32_t x, int32_t 
   res = !ins && fpos >= 0;  // find: found; erase: provisional
   if (ins && fpos >= 0 && (fmeta & kFresh)) claim_min(T, fpos, (int32_t)i);
   if ((ins && fpos < 0) || (era && fpos >= 0)) {
-    const InsertResult r = mutate_locked(T, x, y, z, ins, (int32_t)i, b);
+    const InsertResult r = mutate_locked(T, x, y, z, ins, (int32_t)i, b, (uint32_t)pre.w);
     pos = r.pos;
     res = ins ? r.created : (uint8_t)(r.pos >= 0);
     delta = ins ? (int)r.created : -(int)(r.pos >= 0);
