@@ -100,6 +100,12 @@ vs_status vs_table_info(const vs_table *t, uint64_t *bucket_count_host,
 vs_status vs_table_insert(vs_table *t, const int32_t *keys, uint64_t n,
                           uint8_t *created, int32_t *index, vs_stream_t stream);
 
+/* Same, for the first min(*n_dev, n) keys only (n_dev: device uint64, e.g.
+ * a count produced by a previous kernel): no host synchronisation; ops past
+ * the count get created 0 and index -1. */
+vs_status vs_table_insert_bounded(vs_table *t, const int32_t *keys, uint64_t n, const uint64_t *n_dev,
+                                  uint8_t *created, int32_t *index, vs_stream_t stream);
+
 /* _find / __contains__ / BlockHashMap.get (concurrent_hash.py:146-157,
  * 297-298, 449-460).  Read-only.  index[i] = position or -1. */
 vs_status vs_table_find(vs_table *t, const int32_t *keys, uint64_t n,

@@ -56,6 +56,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_table_destroy": (_i32, [_vp]),
     "vs_table_info": (_i32, [_vp, _pu64, _pu64, _pu64]),
     "vs_table_insert": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp]),
+    "vs_table_insert_bounded": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "vs_table_find": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp]),
     "vs_table_erase": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp]),
     "vs_table_apply": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp, _vp]),

@@ -106,10 +106,16 @@ __global__ void k_reset_ctl(TableView T) {
 }
 
 __global__ void __launch_bounds__(kOpBlock) k_insert(TableView T, const int32_t* __restrict__ keys, uint64_t n,
+                                                     const uint64_t* __restrict__ n_dev,
                                                      uint8_t* __restrict__ created, int32_t* __restrict__ index) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nv = n_dev && *n_dev < n ? *n_dev : n;  // ops past a device count: created 0, index -1
   int delta = 0;
-  if (i < n) {
+  if (i >= nv && i < n) {
+    created[i] = 0;
+    index[i] = -1;
+  }
+  if (i < nv) {
     const int32_t x = keys[3 * i], y = keys[3 * i + 1], z = keys[3 * i + 2];
     const InsertResult r = insert_key(T, x, y, z, (int32_t)i);
     created[i] = r.created;
@@ -745,8 +751,8 @@ static vs_status check_batch(const vs_table* t, uint64_t n) {
   return VS_OK;
 }
 
-vs_status vs_table_insert(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* created, int32_t* index,
-                          vs_stream_t stream) {
+static vs_status table_insert(vs_table* t, const int32_t* keys, uint64_t n, const uint64_t* n_dev, uint8_t* created,
+                              int32_t* index, vs_stream_t stream) {
   vs_status st = check_batch(t, n);
   if (st != VS_OK || n == 0) return st;
   if (!keys || !created || !index) {
@@ -758,11 +764,25 @@ vs_status vs_table_insert(vs_table* t, const int32_t* keys, uint64_t n, uint8_t*
   const TableView v = t->next_view();
   {
     ProfScope prof(0, s);
-    { k_insert<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, created, index); vsb::count_launch(); }
+    { k_insert<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, n_dev, created, index); vsb::count_launch(); }
   }
   { k_post<<<grid_for(n, kPostBlock * kPostOps), kPostBlock, 0, s>>>(v, keys, nullptr, n, created, index); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_insert");
   return VS_OK;
+}
+
+vs_status vs_table_insert(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* created, int32_t* index,
+                          vs_stream_t stream) {
+  return table_insert(t, keys, n, nullptr, created, index, stream);
+}
+
+vs_status vs_table_insert_bounded(vs_table* t, const int32_t* keys, uint64_t n, const uint64_t* n_dev,
+                                  uint8_t* created, int32_t* index, vs_stream_t stream) {
+  if (!n_dev) {
+    set_error("n_dev must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  return table_insert(t, keys, n, n_dev, created, index, stream);
 }
 
 vs_status vs_table_find(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* found, int32_t* index,

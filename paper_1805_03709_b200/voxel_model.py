@@ -229,6 +229,56 @@ class GpuVoxelModel:
         enc = ((k[:, 0] + off) << 42) | ((k[:, 1] + off) << 21) | (k[:, 2] + off)
         return new[torch.argsort(enc)]
 
+    def fuse_frame_async(self, depth, color, pose, intrinsics):
+        """allocate_blocks + integrate_frame of one frame with NO host
+        synchronisation (pipelines and the bench): candidates into a buffer
+        sized by the largest count seen so far, a device-count-bounded insert
+        (vs_table_insert_bounded), fresh rows zeroed, integration over the
+        map.  Returns (touched_keys_buffer, touched_n_dev).  The exact
+        per-frame failure semantics of allocate_blocks are not kept here:
+        call check_async() (synchronising) after a run of frames -- it raises
+        if a candidate buffer overflowed or the excess list ran dry."""
+        torch = self._torch
+        lib = self._lib
+        L = lib.load()
+        d = self._img(depth, torch.float32)
+        c = self._img(color, torch.uint8)
+        cap = max(getattr(self, "_cand_cap", 0), 1 << 16, 2 * d.numel())
+        if getattr(self, "_async", None) is None or self._async["cap"] < cap:
+            self._async = {"cap": cap,
+                           "cand": torch.empty((cap, 3), dtype=torch.int32, device=self.device),
+                           "created": torch.empty(cap, dtype=torch.uint8, device=self.device),
+                           "pos": torch.empty(cap, dtype=torch.int32, device=self.device),
+                           "n": torch.zeros(1, dtype=torch.int64, device=self.device),
+                           "n_max": torch.zeros(1, dtype=torch.int64, device=self.device)}
+        if getattr(self, "_touched_buf", None) is None:
+            self._touched_buf = torch.empty((self.blocks.capacity, 3), dtype=torch.int32, device=self.device)
+            self._touched_n = torch.zeros(1, dtype=torch.int64, device=self.device)
+        a = self._async
+        s = self.blocks._stream()
+        st = _ct.c_void_p(s.cuda_stream)
+        P = self._params(pose, intrinsics, planes=False)
+        lib.check(L.vs_rc_candidates(lib.ptr(d), _ct.byref(P), lib.ptr(a["cand"]), a["cap"], lib.ptr(a["n"]), st),
+                  "rc_candidates")
+        torch.maximum(a["n_max"], a["n"], out=a["n_max"])  # overflow check deferred to check_async
+        lib.check(L.vs_table_insert_bounded(self.blocks.handle, lib.ptr(a["cand"]), a["cap"], lib.ptr(a["n"]),
+                                            lib.ptr(a["created"]), lib.ptr(a["pos"]), st), "insert_bounded")
+        lib.check(L.vs_rc_zero_rows(lib.ptr(a["pos"]), lib.ptr(a["created"]), a["cap"], lib.ptr(self.pool), st),
+                  "rc_zero_rows")
+        P = self._params(pose, intrinsics, planes=True)
+        lib.check(L.vs_rc_integrate_table(self.blocks._h, lib.ptr(d), lib.ptr(c), _ct.byref(P), lib.ptr(self.pool),
+                                          lib.ptr(self._touched_buf), lib.ptr(self._touched_n), st), "rc_integrate")
+        self.blocks._done(s)
+        return self._touched_buf, self._touched_n
+
+    def check_async(self) -> None:
+        """Synchronise and verify a run of fuse_frame_async frames."""
+        a = getattr(self, "_async", None)
+        if a is not None and int(a["n_max"].item()) > a["cap"]:
+            raise RuntimeError(f"candidate buffer overflow ({int(a['n_max'].item())} > {a['cap']}): "
+                               "run a synchronous frame first to size it")
+        self.blocks.check_capacity()
+
     def integrate_frame(self, depth, color, pose, intrinsics) -> list:
         """Fuse one registered RGB-D frame into all allocated in-view blocks;
         returns the keys that received at least one voxel update."""

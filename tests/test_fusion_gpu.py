@@ -50,6 +50,29 @@ def test_sphere_fusion_bit_exact_and_model_digest(dev, golden):
     assert hashlib.sha256(mc.cpu().numpy().tobytes()).hexdigest() == meta["model_sha256"]
 
 
+def test_sync_free_fusion_path_reproduces_the_reference_model(dev, golden):
+    """fuse_frame_async (no host sync per frame: device-bounded insert,
+    zeroed rows, integration over the map) on the reference's sphere
+    sequence: the same keys and the same voxels bit for bit, and the MC
+    digest of manifest.json."""
+    from paper_1805_03709_b200 import encode_keys
+    from paper_1805_03709_b200.voxel_model import GpuVoxelModel, rows_from_soa
+
+    d, intr, cfg = _inputs(golden)
+    model = GpuVoxelModel(cfg, bucket_count=1 << 13, excess_capacity=1 << 13)
+    for f in range(d["depth"].shape[0]):
+        R, t = d["pose"][f][:9].reshape(3, 3), d["pose"][f][9:]
+        model.fuse_frame_async(d["depth"][f], d["color"][f], (R, t), intr)
+    model.check_async()
+    s = np.load(golden / "mc_sphere.npz")
+    keys = s["keys"]
+    assert sorted(model.keys()) == [tuple(k) for k in keys.tolist()]
+    assert np.array_equal(model.rows(keys).cpu().numpy(), rows_from_soa(s["tsdf"], s["weight"], s["color"]))
+    mc, _, _ = encode_keys(model.blocks, model.pool, keys)
+    meta = json.loads((golden / "mc_sphere.json").read_text())
+    assert hashlib.sha256(mc.cpu().numpy().tobytes()).hexdigest() == meta["model_sha256"]
+
+
 def test_reallocation_is_idempotent_and_get_block(dev, golden):
     from paper_1805_03709_b200.voxel_model import GpuVoxelModel
 
