@@ -224,7 +224,7 @@ __device__ __forceinline__ void post_op(const TableView& T, const int32_t* __res
 // Returns {position, created} for an insert, {vacated position or -1, 0}
 // for an erase.
 __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_t x, int32_t y, int32_t z, bool ins,
-                                                      int32_t op, uint32_t b, uint32_t snap) {
+                                                      int32_t op, uint32_t b, uint32_t snap, int32_t fpos = -1) {
   uint32_t* bmeta = &T.e[b].meta;
 #pragma unroll 1
   for (int attempt = 0;; ++attempt) {
@@ -242,8 +242,16 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
     // (OCC changes) or link at the head (NEXT changes), and an unlinked
     // position is not reused inside a launch, so an unchanged word means
     // no key entered this chain since the lookup found the key absent.
-    const bool rescan = !(VSB_HASH_HEAD_INSERT && ins && old == snap);
-    if (rescan) {
+    // Likewise an erase whose key sat in the bucket entry itself: an unchanged
+    // word that was not FRESH cannot have been re-claimed by another key (a
+    // claim sets FRESH), so the entry still holds this key.
+    const bool skip_ins = VSB_HASH_HEAD_INSERT && ins && old == snap;
+    const bool skip_era = !ins && fpos == (int32_t)b && old == snap && !(snap & kFresh);
+    if (skip_era) {
+      found = (int32_t)b;
+      fmeta = old;
+    }
+    if (!skip_ins && !skip_era) {
       const int4 s = ld_entry(T.e + b + dep);
       if ((old & kOcc) && key_eq(s, x, y, z)) {
         found = (int32_t)b;
@@ -348,8 +356,10 @@ __device__ __forceinline__ int32_t erase_key(const TableView& T, int32_t x, int3
                                             const int4* pre = nullptr) {
   const uint32_t b = bucket_of(T, x, y, z);
   uint32_t fmeta;
-  if (find_pos_from(T, x, y, z, b, pre ? *pre : ld_bucket(T.e + b), &fmeta) < 0) return -1;
-  return mutate_locked(T, x, y, z, false, 0, b, 0u).pos;
+  const int4 s0 = pre ? *pre : ld_bucket(T.e + b);
+  const int32_t fpos = find_pos_from(T, x, y, z, b, s0, &fmeta);
+  if (fpos < 0) return -1;
+  return mutate_locked(T, x, y, z, false, 0, b, (uint32_t)s0.w, fpos).pos;
 }
 
 // One mixed op (insert / find / erase) with its bucket entry already loaded.
@@ -370,7 +380,7 @@ __device__ __forceinline__ int apply_one(const TableView& T, int32_t x, int32_t 
   res = !ins && fpos >= 0;  // find: found; erase: provisional
   if (ins && fpos >= 0 && (fmeta & kFresh)) claim_min(T, fpos, (int32_t)i);
   if ((ins && fpos < 0) || (era && fpos >= 0)) {
-    const InsertResult r = mutate_locked(T, x, y, z, ins, (int32_t)i, b, (uint32_t)pre.w);
+    const InsertResult r = mutate_locked(T, x, y, z, ins, (int32_t)i, b, (uint32_t)pre.w, fpos);
     pos = r.pos;
     res = ins ? r.created : (uint8_t)(r.pos >= 0);
     delta = ins ? (int)r.created : -(int)(r.pos >= 0);
