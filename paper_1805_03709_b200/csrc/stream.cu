@@ -18,6 +18,8 @@
 #include <cstdint>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "hash_ops.cuh"
 #include "scan.cuh"
 #include "table.h"
@@ -134,11 +136,24 @@ __device__ __forceinline__ bool block_visible(const Frustum& F, int32_t kx, int3
 constexpr int kExtractThreads = VSB_EXTRACT_THREADS;
 constexpr int kExtractK = VSB_EXTRACT_K;
 
-__global__ void __launch_bounds__(kExtractThreads) k_multi_extract(const __grid_constant__ SetViews V,
-                                                       const __grid_constant__ FifoViews S,
-                                                       const __grid_constant__ Frustum F, uint64_t max_n,
-                                                       int32_t* __restrict__ keys_out, uint64_t* __restrict__ n_out) {
-  const int c = blockIdx.x;
+// One CLUSTER of kExtractCtas CTAs per client set: a round scans
+// kExtractCtas contiguous chunks of kExtractThreads x kExtractK positions
+// (CTA r takes chunk r), every CTA ranks its live entries in position order,
+// the chunk counts are exchanged through distributed shared memory, and each
+// CTA writes its entries at (found so far + counts of the lower chunks +
+// own rank) -- the first max_n live entries from the random start, in
+// position order, exactly as one CTA scanning alone would take them.  The
+// removals are then spread over the whole cluster.
+constexpr int kExtractCtas = 8;
+
+__global__ void __cluster_dims__(kExtractCtas, 1, 1) __launch_bounds__(kExtractThreads)
+    k_multi_extract(const __grid_constant__ SetViews V, const __grid_constant__ FifoViews S,
+                    const __grid_constant__ Frustum F, uint64_t max_n, int32_t* __restrict__ keys_out,
+                    uint64_t* __restrict__ n_out) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int c = blockIdx.x / kExtractCtas;
+  const uint32_t rank = cluster.block_rank();
   const TableView& T = V.v[c];
   const uint32_t cap = T.n + T.excess;
   const uint64_t seed = S.cap[c];  // per-client seed rides in the cap slot
@@ -149,20 +164,18 @@ __global__ void __launch_bounds__(kExtractThreads) k_multi_extract(const __grid_
   const uint32_t start = (uint32_t)(x % cap);
   int32_t* out = keys_out + (uint64_t)c * max_n * 3;
   constexpr uint32_t kWarps = kExtractThreads / 32;
-  __shared__ uint32_t wcnt[kWarps];
-  __shared__ uint64_t found_s;
-  if (threadIdx.x == 0) found_s = 0;
-  __syncthreads();
+  constexpr uint64_t kChunk = (uint64_t)kExtractThreads * kExtractK;
+  __shared__ uint32_t wcnt[kExtractK][kWarps];
+  __shared__ uint32_t chunk_cnt;  // read by the other CTAs of the cluster
   const uint32_t warp = threadIdx.x >> 5;
-  // chunks of kExtractK x kExtractThreads positions: all loads of a chunk in
-  // flight first, then the ordered selection round by round (position order)
-  for (uint64_t scanned = 0; scanned < cap; scanned += (uint64_t)kExtractThreads * kExtractK) {
-    if (found_s >= max_n) break;
+  uint64_t found = 0;  // identical in every CTA of the cluster
+  for (uint64_t base = 0; base < cap && found < max_n; base += kChunk * kExtractCtas) {
+    const uint64_t c0 = base + rank * kChunk;
     int4 e[kExtractK];
     bool live[kExtractK];
 #pragma unroll
     for (int k = 0; k < kExtractK; ++k) {
-      const uint64_t q = scanned + (uint64_t)k * kExtractThreads + threadIdx.x;
+      const uint64_t q = c0 + (uint64_t)k * kExtractThreads + threadIdx.x;
       uint64_t p = (uint64_t)start + q;
       p = p >= cap ? p - cap : p;
       live[k] = false;
@@ -171,35 +184,55 @@ __global__ void __launch_bounds__(kExtractThreads) k_multi_extract(const __grid_
         live[k] = ((uint32_t)e[k].w & kOcc) != 0;
       }
     }
+    uint32_t bal[kExtractK];
 #pragma unroll
     for (int k = 0; k < kExtractK; ++k) {
       if (live[k] && F.enabled) live[k] = block_visible(F, e[k].x, e[k].y, e[k].z);
-      const uint64_t found = found_s;
-      const uint32_t bal = __ballot_sync(0xffffffffu, live[k]);
-      if (lane_id() == 0) wcnt[warp] = __popc(bal);
-      __syncthreads();
-      uint32_t before = 0, total = 0;
+      bal[k] = __ballot_sync(0xffffffffu, live[k]);
+      if (lane_id() == 0) wcnt[k][warp] = __popc(bal[k]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t a = 0;
+      for (int k = 0; k < kExtractK; ++k)
+        for (uint32_t w = 0; w < kWarps; ++w) a += wcnt[k][w];
+      chunk_cnt = a;
+    }
+    cluster.sync();  // every chunk count published
+    uint64_t lower = 0, total = 0;
+    for (uint32_t r = 0; r < kExtractCtas; ++r) {
+      const uint32_t v = *cluster.map_shared_rank(&chunk_cnt, r);
+      lower += r < rank ? v : 0u;
+      total += v;
+    }
+    // ranks inside the chunk: (k, warp, lane) order = position order
+    uint64_t o = found + lower;
+#pragma unroll
+    for (int k = 0; k < kExtractK; ++k) {
+      uint32_t before = 0, all = 0;
       for (uint32_t w = 0; w < kWarps; ++w) {
-        before += (w < warp) ? wcnt[w] : 0;
-        total += wcnt[w];
+        before += (w < warp) ? wcnt[k][w] : 0u;
+        all += wcnt[k][w];
       }
       if (live[k]) {
-        const uint64_t o = found + before + __popc(bal & lanemask_lt());
-        if (o < max_n) {
-          out[3 * o] = e[k].x;
-          out[3 * o + 1] = e[k].y;
-          out[3 * o + 2] = e[k].z;
+        const uint64_t d = o + before + __popc(bal[k] & lanemask_lt());
+        if (d < max_n) {
+          out[3 * d] = e[k].x;
+          out[3 * d + 1] = e[k].y;
+          out[3 * d + 2] = e[k].z;
         }
       }
-      __syncthreads();
-      if (threadIdx.x == 0) found_s = found + total;
-      __syncthreads();
+      o += all;
     }
+    found += total;
+    cluster.sync();  // chunk_cnt / wcnt reused by the next round
   }
-  const uint64_t m = found_s < max_n ? found_s : max_n;
-  __syncthreads();  // keys_out complete before the removals read it
+  const uint64_t m = found < max_n ? found : max_n;
+  // keys_out complete (written by the whole cluster) before the removals
+  __threadfence();
+  cluster.sync();
   int delta = 0;
-  for (uint64_t j = threadIdx.x; j < m; j += blockDim.x) {
+  for (uint64_t j = rank * kExtractThreads + threadIdx.x; j < m; j += (uint64_t)kExtractCtas * kExtractThreads) {
     const int32_t pos = erase_key(T, out[3 * j], out[3 * j + 1], out[3 * j + 2]);
     if (pos >= 0) {
       --delta;
@@ -207,7 +240,7 @@ __global__ void __launch_bounds__(kExtractThreads) k_multi_extract(const __grid_
     }
   }
   add_size_cta(T, delta);
-  if (threadIdx.x == 0) n_out[c] = m;
+  if (rank == 0 && threadIdx.x == 0) n_out[c] = m;
 }
 
 __global__ void __launch_bounds__(256) k_multi_erase(const __grid_constant__ SetViews V,
@@ -419,7 +452,7 @@ static vs_status multi_extract(vs_table* const* sets_host, int n_sets, uint64_t 
   cudaStream_t s = (cudaStream_t)stream;
   FifoViews S{};
   for (int c = 0; c < n_sets; ++c) S.cap[c] = seeds_host[c];
-  { k_multi_extract<<<n_sets, kExtractThreads, 0, s>>>(V, S, F, max_n, keys_out, n_out); vsb::count_launch(); }
+  { k_multi_extract<<<n_sets * kExtractCtas, kExtractThreads, 0, s>>>(V, S, F, max_n, keys_out, n_out); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_stream_extract");
   return VS_OK;
 }
