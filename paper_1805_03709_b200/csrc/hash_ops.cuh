@@ -8,8 +8,10 @@
 //   * the reference's 1024 striped try-locks + seqlock versions become ONE
 //     lock bit in each bucket entry's meta word, so a lock costs no extra
 //     memory traffic;
-//   * readers need no version validation: chains change only by tail append
-//     (published last) and by unlinking (victim keeps its stale NEXT, like
+//   * readers need no version validation: chains change only by a link at
+//     the head (published by one release exchange of the bucket word; the
+//     tail append with VSB_HASH_HEAD_INSERT=0) and by unlinking (victim
+//     keeps its stale NEXT, like
 //     concurrent_hash.py:286-288), and unlinked excess entries are NOT reused
 //     inside the launch -- they are recycled into the free list by a separate
 //     launch, which removes the ABA case the seqlock guards;
