@@ -746,33 +746,51 @@ def main():
     if world > 1:  # the route actually used (auto falls back when peer access is unavailable)
         config["exchange"] = ("peer stores into CUDA-IPC windows over NVLink (csrc/shard.cu)"
                               if h.get("exchange") == "peer" else "collective all-to-all (shard.py)")
+    def section(fn, *a):
+        """A secondary section must never cost the headline line: its failure
+        is reported in its own field."""
+        try:
+            return fn(*a)
+        except Exception as exc:  # noqa: BLE001
+            import traceback
+
+            traceback.print_exc()
+            return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     mc = None
     if not args.no_mc:
-        mc = run_mc(args, dev, world)
+        mc = section(run_mc, args, dev, world)
     stream = None
     if not args.no_stream and world == 1:
-        stream = run_stream(args, dev)
+        stream = section(run_stream, args, dev)
     rc = None
     if not args.no_rc and world == 1:
-        rc = run_rc(args, dev)
+        rc = section(run_rc, args, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        times, ok, _ = cpu_hash_sample(spec, threads, batches=1)
-        mc_t, mc_n = (None, None) if args.no_mc else cpu_mc_sample(threads)
-        cpu = {"value": spec.batch / times[0] / 1e6, "unit": "M ops/s", "cores": threads, "kind": "port",
-               "sample": f"1 mixed batch of {spec.batch} ops on the 10M-key config-2 table (C restatement of "
-                         "concurrent_hash.py, bucket-partitioned threads)", "ok": ok}
-        if mc_t:
-            cpu["mc"] = {"value": mc_n / mc_t, "unit": "blocks/s", "cores": threads, "kind": "port",
-                         "sample": f"{mc_n} room blocks (C restatement of recompute_mc_block)"}
+        def cpu_hash():
+            times, ok, _ = cpu_hash_sample(spec, threads, batches=1)
+            return {"value": spec.batch / times[0] / 1e6, "unit": "M ops/s", "cores": threads, "kind": "port",
+                    "sample": f"1 mixed batch of {spec.batch} ops on the 10M-key config-2 table (C restatement of "
+                              "concurrent_hash.py, bucket-partitioned threads)", "ok": ok}
+
+        def cpu_mc():
+            mc_t, mc_n = cpu_mc_sample(threads)
+            return {"value": mc_n / mc_t, "unit": "blocks/s", "cores": threads, "kind": "port",
+                    "sample": f"{mc_n} room blocks (C restatement of recompute_mc_block)"}
+
+        cpu = section(cpu_hash)
+        if not args.no_mc:
+            cpu["mc"] = section(cpu_mc)
         if not args.no_rc:
-            cpu["rc"] = {"value": cpu_rc_sample(), "unit": "frames/s", "cores": 1, "kind": "port",
-                         "sample": "1 frame 640x480 of the RC workload (numpy restatement of allocate_blocks + "
-                                   "integrate_frame)"}
+            cpu["rc"] = section(lambda: {"value": cpu_rc_sample(), "unit": "frames/s", "cores": 1, "kind": "port",
+                                         "sample": "1 frame 640x480 of the RC workload (numpy restatement of "
+                                                   "allocate_blocks + integrate_frame)"})
         if not args.no_stream:
-            cpu["stream"] = {"value": cpu_stream_sample(), "unit": "M key-ops/s", "cores": 1, "kind": "port",
-                             "sample": "1 client: fill with the 2.08M-key scene + update ticks for ~5 s "
-                                       "(Python set + deque restatement of StreamSet)"}
+            cpu["stream"] = section(lambda: {"value": cpu_stream_sample(), "unit": "M key-ops/s", "cores": 1,
+                                             "kind": "port",
+                                             "sample": "1 client: fill with the 2.08M-key scene + update ticks for "
+                                                       "~5 s (Python set + deque restatement of StreamSet)"})
     if world > 1:
         import torch.distributed as dist
 
