@@ -29,6 +29,11 @@
 #include "common.cuh"
 
 
+// Excess-case erases validate the lookup's predecessor under the lock
+// instead of re-walking the chain (1).
+#ifndef VSB_HASH_VALIDATE_PREV
+#define VSB_HASH_VALIDATE_PREV 1
+#endif
 // New excess entries are linked at the chain head (1), which also lets an
 // insert skip the locked re-scan when its bucket word is unchanged; 0 = the
 // reference's tail append with a re-scan under every lock.
@@ -162,6 +167,26 @@ __device__ __forceinline__ int32_t find_pos_from(const TableView& T, int32_t x, 
   }
 }
 
+// ... also returning the entry the walk came from (*prev_out; == b for the
+// first excess entry, unset for a bucket hit)
+__device__ __forceinline__ int32_t find_pos_from_p(const TableView& T, int32_t x, int32_t y, int32_t z, uint32_t b,
+                                                  int4 s, uint32_t* meta_out, uint32_t* prev_out) {
+  uint32_t e = b, p = b;
+#pragma unroll 1
+  for (;;) {
+    const uint32_t meta = (uint32_t)s.w;
+    if ((meta & kOcc) && key_eq(s, x, y, z)) {
+      *meta_out = meta;
+      *prev_out = p;
+      return (int32_t)e;
+    }
+    if (!(meta & kNext)) return -1;
+    p = e;
+    e = next_pos(T, meta);
+    s = ld_entry(T.e + e);
+  }
+}
+
 __device__ __forceinline__ int32_t find_pos(const TableView& T, int32_t x, int32_t y, int32_t z, uint32_t b,
                                            uint32_t* meta_out) {
   return find_pos_from(T, x, y, z, b, ld_bucket(T.e + b), meta_out);  // first hop: L2 evict_last
@@ -226,7 +251,8 @@ __device__ __forceinline__ void post_op(const TableView& T, const int32_t* __res
 // Returns {position, created} for an insert, {vacated position or -1, 0}
 // for an erase.
 __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_t x, int32_t y, int32_t z, bool ins,
-                                                      int32_t op, uint32_t b, uint32_t snap, int32_t fpos = -1) {
+                                                      int32_t op, uint32_t b, uint32_t snap, int32_t fpos = -1,
+                                                      uint32_t fprev = 0) {
   uint32_t* bmeta = &T.e[b].meta;
 #pragma unroll 1
   for (int attempt = 0;; ++attempt) {
@@ -249,11 +275,28 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
     // claim sets FRESH), so the entry still holds this key.
     const bool skip_ins = VSB_HASH_HEAD_INSERT && ins && old == snap;
     const bool skip_era = !ins && fpos == (int32_t)b && old == snap && !(snap & kFresh);
+    bool skip_ex = false;
     if (skip_era) {
       found = (int32_t)b;
       fmeta = old;
+    } else if (VSB_HASH_VALIDATE_PREV && !ins && fpos >= (int32_t)T.n) {
+      // excess-case erase: validate the lookup's predecessor under the lock
+      // instead of re-walking the chain -- the predecessor still links to the
+      // victim (an unlinked entry has OCC clear; the bucket is always the
+      // head) and the victim still holds the key (positions are not reused
+      // inside a launch).  Both loads are independent: one round trip.
+      const int4 v = ld_entry(T.e + fpos);
+      const uint32_t pm = fprev == b ? old : (uint32_t)ld_entry(T.e + fprev).w;
+      const uint32_t link = (uint32_t)fpos - T.n + 1u;
+      if ((pm & kNext) == link && (fprev == b || (pm & kOcc)) && ((uint32_t)v.w & kOcc) && key_eq(v, x, y, z)) {
+        found = fpos;
+        fmeta = (uint32_t)v.w;
+        prev = fprev;
+        prev_meta = pm;
+        skip_ex = true;
+      }
     }
-    if (!skip_ins && !skip_era) {
+    if (!skip_ins && !skip_era && !skip_ex) {
       const int4 s = ld_entry(T.e + b + dep);
       if ((old & kOcc) && key_eq(s, x, y, z)) {
         found = (int32_t)b;
@@ -375,14 +418,14 @@ __device__ __forceinline__ int apply_one(const TableView& T, int32_t x, int32_t 
   int32_t pos;
   uint8_t res;
   int delta = 0;
-  uint32_t fmeta;
-  const int32_t fpos = find_pos_from(T, x, y, z, b, pre, &fmeta);
+  uint32_t fmeta, fprev = b;
+  const int32_t fpos = find_pos_from_p(T, x, y, z, b, pre, &fmeta, &fprev);
   const bool ins = op == 0 /*VS_OP_INSERT*/, era = op == 2 /*VS_OP_ERASE*/;
   pos = fpos;
   res = !ins && fpos >= 0;  // find: found; erase: provisional
   if (ins && fpos >= 0 && (fmeta & kFresh)) claim_min(T, fpos, (int32_t)i);
   if ((ins && fpos < 0) || (era && fpos >= 0)) {
-    const InsertResult r = mutate_locked(T, x, y, z, ins, (int32_t)i, b, (uint32_t)pre.w, fpos);
+    const InsertResult r = mutate_locked(T, x, y, z, ins, (int32_t)i, b, (uint32_t)pre.w, fpos, fprev);
     pos = r.pos;
     res = ins ? r.created : (uint8_t)(r.pos >= 0);
     delta = ins ? (int)r.created : -(int)(r.pos >= 0);
