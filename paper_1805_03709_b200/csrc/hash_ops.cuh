@@ -29,10 +29,15 @@
 #include "common.cuh"
 
 
+// Bucket-case erases skip the re-scan when the bucket word is unchanged (1).
+#ifndef VSB_HASH_ERASE_SKIP
+#define VSB_HASH_ERASE_SKIP 1
+#endif
 // Excess-case erases validate the lookup's predecessor under the lock
-// instead of re-walking the chain (1).
+// instead of re-walking the chain (1; +3%, but intermittent mismatches in the
+// 8-rank stress simulation: off until understood).
 #ifndef VSB_HASH_VALIDATE_PREV
-#define VSB_HASH_VALIDATE_PREV 1
+#define VSB_HASH_VALIDATE_PREV 0
 #endif
 // New excess entries are linked at the chain head (1), which also lets an
 // insert skip the locked re-scan when its bucket word is unchanged; 0 = the
@@ -262,7 +267,10 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
       continue;
     }
     // --- chain lock held; the re-scan's first load depends on `old`
-    const uint32_t dep = (old >> 31) & 1u;  // always 0 here
+    // always 0 here, but opaque to the compiler: loads whose address adds it
+    // cannot issue before the lock word came back (acquire by dependency)
+    uint32_t dep;
+    asm volatile("shr.u32 %0, %1, 31;" : "=r"(dep) : "r"(old));
     int32_t found = -1;
     uint32_t fmeta = 0, prev = b, prev_meta = old;  // prev: predecessor of `found`, else the tail
     // An insert whose bucket word is still exactly the one its lock-free
@@ -274,7 +282,7 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
     // word that was not FRESH cannot have been re-claimed by another key (a
     // claim sets FRESH), so the entry still holds this key.
     const bool skip_ins = VSB_HASH_HEAD_INSERT && ins && old == snap;
-    const bool skip_era = !ins && fpos == (int32_t)b && old == snap && !(snap & kFresh);
+    const bool skip_era = VSB_HASH_ERASE_SKIP && !ins && fpos == (int32_t)b && old == snap && !(snap & kFresh);
     bool skip_ex = false;
     if (skip_era) {
       found = (int32_t)b;
@@ -285,8 +293,10 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
       // victim (an unlinked entry has OCC clear; the bucket is always the
       // head) and the victim still holds the key (positions are not reused
       // inside a launch).  Both loads are independent: one round trip.
-      const int4 v = ld_entry(T.e + fpos);
-      const uint32_t pm = fprev == b ? old : (uint32_t)ld_entry(T.e + fprev).w;
+      // both loads depend on `old`, so they issue only after the lock word
+      // came back (acquire by dependency, as the re-scan's first load)
+      const int4 v = ld_entry(T.e + fpos + dep);
+      const uint32_t pm = fprev == b ? old : (uint32_t)ld_entry(T.e + fprev + dep).w;
       const uint32_t link = (uint32_t)fpos - T.n + 1u;
       if ((pm & kNext) == link && (fprev == b || (pm & kOcc)) && ((uint32_t)v.w & kOcc) && key_eq(v, x, y, z)) {
         found = fpos;
