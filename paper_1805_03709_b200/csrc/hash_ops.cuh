@@ -34,8 +34,8 @@
 #define VSB_HASH_ERASE_SKIP 1
 #endif
 // Excess-case erases validate the lookup's predecessor under the lock
-// instead of re-walking the chain (1; +3%, but intermittent mismatches in the
-// 8-rank stress simulation: off until understood).
+// instead of re-walking the chain (1; needs a release unlock on the head
+// relink, which costs what it saves: off).
 #ifndef VSB_HASH_VALIDATE_PREV
 #define VSB_HASH_VALIDATE_PREV 0
 #endif
@@ -379,7 +379,15 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
     st_relaxed_u32(&T.e[found].meta, fmeta & ~(kOcc | kFresh));
     const uint32_t vnext = fmeta & kNext;
     if (prev == b) {
-      atom_exch_relaxed(bmeta, (old & ~kNext) | vnext);  // relink + unlock, one word
+      // relink + unlock, one word.  With predecessor validation the unlock
+      // must be a release: the next holder of this lock validates through
+      // the victim's and predecessor's OCC bits, so the OCC clear above has
+      // to be visible before the chain change (a relaxed unlock let a later
+      // erase see the unlinked victim still occupied and relink it again).
+      if (VSB_HASH_VALIDATE_PREV)
+        atom_exch_release(bmeta, (old & ~kNext) | vnext);
+      else
+        atom_exch_relaxed(bmeta, (old & ~kNext) | vnext);
     } else {
       st_relaxed_u32(&T.e[prev].meta, (prev_meta & ~kNext) | vnext);
       atom_exch_release(bmeta, old);  // unlock only after the relink
