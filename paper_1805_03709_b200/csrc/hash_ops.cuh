@@ -42,6 +42,9 @@
 // New excess entries are linked at the chain head (1), which also lets an
 // insert skip the locked re-scan when its bucket word is unchanged; 0 = the
 // reference's tail append with a re-scan under every lock.
+#ifndef VSB_HASH_ST_UNLOCK
+#define VSB_HASH_ST_UNLOCK 1
+#endif
 #ifndef VSB_HASH_HEAD_INSERT
 #define VSB_HASH_HEAD_INSERT 1
 #endif
@@ -66,6 +69,27 @@ __device__ __forceinline__ uint32_t atom_exch_relaxed(uint32_t* p, uint32_t v) {
 
 __device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Bucket unlock (the holder writes the whole word back).  A plain strong
+// store suffices: while the lock is held no one else changes the word (a
+// competing locker's OR of an already-set LOCK bit writes it unchanged, and
+// L2 serialises it against the store), and the store carries the release
+// ordering the link needs.  VSB_HASH_ST_UNLOCK=0 keeps exchange atomics (-1%).
+__device__ __forceinline__ void unlock_release(uint32_t* p, uint32_t v) {
+#if VSB_HASH_ST_UNLOCK
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#else
+  atom_exch_release(p, v);
+#endif
+}
+
+__device__ __forceinline__ void unlock_relaxed(uint32_t* p, uint32_t v) {
+#if VSB_HASH_ST_UNLOCK
+  st_relaxed_u32(p, v);
+#else
+  atom_exch_relaxed(p, v);
+#endif
 }
 
 // Pop one excess entry (FreeListStack.pop, concurrent_hash.py:75-79) from the
@@ -329,7 +353,7 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
     }
     if (ins) {
       if (found >= 0) {  // inserted by another op since the lookup
-        atom_exch_relaxed(bmeta, old);
+        unlock_relaxed(bmeta, old);
         if (fmeta & kFresh) claim_min(T, found, op);
         return {found, 0};
       }
@@ -341,7 +365,7 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
       }
       const int64_t ne = pop_free(T);
       if (ne < 0) {
-        atom_exch_relaxed(bmeta, old);
+        unlock_relaxed(bmeta, old);
         atomicOr(&T.ctl->error, 1u);
         return {-1, 0};
       }
@@ -354,25 +378,25 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
       // lock-free readers see either the old chain or the new one)
       (void)prev_meta;
       st_entry(T.e + e, x, y, z, kOcc | kFresh | (old & kNext));
-      atom_exch_release(bmeta, (old & ~kNext) | link);
+      unlock_release(bmeta, (old & ~kNext) | link);
 #else
       st_entry(T.e + e, x, y, z, kOcc | kFresh);  // NEXT = 0 clears the stale offset (:200)
       if (prev == b) {
-        atom_exch_release(bmeta, (old & ~kNext) | link);  // publish + unlock
+        unlock_release(bmeta, (old & ~kNext) | link);  // publish + unlock
       } else {
         st_release_u32(&T.e[prev].meta, (prev_meta & ~kNext) | link);  // publish last (:204)
-        atom_exch_release(bmeta, old);                                  // unlock after the link
+        unlock_release(bmeta, old);                                  // unlock after the link
       }
 #endif
       return {(int32_t)e, 1};
     }
     if (found < 0) {  // erased by another op since the lookup
-      atom_exch_relaxed(bmeta, old);
+      unlock_relaxed(bmeta, old);
       return {-1, 0};
     }
     if (found == (int32_t)b) {
       // bucket case: clear occupancy only; NEXT and the chain stay (:266-275)
-      atom_exch_relaxed(bmeta, old & ~(kOcc | kFresh));
+      unlock_relaxed(bmeta, old & ~(kOcc | kFresh));
       return {found, 0};
     }
     // excess case: clear the victim but keep its stale NEXT (:280-289)
@@ -385,12 +409,12 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
       // to be visible before the chain change (a relaxed unlock let a later
       // erase see the unlinked victim still occupied and relink it again).
       if (VSB_HASH_VALIDATE_PREV)
-        atom_exch_release(bmeta, (old & ~kNext) | vnext);
+        unlock_release(bmeta, (old & ~kNext) | vnext);
       else
-        atom_exch_relaxed(bmeta, (old & ~kNext) | vnext);
+        unlock_relaxed(bmeta, (old & ~kNext) | vnext);
     } else {
       st_relaxed_u32(&T.e[prev].meta, (prev_meta & ~kNext) | vnext);
-      atom_exch_release(bmeta, old);  // unlock only after the relink
+      unlock_release(bmeta, old);  // unlock only after the relink
     }
     return {found, 0};
   }
