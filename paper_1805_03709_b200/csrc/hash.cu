@@ -9,6 +9,9 @@
 //                       striped free list (FreeListStack.push,
 //                       concurrent_hash.py:72-73), in one pass, so the op
 //                       kernel itself needs no atomics for either.
+#ifndef VSB_PDL
+#define VSB_PDL 1
+#endif
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -319,6 +322,11 @@ constexpr int kPostBlock = 256;
 __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t* __restrict__ keys,
                                                      const uint8_t* __restrict__ ops, uint64_t n,
                                                      uint8_t* __restrict__ result, const int32_t* __restrict__ index) {
+#if VSB_PDL
+  // launched as a programmatic dependent of the op kernel: everything below
+  // reads its results, so wait for its grid to complete and flush
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   const uint64_t base = (uint64_t)blockIdx.x * (kPostBlock * kPostOps) + threadIdx.x;
   uint8_t op[kPostOps], res[kPostOps];
   int32_t pos[kPostOps];
@@ -344,6 +352,22 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
     }
   }
   push_free_many<kPostOps>(T, vac, nv);
+}
+
+// k_post as a programmatic dependent launch (VSB_PDL): its launch and CTA
+// setup overlap the op kernel's tail instead of following its completion.
+static cudaError_t launch_post(const TableView& v, const int32_t* keys, const uint8_t* ops, uint64_t n,
+                               uint8_t* result, const int32_t* index, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid_for(n, kPostBlock * kPostOps));
+  cfg.blockDim = dim3(kPostBlock);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = VSB_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_post, v, keys, ops, n, result, index);
 }
 
 // Push vacated excess positions back onto the striped free list (warp-
@@ -766,7 +790,7 @@ static vs_status table_insert(vs_table* t, const int32_t* keys, uint64_t n, cons
     ProfScope prof(0, s);
     { k_insert<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, n_dev, created, index); vsb::count_launch(); }
   }
-  { k_post<<<grid_for(n, kPostBlock * kPostOps), kPostBlock, 0, s>>>(v, keys, nullptr, n, created, index); vsb::count_launch(); }
+  { VS_CK(launch_post(v, keys, nullptr, n, created, index, s)); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_insert");
   return VS_OK;
 }
@@ -842,7 +866,7 @@ vs_status vs_table_apply(vs_table* t, const int32_t* keys, const uint8_t* ops, u
     ProfScope prof(0, s);
     { VS_CK(launch_apply(v, keys, ops, n, result, index, s)); vsb::count_launch(); }
   }
-  { k_post<<<grid_for(n, kPostBlock * kPostOps), kPostBlock, 0, s>>>(v, keys, ops, n, result, index); vsb::count_launch(); }
+  { VS_CK(launch_post(v, keys, ops, n, result, index, s)); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_table_apply");
   return VS_OK;
 }
