@@ -364,7 +364,8 @@ static cudaError_t launch_post(const TableView& v, const int32_t* keys, const ui
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = VSB_PDL;
+  // small batches (server-side scratch sets) gain nothing from the overlap
+  attr[0].val.programmaticStreamSerializationAllowed = VSB_PDL && n >= (1u << 16);
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_post, v, keys, ops, n, result, index);
