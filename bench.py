@@ -503,23 +503,23 @@ def run_stream(args, dev):
     gen = torch.Generator(device=dev)
     gen.manual_seed(44)
     aff = torch.empty((8 * U, 3), dtype=torch.int32, device=dev)
-    n_aff = torch.empty(1, dtype=torch.int64, device=dev)
     lib = _lib.load()
     ops = {"insert": 0, "remove": 0}
-
-    done_removes = torch.zeros(1, dtype=torch.int64, device=dev)
-    done_inserts = torch.zeros(1, dtype=torch.int64, device=dev)  # affected keys per tick (x C below)
+    ticks = max(args.stream_ticks, 20)
+    # device-side per-tick counts (summed once after the timed region):
+    # affected keys per tick (x C below) and keys extracted per client
+    aff_log = torch.zeros((ticks + 1, 1), dtype=torch.int64, device=dev)
+    ex_log = torch.zeros((ticks + 1, C), dtype=torch.int64, device=dev)
 
     def tick(t):
         upd = keys[torch.randint(0, M, (U,), generator=gen, device=dev)]
         st = torch.cuda.current_stream(dev)
+        n_aff = aff_log[t]
         _lib.check(lib.vs_affected_dedup(scratch.handle, _lib.ptr(upd), U, _lib.ptr(aff), _lib.ptr(n_aff),
                                          ctypes.c_void_p(st.cuda_stream)))
         # no host sync: the fan-out takes the device-side affected count
         fan_out(clients, aff, sync=False, n_dev=n_aff)
-        done_inserts.add_(n_aff)
-        _, n_ex = extract_random_many(clients, X)  # one launch for all 16 clients
-        done_removes.add_(n_ex.sum())
+        extract_random_many(clients, X, n_out=ex_log[t])  # one launch for all 16 clients
         if t % 20 == 19:
             victim = clients[(t // 20) % C]
             victim.clear()
@@ -540,9 +540,6 @@ def run_stream(args, dev):
     tick(0)
     torch.cuda.synchronize()
     ops["insert"] = ops["remove"] = 0
-    done_removes.zero_()
-    done_inserts.zero_()
-    ticks = max(args.stream_ticks, 20)
     torch.cuda.synchronize()
     clocks = Clocks(dev.index).start()
     time.sleep(0.12)
@@ -557,8 +554,8 @@ def run_stream(args, dev):
     wall = time.perf_counter() - t0
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
-    ops["remove"] += int(done_removes.item())
-    ops["insert"] += C * int(done_inserts.item())
+    ops["remove"] += int(ex_log[1:].sum().item())
+    ops["insert"] += C * int(aff_log[1:].sum().item())
     total = ops["insert"] + ops["remove"]
     ok = ok and all(0 <= c.size() <= M for c in clients)
     return {"workload": "config 4: 16 clients x 2,080,160-block scene; per tick 512 updated TSDF keys -> "

@@ -143,6 +143,7 @@ class _HashCore:
         self._values: Optional[list[Any]] = [None] * self.capacity if store_values else None
         self._mutex = threading.RLock()
         self._last_stream = None
+        self._last_sid = None  # raw handle of _last_stream (cheap comparisons)
         self._n_dev = torch.empty(1, dtype=torch.int64, device=self.device)
 
     # -- lifetime ----------------------------------------------------------
@@ -167,15 +168,15 @@ class _HashCore:
 
     def _stream(self):
         s = self._torch.cuda.current_stream(self.device)
-        last = self._last_stream
-        if last is not None and last != s:
+        if self._last_sid is not None and self._last_sid != s.cuda_stream:
             ev = self._torch.cuda.Event()
-            ev.record(last)
+            ev.record(self._last_stream)
             s.wait_event(ev)
         return s
 
     def _done(self, s) -> None:
         self._last_stream = s
+        self._last_sid = s.cuda_stream
 
     def _keys(self, keys):
         return _as_keys(keys, self.device)

@@ -279,6 +279,105 @@ __global__ void k_expand_affected(const int32_t* __restrict__ updated, uint64_t 
   out[3 * j + 2] = updated[3 * i + 2] - (d & 1);
 }
 
+// Small batches (the per-tick case: u <= 1024 updated keys, m = 8u <= 8192
+// affected keys) are deduplicated by ONE CTA in shared memory: the expanded
+// keys, then an open-addressing table of key indices where each slot keeps
+// the LOWEST index of its key (CAS to claim, atomicMin on a key match), then
+// a block scan of the first-occurrence flags in input order.  One launch and
+// no scratch allocations instead of the table path's ~20 API calls.
+constexpr int kDedupThreads = 1024;
+constexpr int kDedupPer = 8;                                 // keys per thread
+constexpr uint32_t kDedupMax = kDedupThreads * kDedupPer;    // 8192 keys
+constexpr uint32_t kDedupSlots = 2 * kDedupMax;              // load <= 0.5
+constexpr size_t kDedupSmem = 12 * (size_t)kDedupMax + 4 * (size_t)kDedupSlots;
+
+__global__ void __launch_bounds__(kDedupThreads) k_dedup_small(const int32_t* __restrict__ updated, uint32_t u,
+                                                               int32_t* __restrict__ out, uint64_t* __restrict__ n_dev) {
+  extern __shared__ int32_t dsm[];
+  int32_t* kx = dsm;                                   // [kDedupMax] x, then y, then z
+  int32_t* ky = kx + kDedupMax;
+  int32_t* kz = ky + kDedupMax;
+  uint32_t* slot = (uint32_t*)(kz + kDedupMax);        // [kDedupSlots] lowest key index or ~0
+  __shared__ uint32_t wsum[kDedupThreads / 32];
+  const uint32_t m = 8 * u, t = threadIdx.x;
+  for (uint32_t i = t; i < kDedupSlots; i += kDedupThreads) slot[i] = 0xFFFFFFFFu;
+  // contiguous ownership: thread t holds keys [t*8, t*8+8), so the scan below
+  // runs in input order; expansion order = affected_mc_blocks (dx slowest)
+  int32_t x[kDedupPer], y[kDedupPer], z[kDedupPer];
+  uint32_t where[kDedupPer];
+#pragma unroll
+  for (int k = 0; k < kDedupPer; ++k) {
+    const uint32_t j = t * kDedupPer + k;
+    if (j < m) {
+      const uint32_t i = j >> 3, d = j & 7;
+      x[k] = updated[3 * i] - (int32_t)((d >> 2) & 1);
+      y[k] = updated[3 * i + 1] - (int32_t)((d >> 1) & 1);
+      z[k] = updated[3 * i + 2] - (int32_t)(d & 1);
+      kx[j] = x[k];
+      ky[j] = y[k];
+      kz[j] = z[k];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kDedupPer; ++k) {
+    const uint32_t j = t * kDedupPer + k;
+    if (j >= m) continue;
+    uint32_t h = hash_raw(x[k], y[k], z[k]) & (kDedupSlots - 1);
+    for (;;) {
+      const uint32_t old = atomicCAS(&slot[h], 0xFFFFFFFFu, j);
+      if (old == 0xFFFFFFFFu) break;
+      if (kx[old] == x[k] && ky[old] == y[k] && kz[old] == z[k]) {
+        atomicMin(&slot[h], j);
+        break;
+      }
+      h = (h + 1) & (kDedupSlots - 1);
+    }
+    where[k] = h;
+  }
+  __syncthreads();
+  uint32_t first = 0, cnt = 0;
+#pragma unroll
+  for (int k = 0; k < kDedupPer; ++k) {
+    const uint32_t j = t * kDedupPer + k;
+    if (j < m && slot[where[k]] == j) {
+      first |= 1u << k;
+      ++cnt;
+    }
+  }
+  // block-wide exclusive scan of the per-thread counts
+  const uint32_t lane = t & 31, warp = t >> 5;
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= (uint32_t)o) w += v;
+    }
+    wsum[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  uint32_t o = incl - cnt + (warp ? wsum[warp - 1] : 0u);
+#pragma unroll
+  for (int k = 0; k < kDedupPer; ++k) {
+    if (first & (1u << k)) {
+      out[3 * o] = x[k];
+      out[3 * o + 1] = y[k];
+      out[3 * o + 2] = z[k];
+      ++o;
+    }
+  }
+  if (t == kDedupThreads - 1) *n_dev = wsum[31];
+}
+
 __global__ void k_scatter_flagged(const int32_t* __restrict__ keys, uint64_t n, const uint8_t* __restrict__ flag,
                                   const uint64_t* __restrict__ off, int32_t* __restrict__ out) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -353,6 +452,17 @@ vs_status vs_affected_dedup(vs_table* scratch, const int32_t* updated, uint64_t 
     return VS_OK;
   }
   const uint64_t m = 8 * u;
+  if (m <= kDedupMax) {
+    static bool attr_set[64] = {};  // the opt-in is per device
+    const int d = scratch->device;
+    if (d < 0 || d >= 64 || !attr_set[d]) {
+      VS_CK(cudaFuncSetAttribute(k_dedup_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDedupSmem));
+      if (d >= 0 && d < 64) attr_set[d] = true;
+    }
+    { k_dedup_small<<<1, kDedupThreads, kDedupSmem, s>>>(updated, (uint32_t)u, out_keys, n_dev); vsb::count_launch(); }
+    VS_CK_LAUNCH("vs_affected_dedup");
+    return VS_OK;
+  }
   int32_t* all = nullptr;
   uint8_t* created = nullptr;
   int32_t* index = nullptr;
@@ -411,11 +521,13 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
     return VS_ERR_INVALID;
   }
   const uint64_t total = (uint64_t)n_sets * n;
-  int32_t* index = nullptr;
-  uint64_t *off = nullptr, *work = nullptr;
-  VS_CK(cudaMallocAsync((void**)&index, 4 * total, s));
-  VS_CK(cudaMallocAsync((void**)&off, 8 * (total + 1), s));
-  VS_CK(cudaMallocAsync((void**)&work, 8 * (scan_tiles(total) + 1), s));
+  // one stream-ordered allocation carved into the three scratch arrays
+  const size_t b_index = (4 * total + 255) & ~(size_t)255, b_off = (8 * (total + 1) + 255) & ~(size_t)255;
+  char* scratch_mem = nullptr;
+  VS_CK(cudaMallocAsync((void**)&scratch_mem, b_index + b_off + 8 * (scan_tiles(total) + 1), s));
+  int32_t* index = (int32_t*)scratch_mem;
+  uint64_t* off = (uint64_t*)(scratch_mem + b_index);
+  uint64_t* work = (uint64_t*)(scratch_mem + b_index + b_off);
   const dim3 grid(grid_for(n, 256), n_sets);
   { ProfScope prof(2, s); k_multi_insert<<<grid, 256, 0, s>>>(V, keys, n, n_dev, created, index); vsb::count_launch(); }
   { k_multi_fixup<<<grid, 256, 0, s>>>(V, keys, n, created, index); vsb::count_launch(); }
@@ -431,9 +543,7 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
   }
   if (e == cudaSuccess && fifo) { k_fifo_append<<<grid, 256, 0, s>>>(F, keys, n, created, off); vsb::count_launch(); }
   if (e == cudaSuccess) { k_fifo_tail<<<1, 32, 0, s>>>(F, fifo, off, n, n_sets, n_created); vsb::count_launch(); }
-  cudaFreeAsync(index, s);
-  cudaFreeAsync(off, s);
-  cudaFreeAsync(work, s);
+  cudaFreeAsync(scratch_mem, s);
   if (e != cudaSuccess) return cuda_status(e, "vs_stream_insert_many");
   VS_CK_LAUNCH("vs_stream_insert_many");
   return VS_OK;

@@ -82,6 +82,7 @@ class StreamSet:
         fifo = torch.empty((cap, 3), dtype=torch.int32, device=self.device)
         fifo[: live.shape[0]] = live
         self._fifo = fifo
+        _FIFO_GEN[0] += 1
         self._tail_dev.fill_(tail - self._head)
         self._tail_bound = tail - self._head
         self._head = 0
@@ -163,18 +164,51 @@ def _order_streams(tables):
     """Current stream, ordered after the last launch on every table."""
     torch = tables[0]._torch
     s = torch.cuda.current_stream(tables[0].device)
+    sid = s.cuda_stream
     for t in tables:
-        last = t._last_stream
-        if last is not None and last != s:
+        if t._last_sid is not None and t._last_sid != sid:
             ev = torch.cuda.Event()
-            ev.record(last)
+            ev.record(t._last_stream)
             s.wait_event(ev)
     return s
 
 
 def _mark_done(tables, s) -> None:
+    sid = s.cuda_stream
     for t in tables:
         t._last_stream = s
+        t._last_sid = sid
+
+
+# ctypes argument arrays of a client group, reused while the group's sets and
+# FIFO rings are unchanged (a tick calls fan_out / extract on the same 16
+# clients every time; rebuilding the arrays was a third of the host cost).
+# Entries hold weak references, so a dead set never matches a new one.
+_GROUP_CACHE: dict = {}
+_FIFO_GEN = [0]  # bumped whenever a FIFO ring is reallocated
+
+
+def _group_args(group):
+    import weakref
+
+    key = (tuple(map(id, group)), _FIFO_GEN[0])
+    hit = _GROUP_CACHE.get(key)
+    if hit is not None and all(r() is st for r, st in zip(hit[0], group)):
+        return hit[1]
+    C = len(group)
+    tables = [st._set if isinstance(st, StreamSet) else st for st in group]
+    args = {
+        "tables": tables,
+        "handles": (ctypes.c_void_p * C)(*[t.handle.value for t in tables]),
+    }
+    if all(isinstance(st, StreamSet) for st in group):
+        args["fifos"] = (ctypes.c_void_p * C)(*[st._fifo.data_ptr() for st in group])
+        args["caps"] = (ctypes.c_uint64 * C)(*[st.fifo_capacity for st in group])
+        args["tails"] = (ctypes.c_void_p * C)(*[st._tail_dev.data_ptr() for st in group])
+    if len(_GROUP_CACHE) >= 16:
+        _GROUP_CACHE.clear()
+    _GROUP_CACHE[key] = ([weakref.ref(st) for st in group], args)
+    return args
 
 
 def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True, n_dev=None):
@@ -200,18 +234,17 @@ def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True, n_dev=None):
     counts = torch.empty(len(sets), dtype=torch.int64, device=dev)
     created = torch.empty(min(len(sets), _MAX_SETS_PER_LAUNCH) * n, dtype=torch.uint8, device=dev)
     for g0 in range(0, len(sets), _MAX_SETS_PER_LAUNCH):
-        group = list(sets[g0:g0 + _MAX_SETS_PER_LAUNCH])
+        group = sets[g0:g0 + _MAX_SETS_PER_LAUNCH]
         C = len(group)
         for st in group:
-            st._ensure_fifo(n)
-        tables = [st._set for st in group]
-        handles = (ctypes.c_void_p * C)(*[t.handle.value for t in tables])
-        fifos = (ctypes.c_void_p * C)(*[st._fifo.data_ptr() for st in group])
-        caps = (ctypes.c_uint64 * C)(*[st.fifo_capacity for st in group])
-        tails = (ctypes.c_void_p * C)(*[st._tail_dev.data_ptr() for st in group])
+            if st._tail_bound + n - st._head > st._fifo.shape[0]:
+                st._ensure_fifo(n)
+        a = _group_args(group)
+        tables = a["tables"]
         s = _order_streams(tables)
-        check(lib.vs_stream_insert_many(handles, C, ptr(k), n, ptr(n_dev), ptr(created), fifos, caps, tails,
-                                        ptr(counts[g0:g0 + C]), ctypes.c_void_p(s.cuda_stream)), "fan_out")
+        check(lib.vs_stream_insert_many(a["handles"], C, ptr(k), n, ptr(n_dev), ptr(created), a["fifos"], a["caps"],
+                                        a["tails"], ptr(counts[g0:g0 + C]), ctypes.c_void_p(s.cuda_stream)),
+              "fan_out")
         _mark_done(tables, s)
         for st in group:
             st._tail_bound += n
@@ -220,27 +253,31 @@ def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True, n_dev=None):
     return [int(c) for c in counts.cpu().tolist()]
 
 
-def extract_random_many(sets: Sequence[StreamSet], max_n: int, seeds: Optional[Sequence[int]] = None):
+def extract_random_many(sets: Sequence[StreamSet], max_n: int, seeds: Optional[Sequence[int]] = None, *,
+                        n_out=None):
     """``[s.extract_random(max_n) for s in sets]`` in one launch per 32
-    clients.  Returns (keys int32[C, max_n, 3], n int64[C]) device tensors."""
+    clients.  Returns (keys int32[C, max_n, 3], n int64[C]) device tensors;
+    ``n_out`` (optional device int64[C]) receives the counts instead of a
+    new tensor."""
     import random
 
     torch = sets[0]._torch
     dev = sets[0].device
     C = len(sets)
     keys = torch.empty((C, max(max_n, 1), 3), dtype=torch.int32, device=dev)
-    n = torch.zeros(C, dtype=torch.int64, device=dev)
+    n = n_out if n_out is not None else torch.empty(C, dtype=torch.int64, device=dev)
     if max_n <= 0:
+        n.zero_()
         return keys[:, :0], n
     lib = _lib.load()
     for g0 in range(0, C, _MAX_SETS_PER_LAUNCH):
-        group = list(sets[g0:g0 + _MAX_SETS_PER_LAUNCH])
+        group = sets[g0:g0 + _MAX_SETS_PER_LAUNCH]
         G = len(group)
-        tables = [st._set if isinstance(st, StreamSet) else st for st in group]
-        handles = (ctypes.c_void_p * G)(*[t.handle.value for t in tables])
-        sd = (ctypes.c_uint64 * G)(*[(seeds[g0 + i] if seeds else random.getrandbits(64)) for i in range(G)])
+        a = _group_args(group)
+        tables = a["tables"]
+        sd = (ctypes.c_uint64 * G)(*(seeds[g0:g0 + G] if seeds else [random.getrandbits(64) for _ in range(G)]))
         s = _order_streams(tables)
-        check(lib.vs_stream_extract_random(handles, G, max_n, sd, ptr(keys[g0:g0 + G]), ptr(n[g0:g0 + G]),
+        check(lib.vs_stream_extract_random(a["handles"], G, max_n, sd, ptr(keys[g0:g0 + G]), ptr(n[g0:g0 + G]),
                                            ctypes.c_void_p(s.cuda_stream)), "extract_random_many")
         _mark_done(tables, s)
     return keys, n

@@ -117,23 +117,25 @@ def test_fan_out_device_count_bound(dev):
             assert set(x.snapshot()) == set(y.snapshot())
 
 
-def test_affected_dedup_order(dev):
-    import ctypes
-
+@pytest.mark.parametrize("u,span", [(700, 5), (1, 5), (1024, 5), (1024, 1000), (1025, 5), (3000, 40)])
+def test_affected_dedup_order(dev, u, span):
+    """u <= 1024 runs the one-CTA shared-memory dedup, larger batches the
+    scratch-table path; both must give the first-occurrence order."""
     import torch
 
     from paper_1805_03709_b200 import BlockHashSet, _lib
 
-    rng = np.random.default_rng(9)
-    upd = rng.integers(-5, 5, (700, 3)).astype(np.int32)
+    rng = np.random.default_rng(9 + u)
+    upd = rng.integers(-span, span, (u, 3)).astype(np.int32)
     scratch = BlockHashSet(1 << 14, 1 << 14)
-    out = torch.empty((8 * 700, 3), dtype=torch.int32, device=dev)
+    out = torch.empty((8 * u, 3), dtype=torch.int32, device=dev)
     n = torch.empty(1, dtype=torch.int64, device=dev)
     k = torch.from_numpy(upd).to(dev)
-    _lib.check(_lib.load().vs_affected_dedup(scratch.handle, _lib.ptr(k), 700, _lib.ptr(out), _lib.ptr(n),
-                                             _lib.stream_of(dev)))
-    got = [tuple(r) for r in out[: int(n.item())].cpu().tolist()]
-    assert got == oracle.affected_dedup(upd.tolist())
+    for _ in range(2):  # the scratch path must also work on a reused scratch set
+        _lib.check(_lib.load().vs_affected_dedup(scratch.handle, _lib.ptr(k), u, _lib.ptr(out), _lib.ptr(n),
+                                                 _lib.stream_of(dev)))
+        got = [tuple(r) for r in out[: int(n.item())].cpu().tolist()]
+        assert got == oracle.affected_dedup(upd.tolist())
 
 
 def test_server_core_replays_reference_server(dev, golden):
