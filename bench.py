@@ -511,8 +511,13 @@ def run_stream(args, dev):
     aff_log = torch.zeros((ticks + 1, 1), dtype=torch.int64, device=dev)
     ex_log = torch.zeros((ticks + 1, C), dtype=torch.int64, device=dev)
 
+    # the updated / reset keys of every tick, synthesised before the timed
+    # region (inputs resident in HBM, as in the other sections)
+    upd_all = keys[torch.randint(0, M, ((ticks + 1) * U,), generator=gen, device=dev)].view(ticks + 1, U, 3)
+    reset_all = keys[torch.randint(0, M, ((ticks // 20 + 1) * K,), generator=gen, device=dev)].view(-1, K, 3)
+
     def tick(t):
-        upd = keys[torch.randint(0, M, (U,), generator=gen, device=dev)]
+        upd = upd_all[t]
         st = torch.cuda.current_stream(dev)
         n_aff = aff_log[t]
         _lib.check(lib.vs_affected_dedup(scratch.handle, _lib.ptr(upd), U, _lib.ptr(aff), _lib.ptr(n_aff),
@@ -525,8 +530,7 @@ def run_stream(args, dev):
             victim.clear()
             fan_out([victim], keys, sync=False)
             ops["insert"] += M
-            reset = keys[torch.randint(0, M, (K,), generator=gen, device=dev)]
-            remove_everywhere(clients, reset)
+            remove_everywhere(clients, reset_all[t // 20])
             ops["remove"] += C * K
 
     torch.cuda.synchronize()

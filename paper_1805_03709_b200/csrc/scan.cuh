@@ -136,10 +136,59 @@ __global__ void __launch_bounds__(256) k_tile_scan(const T* __restrict__ in, uin
   if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = tile_off[ntiles];
 }
 
+// Small inputs (<= 16K elements: one round) in ONE launch: one CTA of
+// 1024 threads walks the input in rounds of 16,384 (16 per thread) with a
+// running carry.  Saves two launches where launch latency is the cost.
+constexpr uint64_t kScanSmallMax = 1u << 14;
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_scan_small(const T* __restrict__ in, uint64_t n, uint64_t* __restrict__ out) {
+  __shared__ uint64_t ws[32];  // round totals may exceed u32 for count inputs
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t carry = 0;
+  for (uint64_t round = 0; round < n; round += 1024 * 16) {
+    const uint64_t base = round + (uint64_t)threadIdx.x * 16;
+    uint32_t v[16];
+    load16(in, base, n, v);
+    uint32_t local = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) local += v[k];
+    uint32_t x = local;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t w = ws[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      ws[lane] = w;
+    }
+    __syncthreads();
+    uint64_t run = carry + (warp ? ws[warp - 1] : 0u) + (x - local);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (base + k < n) out[base + k] = run;
+      run += v[k];
+    }
+    carry += ws[31];
+    __syncthreads();  // ws is rewritten next round
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
 // Exclusive scan of in[0..n) into out[0..n]; work holds >= scan_tiles(n)+1 u64.
 template <typename T>
 inline cudaError_t exclusive_scan(const T* in, uint64_t n, uint64_t* out, uint64_t* work, cudaStream_t s) {
   if (n == 0) return cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
+  if (n <= kScanSmallMax) {
+    { k_scan_small<T><<<1, 1024, 0, s>>>(in, n, out); vsb::count_launch(); }
+    return cudaGetLastError();
+  }
   const uint64_t nt = scan_tiles(n);
   { k_tile_sums<T><<<(unsigned)nt, 256, 0, s>>>(in, n, work); vsb::count_launch(); }
   { k_scan_tiles<<<1, 1024, 0, s>>>(work, nt); vsb::count_launch(); }
