@@ -24,6 +24,10 @@
 #include "scan.cuh"
 #include "table.h"
 
+#ifndef VSB_DEDUP_MIX
+#define VSB_DEDUP_MIX 1
+#endif
+
 namespace vsb {
 
 constexpr int kMaxSets = 32;
@@ -323,7 +327,17 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup_small(const int32_t* __
   for (int k = 0; k < kDedupPer; ++k) {
     const uint32_t j = t * kDedupPer + k;
     if (j >= m) continue;
-    uint32_t h = hash_raw(x[k], y[k], z[k]) & (kDedupSlots - 1);
+    uint32_t h = hash_raw(x[k], y[k], z[k]);
+#if VSB_DEDUP_MIX
+    // neighbouring keys share low hash bits; mix before masking so linear
+    // probing does not cluster (murmur3 finaliser)
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+#endif
+    h &= kDedupSlots - 1;
     for (;;) {
       const uint32_t old = atomicCAS(&slot[h], 0xFFFFFFFFu, j);
       if (old == 0xFFFFFFFFu) break;
