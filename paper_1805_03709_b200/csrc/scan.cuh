@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "pdl.cuh"
+
 namespace vsb {
 
 void count_launch();  // defined in hash.cu
@@ -42,6 +44,7 @@ __device__ __forceinline__ void load16(const T* __restrict__ in, uint64_t base, 
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_tile_sums(const T* __restrict__ in, uint64_t n, uint64_t* __restrict__ sums) {
+  pdl_wait();
   uint32_t v[16];
   load16(in, (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * 16, n, v);
   uint64_t s = 0;
@@ -60,6 +63,7 @@ __global__ void __launch_bounds__(256) k_tile_sums(const T* __restrict__ in, uin
 
 // exclusive scan of the tile sums in place; sums[ntiles] = total
 static __global__ void __launch_bounds__(1024) k_scan_tiles(uint64_t* __restrict__ sums, uint64_t ntiles) {
+  pdl_wait();
   __shared__ uint64_t ws[32];
   __shared__ uint64_t carry_s;
   if (threadIdx.x == 0) carry_s = 0;
@@ -102,6 +106,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_tile_scan(const T* __restrict__ in, uint64_t n,
                                                    const uint64_t* __restrict__ tile_off, uint64_t ntiles,
                                                    uint64_t* __restrict__ out) {
+  pdl_wait();
   __shared__ uint32_t stage[256 * 17];
   __shared__ uint32_t ws[8];
   const uint64_t tile = (uint64_t)blockIdx.x * kScanTile;
@@ -143,6 +148,7 @@ constexpr uint64_t kScanSmallMax = 1u << 14;
 
 template <typename T>
 __global__ void __launch_bounds__(1024) k_scan_small(const T* __restrict__ in, uint64_t n, uint64_t* __restrict__ out) {
+  pdl_wait();
   __shared__ uint64_t ws[32];  // round totals may exceed u32 for count inputs
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t carry = 0;
@@ -186,13 +192,13 @@ template <typename T>
 inline cudaError_t exclusive_scan(const T* in, uint64_t n, uint64_t* out, uint64_t* work, cudaStream_t s) {
   if (n == 0) return cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
   if (n <= kScanSmallMax) {
-    { k_scan_small<T><<<1, 1024, 0, s>>>(in, n, out); vsb::count_launch(); }
+    { cudaError_t e = launch_pdl(k_scan_small<T>, 1, 1024, 0, s, in, n, out); vsb::count_launch(); if (e != cudaSuccess) return e; }
     return cudaGetLastError();
   }
   const uint64_t nt = scan_tiles(n);
-  { k_tile_sums<T><<<(unsigned)nt, 256, 0, s>>>(in, n, work); vsb::count_launch(); }
-  { k_scan_tiles<<<1, 1024, 0, s>>>(work, nt); vsb::count_launch(); }
-  { k_tile_scan<T><<<(unsigned)nt, 256, 0, s>>>(in, n, work, nt, out); vsb::count_launch(); }
+  { cudaError_t e = launch_pdl(k_tile_sums<T>, (unsigned)nt, 256, 0, s, in, n, work); vsb::count_launch(); if (e != cudaSuccess) return e; }
+  { cudaError_t e = launch_pdl(k_scan_tiles, 1, 1024, 0, s, work, nt); vsb::count_launch(); if (e != cudaSuccess) return e; }
+  { cudaError_t e = launch_pdl(k_tile_scan<T>, (unsigned)nt, 256, 0, s, in, n, (const uint64_t*)work, nt, out); vsb::count_launch(); if (e != cudaSuccess) return e; }
   return cudaGetLastError();
 }
 

@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include "hash_ops.cuh"
+#include "pdl.cuh"
 #include "scan.cuh"
 #include "table.h"
 
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(256) k_multi_insert(const __grid_constant__ Se
                                                       const int32_t* __restrict__ keys, uint64_t n,
                                                       const uint64_t* __restrict__ n_dev,
                                                       uint8_t* __restrict__ created, int32_t* __restrict__ index) {
+  pdl_wait();
   const int c = blockIdx.y;
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const TableView& T = V.v[c];
@@ -66,6 +68,7 @@ __global__ void __launch_bounds__(256) k_multi_insert(const __grid_constant__ Se
 
 __global__ void k_multi_fixup(const __grid_constant__ SetViews V, const int32_t* __restrict__ keys, uint64_t n,
                               uint8_t* __restrict__ created, const int32_t* __restrict__ index) {
+  pdl_wait();
   const int c = blockIdx.y;
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -74,6 +77,7 @@ __global__ void k_multi_fixup(const __grid_constant__ SetViews V, const int32_t*
 
 __global__ void k_fifo_append(const __grid_constant__ FifoViews F, const int32_t* __restrict__ keys, uint64_t n,
                               const uint8_t* __restrict__ created, const uint64_t* __restrict__ off) {
+  pdl_wait();
   const int c = blockIdx.y;
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -89,6 +93,7 @@ __global__ void k_fifo_append(const __grid_constant__ FifoViews F, const int32_t
 
 __global__ void k_fifo_tail(const __grid_constant__ FifoViews F, bool fifo, const uint64_t* __restrict__ off,
                             uint64_t n, int C, uint64_t* __restrict__ n_created) {
+  pdl_wait();
   const int c = threadIdx.x;
   if (c >= C) return;
   const uint64_t cnt = off[(uint64_t)(c + 1) * n] - off[(uint64_t)c * n];
@@ -154,6 +159,7 @@ __global__ void __cluster_dims__(kExtractCtas, 1, 1) __launch_bounds__(kExtractT
     k_multi_extract(const __grid_constant__ SetViews V, const __grid_constant__ FifoViews S,
                     const __grid_constant__ Frustum F, uint64_t max_n, int32_t* __restrict__ keys_out,
                     uint64_t* __restrict__ n_out) {
+  pdl_wait();
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int c = blockIdx.x / kExtractCtas;
@@ -297,6 +303,7 @@ constexpr size_t kDedupSmem = 12 * (size_t)kDedupMax + 4 * (size_t)kDedupSlots;
 
 __global__ void __launch_bounds__(kDedupThreads) k_dedup_small(const int32_t* __restrict__ updated, uint32_t u,
                                                                int32_t* __restrict__ out, uint64_t* __restrict__ n_dev) {
+  pdl_wait();
   extern __shared__ int32_t dsm[];
   int32_t* kx = dsm;                                   // [kDedupMax] x, then y, then z
   int32_t* ky = kx + kDedupMax;
@@ -473,7 +480,7 @@ vs_status vs_affected_dedup(vs_table* scratch, const int32_t* updated, uint64_t 
       VS_CK(cudaFuncSetAttribute(k_dedup_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDedupSmem));
       if (d >= 0 && d < 64) attr_set[d] = true;
     }
-    { k_dedup_small<<<1, kDedupThreads, kDedupSmem, s>>>(updated, (uint32_t)u, out_keys, n_dev); vsb::count_launch(); }
+    { VS_CK(launch_pdl(k_dedup_small, 1, kDedupThreads, kDedupSmem, s, updated, (uint32_t)u, out_keys, n_dev)); vsb::count_launch(); }
     VS_CK_LAUNCH("vs_affected_dedup");
     return VS_OK;
   }
@@ -543,8 +550,8 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
   uint64_t* off = (uint64_t*)(scratch_mem + b_index);
   uint64_t* work = (uint64_t*)(scratch_mem + b_index + b_off);
   const dim3 grid(grid_for(n, 256), n_sets);
-  { ProfScope prof(2, s); k_multi_insert<<<grid, 256, 0, s>>>(V, keys, n, n_dev, created, index); vsb::count_launch(); }
-  { k_multi_fixup<<<grid, 256, 0, s>>>(V, keys, n, created, index); vsb::count_launch(); }
+  { ProfScope prof(2, s); VS_CK(launch_pdl(k_multi_insert, grid, 256, 0, s, V, keys, n, n_dev, created, index)); vsb::count_launch(); }
+  { VS_CK(launch_pdl(k_multi_fixup, grid, 256, 0, s, V, keys, n, created, index)); vsb::count_launch(); }
   cudaError_t e = exclusive_scan<uint8_t>(created, total, off, work, s);
   const bool fifo = fifo_keys_host && fifo_cap_host && fifo_tail_host;
   FifoViews F{};
@@ -555,8 +562,8 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
       F.tail[c] = fifo_tail_host[c];
     }
   }
-  if (e == cudaSuccess && fifo) { k_fifo_append<<<grid, 256, 0, s>>>(F, keys, n, created, off); vsb::count_launch(); }
-  if (e == cudaSuccess) { k_fifo_tail<<<1, 32, 0, s>>>(F, fifo, off, n, n_sets, n_created); vsb::count_launch(); }
+  if (e == cudaSuccess && fifo) { e = launch_pdl(k_fifo_append, grid, 256, 0, s, F, keys, n, created, off); vsb::count_launch(); }
+  if (e == cudaSuccess) { e = launch_pdl(k_fifo_tail, 1, 32, 0, s, F, fifo, off, n, n_sets, n_created); vsb::count_launch(); }
   cudaFreeAsync(scratch_mem, s);
   if (e != cudaSuccess) return cuda_status(e, "vs_stream_insert_many");
   VS_CK_LAUNCH("vs_stream_insert_many");
@@ -576,7 +583,7 @@ static vs_status multi_extract(vs_table* const* sets_host, int n_sets, uint64_t 
   cudaStream_t s = (cudaStream_t)stream;
   FifoViews S{};
   for (int c = 0; c < n_sets; ++c) S.cap[c] = seeds_host[c];
-  { k_multi_extract<<<n_sets * kExtractCtas, kExtractThreads, 0, s>>>(V, S, F, max_n, keys_out, n_out); vsb::count_launch(); }
+  { VS_CK(launch_pdl(k_multi_extract, n_sets * kExtractCtas, kExtractThreads, 0, s, V, S, F, max_n, keys_out, n_out)); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_stream_extract");
   return VS_OK;
 }
