@@ -15,6 +15,7 @@
 #include <cstdint>
 
 #include "hash_ops.cuh"
+#include "pdl.cuh"
 #include "scan.cuh"
 #include "table.h"
 
@@ -73,6 +74,7 @@ constexpr int kCandStage = 256;  // >= 32 lanes x 8 emissions per step
 __global__ void __launch_bounds__(256) k_rc_candidates(const float* __restrict__ depth, const __grid_constant__ RcParams P,
                                                        int32_t ws, int32_t hs, int32_t* __restrict__ out,
                                                        unsigned long long* __restrict__ count, uint64_t cap) {
+  pdl_wait();
   // tile-major pixel order: warp w -> 8x4 tile, lane -> (lane & 7, lane >> 3)
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = (int)lane_id();
@@ -176,6 +178,7 @@ __global__ void __launch_bounds__(256) k_rc_candidates(const float* __restrict__
 // Zero the pool rows of newly created blocks (TsdfBlock(): all zero).
 __global__ void k_rc_zero_rows(const int32_t* __restrict__ pos, const uint8_t* __restrict__ created, uint64_t n,
                                uint4* __restrict__ pool) {
+  pdl_wait();
   // one candidate per lane; the whole warp zeroes each created row in turn
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -206,6 +209,7 @@ __device__ __forceinline__ bool rc_block_candidate(const RcParams& P, const floa
 
 __global__ void k_rc_cull(const int32_t* __restrict__ keys, uint64_t n, const float* __restrict__ depth,
                           const __grid_constant__ RcParams P, uint8_t* __restrict__ keep) {
+  pdl_wait();
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   keep[i] = rc_block_candidate(P, depth, keys[3 * i], keys[3 * i + 1], keys[3 * i + 2]);
@@ -216,6 +220,7 @@ __global__ void k_rc_cull(const int32_t* __restrict__ keys, uint64_t n, const fl
 __global__ void k_rc_cull_table(const Entry* __restrict__ e, uint32_t cap, const float* __restrict__ depth,
                                 const __grid_constant__ RcParams P, uint32_t* __restrict__ list,
                                 unsigned long long* __restrict__ n_list) {
+  pdl_wait();
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool keep = false;
   if (i < cap) {
@@ -233,6 +238,7 @@ __global__ void k_rc_cull_table(const Entry* __restrict__ e, uint32_t cap, const
 // touched slots -> their keys, ascending slot order
 __global__ void k_rc_touched_keys(const uint8_t* __restrict__ touched, const uint64_t* __restrict__ off, uint32_t cap,
                                   const Entry* __restrict__ e, int32_t* __restrict__ keys_out) {
+  pdl_wait();
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cap || !touched[i]) return;
   const int4 k = ld_entry_ro(e + i);
@@ -242,6 +248,7 @@ __global__ void k_rc_touched_keys(const uint8_t* __restrict__ touched, const uin
 
 __global__ void k_rc_gather(const uint8_t* __restrict__ keep, const uint64_t* __restrict__ off, uint64_t n,
                             uint32_t* __restrict__ list) {
+  pdl_wait();
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && keep[i]) list[off[i]] = (uint32_t)i;
 }
@@ -292,6 +299,7 @@ __global__ void __launch_bounds__(128) k_rc_integrate(const int32_t* __restrict_
                                                       const float* __restrict__ depth, const uint8_t* __restrict__ color,
                                                       const __grid_constant__ RcParams P, uint8_t* __restrict__ pool,
                                                       uint8_t* __restrict__ touched) {
+  pdl_wait();
   const uint64_t n_live = *n_list;
   const float fx = (float)P.fx, fy = (float)P.fy, cx = (float)P.cx, cy = (float)P.cy;
   const float mu = (float)P.mu, neg_mu = (float)(-P.mu), maxw = (float)P.max_weight;
@@ -390,7 +398,7 @@ vs_status vs_rc_candidates(const float* depth, const void* params_host, int32_t*
   const uint64_t tiles = (uint64_t)((ws + 7) / 8) * (uint64_t)((hs + 3) / 4);
   VS_CK(cudaMemsetAsync(n_dev, 0, 8, s));
   if (tiles == 0) return VS_OK;
-  { k_rc_candidates<<<grid_for(32 * tiles, 256), 256, 0, s>>>(depth, P, ws, hs, keys_out, (unsigned long long*)n_dev, cap); vsb::count_launch(); }
+  { VS_CK(launch_pdl(k_rc_candidates, grid_for(32 * tiles, 256), 256, 0, s, depth, P, ws, hs, keys_out, (unsigned long long*)n_dev, cap)); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_rc_candidates");
   return VS_OK;
 }
@@ -401,7 +409,7 @@ vs_status vs_rc_zero_rows(const int32_t* pos, const uint8_t* created, uint64_t n
     set_error("pos/created/pool must be non-NULL");
     return VS_ERR_INVALID;
   }
-  { k_rc_zero_rows<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(pos, created, n, (uint4*)pool); vsb::count_launch(); }
+  { VS_CK(launch_pdl(k_rc_zero_rows, grid_for(n, 256), 256, 0, (cudaStream_t)stream, pos, created, n, (uint4*)pool)); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_rc_zero_rows");
   return VS_OK;
 }
@@ -447,10 +455,10 @@ vs_status vs_rc_integrate(const int32_t* keys, const int32_t* pos, uint64_t n, c
   VS_CK(cudaMemsetAsync(touched, 0, n, s));
   {
     ProfScope prof(3, s);
-    { k_rc_cull<<<grid_for(n, 256), 256, 0, s>>>(keys, n, depth, P, keep); vsb::count_launch(); }
+    { VS_CK(launch_pdl(k_rc_cull, grid_for(n, 256), 256, 0, s, keys, n, depth, P, keep)); vsb::count_launch(); }
     VS_CK(exclusive_scan<uint8_t>(keep, n, off, work, s));
-    { k_rc_gather<<<grid_for(n, 256), 256, 0, s>>>(keep, off, n, list); vsb::count_launch(); }
-    { k_rc_integrate<<<integrate_grid(n), 128, 0, s>>>(keys, pos, nullptr, list, off + n, depth, color, P, pool, touched); vsb::count_launch(); }
+    { VS_CK(launch_pdl(k_rc_gather, grid_for(n, 256), 256, 0, s, keep, off, n, list)); vsb::count_launch(); }
+    { VS_CK(launch_pdl(k_rc_integrate, integrate_grid(n), 128, 0, s, keys, pos, nullptr, list, off + n, depth, color, P, pool, touched)); vsb::count_launch(); }
   }
   cudaFreeAsync(keep, s);
   cudaFreeAsync(off, s);
@@ -483,11 +491,11 @@ vs_status vs_rc_integrate_table(const vs_table* t, const float* depth, const uin
   {
     ProfScope prof(3, s);
     VS_CK(cudaMemsetAsync(off + n, 0, 8, s));
-    { k_rc_cull_table<<<grid_for(n, 256), 256, 0, s>>>(t->e, t->cap, depth, P, list, (unsigned long long*)(off + n)); vsb::count_launch(); }
-    { k_rc_integrate<<<integrate_grid(n), 128, 0, s>>>(nullptr, nullptr, t->e, list, off + n, depth, color, P, pool, touched); vsb::count_launch(); }
+    { VS_CK(launch_pdl(k_rc_cull_table, grid_for(n, 256), 256, 0, s, t->e, t->cap, depth, P, list, (unsigned long long*)(off + n))); vsb::count_launch(); }
+    { VS_CK(launch_pdl(k_rc_integrate, integrate_grid(n), 128, 0, s, nullptr, nullptr, t->e, list, off + n, depth, color, P, pool, touched)); vsb::count_launch(); }
   }
   VS_CK(exclusive_scan<uint8_t>(touched, n, off, work, s));
-  { k_rc_touched_keys<<<grid_for(n, 256), 256, 0, s>>>(touched, off, t->cap, t->e, touched_keys_out); vsb::count_launch(); }
+  { VS_CK(launch_pdl(k_rc_touched_keys, grid_for(n, 256), 256, 0, s, touched, off, t->cap, t->e, touched_keys_out)); vsb::count_launch(); }
   VS_CK(cudaMemcpyAsync(n_touched_dev, off + n, 8, cudaMemcpyDeviceToDevice, s));
   cudaFreeAsync(touched, s);
   cudaFreeAsync(off, s);
