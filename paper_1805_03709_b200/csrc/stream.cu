@@ -550,7 +550,8 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
   uint64_t* off = (uint64_t*)(scratch_mem + b_index);
   uint64_t* work = (uint64_t*)(scratch_mem + b_index + b_off);
   const dim3 grid(grid_for(n, 256), n_sets);
-  { ProfScope prof(2, s); VS_CK(launch_pdl(k_multi_insert, grid, 256, 0, s, V, keys, n, n_dev, created, index)); vsb::count_launch(); }
+  // (no ProfScope here: its events would sit between the PDL-linked kernels)
+  { VS_CK(launch_pdl(k_multi_insert, grid, 256, 0, s, V, keys, n, n_dev, created, index)); vsb::count_launch(); }
   { VS_CK(launch_pdl(k_multi_fixup, grid, 256, 0, s, V, keys, n, created, index)); vsb::count_launch(); }
   cudaError_t e = exclusive_scan<uint8_t>(created, total, off, work, s);
   const bool fifo = fifo_keys_host && fifo_cap_host && fifo_tail_host;

@@ -77,8 +77,8 @@ struct DeviceGuard {
 void count_launch();
 
 // Event-timed scope around the dominant kernel of a call while profiling is
-// on (vs_profile_begin/end).  Tags: 0 hash op kernel, 1 MC encode, 2 stream
-// multi-set insert.
+// on (vs_profile_begin/end).  Tags: 0 hash op kernel, 1 MC encode, 2 reserved
+// (the stream insert chain is PDL-linked, so it is not bracketed), 3 other.
 struct ProfScope {
   int tag;
   cudaStream_t s;
