@@ -387,16 +387,23 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup_small(const int32_t* __
   }
   __syncthreads();
   uint32_t o = incl - cnt + (warp ? wsum[warp - 1] : 0u);
+  // stage the compacted keys in shared memory (the key arrays are free now:
+  // every probe is done) and leave with coalesced stores -- scattered 12-B
+  // stores from ONE SM were two thirds of the kernel's time
+  int32_t* stage = kx;  // 3 * kDedupMax words span kx, ky, kz
 #pragma unroll
   for (int k = 0; k < kDedupPer; ++k) {
     if (first & (1u << k)) {
-      out[3 * o] = x[k];
-      out[3 * o + 1] = y[k];
-      out[3 * o + 2] = z[k];
+      stage[3 * o] = x[k];
+      stage[3 * o + 1] = y[k];
+      stage[3 * o + 2] = z[k];
       ++o;
     }
   }
-  if (t == kDedupThreads - 1) *n_dev = wsum[31];
+  __syncthreads();
+  const uint32_t total = wsum[31];
+  for (uint32_t i = t; i < 3 * total; i += kDedupThreads) out[i] = stage[i];
+  if (t == 0) *n_dev = total;
 }
 
 __global__ void k_scatter_flagged(const int32_t* __restrict__ keys, uint64_t n, const uint8_t* __restrict__ flag,
