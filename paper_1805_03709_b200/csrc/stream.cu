@@ -314,12 +314,14 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup_small(const int32_t* __
   for (uint32_t i = t; i < kDedupSlots; i += kDedupThreads) slot[i] = 0xFFFFFFFFu;
   // contiguous ownership: thread t holds keys [t*8, t*8+8), so the scan below
   // runs in input order; expansion order = affected_mc_blocks (dx slowest)
+  // `per` keys per thread (<= kDedupPer) so every thread of the CTA works
+  const uint32_t per = (m + kDedupThreads - 1) / kDedupThreads;
   int32_t x[kDedupPer], y[kDedupPer], z[kDedupPer];
   uint32_t where[kDedupPer];
 #pragma unroll
   for (int k = 0; k < kDedupPer; ++k) {
-    const uint32_t j = t * kDedupPer + k;
-    if (j < m) {
+    const uint32_t j = t * per + k;
+    if ((uint32_t)k < per && j < m) {
       const uint32_t i = j >> 3, d = j & 7;
       x[k] = updated[3 * i] - (int32_t)((d >> 2) & 1);
       y[k] = updated[3 * i + 1] - (int32_t)((d >> 1) & 1);
@@ -332,8 +334,8 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup_small(const int32_t* __
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < kDedupPer; ++k) {
-    const uint32_t j = t * kDedupPer + k;
-    if (j >= m) continue;
+    const uint32_t j = t * per + k;
+    if ((uint32_t)k >= per || j >= m) continue;
     uint32_t h = hash_raw(x[k], y[k], z[k]);
 #if VSB_DEDUP_MIX
     // neighbouring keys share low hash bits; mix before masking so linear
@@ -360,8 +362,8 @@ __global__ void __launch_bounds__(kDedupThreads) k_dedup_small(const int32_t* __
   uint32_t first = 0, cnt = 0;
 #pragma unroll
   for (int k = 0; k < kDedupPer; ++k) {
-    const uint32_t j = t * kDedupPer + k;
-    if (j < m && slot[where[k]] == j) {
+    const uint32_t j = t * per + k;
+    if ((uint32_t)k < per && j < m && slot[where[k]] == j) {
       first |= 1u << k;
       ++cnt;
     }
