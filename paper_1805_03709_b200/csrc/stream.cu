@@ -136,6 +136,9 @@ __device__ __forceinline__ bool block_visible(const Frustum& F, int32_t kx, int3
 // vacated excess entries go straight back to the free list (no pops run in
 // this launch, so the push cannot race a pop).
 // extraction CTA shape (one CTA per client set; measured: see DESIGN §4)
+#ifndef VSB_EXTRACT_ERASE_AT_SCAN
+#define VSB_EXTRACT_ERASE_AT_SCAN 0  // measured: no gain over the write-out-then-erase pass (scripts/extract_ab.sh)
+#endif
 #ifndef VSB_EXTRACT_THREADS
 #define VSB_EXTRACT_THREADS 256
 #endif
@@ -179,15 +182,18 @@ __global__ void __cluster_dims__(kExtractCtas, 1, 1) __launch_bounds__(kExtractT
   __shared__ uint32_t chunk_cnt;  // read by the other CTAs of the cluster
   const uint32_t warp = threadIdx.x >> 5;
   uint64_t found = 0;  // identical in every CTA of the cluster
+  int delta = 0;
   for (uint64_t base = 0; base < cap && found < max_n; base += kChunk * kExtractCtas) {
     const uint64_t c0 = base + rank * kChunk;
     int4 e[kExtractK];
     bool live[kExtractK];
+    uint32_t pk[kExtractK];
 #pragma unroll
     for (int k = 0; k < kExtractK; ++k) {
       const uint64_t q = c0 + (uint64_t)k * kExtractThreads + threadIdx.x;
       uint64_t p = (uint64_t)start + q;
       p = p >= cap ? p - cap : p;
+      pk[k] = (uint32_t)p;
       live[k] = false;
       if (q < cap) {
         e[k] = ld_entry(T.e + p);
@@ -230,6 +236,24 @@ __global__ void __cluster_dims__(kExtractCtas, 1, 1) __launch_bounds__(kExtractT
           out[3 * d] = e[k].x;
           out[3 * d + 1] = e[k].y;
           out[3 * d + 2] = e[k].z;
+#if VSB_EXTRACT_ERASE_AT_SCAN
+          // remove it now, from the position the scan found it at: a bucket
+          // entry is its own bucket, so an unchanged, non-FRESH bucket word
+          // takes the locked fast path with no chain walk; an excess entry
+          // re-scans its chain under the lock (snap kLock never matches).
+          // Chunks are disjoint, and a removal changes only the victim's
+          // OCC and a predecessor's NEXT, so the scan of later positions
+          // still sees exactly the live keys it would have seen.
+          const uint32_t p = pk[k];
+          const bool bucket = p < T.n;
+          const uint32_t b = bucket ? p : bucket_of(T, e[k].x, e[k].y, e[k].z);
+          const int32_t pos = mutate_locked(T, e[k].x, e[k].y, e[k].z, false, 0, b,
+                                            bucket ? (uint32_t)e[k].w : kLock, (int32_t)p).pos;
+          if (pos >= 0) {
+            --delta;
+            if (pos >= (int32_t)T.n) push_free(T, (uint32_t)pos);
+          }
+#endif
         }
       }
       o += all;
@@ -238,10 +262,10 @@ __global__ void __cluster_dims__(kExtractCtas, 1, 1) __launch_bounds__(kExtractT
     cluster.sync();  // chunk_cnt / wcnt reused by the next round
   }
   const uint64_t m = found < max_n ? found : max_n;
+#if !VSB_EXTRACT_ERASE_AT_SCAN
   // keys_out complete (written by the whole cluster) before the removals
   __threadfence();
   cluster.sync();
-  int delta = 0;
   for (uint64_t j = rank * kExtractThreads + threadIdx.x; j < m; j += (uint64_t)kExtractCtas * kExtractThreads) {
     const int32_t pos = erase_key(T, out[3 * j], out[3 * j + 1], out[3 * j + 2]);
     if (pos >= 0) {
@@ -249,6 +273,7 @@ __global__ void __cluster_dims__(kExtractCtas, 1, 1) __launch_bounds__(kExtractT
       if (pos >= (int32_t)T.n) push_free(T, (uint32_t)pos);
     }
   }
+#endif
   add_size_cta(T, delta);
   if (rank == 0 && threadIdx.x == 0) n_out[c] = m;
 }
