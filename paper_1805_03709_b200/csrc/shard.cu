@@ -37,6 +37,7 @@
 #include <vector>
 
 #include "hash_ops.cuh"
+#include "pdl.cuh"
 #include "table.h"
 
 namespace vsb {
@@ -162,6 +163,7 @@ __device__ __forceinline__ void stage_tile(const int32_t* __restrict__ keys, con
 __global__ void __launch_bounds__(kPartThreads) k_wpart_count(const int32_t* __restrict__ keys, uint64_t n, int world,
                                                               uint64_t wmagic, uint32_t nwt,
                                                               uint32_t* __restrict__ tile_cnt) {
+  pdl_wait();
   __shared__ uint32_t c[kPartThreads / 32][kMaxWorld];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t wt = blockIdx.x * (kPartThreads / 32) + warp;
@@ -193,6 +195,7 @@ constexpr uint32_t kTilesPerCta = kPartThreads / 32;
 static_assert(kTilesPerCta == 8, "k_wpart_scan sums groups with 8-lane shuffles");
 __global__ void __launch_bounds__(1024) k_wpart_scan(const uint32_t* __restrict__ tile_cnt, uint32_t nwt,
                                                      uint32_t* __restrict__ grp_off, uint32_t* __restrict__ totals) {
+  pdl_wait();
   constexpr int kPer = 4;
   constexpr uint32_t kChunk = 1024 * kPer;  // groups per chunk
   __shared__ uint32_t gsum[kChunk];
@@ -259,6 +262,7 @@ __global__ void __launch_bounds__(kPartThreads) k_wpart_push(ShardView V, const 
                                                              const uint32_t* __restrict__ grp_off,
                                                              const uint32_t* __restrict__ totals,
                                                              unsigned long long epoch, unsigned int* ctr) {
+  pdl_wait();
   __shared__ uint32_t run[kPartThreads / 32][kMaxWorld];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t wt = blockIdx.x * (kPartThreads / 32) + warp;
@@ -312,6 +316,7 @@ __global__ void __launch_bounds__(kPartThreads) k_wpart_push(ShardView V, const 
 // hang the GPU).
 __global__ void k_wait(const unsigned long long* flags, int world, unsigned long long epoch, unsigned int* err,
                        uint64_t timeout_ns) {
+  pdl_wait();
   const int r = threadIdx.x;
   if (r >= world) return;
   const uint64_t t0 = globaltimer();
@@ -358,6 +363,7 @@ __device__ __forceinline__ Routed load_routed(const ShardView& V, uint32_t* spre
 
 __global__ void __launch_bounds__(kShardOpBlock, 2048 / kShardOpBlock) k_shard_apply(TableView T, ShardView V, uint8_t* __restrict__ res,
                                                                int32_t* __restrict__ idx, uint32_t* __restrict__ wv) {
+  pdl_wait();
   __shared__ uint32_t spre[kMaxWorld + 1];
   const Routed R = load_routed(V, spre);
   const int4* rec = rec_of(V, V.rank);
@@ -380,6 +386,7 @@ __global__ void __launch_bounds__(kShardOpBlock, 2048 / kShardOpBlock) k_shard_a
 // back onto the free list with one warp-wide reservation per round.
 __global__ void __launch_bounds__(256) k_shard_post(TableView T, ShardView V, uint8_t* __restrict__ res,
                                                     const int32_t* __restrict__ idx, const uint32_t* __restrict__ wv) {
+  pdl_wait();
   constexpr int kOps = 4;
   __shared__ uint32_t spre[kMaxWorld + 1];
   const Routed R = load_routed(V, spre);
@@ -431,6 +438,7 @@ __global__ void __launch_bounds__(256) k_shard_post(TableView T, ShardView V, ui
 __global__ void __launch_bounds__(256) k_shard_return(ShardView V, const uint8_t* __restrict__ res,
                                                       const uint32_t* __restrict__ wv, unsigned long long epoch,
                                                       unsigned int* ctr) {
+  pdl_wait();
   __shared__ uint32_t spre[kMaxWorld + 1];
   const Routed R = load_routed(V, spre);
   const uint32_t total = R.total();
@@ -631,18 +639,18 @@ vs_status vs_shard_apply(vs_shard* s, const int32_t* keys, const uint8_t* ops, u
     const uint32_t nwt = (uint32_t)((n + kWTile - 1) / kWTile);
     const unsigned ctas = nwt ? (nwt + kPartThreads / 32 - 1) / (kPartThreads / 32) : 1u;
     if (nwt) {
-      k_wpart_count<<<ctas, kPartThreads, 0, st>>>(keys, n, s->world, V.wmagic, nwt, s->tile_cnt);
+      VS_CK(launch_pdl(k_wpart_count, ctas, kPartThreads, 0, st, keys, n, s->world, V.wmagic, nwt, s->tile_cnt));
       count_launch();
-      k_wpart_scan<<<s->world, 1024, 0, st>>>(s->tile_cnt, nwt, s->grp_off, s->totals);
+      VS_CK(launch_pdl(k_wpart_scan, s->world, 1024, 0, st, s->tile_cnt, nwt, s->grp_off, s->totals));
       count_launch();
     } else {
       VS_CK(cudaMemsetAsync(s->totals, 0, kMaxWorld * 4, st));
     }
-    k_wpart_push<<<ctas, kPartThreads, 0, st>>>(V, keys, ops, n, nwt, s->tile_cnt, s->grp_off, s->totals, ep,
-                                                  s->ctl);
+    VS_CK(launch_pdl(k_wpart_push, ctas, kPartThreads, 0, st, V, keys, ops, n, nwt, s->tile_cnt, s->grp_off,
+                     s->totals, ep, s->ctl));
     count_launch();
   }
-  k_wait<<<1, 32, 0, st>>>(own->push_flag, s->world, ep, s->ctl + 64, s->timeout_ns);
+  VS_CK(launch_pdl(k_wait, 1, 32, 0, st, own->push_flag, s->world, ep, s->ctl + 64, s->timeout_ns));
   count_launch();
   // incoming ~ n per rank when the keys hash evenly; the grid-stride loops
   // cover any skew
@@ -653,12 +661,12 @@ vs_status vs_shard_apply(vs_shard* s, const int32_t* keys, const uint8_t* ops, u
     k_shard_apply<<<grid_for(hint, kShardOpBlock), kShardOpBlock, 0, st>>>(T, V, s->res, s->idx, s->wv);
     count_launch();
   }
-  k_shard_post<<<grid_for(hint, 256 * 4), 256, 0, st>>>(T, V, s->res, s->idx, s->wv);
+  VS_CK(launch_pdl(k_shard_post, grid_for(hint, 256 * 4), 256, 0, st, T, V, s->res, s->idx, s->wv));
   count_launch();
   // bounded grid: the last-CTA signal costs one same-address atomic per CTA
-  k_shard_return<<<kReturnCtas, 256, 0, st>>>(V, s->res, s->wv, ep, s->ctl + 32);
+  VS_CK(launch_pdl(k_shard_return, kReturnCtas, 256, 0, st, V, s->res, s->wv, ep, s->ctl + 32));
   count_launch();
-  k_wait<<<1, 32, 0, st>>>(own->ret_flag, s->world, ep, s->ctl + 64, s->timeout_ns);
+  VS_CK(launch_pdl(k_wait, 1, 32, 0, st, own->ret_flag, s->world, ep, s->ctl + 64, s->timeout_ns));
   count_launch();
   if (n) VS_CK(cudaMemcpyAsync(result, s->win + s->out_off, n, cudaMemcpyDeviceToDevice, st));
   VS_CK_LAUNCH("vs_shard_apply");
