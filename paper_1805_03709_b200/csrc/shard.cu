@@ -345,13 +345,17 @@ struct Routed {
   }
 };
 
-// Every thread of the CTA must call it (barrier inside).
-__device__ __forceinline__ Routed load_routed(const ShardView& V, uint32_t* spre) {
+// Every thread of the CTA must call it (barrier inside).  After a k_wait
+// timeout (error bit 1) the regions of a peer that never arrived still hold
+// its PREVIOUS batch: the routed set is then empty, so nothing stale is
+// applied, fixed up or returned (vs_shard_check reports the timeout).
+__device__ __forceinline__ Routed load_routed(const ShardView& V, uint32_t* spre, const unsigned int* err) {
   if (threadIdx.x == 0) {
     const ShardHdr* h = hdr_of(V, V.rank);
+    const bool dead = (*(const volatile unsigned int*)err & 2u) != 0u;
     uint32_t a = 0;
     spre[0] = 0;
-    for (int r = 0; r < V.world; ++r) spre[r + 1] = a += (uint32_t)h->cnt[r];
+    for (int r = 0; r < V.world; ++r) spre[r + 1] = a += dead ? 0u : (uint32_t)h->cnt[r];
   }
   __syncthreads();
   Routed R;
@@ -362,10 +366,11 @@ __device__ __forceinline__ Routed load_routed(const ShardView& V, uint32_t* spre
 }
 
 __global__ void __launch_bounds__(kShardOpBlock, 2048 / kShardOpBlock) k_shard_apply(TableView T, ShardView V, uint8_t* __restrict__ res,
-                                                               int32_t* __restrict__ idx, uint32_t* __restrict__ wv) {
+                                                               int32_t* __restrict__ idx, uint32_t* __restrict__ wv,
+                                                               const unsigned int* err) {
   pdl_wait();
   __shared__ uint32_t spre[kMaxWorld + 1];
-  const Routed R = load_routed(V, spre);
+  const Routed R = load_routed(V, spre, err);
   const int4* rec = rec_of(V, V.rank);
   const uint32_t total = R.total();
   int delta = 0;
@@ -385,11 +390,12 @@ __global__ void __launch_bounds__(kShardOpBlock, 2048 / kShardOpBlock) k_shard_a
 // flight first), created-flag fixup via the records, vacated excess entries
 // back onto the free list with one warp-wide reservation per round.
 __global__ void __launch_bounds__(256) k_shard_post(TableView T, ShardView V, uint8_t* __restrict__ res,
-                                                    const int32_t* __restrict__ idx, const uint32_t* __restrict__ wv) {
+                                                    const int32_t* __restrict__ idx, const uint32_t* __restrict__ wv,
+                                                    const unsigned int* err) {
   pdl_wait();
   constexpr int kOps = 4;
   __shared__ uint32_t spre[kMaxWorld + 1];
-  const Routed R = load_routed(V, spre);
+  const Routed R = load_routed(V, spre, err);
   const int4* rec = rec_of(V, V.rank);
   const uint32_t total = R.total();
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -437,10 +443,10 @@ __global__ void __launch_bounds__(256) k_shard_post(TableView T, ShardView V, ui
 
 __global__ void __launch_bounds__(256) k_shard_return(ShardView V, const uint8_t* __restrict__ res,
                                                       const uint32_t* __restrict__ wv, unsigned long long epoch,
-                                                      unsigned int* ctr) {
+                                                      unsigned int* ctr, const unsigned int* err) {
   pdl_wait();
   __shared__ uint32_t spre[kMaxWorld + 1];
-  const Routed R = load_routed(V, spre);
+  const Routed R = load_routed(V, spre, err);
   const uint32_t total = R.total();
   const uint32_t stride = gridDim.x * blockDim.x;
 #pragma unroll 1
@@ -462,7 +468,8 @@ __global__ void __launch_bounds__(256) k_shard_return(ShardView V, const uint8_t
     for (int k = 0; k < 4; ++k)
       if (v0 + k * stride < total) out_of(V, r[k])[w[k] & kOrigMask] = b[k];  // peer store into the source's window
   }
-  if (last_cta(ctr) && threadIdx.x < V.world) {
+  // after a timeout no return flag is raised: the sources time out too
+  if (last_cta(ctr) && threadIdx.x < V.world && !(*(const volatile unsigned int*)err & 2u)) {
     __threadfence_system();
     st_release_sys(&hdr_of(V, threadIdx.x)->ret_flag[V.rank], epoch);
   }
@@ -658,13 +665,13 @@ vs_status vs_shard_apply(vs_shard* s, const int32_t* keys, const uint8_t* ops, u
   const TableView T = s->table->next_view();
   {
     ProfScope prof(0, st);
-    k_shard_apply<<<grid_for(hint, kShardOpBlock), kShardOpBlock, 0, st>>>(T, V, s->res, s->idx, s->wv);
+    k_shard_apply<<<grid_for(hint, kShardOpBlock), kShardOpBlock, 0, st>>>(T, V, s->res, s->idx, s->wv, s->ctl + 64);
     count_launch();
   }
-  VS_CK(launch_pdl(k_shard_post, grid_for(hint, 256 * 4), 256, 0, st, T, V, s->res, s->idx, s->wv));
+  VS_CK(launch_pdl(k_shard_post, grid_for(hint, 256 * 4), 256, 0, st, T, V, s->res, s->idx, s->wv, s->ctl + 64));
   count_launch();
   // bounded grid: the last-CTA signal costs one same-address atomic per CTA
-  VS_CK(launch_pdl(k_shard_return, kReturnCtas, 256, 0, st, V, s->res, s->wv, ep, s->ctl + 32));
+  VS_CK(launch_pdl(k_shard_return, kReturnCtas, 256, 0, st, V, s->res, s->wv, ep, s->ctl + 32, s->ctl + 64));
   count_launch();
   VS_CK(launch_pdl(k_wait, 1, 32, 0, st, own->ret_flag, s->world, ep, s->ctl + 64, s->timeout_ns));
   count_launch();

@@ -203,6 +203,52 @@ def test_contended_insert_erase_keeps_uniqueness(dev):
         assert a["live"] == s.approx_size() <= 64
 
 
+def test_fresh_erase_reclaim_aba_keeps_uniqueness(dev):
+    """A18-violating batches built to hit the bucket-word ABA: per bucket one
+    insert of K (fresh), erases of K and several inserts of X, all hashing to
+    the same bucket and shuffled over the launch.  A re-claim of the bucket
+    by X after K's erase restores the word an earlier X insert snapshotted
+    (N|OCC|FRESH); that insert must not skip its re-scan.  Every X must end
+    up present exactly once with exactly one created flag."""
+    import torch
+
+    from paper_1805_03709_b200 import BlockHashSet
+
+    n = 4096
+    s = BlockHashSet(n, 1 << 16)
+    rng = np.random.default_rng(7)
+    P = np.array([73856093, 19349669, 83492791], np.uint64)
+    for trial in range(40):
+        cand = rng.integers(-(1 << 20), 1 << 20, (8 * n, 3)).astype(np.int32)
+        cand = np.unique(cand, axis=0)
+        u = cand.astype(np.int64).astype(np.uint64) & np.uint64(0xFFFFFFFF)
+        h = ((u[:, 0] * P[0]) & 0xFFFFFFFF) ^ ((u[:, 1] * P[1]) & 0xFFFFFFFF) ^ ((u[:, 2] * P[2]) & 0xFFFFFFFF)
+        b = (h % np.uint64(n)).astype(np.int64)
+        order = np.argsort(b, kind="stable")
+        bs = b[order]
+        first = np.flatnonzero(np.r_[True, bs[1:] != bs[:-1]])
+        pairs = [(order[i], order[i + 1]) for i in first if i + 1 < len(bs) and bs[i + 1] == bs[i]]
+        K = cand[[p[0] for p in pairs]]
+        X = cand[[p[1] for p in pairs]]
+        m = len(pairs)
+        keys = np.concatenate([K, K, K, X, X, X, X])
+        ops = np.concatenate([np.zeros(m), np.full(2 * m, 2), np.zeros(4 * m)]).astype(np.uint8)
+        xid = np.concatenate([np.full(3 * m, -1), np.tile(np.arange(m), 4)])
+        perm = rng.permutation(len(keys))
+        keys, ops, xid = keys[perm], ops[perm], xid[perm]
+        res, _ = s.apply(keys, torch.from_numpy(ops))
+        s.check_capacity()
+        res = res.cpu().numpy()
+        created_x = np.bincount(xid[xid >= 0], weights=res[xid >= 0], minlength=m)
+        assert np.all(created_x == 1), (trial, np.flatnonzero(created_x != 1)[:8])
+        a = s.audit()
+        assert a["duplicates"] == 0 and a["unreachable_live"] == 0 and a["free_reachable"] == 0, a
+        assert a["free"] + a["reachable_excess"] == s.excess_capacity, a
+        found, _ = s.find_keys(X)
+        assert bool(found.cpu().numpy().all())
+        s.clear()
+
+
 def test_capacity_exhausted_raises_and_preserves(dev):
     from paper_1805_03709_b200 import BlockHashSet, CapacityExhausted
 
