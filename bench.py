@@ -52,6 +52,7 @@ def parse():
                    help="share of the 0.7-load-factor slots in the bucket region (rest: excess)")
     p.add_argument("--mc-steps", type=int, default=10)
     p.add_argument("--no-mc", action="store_true")
+    p.add_argument("--no-mc-parity", action="store_true", help="skip the all-blocks oracle check (experiments)")
     p.add_argument("--no-stream", action="store_true")
     p.add_argument("--no-rc", action="store_true")
     p.add_argument("--rc-frames", type=int, default=20)
@@ -384,15 +385,49 @@ def run_hash(args, dev, rank, world):
     return out
 
 
-def run_mc(args, dev, world=1):
-    """Config 3: full encode of the synthetic room (2,080,160 blocks).  With
-    world > 1 every rank encodes its own replica of the scene (the encoder
-    does not shard): value = world x blocks / max-over-ranks time."""
+def mc_full_parity(t, pool, keys, mc, q, counts, threads: int, chunk: int = 1 << 17):
+    """Every block of the config-3 encode vs the C oracle (recompute_mc_block
+    restated), outside the timed region: per chunk, the neighbour rows are
+    gathered from the device pool and re-encoded on the host cores."""
     import numpy as np
     import torch
 
     import oracle
-    from paper_1805_03709_b200 import BlockHashSet, _lib, encode_blocks, encode_keys, face_packs, neighbors, workloads
+    from paper_1805_03709_b200 import neighbors
+
+    N = keys.shape[0]
+    bad = 0
+    for a in range(0, N, chunk):
+        b = min(N, a + chunk)
+        nbr = neighbors(t, keys[a:b]).reshape(-1)
+        valid = nbr >= 0
+        uniq, inv = torch.unique(nbr[valid], return_inverse=True)
+        rows = pool[uniq.long()].cpu().numpy()
+        local = torch.full_like(nbr, -1)
+        local[valid] = inv.to(torch.int32)
+        omc, oq, oc = oracle.mc_encode(rows, local.view(-1, 8).cpu().numpy(), threads=threads)
+        ok = (np.array_equal(mc[a:b].cpu().numpy(), omc) and np.array_equal(q[a:b].cpu().numpy(), oq)
+              and np.array_equal(counts[a:b].cpu().numpy().astype(np.uint32), oc))
+        bad += 0 if ok else 1
+    return bad == 0
+
+
+def run_mc(args, dev, world=1):
+    """Config 3: full encode of the synthetic room (2,080,160 blocks).  With
+    world > 1 every rank encodes its own replica of the scene (the encoder
+    does not shard): value = world x blocks / max-over-ranks time.
+
+    Headline: vs_mc_encode_full, ONE self-contained launch per step (fused
+    neighbour lookups, face packs computed in-kernel from each staged centre
+    row, MC + quantised TSDF + counts).  Also timed: the same launch with the
+    fused cell compaction, the incremental-ingest variant (face-pack side
+    table rebuilt for every row + encode reading it), the scattered-halo
+    encode (no packs), and the two-pass compaction."""
+    import numpy as np
+    import torch
+
+    from paper_1805_03709_b200 import (BlockHashSet, FaceState, _lib, compact, encode_full, encode_keys, face_packs,
+                                       workloads)
 
     keys_np = workloads.room_block_keys()
     N = len(keys_np)
@@ -406,55 +441,107 @@ def run_mc(args, dev, world=1):
     pool = torch.empty((t.capacity, 6144), dtype=torch.uint8, device=dev)
     for a in range(0, N, 1 << 15):
         pool[pos[a:a + (1 << 15)].long()] = workloads.room_tsdf_rows(keys[a:a + (1 << 15)])
+    state = FaceState(pool)
     mc = torch.empty((N, 2048), dtype=torch.uint8, device=dev)
-    # ingest-side halo side table: face bit-packs of every written row (timed
-    # and reported separately; it is maintained where rows change, like the map)
-    faces = face_packs(pool, rows=pos)
-    torch.cuda.synchronize()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record()
-    face_packs(pool, rows=pos, faces=faces)
-    f1.record()
-    torch.cuda.synchronize()
-    faces_ms = f0.elapsed_time(f1)
-    lib = _lib.load()
+    q = torch.empty((N, 512), dtype=torch.int8, device=dev)
+    cnt = torch.empty(N, dtype=torch.int32, device=dev)
 
     def enc():
-        return encode_keys(t, pool, keys, faces=faces)
+        return encode_full(t, pool, keys, state=state, mc=mc, q=q, counts=cnt)
 
     for _ in range(2):
-        mc, q, counts = enc()
-    # parity: a random sample vs the oracle, neighbours gathered from the pool
-    rng = np.random.default_rng(0)
-    sample = np.sort(rng.choice(N, 1024, replace=False))
-    nbr = neighbors(t, keys[sample]).cpu().numpy()
-    uniq, inv = np.unique(nbr[nbr >= 0], return_inverse=True)
-    rows = pool[torch.from_numpy(uniq).to(dev).long()].cpu().numpy()
-    local = np.full_like(nbr, -1)
-    local[nbr >= 0] = inv
-    omc, oq, oc = oracle.mc_encode(rows, local, threads=8)
-    ok = bool(np.array_equal(mc[torch.from_numpy(sample).to(dev)].cpu().numpy(), omc)
-              and np.array_equal(q[torch.from_numpy(sample).to(dev)].cpu().numpy(), oq))
-    barrier(world)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with _lib.Profile() as prof:
-        ev0.record()
-        for _ in range(args.mc_steps):
-            enc()
-        ev1.record()
+        enc()
+    torch.cuda.synchronize()
+
+    def timed(fn, steps):
         barrier(world)
-    ms = sync_max(ev0.elapsed_time(ev1), world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with _lib.Profile() as prof:
+            e0.record()
+            for _ in range(steps):
+                fn()
+            e1.record()
+            barrier(world)
+        return sync_max(e0.elapsed_time(e1), world) / steps, prof
+
+    lib = _lib.load()
+    fb0 = lib.vs_mc_self_fallbacks()
+    clocks = Clocks(dev.index).start()
+    time.sleep(0.12)
+    ms, prof = timed(enc, args.mc_steps)
+    clk = clocks.stop()
+    fallbacks = (lib.vs_mc_self_fallbacks() - fb0) / args.mc_steps
     k_ms = prof.ms["mc"] / max(1, prof.count["mc"])
+    launches = prof.launches
+    # ---- parity of EVERY block vs the C oracle (outside the timed region)
+    mc_t, q_t, c_t, _ = enc()
+    torch.cuda.synchronize()
+    p0 = time.perf_counter()
+    ok = None if args.no_mc_parity else mc_full_parity(t, pool, keys, mc_t, q_t, c_t, threads=cpu_cores())
+    parity_s = time.perf_counter() - p0
+    # ---- the same launch with the fused compaction of the non-empty cells
+    total_cells = int(c_t.long().sum().item())
+    cap = total_cells + 1024
+    cstate = {}
+
+    def enc_cells():
+        cstate["r"] = encode_full(t, pool, keys, state=state, mc=mc, q=q, counts=cnt, cells=True, cell_cap=cap)
+
+    enc_cells()
+    c_ms, c_prof = timed(enc_cells, args.mc_steps)
+    _, _, c_counts, (offs, flat, cells, cur) = cstate["r"]
+    cells_ok = bool(int(cur.item()) == total_cells and torch.equal(c_counts, c_t))
+    if cells_ok:  # scatter-back of every block's cells == dense MC bytes
+        cl = c_counts.long()
+        blk = torch.repeat_interleave(torch.arange(N, device=dev), cl)
+        src = torch.repeat_interleave(offs.long(), cl) + torch.arange(total_cells, device=dev) - \
+            torch.repeat_interleave(torch.cumsum(cl, 0) - cl, cl)
+        dense = torch.zeros((N, 512), dtype=torch.int32, device=dev)
+        dense[blk, flat[src].long() & 0xFFFF] = cells[src]
+        cells_ok = bool(torch.equal(dense.view(torch.uint8).view(N, 2048), mc_t))
+        del dense, blk, src
+    # ---- incremental-ingest variant: side-table rebuild of every row + encode
+    faces = face_packs(pool, rows=pos)
+
+    def enc_packs():
+        face_packs(pool, rows=pos, faces=faces)
+        encode_keys(t, pool, keys, faces=faces)
+
+    p_ms, p_prof = timed(enc_packs, max(2, args.mc_steps // 2))
+    g_ms, _ = timed(lambda: encode_keys(t, pool, keys), max(2, args.mc_steps // 2))
+
+    def two_pass():
+        m, _, c = encode_keys(t, pool, keys, q=False)
+        compact(m, c, cell_cap=cap)
+
+    tp_ms, _ = timed(two_pass, 2)
     peak, src = peaks()
     achieved = N * BYTES_PER_BLOCK / (k_ms / 1e3) / 1e9
-    out = {"workload": "config 3: room 16x3x16 m, 5 mm voxels, 2,080,160 blocks, fused hash lookups, face-pack halo"
+    cell_bytes = total_cells * 6
+    out = {"workload": "config 3: room 16x3x16 m, 5 mm voxels, 2,080,160 blocks; full encode in ONE self-contained "
+                       "launch (fused hash lookups, in-kernel face packs, MC + quantised TSDF + counts)"
                        + (f"; one replica per GPU x{world}" if world > 1 else ""),
-           "face_packs_ms_all_rows": faces_ms,
-           "value": world * N * args.mc_steps / (ms / 1e3), "unit": "blocks/s", "ms_per_step": ms / args.mc_steps,
-           "steps": args.mc_steps, "blocks": N, "ok": ok, "gpu_launches": prof.launches,
+           "value": world * N / (ms / 1e3), "unit": "blocks/s", "ms_per_step": ms,
+           "steps": args.mc_steps, "blocks": N, "ok": ok, "parity": f"all {N} blocks (MC bytes, quantised bytes, "
+                                                                    f"counts) vs the C oracle, {parity_s:.1f} s",
+           "gpu_launches": launches, "clocks": clk, "pack_fallbacks_per_launch": fallbacks,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                        "traffic": ncu_traffic("k_mc_encode"), "kernel": "vsb::k_mc_encode<true>",
-                        "kernel_ms": k_ms, "bytes_per_launch": N * BYTES_PER_BLOCK, "peak_source": src}}
+                        "traffic": ncu_traffic("k_mc_encode_self"), "kernel": "vsb::k_mc_encode_self<true,false>",
+                        "kernel_ms": k_ms, "bytes_per_launch": N * BYTES_PER_BLOCK, "peak_source": src,
+                        "bytes_per_block": "6144 TSDF read + 2048 MC + 512 quantised (SURVEY §8d)"},
+           "compact": {"value": world * N / (c_ms / 1e3), "unit": "blocks/s", "ms_per_step": c_ms,
+                       "cells": total_cells, "ok": cells_ok,
+                       "kernel_ms": c_prof.ms["mc"] / max(1, c_prof.count["mc"]),
+                       "frac": (N * BYTES_PER_BLOCK + cell_bytes) /
+                               (c_prof.ms["mc"] / max(1, c_prof.count["mc"]) / 1e3) / 1e9 / peak,
+                       "note": "same launch + fused compaction of the non-empty cells (u16 flat + u32 cell, ranges "
+                               "reserved by one atomic per block); frac counts +6 B per cell"},
+           "incremental_packs": {"ms_per_step": p_ms, "value": world * N / (p_ms / 1e3),
+                                 "note": "face-pack side table rebuilt for all rows (k_mc_faces) + encode reading it "
+                                         "(the ingest-maintained variant the server uses)"},
+           "scattered_halo": {"ms_per_step": g_ms, "value": world * N / (g_ms / 1e3),
+                              "note": "encode without packs: 217 halo voxels gathered per block"},
+           "two_pass_compact_ms": tp_ms}
     if not args.no_e2e:
         # e2e: host TSDF rows -> device pool, encode, MC + quantised bytes -> host
         host_rows = pool[pos.long()].cpu().pin_memory()
@@ -468,8 +555,7 @@ def run_mc(args, dev, world=1):
         for _ in range(steps):
             dev_rows = host_rows.to(dev, non_blocking=True)
             pool.index_copy_(0, posl, dev_rows)
-            face_packs(pool, rows=pos, faces=faces)  # ingest: rows changed -> their packs
-            m, qq, _ = encode_keys(t, pool, keys, counts=False, faces=faces)
+            m, qq, _, _ = encode_full(t, pool, keys, state=state, counts=False)
             h_mc.copy_(m, non_blocking=True)
             h_q.copy_(qq, non_blocking=True)
         e1.record()

@@ -95,6 +95,11 @@ def affected_mc_blocks(updated) -> list[tuple[int, int, int]]:
 # ----------------------------------------------------------- device entry
 
 def _out(torch, n, device, want, shape, dtype):
+    """`want`: False (skip), True (allocate) or a caller tensor to write into."""
+    if isinstance(want, torch.Tensor):
+        if want.shape != (n,) + shape or want.dtype != dtype or want.device != device or not want.is_contiguous():
+            raise ValueError(f"output must be a contiguous {dtype}[{n}, ...{shape}] tensor on {device}")
+        return want
     return torch.empty((n,) + shape, dtype=dtype, device=device) if want else None
 
 
@@ -168,6 +173,89 @@ def encode_keys(tsdf_table, pool, keys, *, mc: bool = True, q: bool = True, coun
                                         ptr(c_t), ctypes.c_void_p(s.cuda_stream)), "mc_encode_keys")
     tsdf_table._done(s)
     return mc_t, q_t, c_t
+
+
+PUB_BYTES = 96  # published face pack per pool row (vs_mc_encode_full): 12 {u32 data, u32 epoch}
+
+
+class FaceState:
+    """Published face packs of a TSDF pool for self-packing full encodes
+    (vs_mc_encode_full): per row 12 {u32 word, u32 epoch} pairs, plus the
+    launch epoch.  `faces()` returns the 48-B packs (vs_mc_faces layout) of
+    the rows the last full encode covered."""
+
+    def __init__(self, pool) -> None:
+        torch = _lib.require_cuda()
+        self.pub = torch.zeros((pool.shape[0], PUB_BYTES), dtype=torch.uint8, device=pool.device)
+        self.epoch = 0
+        self.rows = pool.shape[0]
+
+    def next_epoch(self) -> int:
+        self.epoch = (self.epoch % 0xFFFFFFFE) + 1  # never 0 (= never published)
+        return self.epoch
+
+    def faces(self):
+        torch = _lib.require_cuda()
+        w = self.pub.view(torch.int32).view(self.rows, 12, 2)[:, :, 0]
+        return w.contiguous().view(torch.uint8).view(self.rows, FACE_BYTES)
+
+
+def encode_full(tsdf_table, pool, keys=None, *, nbr=None, state: Optional[FaceState] = None, mc: bool = True,
+                q: bool = True, counts: bool = True, cells: bool = False, cell_cap: Optional[int] = None):
+    """Full encode of every block of a map in ONE launch (vs_mc_encode_full):
+    face packs computed in-kernel from each staged centre row (no side-table
+    pass), optional fused compaction of the non-empty cells.
+
+    Neighbour rows from in-kernel lookups of `keys` in `tsdf_table`, or from
+    `nbr` int32[N,8] when tsdf_table is None.  Returns (mc, q, counts, cells)
+    with cells = None or (offsets int32[N], flat int16[M], cell int32[M],
+    cursor int64[1] device total): block i's cells are
+    [offsets[i], offsets[i] + counts[i])."""
+    torch = _lib.require_cuda()
+    dev = pool.device
+    from .concurrent_hash import _as_keys
+
+    if pool.dtype != torch.uint8 or pool.dim() != 2 or pool.shape[1] != TSDF_BLOCK_BYTES:
+        raise ValueError("pool must be uint8[P, 6144]")
+    if state is None:
+        state = FaceState(pool)
+    if state.rows < pool.shape[0]:
+        raise ValueError("FaceState is smaller than the pool")
+    if tsdf_table is not None:
+        k = _as_keys(keys, dev)
+        n = k.shape[0]
+        nb = None
+    else:
+        nb = nbr.to(dev, torch.int32).contiguous().reshape(-1, 8)
+        n = nb.shape[0]
+        k = None
+    want_counts = counts if isinstance(counts, torch.Tensor) else (counts or cells)
+    mc_t = _out(torch, n, dev, mc, (MC_BLOCK_BYTES,), torch.uint8)
+    q_t = _out(torch, n, dev, q, (Q_BLOCK_BYTES,), torch.int8)
+    c_t = _out(torch, n, dev, want_counts, (), torch.int32)
+    cell_out = None
+    cur = offs = flat = cm = None
+    cap = 0
+    if cells:
+        cap = int(cell_cap) if cell_cap is not None else n * 512
+        cur = torch.zeros(1, dtype=torch.int64, device=dev)
+        offs = torch.empty(n, dtype=torch.int32, device=dev)
+        flat = torch.empty(max(cap, 1), dtype=torch.int16, device=dev)
+        cm = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        cell_out = (offs, flat, cm, cur)
+    if tsdf_table is not None:
+        s = tsdf_table._stream()
+        handle = tsdf_table.handle
+    else:
+        s = torch.cuda.current_stream(dev)
+        handle = None
+    check(_lib.load().vs_mc_encode_full(handle, ptr(pool.contiguous()), ptr(k), ptr(nb), n, ptr(state.pub),
+                                        state.next_epoch(), ptr(mc_t), ptr(q_t), ptr(c_t),
+                                        ptr(cur), ptr(offs), ptr(flat), ptr(cm), cap,
+                                        ctypes.c_void_p(s.cuda_stream)), "mc_encode_full")
+    if tsdf_table is not None:
+        tsdf_table._done(s)
+    return mc_t, q_t, (c_t if (counts is not False or cells) else None), cell_out
 
 
 def neighbors(tsdf_table, keys):

@@ -20,7 +20,7 @@ import sys
 ROOT = pathlib.Path(__file__).resolve().parent.parent
 SECTIONS = {
     "hash": ["--no-cpu", "--no-mc", "--no-stream", "--no-rc", "--no-e2e", "--steps", "200"],
-    "mc": ["--no-cpu", "--no-stream", "--no-rc", "--no-e2e", "--steps", "5", "--mc-steps", "20"],
+    "mc": ["--no-cpu", "--no-stream", "--no-rc", "--no-e2e", "--steps", "5", "--mc-steps", "20", "--no-mc-parity"],
     "stream": ["--no-cpu", "--no-mc", "--no-rc", "--no-e2e", "--steps", "5"],
     "rc": ["--no-cpu", "--no-mc", "--no-stream", "--no-e2e", "--steps", "5"],
 }
@@ -35,9 +35,12 @@ def pick(d: dict, section: str):
     if "roofline" in s:
         out["kernel_ms"] = s["roofline"].get("kernel_ms")
         out["frac"] = s["roofline"].get("frac")
-    for k in ("tick_only", "server_tick", "compact"):
+    for k in ("pack_fallbacks_per_launch",):
         if k in s:
-            out[k] = s[k].get("value") if isinstance(s[k], dict) else s[k]
+            out[k] = s[k]
+    for k in ("tick_only", "server_tick", "compact", "incremental_packs", "scattered_halo"):
+        if k in s:
+            out[k] = s[k].get("ms_per_step") if isinstance(s[k], dict) else s[k]
     return out
 
 

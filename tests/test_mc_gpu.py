@@ -32,11 +32,44 @@ def gpu_encode(pool, nbr, dev):
 
     from paper_1805_03709_b200 import encode_blocks, face_packs
 
+    from paper_1805_03709_b200 import encode_full
+
     p, nb = _t(pool, dev), _t(nbr, dev)
     mc, q, c = encode_blocks(p, nb)
     mc2, q2, c2 = encode_blocks(p, nb, faces=face_packs(p))
     assert torch.equal(mc, mc2) and torch.equal(q, q2) and torch.equal(c, c2), "face-pack halo path differs"
+    # the self-packing full encode (packs produced in-kernel, pool fallback
+    # for neighbours that are not centres) + fused compaction
+    mc3, q3, c3, (offs, flat, cells, cur) = encode_full(None, p, nbr=nb, cells=True)
+    assert torch.equal(mc, mc3) and torch.equal(q, q3) and torch.equal(c, c3), "self-packing path differs"
+    assert int(cur.item()) == int(c.sum().item())
+    check_cells_scatter_back(mc, c3, offs, flat, cells)
     return mc.cpu().numpy(), q.cpu().numpy(), c.cpu().numpy().astype(np.uint32)
+
+
+def check_cells_scatter_back(mc, counts, offs, flat, cells):
+    """Fused compaction (A19): every block's cells, read through its range,
+    scatter back to its dense MC bytes; ranges are disjoint."""
+    import torch
+
+    n = mc.shape[0]
+    counts = counts.long()
+    offs = offs.long()
+    total = int(counts.sum().item())
+    blk = torch.repeat_interleave(torch.arange(n, device=mc.device), counts)
+    start = torch.repeat_interleave(offs, counts)
+    within = torch.arange(total, device=mc.device) - torch.repeat_interleave(torch.cumsum(counts, 0) - counts, counts)
+    src = start + within
+    assert total == 0 or int(src.max().item()) < total
+    assert torch.unique(src).numel() == total  # disjoint ranges covering [0, total)
+    dense = torch.zeros((n, 512), dtype=torch.int32, device=mc.device)
+    f = flat[src].long() & 0xFFFF
+    dense[blk, f] = cells[src]
+    assert torch.equal(dense.view(torch.uint8).view(n, 2048), mc)
+    # ascending flat index inside each block
+    if total > 1:
+        same = blk[1:] == blk[:-1]
+        assert bool(torch.all(f[1:][same] > f[:-1][same]))
 
 
 def table_with_pool(tsdf_keys, rows, dev, n=1 << 12, excess=1 << 12):
@@ -107,6 +140,11 @@ def test_fused_sphere_reproduces_manifest_model_sha256(dev, golden):
 
     mc2, _, _ = encode_keys(t, pool, d["keys"], faces=face_packs(pool))
     assert hashlib.sha256(mc2.cpu().numpy().tobytes()).hexdigest() == meta["model_sha256"]
+    from paper_1805_03709_b200 import encode_full
+
+    for _ in range(2):  # epochs advance: the second launch must not trust the first one's flags
+        mc3, _, _, _ = encode_full(t, pool, d["keys"])
+        assert hashlib.sha256(mc3.cpu().numpy().tobytes()).hexdigest() == meta["model_sha256"]
 
 
 @pytest.mark.parametrize("field", ["random", "smooth"])
@@ -186,6 +224,15 @@ def test_room_sample_vs_oracle(dev):
     _, pos = t.find_keys(keys)
     mc2, q2, c2 = encode_keys(t, pool, keys, faces=face_packs(pool, rows=pos))
     assert torch.equal(mc, mc2) and torch.equal(q, q2) and torch.equal(c, c2)
+    from paper_1805_03709_b200 import FaceState, encode_full
+
+    st = FaceState(pool)
+    for _ in range(2):
+        mc3, q3, c3, (offs, flat, cells, cur) = encode_full(t, pool, keys, state=st, cells=True)
+        assert torch.equal(mc, mc3) and torch.equal(q, q3) and torch.equal(c, c3)
+        check_cells_scatter_back(mc, c3, offs, flat, cells)
+    # the packs it published equal the side-table pass's for every encoded row
+    assert torch.equal(st.faces()[pos.long()], face_packs(pool, rows=pos)[pos.long()])
     rows_np = rows.cpu().numpy()
     nbr = oracle.neighbor_table(keys, keys)
     omc, oq, oc = oracle.mc_encode(rows_np, nbr, threads=8)
