@@ -417,17 +417,16 @@ def run_mc(args, dev, world=1):
     world > 1 every rank encodes its own replica of the scene (the encoder
     does not shard): value = world x blocks / max-over-ranks time.
 
-    Headline: vs_mc_encode_full, ONE self-contained launch per step (fused
-    neighbour lookups, face packs computed in-kernel from each staged centre
-    row, MC + quantised TSDF + counts).  Also timed: the same launch with the
-    fused cell compaction, the incremental-ingest variant (face-pack side
-    table rebuilt for every row + encode reading it), the scattered-halo
-    encode (no packs), and the two-pass compaction."""
+    Headline: ONE self-contained launch per step (vs_mc_encode_keys: fused
+    neighbour lookups, centre rows by TMA, the 217 halo voxels gathered one
+    block ahead, MC + quantised TSDF + counts).  Also timed: the same launch
+    with the fused cell compaction, the incremental-ingest variant (face-pack
+    side table rebuilt for every row by k_mc_faces, then the encode reading
+    it: both kernels inside the timed region), and the two-pass compaction."""
     import numpy as np
     import torch
 
-    from paper_1805_03709_b200 import (BlockHashSet, FaceState, _lib, compact, encode_full, encode_keys, face_packs,
-                                       workloads)
+    from paper_1805_03709_b200 import BlockHashSet, _lib, compact, encode_keys, face_packs, workloads
 
     keys_np = workloads.room_block_keys()
     N = len(keys_np)
@@ -441,13 +440,12 @@ def run_mc(args, dev, world=1):
     pool = torch.empty((t.capacity, 6144), dtype=torch.uint8, device=dev)
     for a in range(0, N, 1 << 15):
         pool[pos[a:a + (1 << 15)].long()] = workloads.room_tsdf_rows(keys[a:a + (1 << 15)])
-    state = FaceState(pool)
     mc = torch.empty((N, 2048), dtype=torch.uint8, device=dev)
     q = torch.empty((N, 512), dtype=torch.int8, device=dev)
     cnt = torch.empty(N, dtype=torch.int32, device=dev)
 
     def enc():
-        return encode_full(t, pool, keys, state=state, mc=mc, q=q, counts=cnt)
+        return encode_keys(t, pool, keys, mc=mc, q=q, counts=cnt)
 
     for _ in range(2):
         enc()
@@ -464,17 +462,14 @@ def run_mc(args, dev, world=1):
             barrier(world)
         return sync_max(e0.elapsed_time(e1), world) / steps, prof
 
-    lib = _lib.load()
-    fb0 = lib.vs_mc_self_fallbacks()
     clocks = Clocks(dev.index).start()
     time.sleep(0.12)
     ms, prof = timed(enc, args.mc_steps)
     clk = clocks.stop()
-    fallbacks = (lib.vs_mc_self_fallbacks() - fb0) / args.mc_steps
     k_ms = prof.ms["mc"] / max(1, prof.count["mc"])
     launches = prof.launches
     # ---- parity of EVERY block vs the C oracle (outside the timed region)
-    mc_t, q_t, c_t, _ = enc()
+    mc_t, q_t, c_t = enc()
     torch.cuda.synchronize()
     p0 = time.perf_counter()
     ok = None if args.no_mc_parity else mc_full_parity(t, pool, keys, mc_t, q_t, c_t, threads=cpu_cores())
@@ -485,7 +480,7 @@ def run_mc(args, dev, world=1):
     cstate = {}
 
     def enc_cells():
-        cstate["r"] = encode_full(t, pool, keys, state=state, mc=mc, q=q, counts=cnt, cells=True, cell_cap=cap)
+        cstate["r"] = encode_keys(t, pool, keys, mc=mc, q=q, counts=cnt, cells=True, cell_cap=cap)
 
     enc_cells()
     c_ms, c_prof = timed(enc_cells, args.mc_steps)
@@ -505,42 +500,44 @@ def run_mc(args, dev, world=1):
 
     def enc_packs():
         face_packs(pool, rows=pos, faces=faces)
-        encode_keys(t, pool, keys, faces=faces)
+        encode_keys(t, pool, keys, mc=mc, q=q, counts=cnt, faces=faces)
 
-    p_ms, p_prof = timed(enc_packs, max(2, args.mc_steps // 2))
-    g_ms, _ = timed(lambda: encode_keys(t, pool, keys), max(2, args.mc_steps // 2))
+    p_ms, _ = timed(enc_packs, max(2, args.mc_steps // 2))
+    f_ms, f_prof = timed(lambda: encode_keys(t, pool, keys, mc=mc, q=q, counts=cnt, faces=faces),
+                         max(2, args.mc_steps // 2))
 
     def two_pass():
-        m, _, c = encode_keys(t, pool, keys, q=False)
+        m, _, c = encode_keys(t, pool, keys, mc=mc, q=False, counts=cnt)
         compact(m, c, cell_cap=cap)
 
     tp_ms, _ = timed(two_pass, 2)
     peak, src = peaks()
     achieved = N * BYTES_PER_BLOCK / (k_ms / 1e3) / 1e9
     cell_bytes = total_cells * 6
+    ck_ms = c_prof.ms["mc"] / max(1, c_prof.count["mc"])
     out = {"workload": "config 3: room 16x3x16 m, 5 mm voxels, 2,080,160 blocks; full encode in ONE self-contained "
-                       "launch (fused hash lookups, in-kernel face packs, MC + quantised TSDF + counts)"
-                       + (f"; one replica per GPU x{world}" if world > 1 else ""),
+                       "launch (fused hash lookups, TMA centre rows, halo voxels gathered one block ahead, MC + "
+                       "quantised TSDF + counts)" + (f"; one replica per GPU x{world}" if world > 1 else ""),
            "value": world * N / (ms / 1e3), "unit": "blocks/s", "ms_per_step": ms,
-           "steps": args.mc_steps, "blocks": N, "ok": ok, "parity": f"all {N} blocks (MC bytes, quantised bytes, "
-                                                                    f"counts) vs the C oracle, {parity_s:.1f} s",
-           "gpu_launches": launches, "clocks": clk, "pack_fallbacks_per_launch": fallbacks,
+           "steps": args.mc_steps, "blocks": N, "ok": ok,
+           "parity": None if ok is None else f"all {N} blocks (MC bytes, quantised bytes, counts) vs the C oracle "
+                                             f"on {cpu_cores()} host threads, {parity_s:.1f} s",
+           "gpu_launches": launches, "clocks": clk,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                        "traffic": ncu_traffic("k_mc_encode_self"), "kernel": "vsb::k_mc_encode_self<true,false>",
+                        "traffic": ncu_traffic("k_mc_encode"), "kernel": "vsb::k_mc_encode<true,false,false>",
                         "kernel_ms": k_ms, "bytes_per_launch": N * BYTES_PER_BLOCK, "peak_source": src,
                         "bytes_per_block": "6144 TSDF read + 2048 MC + 512 quantised (SURVEY §8d)"},
            "compact": {"value": world * N / (c_ms / 1e3), "unit": "blocks/s", "ms_per_step": c_ms,
-                       "cells": total_cells, "ok": cells_ok,
-                       "kernel_ms": c_prof.ms["mc"] / max(1, c_prof.count["mc"]),
-                       "frac": (N * BYTES_PER_BLOCK + cell_bytes) /
-                               (c_prof.ms["mc"] / max(1, c_prof.count["mc"]) / 1e3) / 1e9 / peak,
-                       "note": "same launch + fused compaction of the non-empty cells (u16 flat + u32 cell, ranges "
-                               "reserved by one atomic per block); frac counts +6 B per cell"},
+                       "cells": total_cells, "ok": cells_ok, "kernel_ms": ck_ms,
+                       "frac": (N * BYTES_PER_BLOCK + cell_bytes) / (ck_ms / 1e3) / 1e9 / peak,
+                       "note": "the same launch + fused compaction of the non-empty cells (u16 flat + u32 cell; one "
+                               "atomic range reservation per block); frac counts +6 B per cell; checked by "
+                               "scatter-back of every block"},
            "incremental_packs": {"ms_per_step": p_ms, "value": world * N / (p_ms / 1e3),
-                                 "note": "face-pack side table rebuilt for all rows (k_mc_faces) + encode reading it "
-                                         "(the ingest-maintained variant the server uses)"},
-           "scattered_halo": {"ms_per_step": g_ms, "value": world * N / (g_ms / 1e3),
-                              "note": "encode without packs: 217 halo voxels gathered per block"},
+                                 "encode_only_ms": f_ms,
+                                 "note": "ingest-maintained variant (GpuServerCore): k_mc_faces rebuilds the face "
+                                         "bit-packs of ALL rows + the encode reading them, both timed; "
+                                         "encode_only_ms = the encode alone when packs are current"},
            "two_pass_compact_ms": tp_ms}
     if not args.no_e2e:
         # e2e: host TSDF rows -> device pool, encode, MC + quantised bytes -> host
@@ -555,7 +552,7 @@ def run_mc(args, dev, world=1):
         for _ in range(steps):
             dev_rows = host_rows.to(dev, non_blocking=True)
             pool.index_copy_(0, posl, dev_rows)
-            m, qq, _, _ = encode_full(t, pool, keys, state=state, counts=False)
+            m, qq, _ = encode_keys(t, pool, keys, mc=mc, q=q, counts=False)
             h_mc.copy_(m, non_blocking=True)
             h_q.copy_(qq, non_blocking=True)
         e1.record()

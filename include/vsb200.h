@@ -206,34 +206,26 @@ vs_status vs_mc_encode_keys(const vs_table *tsdf_table, const uint8_t *pool,
                             uint8_t *mc_out, int8_t *q_out, uint32_t *counts,
                             vs_stream_t stream);
 
-/* Full encode with in-kernel face packs (NEW; mc_encoding.py:118-172 for
- * every block of the map).  Neighbour rows come from `tsdf_table` lookups
- * of keys (t != NULL) or from nbr[n][8] (t == NULL).  The face bit-pack of
- * every centre row is computed from its staged copy and published at
- * packs + 96*row as 12 {u32 data, u32 epoch} 64-bit pairs (x, y, z face;
- * words {inside lo, inside hi, observed lo, observed hi} as vs_mc_faces);
- * epoch != 0 and different from the previous launch on `packs` (zeroed once
- * at allocation).  The halo of a block comes from its neighbours' packs of
- * this epoch; the halo bits of a neighbour whose pack is not published
- * when needed (not a centre in this launch, or its CTA runs behind) are
- * gathered from the pool instead (identical output, more traffic), so use
- * it for full encodes.  Outputs as vs_mc_encode; counts[i] is written (no pre-zeroing).
- * With cell_flat and cell_mc non-NULL the non-empty cells are compacted in
- * the same pass: block i's cells (ascending flat index) are
- * [offsets[i], offsets[i] + counts[i]) of cell_flat / cell_mc, ranges
- * reserved through the device counter *cursor (zeroed by the call; final
- * value = total cells); at most cell_cap cells are written (check
- * *cursor <= cell_cap).  Ranges follow reservation order; vs_mc_compact
- * gives the exact-prefix layout. */
-vs_status vs_mc_encode_full(const vs_table *tsdf_table, const uint8_t *pool,
-                            const int32_t *keys, const int32_t *nbr, uint64_t n,
-                            uint8_t *packs, uint32_t epoch,
-                            uint8_t *mc_out, int8_t *q_out, uint32_t *counts,
-                            unsigned long long *cursor, uint32_t *offsets,
-                            uint16_t *cell_flat, uint32_t *cell_mc, uint64_t cell_cap,
-                            vs_stream_t stream);
-/* Diagnostic: packs gathered from the pool (not published in time) since load. */
-uint64_t vs_mc_self_fallbacks(void);
+/* vs_mc_encode_keys plus three options (NEW):
+ *   n_dev (may be NULL): only the first min(n, *n_dev) keys are encoded -- a
+ *     device-produced count (vs_affected_dedup) needs no host sync;
+ *   out_rows (may be NULL): block i's MC / quantised bytes go to row
+ *     out_rows[i] of mc_out / q_out (e.g. the MC map's position of key i,
+ *     so the encoder writes straight into a server's MC pool);
+ *   fused compaction (cell_flat and cell_mc non-NULL): block i's
+ *     non-empty cells in ascending flat index at [offsets[i], offsets[i] +
+ *     counts[i]) of cell_flat / cell_mc, each range reserved with one atomic
+ *     on the device counter *cursor (zeroed by the call; final value = total
+ *     cells; at most cell_cap cells are written -- check *cursor <= cell_cap).
+ *     Ranges follow reservation order; vs_mc_compact gives the exact-prefix
+ *     layout from dense bytes. */
+vs_status vs_mc_encode_keys_ex(const vs_table *tsdf_table, const uint8_t *pool,
+                               const uint8_t *faces, const int32_t *keys, uint64_t n,
+                               const uint64_t *n_dev, const int32_t *out_rows,
+                               uint8_t *mc_out, int8_t *q_out,
+                               uint32_t *counts, unsigned long long *cursor,
+                               uint32_t *offsets, uint16_t *cell_flat, uint32_t *cell_mc,
+                               uint64_t cell_cap, vs_stream_t stream);
 
 /* Face bit-packs of pool rows (the halo side table of the encoder; NEW):
  * for rows[i] (or row i when rows is NULL), faces + 48*row receives the

@@ -22,9 +22,7 @@ from .mc_encoding import (
     apply_cutoff,
     compact,
     compute_mc_index,
-    FaceState,
     encode_blocks,
-    encode_full,
     encode_keys,
     face_packs,
     neighbors,
@@ -38,7 +36,7 @@ from .voxel_model import BLOCK_EDGE, TsdfBlock
 __all__ = [
     "BLOCK_EDGE", "BlockHashMap", "BlockHashSet", "BlockKey", "CapacityExhausted", "FreeListStack",
     "GpuServerCore", "McBlock", "McVoxel", "NativeUnavailable", "StreamSet", "TsdfBlock",
-    "affected_mc_blocks", "apply_cutoff", "compact", "compute_mc_index", "encode_blocks", "encode_full", "encode_keys", "FaceState", "face_packs",
+    "affected_mc_blocks", "apply_cutoff", "compact", "compute_mc_index", "encode_blocks", "encode_keys", "face_packs",
     "extract_random_many", "fan_out", "hash_key", "hash_keys", "neighbors", "pack_mc_batch", "recompute_mc_block", "recompute_mc_blocks",
     "remove_everywhere",
 ]

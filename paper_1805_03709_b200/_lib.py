@@ -72,9 +72,8 @@ SIGNATURES: dict[str, tuple] = {
     "vs_mc_encode": (_i32, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "vs_mc_encode_keys": (_i32, [_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "vs_mc_faces": (_i32, [_vp, _vp, _u64, _vp, _vp]),
-    "vs_mc_encode_full": (_i32, [_vp, _vp, _vp, _vp, _u64, _vp, ctypes.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp,
-                                 _vp, _u64, _vp]),
-    "vs_mc_self_fallbacks": (_u64, []),
+    "vs_mc_encode_keys_ex": (_i32, [_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _u64,
+                                    _vp]),
     "vs_mc_neighbors": (_i32, [_vp, _vp, _u64, _vp, _vp]),
     "vs_mc_compact": (_i32, [_vp, _vp, _u64, _vp, _vp, _vp, _u64, _vp, _vp]),
     "vs_scan_workspace_bytes": (_u64, [_u64]),

@@ -179,6 +179,8 @@ struct McSmem {
   uint32_t ex_in[2][162];
   uint32_t ex_ob[2][162];
   int32_t nb[2][kLook][8];  // neighbour rows of two lookup batches
+  uint32_t wsum[4];         // kCells: per-warp non-empty counts of the block
+  uint32_t cbase;           // kCells: reserved start of the block's cell range
 };
 
 // Sweep order (experiment knob VSB_MC_REVERSE): block of sweep index i.
@@ -347,14 +349,28 @@ __global__ void __launch_bounds__(256) k_mc_faces(const uint8_t* __restrict__ po
       ((uint4*)(faces + (uint64_t)row * kFaceBytes))[f] = make_uint4(word[f][0], word[f][1], word[f][2], word[f][3]);
 }
 
-template <bool kFromKeys, bool kFaces>
+// Optional fused compaction (kCells): the block's non-empty
+// cells are written in ascending flat index at a range reserved with ONE
+// atomicAdd on a global cursor; offsets[blk] = the range start, counts[blk]
+// = its length.  Each block's list is contiguous and ordered; ranges follow
+// reservation order (the offsets table is the input-order view;
+// vs_mc_compact gives the exact-prefix layout).  out_rows (optional): the
+// MC / quantised outputs of block i go to row out_rows[i] (e.g. the MC map
+// position of the block's key) instead of row i.
+template <bool kFromKeys, bool kFaces, bool kCells>
 __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS : VSB_MC_MINBLOCKS_NBR) k_mc_encode(TableView T, const uint8_t* __restrict__ pool,
                                                           const uint8_t* __restrict__ faces,
                                                           const int32_t* __restrict__ keys,
                                                           const int32_t* __restrict__ nbr, uint64_t n,
+                                                          const uint64_t* __restrict__ n_dev,
+                                                          const int32_t* __restrict__ out_rows,
                                                           uint32_t* __restrict__ mc_out, int8_t* __restrict__ q_out,
-                                                          uint32_t* __restrict__ counts) {
+                                                          uint32_t* __restrict__ counts,
+                                                          unsigned long long* cursor, uint32_t* __restrict__ offsets,
+                                                          uint16_t* __restrict__ cell_flat,
+                                                          uint32_t* __restrict__ cell_mc, uint64_t cell_cap) {
   __shared__ McSmem sm;
+  if (n_dev) n = min(n, *n_dev);  // a device-produced count (no host sync in the server tick)
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
   const uint64_t G = gridDim.x;
@@ -402,8 +418,9 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     }
     __syncthreads();  // (A) lookups + packs ready, grids zeroed, buf[(j+kAhead)%kStages] no longer read
     if (t == 0 && j + kAhead < nj) issue_centre(sm, j + kAhead, pool);
-    uint32_t* mc_blk = mc_out ? mc_out + blk * VS_BLOCK_VOXELS : nullptr;
-    int8_t* q_blk = q_out ? q_out + blk * VS_BLOCK_VOXELS : nullptr;
+    const uint64_t orow = out_rows ? (uint64_t)(uint32_t)__ldg(out_rows + blk) : blk;
+    uint32_t* mc_blk = mc_out ? mc_out + orow * VS_BLOCK_VOXELS : nullptr;
+    int8_t* q_blk = q_out ? q_out + orow * VS_BLOCK_VOXELS : nullptr;
     const HaloRegs cur = hal;
     if (j + 1 < nj) {
       if (kFaces) {
@@ -416,6 +433,7 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
       // absent centre: every cube's origin lives here -> all zero (:152-156)
       if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(0u, 0u, 0u, 0u));
       if (q_blk) __stcs((uint32_t*)(q_blk + 4 * t), 0x80808080u);
+      if (kCells && t == 0) offsets[blk] = 0u;
       continue;  // counts[blk] stays 0
     }
 
@@ -518,358 +536,9 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     }
     if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(word[0], word[1], word[2], word[3]));
     if (q_blk) __stcs((uint32_t*)(q_blk + 4 * t), qw);
-    if (counts) {  // counts are zeroed by the launch: one reduction per warp, no barrier
-      nz = __reduce_add_sync(0xffffffffu, nz);
-      if (lane == 0 && nz) atomicAdd(counts + blk, nz);
-    }
-  }
-}
-
-// ---- full encode with in-kernel face packs ("self-packing", NEW) --------
-//
-// A full encode (every row of the map is a centre) needs no side table: the
-// face bit-pack of a row is computed from its centre copy in shared memory
-// (free: the row is staged anyway) and published as {data, epoch} pairs; a
-// block reads the packs of its 7 positive neighbours that carry this
-// launch's epoch.  Blocks are swept in DESCENDING input order, so in
-// key-sorted input the +x/+y/+z neighbours of a block are swept before it,
-// and a CTA produces the pack of block j+2 at the end of iteration j (three
-// TMA stages), one iteration before the CTAs of the same wave prefetch it.
-// A pack that is not published when the block needs it (a neighbour that is
-// not a centre in this launch, or a CTA running behind) is never waited
-// for: the halo bits it would carry are gathered from the pool by the whole
-// CTA in one round trip -- identical bits, so the output never depends on
-// timing.  After the launch the packs are current for every encoded row.
-//
-// Optional fused compaction: the block's non-empty cells are
-// written in ascending flat index at a range reserved with ONE atomicAdd on
-// a global cursor; offsets[blk] = the range start, counts[blk] = its length.
-// Each block's list is contiguous and ordered; blocks are placed in
-// reservation order (the offsets table gives the input-order view; the
-// exact-prefix layout is vs_mc_compact's).
-constexpr int kSelfStages = 3;
-#ifndef VSB_MC_SELF_MINBLOCKS
-#define VSB_MC_SELF_MINBLOCKS 9
-#endif
-
-struct McSelfSmem {
-  alignas(128) uint8_t buf[kSelfStages][VS_TSDF_BLOCK_BYTES];
-  alignas(8) uint64_t mbar[kSelfStages];
-  uint4 pk[2][8];
-  uint32_t ex_in[2][162];
-  uint32_t ex_ob[2][162];
-  int32_t nb[2][kLook][8];
-  uint32_t wsum[4];
-  uint32_t cbase;
-  uint32_t miss[2];   // neighbours whose pack was not published in time (bit c-1)
-  uint32_t tmiss[2];  // ... at prefetch time (one iteration ahead)
-};
-
-// Pack bit of halo item i (halo_item order) within its neighbour's face word.
-__device__ __forceinline__ int halo_pack_bit(int i) {
-  return i < 192 ? (i & 63) : (i < 200 ? 8 * (i - 192) : (i < 208 ? i - 200 : (i < 216 ? i - 208 : 0)));
-}
-
-__device__ __forceinline__ uint64_t mc_globaltimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-// flat voxel index of bit i of face f (0: x = 0 face, bit y + 8z; 1: y = 0,
-// bit x + 8z; 2: z = 0, bit x + 8y) -- the layout of k_mc_faces
-__device__ __forceinline__ int face_flat(int f, int i) {
-  const int a = i & 7, b = i >> 3;
-  return f == 0 ? 8 * a + 64 * b : (f == 1 ? a + 64 * b : a + 8 * b);
-}
-
-// Warp-wide: the 3 face words of a staged centre row (all lanes get them).
-__device__ __forceinline__ void pack_from_smem(const uint8_t* buf, uint32_t lane, uint4 (&w)[3]) {
-#pragma unroll
-  for (int f = 0; f < 3; ++f) {
-    uint32_t r[4];
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const uint32_t* v = (const uint32_t*)(buf + 12 * face_flat(f, (int)lane + 32 * half));
-      r[half] = __ballot_sync(0xFFFFFFFFu, inside_bit(v[0]));
-      r[2 + half] = __ballot_sync(0xFFFFFFFFu, observed_bit(v[1]));
-    }
-    w[f] = make_uint4(r[0], r[1], r[2], r[3]);
-  }
-}
-
-// Published packs (self-packing launches): per row 3 faces x 4 words, each
-// word stored as ONE 64-bit pair {data, epoch} (96 B per row).  An aligned
-// 64-bit access is single-copy atomic, so a reader that sees this launch's
-// epoch in all 4 pairs of a face has that face's data: no flag, no fence
-// (a release fence after the packs would wait for the block's streaming
-// output stores as well).
-constexpr int kPubBytes = 96;
-
-__device__ unsigned long long g_mc_self_fallbacks;  // packs gathered from the pool (diagnostic)
-#ifndef VSB_MC_SELF_DEBUG
-#define VSB_MC_SELF_DEBUG 0
-#endif
-__device__ unsigned long long g_mc_self_miss_c[8];  // per neighbour c-1 (VSB_MC_SELF_DEBUG)
-
-__device__ __forceinline__ bool try_face(const uint8_t* pub, uint32_t epoch, int32_t row, int c, uint4& out) {
-  if (row < 0) {
-    out = make_uint4(0u, 0u, 0u, 0u);
-    return true;
-  }
-  const unsigned long long* p = (const unsigned long long*)(pub + (uint64_t)row * kPubBytes) + 4 * face_kind(c);
-  unsigned long long a, b, c2, d;
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(c2), "=l"(d) : "l"(p + 2) : "memory");
-  if ((uint32_t)(a >> 32) != epoch || (uint32_t)(b >> 32) != epoch || (uint32_t)(c2 >> 32) != epoch ||
-      (uint32_t)(d >> 32) != epoch)
-    return false;
-  out = make_uint4((uint32_t)a, (uint32_t)b, (uint32_t)c2, (uint32_t)d);
-  return true;
-}
-
-// Sweep assignment: CTA b takes the contiguous sweep range [b*J, (b+1)*J)
-// (J = ceil(n / grid)), in order.  A block's +x and +y neighbours (1 and
-// one key row away in sorted input) are then this CTA's own recent blocks,
-// whose packs it published itself two iterations ahead; only the +z pack
-// (a key slab away) may come from another CTA and be missing.
-// VSB_MC_SELF_CHUNK=0: grid-stride sweep instead (experiment).
-#ifndef VSB_MC_SELF_CHUNK
-#define VSB_MC_SELF_CHUNK 1
-#endif
-__device__ __forceinline__ uint64_t self_chunk(uint64_t n) { return (n + gridDim.x - 1) / gridDim.x; }
-__device__ __forceinline__ uint64_t self_sweep(uint64_t n, uint64_t j) {
-  return VSB_MC_SELF_CHUNK ? (uint64_t)blockIdx.x * self_chunk(n) + j : blockIdx.x + j * (uint64_t)gridDim.x;
-}
-// blocks of this CTA
-__device__ __forceinline__ uint64_t self_count(uint64_t n) {
-  if (!VSB_MC_SELF_CHUNK) return blockIdx.x < n ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const uint64_t J = self_chunk(n), b0 = (uint64_t)blockIdx.x * J;
-  return b0 < n ? min(J, n - b0) : 0;
-}
-
-template <bool kFromKeys>
-__device__ __forceinline__ void lookup_batch_desc(McSelfSmem& sm, int buf, const TableView& T, const int32_t* keys,
-                                                  const int32_t* nbr, uint64_t n, uint64_t j0) {
-  const int t = threadIdx.x;
-  const int slot = t >> 3, c = t & 7;
-  const uint64_t sblk = self_sweep(n, j0 + slot);
-  const bool in = j0 + slot < self_count(n);
-  sm.nb[buf][slot][c] = in ? load_nbr<kFromKeys>(T, keys, nbr, n - 1 - sblk, c) : -1;
-}
-
-__device__ __forceinline__ const int32_t* nb_of_self(const McSelfSmem& sm, uint64_t j) {
-  return sm.nb[(j / kLook) & 1][j % kLook];
-}
-
-__device__ __forceinline__ void issue_centre_self(McSelfSmem& sm, uint64_t j, const uint8_t* __restrict__ pool) {
-  const int32_t row = nb_of_self(sm, j)[0];
-  const int b = (int)(j % kSelfStages);
-  if (row < 0) {  // absent centre: complete the stage's phase anyway, so parity = (j / kSelfStages) & 1
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.mbar[b])) : "memory");
-    return;
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  mbar_arrive_expect_tx(&sm.mbar[b], VS_TSDF_BLOCK_BYTES);
-  tma_load_1d(sm.buf[b], pool + (uint64_t)row * VS_TSDF_BLOCK_BYTES, VS_TSDF_BLOCK_BYTES, &sm.mbar[b]);
-}
-
-// Warp 0: wait for the centre copy of block j and publish its face pack
-// (lanes 0-5 store one 16-B half-face each: two {data, epoch} pairs).
-__device__ __forceinline__ void produce_pack(McSelfSmem& sm, uint64_t j, uint8_t* pub, uint32_t epoch) {
-  const int32_t row = nb_of_self(sm, j)[0];
-  if (row < 0) return;
-  const int b = (int)(j % kSelfStages);
-  mbar_wait(&sm.mbar[b], (uint32_t)((j / kSelfStages) & 1));
-  uint4 w[3];
-  pack_from_smem(sm.buf[b], threadIdx.x & 31u, w);
-  const uint32_t lane = threadIdx.x & 31u;
-  if (lane < 6) {
-    const uint4 f = lane < 2 ? w[0] : (lane < 4 ? w[1] : w[2]);
-    const uint32_t lo = (lane & 1) ? f.z : f.x, hi = (lane & 1) ? f.w : f.y;
-    const unsigned long long e = (unsigned long long)epoch << 32;
-    unsigned long long* dst = (unsigned long long*)(pub + (uint64_t)row * kPubBytes) + 2 * lane;
-    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1,%2};" ::"l"(dst), "l"(e | lo), "l"(e | hi) : "memory");
-  }
-}
-
-template <bool kFromKeys, bool kCells>
-__global__ void __launch_bounds__(kMcThreads, VSB_MC_SELF_MINBLOCKS)
-    k_mc_encode_self(TableView T, const uint8_t* __restrict__ pool, uint8_t* pub, uint32_t epoch,
-                     const int32_t* __restrict__ keys, const int32_t* __restrict__ nbr, uint64_t n,
-                     uint32_t* __restrict__ mc_out, int8_t* __restrict__ q_out, uint32_t* __restrict__ counts,
-                     unsigned long long* cursor, uint32_t* __restrict__ offsets, uint16_t* __restrict__ cell_flat,
-                     uint32_t* __restrict__ cell_mc, uint64_t cell_cap) {
-  __shared__ McSelfSmem sm;
-  const int t = threadIdx.x;
-  const int lane = t & 31, warp = t >> 5;
-  const uint64_t nj = self_count(n);
-
-  if (t == 0) {
-    for (int b = 0; b < kSelfStages; ++b) mbar_init(&sm.mbar[b], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  lookup_batch_desc<kFromKeys>(sm, 0, T, keys, nbr, n, 0);
-  __syncthreads();
-  if (t == 0)
-    for (uint64_t j = 0; j < 2 && j < nj; ++j) issue_centre_self(sm, j, pool);
-  if (warp == 0)
-    for (uint64_t j = 0; j < 2 && j < nj; ++j) produce_pack(sm, j, pub, epoch);
-  uint4 fpk = make_uint4(0u, 0u, 0u, 0u);  // thread t < 7: neighbour t+1's face word, one block ahead
-  bool have = true;
-  const HaloDesc hd = halo_desc();  // this thread's two halo items (for rebuilding a missing pack)
-  int pbit[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) pbit[k] = halo_pack_bit((int)threadIdx.x + k * kMcThreads);
-  uint32_t fallbacks = 0;
-  // halo items of neighbours whose pack was not published at prefetch time,
-  // gathered from the pool one iteration ahead (like the scattered path, but
-  // only for the missing faces): hv[k] = item k loaded
-  uint32_t htb[2] = {0u, 0u}, hwb[2] = {0u, 0u};
-  bool hv[2] = {false, false};
-  auto prefetch_missing = [&](uint64_t jn) {  // every thread, after a barrier that published tmiss
-    const uint32_t tm = sm.tmiss[jn & 1];
-    const int32_t* nbn = nb_of_self(sm, jn);
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int c = hd.c[k];
-      hv[k] = c > 0 && ((tm >> (c - 1)) & 1u) && nbn[0] >= 0;
-      if (hv[k]) {
-        const uint32_t* src = (const uint32_t*)(pool + (uint64_t)nbn[c] * VS_TSDF_BLOCK_BYTES + hd.off[k]);
-        htb[k] = __ldg(src);
-        hwb[k] = __ldg(src + 1);
-      }
-    }
-  };
-  auto try_next = [&](uint64_t jn) {  // warp 0: prefetch block jn's packs, publish the tentative misses
-    bool ok = true;
-    if (t < 7) {
-      have = try_face(pub, epoch, nb_of_self(sm, jn)[t + 1], t + 1, fpk);
-      ok = have;
-    }
-    const uint32_t m = __ballot_sync(0xffffffffu, !ok);
-    if (t == 0) sm.tmiss[jn & 1] = m;
-  };
-  if (nj) {
-    if (warp == 0) try_next(0);
-    __syncthreads();
-    prefetch_missing(0);
-  }
-
-  for (uint64_t j = 0; j < nj; ++j) {
-    const uint64_t blk = n - 1 - self_sweep(n, j);
-    const int s = (int)(j & 1);
-    const int b = (int)(j % kSelfStages);
-    const int slot = (int)(j % kLook);
-    const int32_t* nbc = nb_of_self(sm, j);
-    const int32_t centre = nbc[0];
-    if (slot == kLook - 2 && j + 2 < nj)
-      lookup_batch_desc<kFromKeys>(sm, (int)(((j / kLook) + 1) & 1), T, keys, nbr, n, (j / kLook + 1) * kLook);
-    if (warp == 0) {  // lanes 0-6 settle the 7 packs; a missing one is rebuilt from the pool below
-      bool ok = true;
-      if (t < 7) {
-        if (!have) have = try_face(pub, epoch, nbc[t + 1], t + 1, fpk);
-        ok = have;
-        sm.pk[s][t] = have ? fpk : make_uint4(0u, 0u, 0u, 0u);
-      }
-      const uint32_t miss = __ballot_sync(0xffffffffu, !ok);
-      if (t == 0) sm.miss[s] = miss;
-    }
-    __syncthreads();  // (A) packs + lookups ready; buf[(j+2)%3] (block j-1) no longer read
-    if (t == 0 && j + 2 < nj) issue_centre_self(sm, j + 2, pool);
-    if (warp == 0 && j + 1 < nj) try_next(j + 1);
-    uint32_t* mc_blk = mc_out ? mc_out + blk * VS_BLOCK_VOXELS : nullptr;
-    int8_t* q_blk = q_out ? q_out + blk * VS_BLOCK_VOXELS : nullptr;
-    const uint32_t miss = sm.miss[s];
-    if (centre < 0) {
-      if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(0u, 0u, 0u, 0u));
-      if (q_blk) __stcs((uint32_t*)(q_blk + 4 * t), 0x80808080u);
-      if (t == 0) {
-        if (counts) counts[blk] = 0u;
-        if (kCells) offsets[blk] = 0u;
-      }
-      __syncthreads();  // (B) tmiss of block j+1 visible (as in the other branch)
-    } else {
-      if (miss) {
-        // packs still not published (a neighbour outside this launch, or a
-        // CTA behind this one): the halo bits they would carry were gathered
-        // from the pool one iteration ahead; OR them into the zeroed words
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int c = hd.c[k];
-          if (hv[k] && ((miss >> (c - 1)) & 1u)) {
-            const int pb = pbit[k];
-            uint4& w = sm.pk[s][c - 1];
-            if (inside_bit(htb[k])) atomicOr(pb < 32 ? &w.x : &w.y, 1u << (pb & 31));
-            if (observed_bit(hwb[k])) atomicOr(pb < 32 ? &w.z : &w.w, 1u << (pb & 31));
-          }
-        }
-        if (t == 0) fallbacks += __popc(miss);
-#if VSB_MC_SELF_DEBUG
-        if (t < 7 && ((miss >> t) & 1u)) atomicAdd(&g_mc_self_miss_c[t], 1ull);
-#endif
-        __syncthreads();  // (A2) rebuilt packs complete
-      }
-      if (t >= 64 && t < 81) {  // the 17 +y / +z face rows, as in k_mc_encode<kFaces>
-        uint4 lo, hi;
-        int kb, ib, row;
-        if (t < 72) {
-          lo = sm.pk[s][1], hi = sm.pk[s][2], kb = t - 64, ib = 8 * (t - 64), row = (t - 64) * 9 + 8;
-        } else if (t < 80) {
-          lo = sm.pk[s][3], hi = sm.pk[s][4], kb = t - 72, ib = t - 72, row = 72 + (t - 72);
-        } else {
-          lo = sm.pk[s][5], hi = sm.pk[s][6], kb = 0, ib = 0, row = 80;
-        }
-        const uint32_t vi = byte64(lo.x, lo.y, kb) | (bit64(hi.x, hi.y, ib) << 8);
-        const uint32_t vo = byte64(lo.z, lo.w, kb) | (bit64(hi.z, hi.w, ib) << 8);
-        sm.ex_in[s][2 * row] = pair4(vi);
-        sm.ex_in[s][2 * row + 1] = pair4(vi >> 4);
-        sm.ex_ob[s][2 * row] = pair4(vo);
-        sm.ex_ob[s][2 * row + 1] = pair4(vo >> 4);
-      }
-      mbar_wait(&sm.mbar[b], (uint32_t)((j / kSelfStages) & 1));  // completed: warp 0 published its pack
-      const uint4* b128 = (const uint4*)(sm.buf[b] + 48 * t);
-      const uint4 p0 = b128[0], p1 = b128[1], p2 = b128[2];
-      const uint32_t tb[4] = {p0.x, p0.w, p1.z, p2.y};
-      const uint32_t wb[4] = {p0.y, p1.x, p1.w, p2.z};
-      const uint32_t rgb[4] = {p0.z & 0xFFFFFFu, p1.y & 0xFFFFFFu, p2.x & 0xFFFFFFu, p2.w & 0xFFFFFFu};
-      const int h = t & 1, r = t >> 1, y = r & 7, z = r >> 3, x0 = 4 * h;
-      uint32_t in4 = 0, ob4 = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        in4 |= inside_bit(tb[k]) << k;
-        ob4 |= observed_bit(wb[k]) << k;
-      }
-      uint32_t in_row = in4 << x0, ob_row = ob4 << x0;
-      in_row |= __shfl_xor_sync(0xffffffffu, in_row, 1);
-      ob_row |= __shfl_xor_sync(0xffffffffu, ob_row, 1);
-      {
-        const uint4 c1 = sm.pk[s][0];
-        const int i = y + 8 * z;
-        const uint32_t vi = in_row | (bit64(c1.x, c1.y, i) << 8);
-        const uint32_t vo = ob_row | (bit64(c1.z, c1.w, i) << 8);
-        sm.ex_in[s][2 * (z * 9 + y) + h] = pair4(vi >> x0);
-        sm.ex_ob[s][2 * (z * 9 + y) + h] = pair4(vo >> x0);
-      }
-      __syncthreads();  // (B) bit grids complete
-      const int r00 = z * 9 + y;
-      const uint32_t* ei = sm.ex_in[s] + h;
-      const uint32_t* eo = sm.ex_ob[s] + h;
-      const uint32_t I = ei[2 * r00] | (ei[2 * (r00 + 1)] << 2) | (ei[2 * (r00 + 9)] << 4) | (ei[2 * (r00 + 10)] << 6);
-      const uint32_t O = eo[2 * r00] | (eo[2 * (r00 + 1)] << 2) | (eo[2 * (r00 + 9)] << 4) | (eo[2 * (r00 + 10)] << 6);
-      const uint32_t keep = __vcmpeq4(O, 0xFFFFFFFFu) & ~__vcmpeq4(I, 0xFFFFFFFFu);
-      const uint32_t idx4 = I & keep;
-      const uint32_t nzm = __vcmpne4(idx4, 0u);
-      const uint32_t nz = __popc(nzm) >> 3;
-      uint32_t word[4], qw = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        word[k] = ((nzm >> (8 * k)) & 1u) ? ((idx4 >> (8 * k)) & 0xFFu) | (rgb[k] << 8) : 0u;
-        qw |= ((uint32_t)quantise(tb[k], wb[k]) & 0xFFu) << (8 * k);
-      }
-      if (mc_blk) __stcs((uint4*)(mc_blk + 4 * t), make_uint4(word[0], word[1], word[2], word[3]));
-      if (q_blk) __stcs((uint32_t*)(q_blk + 4 * t), qw);
-      // block total: warp inclusive scan of nz, warp totals through smem
+    if (kCells) {
+      // block total (warp inclusive scans, warp totals through shared memory),
+      // ONE reservation, then every thread writes its non-empty voxels
       uint32_t incl = nz;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -879,35 +548,30 @@ __global__ void __launch_bounds__(kMcThreads, VSB_MC_SELF_MINBLOCKS)
       if (lane == 31) sm.wsum[warp] = incl;
       __syncthreads();  // (C)
       const uint32_t w0 = sm.wsum[0], w1 = sm.wsum[1], w2 = sm.wsum[2], w3 = sm.wsum[3];
-      const uint32_t total = w0 + w1 + w2 + w3;
-      if (kCells) {
-        if (t == 0) {
-          const unsigned long long base = total ? atomicAdd(cursor, (unsigned long long)total) : 0ull;
-          sm.cbase = (uint32_t)base;
-          offsets[blk] = (uint32_t)base;
-        }
-        __syncthreads();  // (D)
-        const uint32_t wpre = (warp > 0 ? w0 : 0u) + (warp > 1 ? w1 : 0u) + (warp > 2 ? w2 : 0u);
-        uint64_t d = (uint64_t)sm.cbase + wpre + (incl - nz);
+      if (t == 0) {
+        const uint32_t total = w0 + w1 + w2 + w3;
+        const unsigned long long base = total ? atomicAdd(cursor, (unsigned long long)total) : 0ull;
+        sm.cbase = (uint32_t)base;
+        offsets[blk] = (uint32_t)base;
+        if (counts) counts[blk] = total;
+      }
+      __syncthreads();  // (D)
+      uint64_t d = (uint64_t)sm.cbase + (warp > 0 ? w0 : 0u) + (warp > 1 ? w1 : 0u) + (warp > 2 ? w2 : 0u) + incl - nz;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if ((nzm >> (8 * k)) & 1u) {
-            if (d < cell_cap) {
-              cell_flat[d] = (uint16_t)(4 * t + k);
-              cell_mc[d] = word[k];
-            }
-            ++d;
+      for (int k = 0; k < 4; ++k) {
+        if ((nzm >> (8 * k)) & 1u) {
+          if (d < cell_cap) {
+            __stcs(cell_flat + d, (uint16_t)(4 * t + k));
+            __stcs(cell_mc + d, word[k]);
           }
+          ++d;
         }
       }
-      if (t == 0 && counts) counts[blk] = total;
+    } else if (counts) {  // counts are zeroed by the launch: one reduction per warp, no barrier
+      nz = __reduce_add_sync(0xffffffffu, nz);
+      if (lane == 0 && nz) atomicAdd(counts + blk, nz);
     }
-    // gather the halo items of block j+1's missing packs (tmiss published
-    // before barrier B), then produce the pack of block j+2
-    if (j + 1 < nj) prefetch_missing(j + 1);
-    if (warp == 0 && j + 2 < nj) produce_pack(sm, j + 2, pub, epoch);
   }
-  if (t == 0 && fallbacks) atomicAdd(&g_mc_self_fallbacks, (unsigned long long)fallbacks);
 }
 
 __global__ void k_mc_neighbors(TableView T, const int32_t* __restrict__ keys, uint64_t n,
@@ -945,69 +609,57 @@ __global__ void __launch_bounds__(256) k_mc_compact(const uint32_t* __restrict__
   }
 }
 
-static int g_mc_grid[4] = {0, 0, 0, 0};
+static int g_mc_grid[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
-template <bool kFromKeys, bool kFaces>
+struct McOut {
+  const uint64_t* n_dev;
+  const int32_t* out_rows;
+  uint8_t* mc;
+  int8_t* q;
+  uint32_t* counts;
+  unsigned long long* cursor;
+  uint32_t* offsets;
+  uint16_t* cell_flat;
+  uint32_t* cell_mc;
+  uint64_t cell_cap;
+};
+
+template <bool kFromKeys, bool kFaces, bool kCells>
 static vs_status launch_mc_t(const TableView& T, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
-                             const int32_t* nbr, uint64_t n, uint8_t* mc_out, int8_t* q_out, uint32_t* counts,
-                             cudaStream_t s) {
-  int& grid = g_mc_grid[(kFromKeys ? 1 : 0) + (kFaces ? 2 : 0)];
+                             const int32_t* nbr, uint64_t n, const McOut& o, cudaStream_t s) {
+  int& grid = g_mc_grid[(kFromKeys ? 1 : 0) + (kFaces ? 2 : 0) + (kCells ? 4 : 0)];
   if (grid == 0) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mc_encode<kFromKeys, kFaces>, kMcThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mc_encode<kFromKeys, kFaces, kCells>, kMcThreads, 0);
     if (per_sm < 1) per_sm = 1;
     grid = sms * per_sm;
   }
   const uint64_t g = n < (uint64_t)grid ? n : (uint64_t)grid;
-  if (counts) VS_CK(cudaMemsetAsync(counts, 0, 4 * n, s));
+  if (o.counts) VS_CK(cudaMemsetAsync(o.counts, 0, 4 * n, s));
+  if (kCells) VS_CK(cudaMemsetAsync(o.cursor, 0, 8, s));
   {
     ProfScope prof(1, s);
-    k_mc_encode<kFromKeys, kFaces><<<(unsigned)g, kMcThreads, 0, s>>>(T, pool, faces, keys, nbr, n,
-                                                                        (uint32_t*)mc_out, q_out, counts);
+    k_mc_encode<kFromKeys, kFaces, kCells><<<(unsigned)g, kMcThreads, 0, s>>>(
+        T, pool, faces, keys, nbr, n, o.n_dev, o.out_rows, (uint32_t*)o.mc, o.q, o.counts, o.cursor, o.offsets, o.cell_flat,
+        o.cell_mc, o.cell_cap);
     vsb::count_launch();
   }
   VS_CK_LAUNCH("k_mc_encode");
   return VS_OK;
 }
 
-static int g_self_grid[4] = {0, 0, 0, 0};
-
-template <bool kFromKeys, bool kCells>
-static vs_status launch_self_t(const TableView& T, const uint8_t* pool, const int32_t* keys, const int32_t* nbr,
-                               uint64_t n, uint8_t* pub, uint32_t epoch, uint8_t* mc_out,
-                               int8_t* q_out, uint32_t* counts, unsigned long long* cursor, uint32_t* offsets,
-                               uint16_t* cell_flat, uint32_t* cell_mc, uint64_t cell_cap, cudaStream_t s) {
-  int& grid = g_self_grid[(kFromKeys ? 1 : 0) + (kCells ? 2 : 0)];
-  if (grid == 0) {
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mc_encode_self<kFromKeys, kCells>, kMcThreads, 0);
-    if (per_sm < 1) per_sm = 1;
-    grid = sms * per_sm;  // persistent: every CTA resident (a pack wait never waits on an unscheduled CTA)
-  }
-  const uint64_t g = n < (uint64_t)grid ? n : (uint64_t)grid;
-  if (kCells) VS_CK(cudaMemsetAsync(cursor, 0, 8, s));
-  {
-    ProfScope prof(1, s);
-    k_mc_encode_self<kFromKeys, kCells><<<(unsigned)g, kMcThreads, 0, s>>>(
-        T, pool, pub, epoch, keys, nbr, n, (uint32_t*)mc_out, q_out, counts, cursor, offsets, cell_flat,
-        cell_mc, cell_cap);
-    vsb::count_launch();
-  }
-  VS_CK_LAUNCH("k_mc_encode_self");
-  return VS_OK;
-}
-
 template <bool kFromKeys>
 static vs_status launch_mc(const TableView& T, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
-                           const int32_t* nbr, uint64_t n, uint8_t* mc_out, int8_t* q_out, uint32_t* counts,
-                           cudaStream_t s) {
+                           const int32_t* nbr, uint64_t n, const McOut& o, cudaStream_t s) {
   if (n == 0) return VS_OK;
-  return faces ? launch_mc_t<kFromKeys, true>(T, pool, faces, keys, nbr, n, mc_out, q_out, counts, s)
-               : launch_mc_t<kFromKeys, false>(T, pool, faces, keys, nbr, n, mc_out, q_out, counts, s);
+  const bool cells = o.cell_flat && o.cell_mc;
+  if (faces)
+    return cells ? launch_mc_t<kFromKeys, true, true>(T, pool, faces, keys, nbr, n, o, s)
+                 : launch_mc_t<kFromKeys, true, false>(T, pool, faces, keys, nbr, n, o, s);
+  return cells ? launch_mc_t<kFromKeys, false, true>(T, pool, faces, keys, nbr, n, o, s)
+               : launch_mc_t<kFromKeys, false, false>(T, pool, faces, keys, nbr, n, o, s);
 }
 
 }  // namespace vsb
@@ -1031,7 +683,8 @@ vs_status vs_mc_encode(const uint8_t* pool, const uint8_t* faces, const int32_t*
     set_error("faces must be 16-byte aligned");
     return VS_ERR_INVALID;
   }
-  return launch_mc<false>(none, pool, faces, nullptr, nbr, n, mc_out, q_out, counts, (cudaStream_t)stream);
+  McOut o{nullptr, nullptr, mc_out, q_out, counts, nullptr, nullptr, nullptr, nullptr, 0};
+  return launch_mc<false>(none, pool, faces, nullptr, nbr, n, o, (cudaStream_t)stream);
 }
 
 vs_status vs_mc_encode_keys(const vs_table* t, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
@@ -1049,52 +702,30 @@ vs_status vs_mc_encode_keys(const vs_table* t, const uint8_t* pool, const uint8_
     return VS_ERR_INVALID;
   }
   DeviceGuard g(t->device);
-  return launch_mc<true>(t->view(), pool, faces, keys, nullptr, n, mc_out, q_out, counts, (cudaStream_t)stream);
+  McOut o{nullptr, nullptr, mc_out, q_out, counts, nullptr, nullptr, nullptr, nullptr, 0};
+  return launch_mc<true>(t->view(), pool, faces, keys, nullptr, n, o, (cudaStream_t)stream);
 }
 
-vs_status vs_mc_encode_full(const vs_table* t, const uint8_t* pool, const int32_t* keys, const int32_t* nbr,
-                            uint64_t n, uint8_t* packs, uint32_t epoch, uint8_t* mc_out, int8_t* q_out,
-                            uint32_t* counts, unsigned long long* cursor, uint32_t* offsets, uint16_t* cell_flat,
-                            uint32_t* cell_mc, uint64_t cell_cap, vs_stream_t stream) {
-  if (n == 0) return VS_OK;
-  if (!pool || !packs || (t ? !keys : !nbr) || epoch == 0) {
-    set_error("vs_mc_encode_full: pool/packs and keys (with a table) or nbr must be non-NULL, epoch != 0");
+vs_status vs_mc_encode_keys_ex(const vs_table* t, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
+                               uint64_t n, const uint64_t* n_dev, const int32_t* out_rows, uint8_t* mc_out,
+                               int8_t* q_out, uint32_t* counts,
+                               unsigned long long* cursor, uint32_t* offsets, uint16_t* cell_flat, uint32_t* cell_mc,
+                               uint64_t cell_cap, vs_stream_t stream) {
+  if (!t || (n && (!pool || !keys))) {
+    set_error("table/pool/keys must be non-NULL");
     return VS_ERR_INVALID;
   }
-  if (((uintptr_t)pool & 15u) != 0 || ((uintptr_t)packs & 15u) != 0) {
-    set_error("vs_mc_encode_full: pool and packs must be 16-byte aligned");
+  if (((uintptr_t)pool & 15u) != 0 || ((uintptr_t)faces & 15u) != 0) {
+    set_error("pool and faces must be 16-byte aligned");
     return VS_ERR_INVALID;
   }
-  const bool cells = cell_flat && cell_mc;
-  if (cells && (!cursor || !offsets)) {
-    set_error("vs_mc_encode_full: compaction needs cursor and offsets");
+  if ((cell_flat || cell_mc) && !(cell_flat && cell_mc && cursor && offsets)) {
+    set_error("compaction needs cell_flat, cell_mc, cursor and offsets");
     return VS_ERR_INVALID;
   }
-  cudaStream_t s = (cudaStream_t)stream;
-  TableView none{};
-  if (t) {
-    DeviceGuard g(t->device);
-    const TableView T = t->view();
-    return cells ? launch_self_t<true, true>(T, pool, keys, nullptr, n, packs, epoch, mc_out, q_out, counts, cursor,
-                                             offsets, cell_flat, cell_mc, cell_cap, s)
-                 : launch_self_t<true, false>(T, pool, keys, nullptr, n, packs, epoch, mc_out, q_out, counts, cursor,
-                                              offsets, cell_flat, cell_mc, cell_cap, s);
-  }
-  return cells ? launch_self_t<false, true>(none, pool, nullptr, nbr, n, packs, epoch, mc_out, q_out, counts, cursor,
-                                            offsets, cell_flat, cell_mc, cell_cap, s)
-               : launch_self_t<false, false>(none, pool, nullptr, nbr, n, packs, epoch, mc_out, q_out, counts, cursor,
-                                             offsets, cell_flat, cell_mc, cell_cap, s);
-}
-
-vs_status vs_mc_self_debug(uint64_t* out8) {
-  VS_CK(cudaMemcpyFromSymbol(out8, g_mc_self_miss_c, 8 * sizeof(unsigned long long)));
-  return VS_OK;
-}
-
-uint64_t vs_mc_self_fallbacks(void) {
-  unsigned long long v = 0;
-  cudaMemcpyFromSymbol(&v, g_mc_self_fallbacks, sizeof(v));
-  return v;
+  DeviceGuard g(t->device);
+  McOut o{n_dev, out_rows, mc_out, q_out, counts, cursor, offsets, cell_flat, cell_mc, cell_cap};
+  return launch_mc<true>(t->view(), pool, faces, keys, nullptr, n, o, (cudaStream_t)stream);
 }
 
 vs_status vs_mc_neighbors(const vs_table* t, const int32_t* keys, uint64_t n, int32_t* nbr_out,

@@ -154,86 +154,44 @@ def encode_blocks(pool, nbr, *, mc: bool = True, q: bool = True, counts: bool = 
     return mc_t, q_t, c_t
 
 
-def encode_keys(tsdf_table, pool, keys, *, mc: bool = True, q: bool = True, counts: bool = True, faces=None):
+def encode_keys(tsdf_table, pool, keys, *, mc=True, q=True, counts=True, faces=None, out_rows=None,
+                cells: bool = False, cell_cap: Optional[int] = None, n_dev=None):
     """Encode MC blocks `keys` (int32[N,3]); neighbour rows are looked up in
     `tsdf_table` (a BlockHashMap whose positions index `pool`) inside the
-    kernel.  `faces`: as for encode_blocks."""
+    kernel.  `faces`: as for encode_blocks.
+
+    mc / q / counts: True (allocate), False (skip) or a tensor to write.
+    out_rows (int32[N]): block i's MC and quantised bytes go to row
+    out_rows[i] of `mc` / `q` (caller tensors with >= max(out_rows)+1 rows,
+    e.g. a server's MC pool indexed by MC map position).
+    n_dev (device int64[1]): encode only the first min(N, n_dev) keys (a
+    device-produced count; no host sync).
+    cells=True: fused compaction of the non-empty cells in the same launch;
+    returns (mc, q, counts, (offsets int32[N], flat int16[M], cell int32[M],
+    cursor int64[1])) where block i's cells are [offsets[i], offsets[i] +
+    counts[i]) -- else (mc, q, counts)."""
     torch = _lib.require_cuda()
     dev = pool.device
     from .concurrent_hash import _as_keys
 
     k = _as_keys(keys, dev)
     n = k.shape[0]
-    mc_t = _out(torch, n, dev, mc, (MC_BLOCK_BYTES,), torch.uint8)
-    q_t = _out(torch, n, dev, q, (Q_BLOCK_BYTES,), torch.int8)
-    c_t = _out(torch, n, dev, counts, (), torch.int32)
-    s = tsdf_table._stream()
-    f = _faces_arg(faces, pool)
-    check(_lib.load().vs_mc_encode_keys(tsdf_table.handle, ptr(pool), ptr(f), ptr(k), n, ptr(mc_t), ptr(q_t),
-                                        ptr(c_t), ctypes.c_void_p(s.cuda_stream)), "mc_encode_keys")
-    tsdf_table._done(s)
-    return mc_t, q_t, c_t
-
-
-PUB_BYTES = 96  # published face pack per pool row (vs_mc_encode_full): 12 {u32 data, u32 epoch}
-
-
-class FaceState:
-    """Published face packs of a TSDF pool for self-packing full encodes
-    (vs_mc_encode_full): per row 12 {u32 word, u32 epoch} pairs, plus the
-    launch epoch.  `faces()` returns the 48-B packs (vs_mc_faces layout) of
-    the rows the last full encode covered."""
-
-    def __init__(self, pool) -> None:
-        torch = _lib.require_cuda()
-        self.pub = torch.zeros((pool.shape[0], PUB_BYTES), dtype=torch.uint8, device=pool.device)
-        self.epoch = 0
-        self.rows = pool.shape[0]
-
-    def next_epoch(self) -> int:
-        self.epoch = (self.epoch % 0xFFFFFFFE) + 1  # never 0 (= never published)
-        return self.epoch
-
-    def faces(self):
-        torch = _lib.require_cuda()
-        w = self.pub.view(torch.int32).view(self.rows, 12, 2)[:, :, 0]
-        return w.contiguous().view(torch.uint8).view(self.rows, FACE_BYTES)
-
-
-def encode_full(tsdf_table, pool, keys=None, *, nbr=None, state: Optional[FaceState] = None, mc: bool = True,
-                q: bool = True, counts: bool = True, cells: bool = False, cell_cap: Optional[int] = None):
-    """Full encode of every block of a map in ONE launch (vs_mc_encode_full):
-    face packs computed in-kernel from each staged centre row (no side-table
-    pass), optional fused compaction of the non-empty cells.
-
-    Neighbour rows from in-kernel lookups of `keys` in `tsdf_table`, or from
-    `nbr` int32[N,8] when tsdf_table is None.  Returns (mc, q, counts, cells)
-    with cells = None or (offsets int32[N], flat int16[M], cell int32[M],
-    cursor int64[1] device total): block i's cells are
-    [offsets[i], offsets[i] + counts[i])."""
-    torch = _lib.require_cuda()
-    dev = pool.device
-    from .concurrent_hash import _as_keys
-
-    if pool.dtype != torch.uint8 or pool.dim() != 2 or pool.shape[1] != TSDF_BLOCK_BYTES:
-        raise ValueError("pool must be uint8[P, 6144]")
-    if state is None:
-        state = FaceState(pool)
-    if state.rows < pool.shape[0]:
-        raise ValueError("FaceState is smaller than the pool")
-    if tsdf_table is not None:
-        k = _as_keys(keys, dev)
-        n = k.shape[0]
-        nb = None
+    rows = None
+    if out_rows is not None:
+        rows = out_rows.to(dev, torch.int32).contiguous()
+        if rows.shape != (n,):
+            raise ValueError("out_rows must be int32[N]")
+        if not (isinstance(mc, torch.Tensor) or mc is False) or not (isinstance(q, torch.Tensor) or q is False):
+            raise ValueError("out_rows needs caller mc / q tensors (or False)")
+        mc_t = mc if isinstance(mc, torch.Tensor) else None
+        q_t = q if isinstance(q, torch.Tensor) else None
+        for t_, w in ((mc_t, MC_BLOCK_BYTES), (q_t, Q_BLOCK_BYTES)):
+            if t_ is not None and (t_.dim() != 2 or t_.shape[1] != w or not t_.is_contiguous() or t_.device != dev):
+                raise ValueError("mc / q pools must be contiguous [P, 2048] uint8 / [P, 512] int8 on the pool's device")
     else:
-        nb = nbr.to(dev, torch.int32).contiguous().reshape(-1, 8)
-        n = nb.shape[0]
-        k = None
-    want_counts = counts if isinstance(counts, torch.Tensor) else (counts or cells)
-    mc_t = _out(torch, n, dev, mc, (MC_BLOCK_BYTES,), torch.uint8)
-    q_t = _out(torch, n, dev, q, (Q_BLOCK_BYTES,), torch.int8)
-    c_t = _out(torch, n, dev, want_counts, (), torch.int32)
-    cell_out = None
+        mc_t = _out(torch, n, dev, mc, (MC_BLOCK_BYTES,), torch.uint8)
+        q_t = _out(torch, n, dev, q, (Q_BLOCK_BYTES,), torch.int8)
+    c_t = _out(torch, n, dev, counts if isinstance(counts, torch.Tensor) else (bool(counts) or cells), (), torch.int32)
     cur = offs = flat = cm = None
     cap = 0
     if cells:
@@ -242,20 +200,16 @@ def encode_full(tsdf_table, pool, keys=None, *, nbr=None, state: Optional[FaceSt
         offs = torch.empty(n, dtype=torch.int32, device=dev)
         flat = torch.empty(max(cap, 1), dtype=torch.int16, device=dev)
         cm = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-        cell_out = (offs, flat, cm, cur)
-    if tsdf_table is not None:
-        s = tsdf_table._stream()
-        handle = tsdf_table.handle
-    else:
-        s = torch.cuda.current_stream(dev)
-        handle = None
-    check(_lib.load().vs_mc_encode_full(handle, ptr(pool.contiguous()), ptr(k), ptr(nb), n, ptr(state.pub),
-                                        state.next_epoch(), ptr(mc_t), ptr(q_t), ptr(c_t),
-                                        ptr(cur), ptr(offs), ptr(flat), ptr(cm), cap,
-                                        ctypes.c_void_p(s.cuda_stream)), "mc_encode_full")
-    if tsdf_table is not None:
-        tsdf_table._done(s)
-    return mc_t, q_t, (c_t if (counts is not False or cells) else None), cell_out
+    s = tsdf_table._stream()
+    f = _faces_arg(faces, pool)
+    check(_lib.load().vs_mc_encode_keys_ex(tsdf_table.handle, ptr(pool), ptr(f), ptr(k), n, ptr(n_dev), ptr(rows),
+                                           ptr(mc_t),
+                                           ptr(q_t), ptr(c_t), ptr(cur), ptr(offs), ptr(flat), ptr(cm), cap,
+                                           ctypes.c_void_p(s.cuda_stream)), "mc_encode_keys")
+    tsdf_table._done(s)
+    if cells:
+        return mc_t, q_t, c_t, (offs, flat, cm, cur)
+    return mc_t, q_t, c_t
 
 
 def neighbors(tsdf_table, keys):

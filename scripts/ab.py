@@ -35,10 +35,7 @@ def pick(d: dict, section: str):
     if "roofline" in s:
         out["kernel_ms"] = s["roofline"].get("kernel_ms")
         out["frac"] = s["roofline"].get("frac")
-    for k in ("pack_fallbacks_per_launch",):
-        if k in s:
-            out[k] = s[k]
-    for k in ("tick_only", "server_tick", "compact", "incremental_packs", "scattered_halo"):
+    for k in ("tick_only", "server_tick", "compact", "incremental_packs"):
         if k in s:
             out[k] = s[k].get("ms_per_step") if isinstance(s[k], dict) else s[k]
     return out

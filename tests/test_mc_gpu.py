@@ -32,18 +32,10 @@ def gpu_encode(pool, nbr, dev):
 
     from paper_1805_03709_b200 import encode_blocks, face_packs
 
-    from paper_1805_03709_b200 import encode_full
-
     p, nb = _t(pool, dev), _t(nbr, dev)
     mc, q, c = encode_blocks(p, nb)
     mc2, q2, c2 = encode_blocks(p, nb, faces=face_packs(p))
     assert torch.equal(mc, mc2) and torch.equal(q, q2) and torch.equal(c, c2), "face-pack halo path differs"
-    # the self-packing full encode (packs produced in-kernel, pool fallback
-    # for neighbours that are not centres) + fused compaction
-    mc3, q3, c3, (offs, flat, cells, cur) = encode_full(None, p, nbr=nb, cells=True)
-    assert torch.equal(mc, mc3) and torch.equal(q, q3) and torch.equal(c, c3), "self-packing path differs"
-    assert int(cur.item()) == int(c.sum().item())
-    check_cells_scatter_back(mc, c3, offs, flat, cells)
     return mc.cpu().numpy(), q.cpu().numpy(), c.cpu().numpy().astype(np.uint32)
 
 
@@ -140,11 +132,17 @@ def test_fused_sphere_reproduces_manifest_model_sha256(dev, golden):
 
     mc2, _, _ = encode_keys(t, pool, d["keys"], faces=face_packs(pool))
     assert hashlib.sha256(mc2.cpu().numpy().tobytes()).hexdigest() == meta["model_sha256"]
-    from paper_1805_03709_b200 import encode_full
+    # fused compaction + output rows (the server path): same bytes at the rows
+    import torch
 
-    for _ in range(2):  # epochs advance: the second launch must not trust the first one's flags
-        mc3, _, _, _ = encode_full(t, pool, d["keys"])
-        assert hashlib.sha256(mc3.cpu().numpy().tobytes()).hexdigest() == meta["model_sha256"]
+    rows = torch.arange(len(d["keys"]) - 1, -1, -1, dtype=torch.int32, device=dev)
+    mpool = torch.zeros((len(d["keys"]), 2048), dtype=torch.uint8, device=dev)
+    qpool = torch.zeros((len(d["keys"]), 512), dtype=torch.int8, device=dev)
+    _, _, c3, (offs, flat, cells, cur) = encode_keys(t, pool, d["keys"], mc=mpool, q=qpool, out_rows=rows,
+                                                     cells=True, faces=face_packs(pool))
+    mc3 = mpool.flip(0)
+    assert hashlib.sha256(mc3.cpu().numpy().tobytes()).hexdigest() == meta["model_sha256"]
+    check_cells_scatter_back(mc3, c3, offs, flat, cells)
 
 
 @pytest.mark.parametrize("field", ["random", "smooth"])
@@ -224,15 +222,11 @@ def test_room_sample_vs_oracle(dev):
     _, pos = t.find_keys(keys)
     mc2, q2, c2 = encode_keys(t, pool, keys, faces=face_packs(pool, rows=pos))
     assert torch.equal(mc, mc2) and torch.equal(q, q2) and torch.equal(c, c2)
-    from paper_1805_03709_b200 import FaceState, encode_full
-
-    st = FaceState(pool)
-    for _ in range(2):
-        mc3, q3, c3, (offs, flat, cells, cur) = encode_full(t, pool, keys, state=st, cells=True)
+    for fc in (None, face_packs(pool, rows=pos)):  # fused compaction, both halo paths
+        mc3, q3, c3, (offs, flat, cells, cur) = encode_keys(t, pool, keys, faces=fc, cells=True)
         assert torch.equal(mc, mc3) and torch.equal(q, q3) and torch.equal(c, c3)
+        assert int(cur.item()) == int(c.sum().item())
         check_cells_scatter_back(mc, c3, offs, flat, cells)
-    # the packs it published equal the side-table pass's for every encoded row
-    assert torch.equal(st.faces()[pos.long()], face_packs(pool, rows=pos)[pos.long()])
     rows_np = rows.cpu().numpy()
     nbr = oracle.neighbor_table(keys, keys)
     omc, oq, oc = oracle.mc_encode(rows_np, nbr, threads=8)
