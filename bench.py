@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--no-mc-parity", action="store_true", help="skip the all-blocks oracle check (experiments)")
     p.add_argument("--no-stream", action="store_true")
     p.add_argument("--no-rc", action="store_true")
+    p.add_argument("--no-server", action="store_true")
     p.add_argument("--rc-frames", type=int, default=20)
     p.add_argument("--stream-ticks", type=int, default=200)
     p.add_argument("--no-cpu", action="store_true")
@@ -197,6 +198,17 @@ def cpu_mc_sample(threads: int, n_blocks: int = 32768):
 
 
 # --------------------------------------------------------------- GPU arms
+
+def _free_cuda():
+    """Return the previous section's cached blocks (each section sizes its
+    own multi-GB pools)."""
+    import gc
+
+    import torch
+
+    gc.collect()
+    torch.cuda.empty_cache()
+
 
 def sync_max(x: float, world: int) -> float:
     if world == 1:
@@ -563,6 +575,64 @@ def run_mc(args, dev, world=1):
     return out
 
 
+STREAM_C, STREAM_U, STREAM_X, STREAM_K, STREAM_EVERY = 16, 512, 512, 256, 20
+BYTES_PER_STREAM_INSERT = 48  # one hash insert per (client, key)
+
+
+def stream_script(keys_np, ticks: int, seed: int = 44):
+    """Config-4 tick script (host copy, identical for the GPU run, the
+    oracle replay and the CPU baseline): updated keys per tick and reset
+    keys per reconnect tick."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    M = len(keys_np)
+    upd = keys_np[rng.integers(0, M, (ticks + 1) * STREAM_U)].reshape(ticks + 1, STREAM_U, 3)
+    resets = keys_np[rng.integers(0, M, (ticks // STREAM_EVERY + 1) * STREAM_K)].reshape(-1, STREAM_K, 3)
+    return np.ascontiguousarray(upd), np.ascontiguousarray(resets)
+
+
+def stream_replay_client(c, scene, aff, resets, ticks, extracted=None, seed=0):
+    """One client of the config-4 script on the CPU: the reference StreamSet
+    semantics (server.py:49-95) over the C restatement of BlockHashSet --
+    created = the set difference, appended to the generation FIFO in order;
+    extract_batch either ADOPTS the keys the GPU extracted (parity: they must
+    be pending and as many as min(512, size)) or runs the port's own
+    extraction (CPU baseline).  Returns (table, fifo parts, key-ops, ok)."""
+    import numpy as np
+
+    import oracle
+
+    o = oracle.OracleHashSet(1 << 21, 1 << 21)
+    cr, _, _ = o.insert_batch(scene)
+    fifo = [scene[cr.astype(bool)]]
+    ops, ok = len(scene), True
+    rs = np.random.default_rng(seed)
+    for t in range(ticks + 1):
+        a = aff[t]
+        cr, _, fail = o.insert_batch(a)
+        ok &= fail == -1
+        fifo.append(a[cr.astype(bool)])
+        ops += len(a)
+        if extracted is not None:
+            ex = extracted[t]
+            want = min(STREAM_X, o.size())
+            er, _ = o.erase_batch(ex)
+            ok &= bool(er.all()) and len(ex) == want
+        else:
+            ex = o.extract(STREAM_X, int(rs.integers(0, o.capacity)))
+        ops += len(ex)
+        if t % STREAM_EVERY == STREAM_EVERY - 1:
+            if (t // STREAM_EVERY) % STREAM_C == c:  # fresh reconnect: clear + fill
+                o.clear()
+                cr, _, _ = o.insert_batch(scene)
+                fifo = [scene[cr.astype(bool)]]
+                ops += len(scene)
+            o.erase_batch(resets[t // STREAM_EVERY])
+            ops += STREAM_K
+    return o, fifo, ops, ok
+
+
 def run_stream(args, dev):
     """Config 4: 16 clients' stream sets over the 2.08M-block room scene.
 
@@ -570,51 +640,51 @@ def run_stream(args, dev):
     TSDF keys -> affected dedup -> insert into all 16 sets (one launch) ->
     every client extract_random(512).  Every 20 ticks one client reconnects
     fresh (clear + full fill) and a reset of 256 keys is removed from every
-    set.  Unit: stream-set key ops (inserts + removals) per second."""
+    set.  Unit: stream-set key ops (inserts + removals) per second.  After
+    the timed script every client's sorted pending set and FIFO are compared
+    with a replay of the same script on the CPU restatement."""
     import ctypes
+    from concurrent.futures import ThreadPoolExecutor
 
+    import numpy as np
     import torch
 
+    import oracle
     from paper_1805_03709_b200 import (BlockHashSet, StreamSet, _lib, extract_random_many, fan_out,
                                        remove_everywhere, workloads)
 
-    keys = torch.from_numpy(workloads.room_block_keys()).to(dev)
+    scene_np = workloads.room_block_keys()
+    keys = torch.from_numpy(scene_np).to(dev)
     M = keys.shape[0]
-    C, U, X, K = 16, 512, 512, 256
+    C, U, X, K = STREAM_C, STREAM_U, STREAM_X, STREAM_K
+    ticks = max(args.stream_ticks, STREAM_EVERY)
+    upd_np, resets_np = stream_script(scene_np, ticks)
     clients = [StreamSet(1 << 21, 1 << 21, device=dev, fifo_capacity=1 << 22) for _ in range(C)]
     scratch = BlockHashSet(1 << 14, 1 << 14, device=dev)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(44)
-    aff = torch.empty((8 * U, 3), dtype=torch.int32, device=dev)
     lib = _lib.load()
-    ops = {"insert": 0, "remove": 0}
-    ticks = max(args.stream_ticks, 20)
-    # device-side per-tick counts (summed once after the timed region):
-    # affected keys per tick (x C below) and keys extracted per client
+    # device-side logs (read once after the timed region): affected keys and
+    # counts per tick, extracted keys and counts per tick and client
+    aff_keys = torch.zeros((ticks + 1, 8 * U, 3), dtype=torch.int32, device=dev)
     aff_log = torch.zeros((ticks + 1, 1), dtype=torch.int64, device=dev)
+    ex_keys = torch.zeros((ticks + 1, C, X, 3), dtype=torch.int32, device=dev)
     ex_log = torch.zeros((ticks + 1, C), dtype=torch.int64, device=dev)
-
-    # the updated / reset keys of every tick, synthesised before the timed
-    # region (inputs resident in HBM, as in the other sections)
-    upd_all = keys[torch.randint(0, M, ((ticks + 1) * U,), generator=gen, device=dev)].view(ticks + 1, U, 3)
-    reset_all = keys[torch.randint(0, M, ((ticks // 20 + 1) * K,), generator=gen, device=dev)].view(-1, K, 3)
+    # inputs resident in HBM before the timed region, as in the other sections
+    upd_all = torch.from_numpy(upd_np).to(dev)
+    reset_all = torch.from_numpy(resets_np).to(dev)
+    seeds = [[(t * C + c) * 2654435761 + 17 for c in range(C)] for t in range(ticks + 1)]
 
     def tick(t):
-        upd = upd_all[t]
         st = torch.cuda.current_stream(dev)
-        n_aff = aff_log[t]
-        _lib.check(lib.vs_affected_dedup(scratch.handle, _lib.ptr(upd), U, _lib.ptr(aff), _lib.ptr(n_aff),
-                                         ctypes.c_void_p(st.cuda_stream)))
+        _lib.check(lib.vs_affected_dedup(scratch.handle, _lib.ptr(upd_all[t]), U, _lib.ptr(aff_keys[t]),
+                                         _lib.ptr(aff_log[t]), ctypes.c_void_p(st.cuda_stream)))
         # no host sync: the fan-out takes the device-side affected count
-        fan_out(clients, aff, sync=False, n_dev=n_aff)
-        extract_random_many(clients, X, n_out=ex_log[t])  # one launch for all 16 clients
-        if t % 20 == 19:
-            victim = clients[(t // 20) % C]
+        fan_out(clients, aff_keys[t], sync=False, n_dev=aff_log[t])
+        extract_random_many(clients, X, seeds[t], n_out=ex_log[t], keys_out=ex_keys[t])  # one launch, 16 clients
+        if t % STREAM_EVERY == STREAM_EVERY - 1:
+            victim = clients[(t // STREAM_EVERY) % C]
             victim.clear()
             fan_out([victim], keys, sync=False)
-            ops["insert"] += M
-            remove_everywhere(clients, reset_all[t // 20])
-            ops["remove"] += C * K
+            remove_everywhere(clients, reset_all[t // STREAM_EVERY])
 
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -626,58 +696,216 @@ def run_stream(args, dev):
     ok = all(c.size() == M for c in clients)
     tick(0)
     torch.cuda.synchronize()
-    ops["insert"] = ops["remove"] = 0
-    torch.cuda.synchronize()
     clocks = Clocks(dev.index).start()
     time.sleep(0.12)
     t0 = time.perf_counter()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(ticks + 1)]
     with _lib.Profile() as prof:
-        e0.record()
         for t in range(1, ticks + 1):
+            evs[t - 1].record()
             tick(t)
-        e1.record()
+        evs[ticks].record()
         torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    ops["remove"] += int(ex_log[1:].sum().item())
-    ops["insert"] += C * int(aff_log[1:].sum().item())
-    total = ops["insert"] + ops["remove"]
-    ok = ok and all(0 <= c.size() <= M for c in clients)
+    ms = evs[0].elapsed_time(evs[ticks])
+    per_tick = [evs[t - 1].elapsed_time(evs[t]) for t in range(1, ticks + 1)]
+    aff_n = aff_log[:, 0].cpu().numpy()
+    ex_n = ex_log.cpu().numpy()
+    reconnect = {t for t in range(1, ticks + 1) if t % STREAM_EVERY == STREAM_EVERY - 1}
+    ins = int(C * aff_n[1:].sum()) + len(reconnect) * M
+    rem = int(ex_n[1:].sum()) + len(reconnect) * C * K
+    total = ins + rem
+    plain = [t for t in range(1, ticks + 1) if t not in reconnect]
+    plain_ms = sum(per_tick[t - 1] for t in plain)
+    plain_ops = int(sum(C * aff_n[t] + ex_n[t].sum() for t in plain))
+    # ---- parity: replay the same script on the CPU restatement, adopting
+    # the GPU's extracted keys; compare every client's sorted pending set and
+    # its FIFO (stale entries included) -- outside the timed region
+    p0 = time.perf_counter()
+    aff_host = [aff_keys[t, : int(aff_n[t])].cpu().numpy() for t in range(ticks + 1)]
+    ex_host = ex_keys.cpu().numpy()
+    dedup_ok = True
+    for t in (0, 1, ticks // 2, ticks):  # the GPU affected dedup vs the reference's dict order
+        want = np.array(oracle.affected_dedup(upd_np[t].tolist()), np.int32).reshape(-1, 3)
+        dedup_ok &= bool(np.array_equal(aff_host[t], want))
+
+    def check_client(c):
+        o, fifo, _, rok = stream_replay_client(
+            c, scene_np, aff_host, resets_np, ticks,
+            extracted=[ex_host[t, c, : int(ex_n[t, c])] for t in range(ticks + 1)])
+        want_keys = o.snapshot()[0]
+        want_keys = want_keys[np.lexsort(want_keys.T[::-1])]
+        return rok, want_keys, np.concatenate(fifo)
+
+    with ThreadPoolExecutor(max_workers=min(C, cpu_cores())) as ex:
+        replays = list(ex.map(check_client, range(C)))
+    parity_ok = dedup_ok
+    bad = []
+    for c, (rok, want_keys, want_fifo) in enumerate(replays):
+        got = clients[c]._set.snapshot_tensor()[0].cpu().numpy()
+        got = got[np.lexsort(got.T[::-1])]
+        fifo = clients[c]._ring_view().cpu().numpy()
+        good = (bool(rok), bool(np.array_equal(got, want_keys)), bool(np.array_equal(fifo, want_fifo)))
+        parity_ok &= all(good)
+        if not all(good):
+            bad.append({"client": c, "replay_ok/set/fifo": good, "sizes": [len(got), len(want_keys)],
+                        "fifo_len": [len(fifo), len(want_fifo)]})
+    parity_s = time.perf_counter() - p0
+    # ---- roofline of the fan-out (the dominant launch chain of a tick):
+    # 48 B per (client, key) insert, timed alone on a tick's affected keys
+    A = int(aff_n[1])
+    for _ in range(3):
+        fan_out(clients, aff_keys[1, :A], sync=False)
+    torch.cuda.synchronize()
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 50
+    r0.record()
+    for _ in range(reps):
+        fan_out(clients, aff_keys[1, :A], sync=False)
+    r1.record()
+    torch.cuda.synchronize()
+    fan_ms = r0.elapsed_time(r1) / reps
+    peak, src = peaks()
+    fan_bytes = C * A * BYTES_PER_STREAM_INSERT
     return {"workload": "config 4: 16 clients x 2,080,160-block scene; per tick 512 updated TSDF keys -> "
                         "affected dedup -> insert into all sets, extract_random(512) per client; every 20 ticks a "
                         "fresh reconnect (clear + full fill) and a 256-key reset from every set",
             "value": total / (ms / 1e3) / 1e6, "unit": "M key-ops/s", "ticks": ticks,
             "ms_per_tick": ms / ticks, "wall_s": wall, "fill_16_clients_ms": fill_ms,
-            "fill_value": C * M / (fill_ms / 1e3) / 1e6, "inserts": ops["insert"], "removes": ops["remove"],
-            "ok": ok, "gpu_launches": prof.launches, "clocks": clk,
+            "fill_value": C * M / (fill_ms / 1e3) / 1e6, "inserts": ins, "removes": rem,
+            "tick_only": {"value": plain_ops / (plain_ms / 1e3) / 1e6, "unit": "M key-ops/s",
+                          "ms_per_tick": plain_ms / len(plain), "ticks": len(plain),
+                          "note": "ticks without a reconnect fill / reset: dedup + 16-client fan-out + 16 extracts"},
+            "ok": bool(ok and parity_ok), "parity_bad_clients": bad[:3],
+            "parity": f"all {C} clients: sorted pending set + FIFO (stale entries included) after the script == a "
+                      f"replay on the C restatement adopting the GPU's extracted keys; affected dedup == the "
+                      f"reference's dict order ({parity_s:.1f} s)",
+            "gpu_launches": prof.launches, "clocks": clk,
+            "roofline": {"bound": "hbm", "kernel": "fan-out chain (k_multi_insert + fixup + scan + FIFO append)",
+                         "achieved": fan_bytes / (fan_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": fan_bytes / (fan_ms / 1e3) / 1e9 / peak, "traffic": None, "kernel_ms": fan_ms,
+                         "bytes_per_launch": fan_bytes, "peak_source": src,
+                         "note": f"48 B per (client, key) insert (SURVEY §8d) x {C} clients x {A} affected keys; "
+                                 "latency-bound: a tick's fan-out is ~65k inserts"},
             "note": "inserts count created-or-not key inserts into every set; removes = extracted + reset keys; "
                     "no host sync inside a tick (device-side affected count bounds the fan-out)"}
 
 
-def cpu_stream_sample(seconds: float = 5.0):
-    """Reference semantics (set + deque StreamSet, server.py:49-95) in Python
-    on a bounded sample: fill one client with the scene, then update ticks."""
+def cpu_stream_baseline(threads: int, ticks: int):
+    """The same 16-client tick script on the CPU port (C restatement of
+    BlockHashSet + the StreamSet FIFO rule, own extraction), one host thread
+    per client (clients are independent), wall-clock timed."""
+    from concurrent.futures import ThreadPoolExecutor
+
     import numpy as np
 
     import oracle
     from paper_1805_03709_b200 import workloads
 
-    keys = [tuple(k) for k in workloads.room_block_keys().tolist()]
-    rng = np.random.default_rng(0)
-    ss = oracle.OracleStreamSet()
+    scene = workloads.room_block_keys()
+    upd, resets = stream_script(scene, ticks)
     t0 = time.perf_counter()
-    n = ss.insert_many(keys)
-    ops = len(keys)
-    while time.perf_counter() - t0 < seconds:
-        upd = [keys[i] for i in rng.integers(0, len(keys), 512)]
-        aff = oracle.affected_dedup(upd)
-        ss.insert_many(aff)
-        ops += len(aff)
-        got = ss.extract_ordered(512)
-        ops += len(got)
-    return ops / (time.perf_counter() - t0) / 1e6
+    aff = [np.array(oracle.affected_dedup(upd[t].tolist()), np.int32).reshape(-1, 3) for t in range(ticks + 1)]
+    with ThreadPoolExecutor(max_workers=min(STREAM_C, threads)) as ex:
+        res = list(ex.map(lambda c: stream_replay_client(c, scene, aff, resets, ticks, seed=c)[2], range(STREAM_C)))
+    dt = time.perf_counter() - t0
+    return sum(res) / dt / 1e6, dt
+
+
+def run_server(args, dev):
+    """SURVEY §3.1, the core server path end to end through
+    GpuServerCore.on_tsdf_batch (server.py:299-315): per tick 512 updated
+    TSDF blocks (wire rows, resident in HBM) -> tsdf_map.put (latest write
+    wins) + face packs of the written rows -> affected dedup (~4k MC keys)
+    -> mc_map.put + recompute straight into the MC / quantised pools ->
+    fan-out into 16 exploration clients.  The scene (2,080,160 blocks) is
+    ingested first and 16 clients attach fresh."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_1805_03709_b200 import GpuServerCore, _lib, neighbors, workloads
+
+    scene_np = workloads.room_block_keys()
+    scene = torch.from_numpy(scene_np).to(dev)
+    M = scene.shape[0]
+    core = GpuServerCore(1 << 21, 1 << 21, stream_buckets=1 << 21, stream_excess=1 << 21, max_batch=1 << 16,
+                         device=dev)
+    torch.cuda.synchronize()
+    i0 = time.perf_counter()
+    chunk = 1 << 16
+    for a in range(0, M, chunk):
+        k = scene[a:a + chunk]
+        core.on_tsdf_batch(k, workloads.room_tsdf_rows(k), sync=False)
+    core.check()
+    torch.cuda.synchronize()
+    ingest_s = time.perf_counter() - i0
+    C = STREAM_C
+    for c in range(C):
+        core.attach(bytes([c]) * 16)
+    torch.cuda.synchronize()
+    T = max(20, args.stream_ticks // 2)
+    Ts = 5
+    rng = np.random.default_rng(77)
+    upd_np = scene_np[rng.integers(0, M, (T + Ts + 3) * STREAM_U)].reshape(T + Ts + 3, STREAM_U, 3)
+    upd = torch.from_numpy(upd_np).to(dev)
+    # updated rows: the scene's rows with every tsdf value nudged (a real update)
+    rows = []
+    for t in range(T + Ts + 3):
+        r = workloads.room_tsdf_rows(upd[t]).view(torch.float32).view(STREAM_U, 512, 3)
+        r[..., 0] = (r[..., 0] * 0.97).clamp(-1, 1)
+        rows.append(r.reshape(STREAM_U, -1).view(torch.uint8).reshape(STREAM_U, 6144))
+    rows = torch.stack(rows)
+    for t in range(3):  # warm-up
+        core.on_tsdf_batch(upd[t], rows[t], sync=False)
+    torch.cuda.synchronize()
+    clocks = Clocks(dev.index).start()
+    time.sleep(0.12)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0 = time.perf_counter()
+    with _lib.Profile() as prof:
+        e0.record()
+        for t in range(3, 3 + T):
+            core.on_tsdf_batch(upd[t], rows[t], sync=False)
+        e1.record()
+        host_s = time.perf_counter() - h0
+        torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / T
+    core.check()
+    # the exact path (reference failure semantics, three host syncs per tick)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for t in range(3 + T, 3 + T + Ts):
+        core.on_tsdf_batch(upd[t], rows[t], sync=True)
+    s1.record()
+    torch.cuda.synchronize()
+    ms_sync = s0.elapsed_time(s1) / Ts
+    # parity: the MC + quantised bytes of the last tick's affected keys in the
+    # pools == the oracle re-encode of the same keys from the device TSDF
+    # pool; the affected set == the reference's dict-order dedup
+    aff = np.array(oracle.affected_dedup(upd_np[3 + T + Ts - 1].tolist()), np.int32).reshape(-1, 3)
+    found, mpos = core.mc_map.find_keys(aff)
+    nbr = neighbors(core.tsdf_map, aff).reshape(-1)
+    valid = nbr >= 0
+    uniq, inv = torch.unique(nbr[valid], return_inverse=True)
+    trows = core.tsdf_pool[uniq.long()].cpu().numpy()
+    local = torch.full_like(nbr, -1)
+    local[valid] = inv.to(torch.int32)
+    omc, oq, _ = oracle.mc_encode(trows, local.view(-1, 8).cpu().numpy(), threads=8)
+    ok = bool(found.all().item()) and np.array_equal(core.mc_pool[mpos.long()].cpu().numpy(), omc) and \
+        np.array_equal(core.q_pool[mpos.long()].cpu().numpy(), oq)
+    ok &= all(st.size() <= core.mc_map.approx_size() for st in core.streams())
+    return {"workload": f"SURVEY §3.1 on_tsdf_batch: {STREAM_U} updated TSDF blocks per tick over the 2,080,160-block "
+                        f"room, ~{len(aff)} affected MC keys re-encoded into the MC pool, fan-out to {C} clients",
+            "value": 1e3 / ms, "unit": "ticks/s", "ms_per_tick": ms, "ticks": T,
+            "blocks_per_s": STREAM_U / (ms / 1e3), "host_ms_per_tick": 1e3 * host_s / T,
+            "ms_per_tick_exact_path": ms_sync,
+            "note_exact_path": "sync=True: the reference's sequential CapacityExhausted semantics (3 host syncs)",
+            "ingest_scene_s": ingest_s, "ok": ok, "gpu_launches": prof.launches, "clocks": clk,
+            "parity": "last tick's affected keys: MC + quantised pool bytes == oracle re-encode; affected set == "
+                      "the reference's dict-order dedup"}
 
 
 def run_rc(args, dev):
@@ -843,12 +1071,19 @@ def main():
 
     mc = None
     if not args.no_mc:
+        _free_cuda()
         mc = section(run_mc, args, dev, world)
     stream = None
     if not args.no_stream and world == 1:
+        _free_cuda()
         stream = section(run_stream, args, dev)
+    server = None
+    if not args.no_server and world == 1:
+        _free_cuda()
+        server = section(run_server, args, dev)
     rc = None
     if not args.no_rc and world == 1:
+        _free_cuda()
         rc = section(run_rc, args, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -871,10 +1106,14 @@ def main():
                                          "sample": "1 frame 640x480 of the RC workload (numpy restatement of "
                                                    "allocate_blocks + integrate_frame)"})
         if not args.no_stream:
-            cpu["stream"] = section(lambda: {"value": cpu_stream_sample(), "unit": "M key-ops/s", "cores": 1,
-                                             "kind": "port",
-                                             "sample": "1 client: fill with the 2.08M-key scene + update ticks for "
-                                                       "~5 s (Python set + deque restatement of StreamSet)"})
+            def cpu_stream():
+                v, dt = cpu_stream_baseline(threads, max(args.stream_ticks, STREAM_EVERY))
+                return {"value": v, "unit": "M key-ops/s", "cores": min(STREAM_C, threads), "kind": "port",
+                        "sample": f"the full config-4 script ({max(args.stream_ticks, STREAM_EVERY)} ticks, 16 clients "
+                                  f"incl. fills, reconnects and resets) on the C restatement of BlockHashSet + the "
+                                  f"StreamSet FIFO rule, one thread per client, {dt:.1f} s"}
+
+            cpu["stream"] = section(cpu_stream)
     if world > 1:
         import torch.distributed as dist
 
@@ -886,7 +1125,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": config,
                 "parity_ok": h["ok"], "roofline": h["roofline"], "gpu_launches": h["gpu_launches"],
-                "clocks": h["clocks"], "cpu_baseline": cpu, "e2e": h.get("e2e"), "mc": mc, "stream": stream, "rc": rc}
+                "clocks": h["clocks"], "cpu_baseline": cpu, "e2e": h.get("e2e"), "mc": mc, "stream": stream, "server": server, "rc": rc}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

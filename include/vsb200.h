@@ -211,7 +211,8 @@ vs_status vs_mc_encode_keys(const vs_table *tsdf_table, const uint8_t *pool,
  *     device-produced count (vs_affected_dedup) needs no host sync;
  *   out_rows (may be NULL): block i's MC / quantised bytes go to row
  *     out_rows[i] of mc_out / q_out (e.g. the MC map's position of key i,
- *     so the encoder writes straight into a server's MC pool);
+ *     so the encoder writes straight into a server's MC pool); rows < 0
+ *     are skipped (e.g. an MC map insert that failed);
  *   fused compaction (cell_flat and cell_mc non-NULL): block i's
  *     non-empty cells in ascending flat index at [offsets[i], offsets[i] +
  *     counts[i]) of cell_flat / cell_mc, each range reserved with one atomic

@@ -16,6 +16,8 @@
  *   _insert_pos     :159-208  (claim free bucket, else pop excess + append tail)
  *   remove          :251-295  (bucket: clear occ; excess: relink, push, stale next)
  *   snapshot_keys   :300-309  (ascending position)
+ *   _extract        :382-402  (occupied positions rotated to a start, first
+ *                              max_n removed; predicate None)
  *
  * Parallel batch mode (CPU baseline with all host threads): ops are
  * partitioned by bucket (a chain belongs to one bucket, so threads never
@@ -351,3 +353,29 @@ const uint8_t *oh_occ(const oh_table *t) { return t->occ; }
 const uint32_t *oh_next(const oh_table *t) { return t->next; }
 const uint32_t *oh_stack(const oh_table *t) { return t->stack; }
 uint32_t oh_capacity(const oh_table *t) { return t->cap; }
+
+/* _extract (concurrent_hash.py:382-402), predicate None: the occupied
+ * positions in ascending order, rotated to begin at the first one >= start
+ * (the reference draws start = random.randrange(capacity)), the first max_n
+ * of them removed in that order.  Returns the count; keys_out = max_n x 3.
+ * The reference materialises every occupied position first; collecting the
+ * first max_n and removing them afterwards takes the same keys (positions
+ * never move while a key is present). */
+uint64_t oh_extract(oh_table *t, uint64_t max_n, uint64_t start, int32_t *keys_out) {
+  if (!max_n || !t->size) return 0;
+  start %= t->cap;
+  uint64_t got = 0;
+  for (uint64_t k = 0; k < t->cap && got < max_n; ++k) {
+    uint64_t e = start + k;
+    if (e >= t->cap) e -= t->cap;
+    if (t->occ[e]) {
+      memcpy(keys_out + 3 * got, t->keys + 3 * e, 12);
+      ++got;
+    }
+  }
+  for (uint64_t i = 0; i < got; ++i) {
+    int64_t pos;
+    t->size -= (uint64_t)erase_one(t, keys_out[3 * i], keys_out[3 * i + 1], keys_out[3 * i + 2], &pos, NULL, NULL);
+  }
+  return got;
+}

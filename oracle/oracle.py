@@ -37,6 +37,7 @@ def lib() -> ctypes.CDLL:
             "oh_apply_batch": (ctypes.c_int64, [_vp, _vp, _vp, ctypes.c_uint64, _vp, _vp]),
             "oh_apply_batch_mt": (ctypes.c_int64, [_vp, _vp, _vp, ctypes.c_uint64, _vp, _vp, ctypes.c_int]),
             "oh_snapshot": (ctypes.c_uint64, [_vp, _vp, _vp, ctypes.c_uint64]),
+            "oh_extract": (ctypes.c_uint64, [_vp, ctypes.c_uint64, ctypes.c_uint64, _vp]),
             "oh_occ": (_vp, [_vp]),
             "oh_next": (_vp, [_vp]),
             "oh_stack": (_vp, [_vp]),
@@ -138,6 +139,12 @@ class OracleHashSet:
         pos = np.zeros(max(n, 1), dtype=np.int32)
         m = lib().oh_snapshot(self._h, _p(keys), _p(pos), n)
         return keys[:m], pos[:m]
+
+    def extract(self, max_n: int, start: int) -> np.ndarray:
+        """_extract (concurrent_hash.py:382-402) with the rotation start given."""
+        out = np.zeros((max(max_n, 1), 3), dtype=np.int32)
+        m = lib().oh_extract(self._h, max_n, start, _p(out))
+        return out[:m]
 
     def size(self) -> int:
         return int(lib().oh_size(self._h))

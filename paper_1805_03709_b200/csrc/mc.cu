@@ -418,9 +418,9 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     }
     __syncthreads();  // (A) lookups + packs ready, grids zeroed, buf[(j+kAhead)%kStages] no longer read
     if (t == 0 && j + kAhead < nj) issue_centre(sm, j + kAhead, pool);
-    const uint64_t orow = out_rows ? (uint64_t)(uint32_t)__ldg(out_rows + blk) : blk;
-    uint32_t* mc_blk = mc_out ? mc_out + orow * VS_BLOCK_VOXELS : nullptr;
-    int8_t* q_blk = q_out ? q_out + orow * VS_BLOCK_VOXELS : nullptr;
+    const int64_t orow = out_rows ? (int64_t)__ldg(out_rows + blk) : (int64_t)blk;  // < 0: no output row
+    uint32_t* mc_blk = mc_out && orow >= 0 ? mc_out + (uint64_t)orow * VS_BLOCK_VOXELS : nullptr;
+    int8_t* q_blk = q_out && orow >= 0 ? q_out + (uint64_t)orow * VS_BLOCK_VOXELS : nullptr;
     const HaloRegs cur = hal;
     if (j + 1 < nj) {
       if (kFaces) {

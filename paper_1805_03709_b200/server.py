@@ -254,17 +254,22 @@ def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True, n_dev=None):
 
 
 def extract_random_many(sets: Sequence[StreamSet], max_n: int, seeds: Optional[Sequence[int]] = None, *,
-                        n_out=None):
+                        n_out=None, keys_out=None):
     """``[s.extract_random(max_n) for s in sets]`` in one launch per 32
     clients.  Returns (keys int32[C, max_n, 3], n int64[C]) device tensors;
-    ``n_out`` (optional device int64[C]) receives the counts instead of a
-    new tensor."""
+    ``n_out`` (optional device int64[C]) / ``keys_out`` (optional contiguous
+    int32[C, max_n, 3]) receive the counts / keys instead of new tensors."""
     import random
 
     torch = sets[0]._torch
     dev = sets[0].device
     C = len(sets)
-    keys = torch.empty((C, max(max_n, 1), 3), dtype=torch.int32, device=dev)
+    if keys_out is not None:
+        if keys_out.shape != (C, max(max_n, 1), 3) or keys_out.dtype != torch.int32 or not keys_out.is_contiguous():
+            raise ValueError("keys_out must be a contiguous int32[C, max_n, 3] tensor")
+        keys = keys_out
+    else:
+        keys = torch.empty((C, max(max_n, 1), 3), dtype=torch.int32, device=dev)
     n = n_out if n_out is not None else torch.empty(C, dtype=torch.int64, device=dev)
     if max_n <= 0:
         n.zero_()
@@ -357,50 +362,75 @@ class GpuServerCore:
 
     # -- model updates (server.py:299-315) ----------------------------------
 
-    def on_tsdf_batch(self, keys, rows):
+    def on_tsdf_batch(self, keys, rows, *, sync: bool = True):
         """Ingest U TSDF blocks (int32[U,3], uint8[U,6144] wire rows) and
-        propagate: affected MC keys are recomputed, stored and queued into
-        every client.  Returns the affected keys (device int32[A,3])."""
+        propagate (server.py:299-315): TSDF put (latest write wins), face
+        packs of the written rows, affected = ordered first-occurrence dedup
+        of the 8 affected MC keys per block, mc_map.put + recompute (the
+        encoder writes straight into mc_pool / q_pool at the MC map
+        positions), insert_many into every client set.
+
+        sync=True keeps the reference's exact failure semantics (a put that
+        finds the excess list empty raises CapacityExhausted with the earlier
+        blocks applied) and returns the affected keys (device int32[A,3]).
+        sync=False queues the whole update with NO host synchronisation (the
+        device-side affected count bounds every later launch) and returns
+        (affected int32[8U,3], n_affected int64[1]) device tensors; a
+        capacity failure is sticky and raised by ``check()``."""
         torch = self._torch
         dev = self.device
         k = _as_keys(keys, dev)
         rows = torch.as_tensor(rows).to(dev, torch.uint8).reshape(-1, TSDF_BLOCK_BYTES)
         U = k.shape[0]
         if U == 0:
-            return k
-        # tsdf_map.put: exact sequential failure semantics first (the reference
-        # raises at the first block that finds the excess list empty), then the
-        # fused put: latest write wins (sequential put order)
-        self.tsdf_map.insert_many_exact(k)
+            return k if sync else (k, torch.zeros(1, dtype=torch.int64, device=dev))
+        lib = _lib.load()
+        if sync:
+            # exact sequential failure semantics first (the reference raises at
+            # the first block that finds the excess list empty)
+            self.tsdf_map.insert_many_exact(k)
         pos = torch.empty(U, dtype=torch.int32, device=dev)
         rows = rows.contiguous()
         st = _order_streams([self.tsdf_map])
-        check(_lib.load().vs_tsdf_put(self.tsdf_map.handle, ptr(k), ptr(rows), U, ptr(self.tsdf_pool), ptr(pos),
-                                      ctypes.c_void_p(st.cuda_stream)), "tsdf_put")
+        check(lib.vs_tsdf_put(self.tsdf_map.handle, ptr(k), ptr(rows), U, ptr(self.tsdf_pool), ptr(pos),
+                              ctypes.c_void_p(st.cuda_stream)), "tsdf_put")
         _mark_done([self.tsdf_map], st)
-        self.tsdf_map.check_capacity()
         face_packs(self.tsdf_pool, rows=pos, faces=self.tsdf_faces)  # halo side table of the written rows
-        # affected = ordered first-occurrence dedup of the 8 affected blocks per key
         if 8 * U > self._dedup.bucket_count:
             self._dedup = BlockHashSet(16 * U, 16 * U, device=dev)
         affected = torch.empty((8 * U, 3), dtype=torch.int32, device=dev)
         n_dev = torch.empty(1, dtype=torch.int64, device=dev)
         s = _order_streams([self._dedup])
-        check(_lib.load().vs_affected_dedup(self._dedup.handle, ptr(k), U, ptr(affected), ptr(n_dev),
-                                            ctypes.c_void_p(s.cuda_stream)), "affected_dedup")
+        check(lib.vs_affected_dedup(self._dedup.handle, ptr(k), U, ptr(affected), ptr(n_dev),
+                                    ctypes.c_void_p(s.cuda_stream)), "affected_dedup")
         _mark_done([self._dedup], s)
-        self._dedup.check_capacity()
-        A = int(n_dev.item())
-        affected = affected[:A]
-        # recompute + mc_map.put
-        self.mc_map.insert_many_exact(affected)
-        _, mpos = self.mc_map.find_keys(affected)
-        mpos = mpos.to(torch.int64)
-        mc, q, _ = encode_keys(self.tsdf_map, self.tsdf_pool, affected, counts=False, faces=self.tsdf_faces)
-        self.mc_pool[mpos] = mc
-        self.q_pool[mpos] = q
-        fan_out(self.streams(), affected)
-        return affected
+        if sync:
+            A = int(n_dev.item())
+            affected = affected[:A]
+            _, mpos = self.mc_map.insert_many_exact(affected)  # mc_map.put (positions of every key)
+            n_bound = None
+        else:
+            mpos = torch.empty(8 * U, dtype=torch.int32, device=dev)
+            created = torch.empty(8 * U, dtype=torch.uint8, device=dev)
+            s = _order_streams([self.mc_map])
+            check(lib.vs_table_insert_bounded(self.mc_map.handle, ptr(affected), 8 * U, ptr(n_dev), ptr(created),
+                                              ptr(mpos), ctypes.c_void_p(s.cuda_stream)), "mc_map insert")
+            _mark_done([self.mc_map], s)
+            n_bound = n_dev
+        # recompute straight into the MC / quantised pools at the map positions
+        encode_keys(self.tsdf_map, self.tsdf_pool, affected, mc=self.mc_pool, q=self.q_pool, counts=False,
+                    faces=self.tsdf_faces, out_rows=mpos, n_dev=n_bound)
+        streams = self.streams()
+        if streams:
+            fan_out(streams, affected, sync=False, n_dev=n_bound)
+        if sync:
+            return affected
+        return affected, n_dev
+
+    def check(self) -> None:
+        """Raise CapacityExhausted if a sync=False update ran out of entries."""
+        self.tsdf_map.check_capacity()
+        self.mc_map.check_capacity()
 
     def on_reset_blocks(self, keys) -> None:
         """server.py:425-436: remove from both maps and every client set."""

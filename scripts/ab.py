@@ -19,10 +19,12 @@ import sys
 
 ROOT = pathlib.Path(__file__).resolve().parent.parent
 SECTIONS = {
-    "hash": ["--no-cpu", "--no-mc", "--no-stream", "--no-rc", "--no-e2e", "--steps", "200"],
-    "mc": ["--no-cpu", "--no-stream", "--no-rc", "--no-e2e", "--steps", "5", "--mc-steps", "20", "--no-mc-parity"],
-    "stream": ["--no-cpu", "--no-mc", "--no-rc", "--no-e2e", "--steps", "5"],
-    "rc": ["--no-cpu", "--no-mc", "--no-stream", "--no-e2e", "--steps", "5"],
+    "hash": ["--no-cpu", "--no-mc", "--no-stream", "--no-rc", "--no-e2e", "--no-server", "--steps", "200"],
+    "mc": ["--no-cpu", "--no-stream", "--no-rc", "--no-e2e", "--no-server", "--steps", "5", "--mc-steps", "20",
+           "--no-mc-parity"],
+    "stream": ["--no-cpu", "--no-mc", "--no-rc", "--no-e2e", "--no-server", "--steps", "5"],
+    "server": ["--no-cpu", "--no-mc", "--no-rc", "--no-e2e", "--no-stream", "--steps", "5"],
+    "rc": ["--no-cpu", "--no-mc", "--no-stream", "--no-e2e", "--no-server", "--steps", "5"],
 }
 
 

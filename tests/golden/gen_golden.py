@@ -401,6 +401,29 @@ def gen_fusion() -> None:
         touched_counts=np.array([len(t) for t in touched]), touched=np.concatenate(touched))
 
 
+def gen_extract() -> None:
+    """BlockHashSet.extract_batch (concurrent_hash.py:366-402): the rotation
+    start it draws (random.randrange(capacity) after random.seed(seed)) and
+    the keys it returns, over a churned table (excess chains, holes)."""
+    out = []
+    for seed in range(6):
+        s = ch.BlockHashSet(64, 64)
+        rng = np.random.default_rng(100 + seed)
+        keys = [tuple(int(v) for v in k) for k in rng.integers(-50, 50, (100, 3))]
+        for k in keys:
+            s.insert(k)
+        for k in keys[::3]:
+            s.remove(k)
+        max_n = [1, 5, 17, 40, 200, 0][seed]
+        random.seed(seed)
+        start = random.randrange(s.capacity)
+        random.seed(seed)
+        got = s.extract_batch(max_n)
+        out.append({"inserted": [list(k) for k in keys], "removed_every": 3, "max_n": max_n, "start": start,
+                    "extracted": [list(k) for k in got], "remaining": sorted(list(k) for k in s.snapshot_keys())})
+    (OUT / "extract.json").write_text(json.dumps(out))
+
+
 def main() -> None:
     gen_hash_kat()
     gen_hash_seq()
@@ -412,6 +435,7 @@ def main() -> None:
     gen_server()
     gen_visibility()
     gen_fusion()
+    gen_extract()
     for p in sorted(OUT.iterdir()):
         if p.suffix in (".json", ".npz"):
             print(f"{p.name:24s} {p.stat().st_size:>9d} B")

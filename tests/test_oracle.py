@@ -262,3 +262,17 @@ def test_fusion_oracle_matches_reference_sequence(golden):
         tsdf, wt, col = m.blocks[k]
         assert np.array_equal(tsdf, s["tsdf"][i]) and np.array_equal(wt, s["weight"][i])
         assert np.array_equal(col, s["color"][i])
+
+
+def test_extract_matches_reference(golden):
+    """oh_extract == BlockHashSet.extract_batch (concurrent_hash.py:366-402)
+    given the rotation start the reference drew (extract.json)."""
+    for case in json.loads((golden / "extract.json").read_text()):
+        o = oracle.OracleHashSet(64, 64)
+        keys = np.array(case["inserted"], np.int32)
+        o.insert_batch(keys)
+        o.erase_batch(keys[:: case["removed_every"]])
+        got = o.extract(case["max_n"], case["start"])
+        assert got.tolist() == case["extracted"]
+        snap = o.snapshot()[0]
+        assert sorted(snap.tolist()) == case["remaining"]
