@@ -46,8 +46,13 @@ def parse():
     p.add_argument("--steps", type=int, default=300)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--live", type=int, default=10_000_000, help="live keys per GPU (config 2: 10M)")
-    p.add_argument("--batch-log2", type=int, default=22)
+    p.add_argument("--live", type=int, default=None,
+                   help="live keys per GPU (default: config 2's 10M at N=1, config 5's 1e9/N at N>1)")
+    p.add_argument("--batch-log2", type=int, default=None,
+                   help="log2 ops per batch per GPU (default: 22 = config 2 at N=1, 24 = config 5 at N>1)")
+    p.add_argument("--config5-slice", type=int, default=0, metavar="G",
+                   help="at N=1: run config 5's per-GPU slice for G GPUs (1e9/G live keys, 2^24-op batches)")
+    p.add_argument("--no-config1", action="store_true")
     p.add_argument("--bucket-frac", type=float, default=0.5,
                    help="share of the 0.7-load-factor slots in the bucket region (rest: excess)")
     p.add_argument("--mc-steps", type=int, default=10)
@@ -74,11 +79,17 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu capture."""
+def ncu_traffic(kernel: str, units: int | None = None):
+    """dram bytes per launch of `kernel` from the committed ncu capture --
+    only when that capture processed the same number of units per launch
+    (ops or blocks) as the launch it is reported beside; else None."""
     try:
         d = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
-        return d.get(kernel, {}).get("dram_bytes_per_launch")
+        for key in (f"{kernel}@{units}", kernel):
+            rec = d.get(key)
+            if rec and rec.get("units_per_launch") == units:
+                return rec.get("dram_bytes_per_launch")
+        return None
     except Exception:
         return None
 
@@ -325,7 +336,7 @@ def run_hash(args, dev, rank, world):
         torch.cuda.synchronize()
         sol[str(hops)] = hops * B / (p0.elapsed_time(p1) / 10 / 1e3) / 1e9
     del probe_out
-    traffic = ncu_traffic("k_apply")
+    traffic = ncu_traffic("k_apply", B)
     out = {
         "value": value, "ms_per_step": ms / args.steps, "ok": ok and size_ok, "clocks": clk,
         "exchange": router.exchange if router else None,
@@ -395,6 +406,129 @@ def run_hash(args, dev, rank, world):
                               "copy-in / compute / copy-out overlapped on three streams"}
     del batches, results
     return out
+
+
+def run_config1(args, dev):
+    """Config 1 (the reference's CPU-runnable case): 100k int3
+    keys with ~20% duplicates inserted into BlockHashSet(2^17, 2^17), found
+    (with 100k absent probes) and erased, plus the MC encode of 10k random
+    blocks.  GPU per step: vs_table_insert + vs_table_find + vs_table_erase
+    (400k ops) and one encode launch; beside it the reference algorithm (C
+    restatement of concurrent_hash.py:159-295 / mc_encoding.py:118-172) on
+    the same inputs on this box's host cores.  Per-op flags are checked
+    against the counts the reference gives (80,000 created, 100,000 found +
+    100,000 absent, 80,000 erased) on every step, and the MC bytes against
+    the oracle once."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_1805_03709_b200 import BlockHashSet, _lib, encode_keys, workloads
+
+    keys, absent = workloads.config1_keys()
+    probe = np.concatenate([keys, absent])
+    dk = torch.from_numpy(keys).to(dev)
+    dp = torch.from_numpy(probe).to(dev)
+    s = BlockHashSet(1 << 17, 1 << 17, device=dev)
+    n_ops = len(keys) * 2 + len(probe)
+    expect_found = torch.cat([torch.ones(len(keys), dtype=torch.uint8), torch.zeros(len(absent), dtype=torch.uint8)])
+
+    def step(k, p):
+        c, _ = s.insert_keys(k)
+        f, _ = s.find_keys(p)
+        e, _ = s.erase_keys(k)
+        return c, f, e
+
+    def check(c, f, e):
+        return (int(c.sum()) == 80_000 and torch.equal(f.cpu(), expect_found) and int(e.sum()) == 80_000)
+
+    ok = True
+    for _ in range(3):
+        ok &= check(*step(dk, dp))
+    steps = 50
+    res = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with _lib.Profile() as prof:
+        e0.record()
+        for _ in range(steps):
+            res.append(step(dk, dp))
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    ok &= all(check(*r) for r in res[-3:])
+    ok &= s.approx_size() == 0
+    # e2e: pinned host keys in, the three flag vectors out, every step
+    hk, hp = torch.from_numpy(keys).pin_memory(), torch.from_numpy(probe).pin_memory()
+    hc = torch.empty(len(keys), dtype=torch.uint8).pin_memory()
+    hf = torch.empty(len(probe), dtype=torch.uint8).pin_memory()
+    he = torch.empty(len(keys), dtype=torch.uint8).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(steps):
+        c, f, e = step(hk.to(dev, non_blocking=True), hp.to(dev, non_blocking=True))
+        hc.copy_(c, non_blocking=True)
+        hf.copy_(f, non_blocking=True)
+        he.copy_(e, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / steps
+    ok &= check(hc, hf, he)
+    # MC: 10k blocks, field (a) of SURVEY §8d, one encode launch per step
+    mkeys = workloads.config1_mc_keys()
+    tsdf, weight, color = workloads.random_field(len(mkeys))
+    rows = oracle.make_pool(tsdf, weight, color)
+    t = BlockHashSet(1 << 14, 1 << 14, device=dev)
+    dmk = torch.from_numpy(mkeys).to(dev)
+    _, pos = t.insert_keys(dmk)
+    pool = torch.zeros((t.capacity, 6144), dtype=torch.uint8, device=dev)
+    pool[pos.long()] = torch.from_numpy(rows).to(dev)
+    mc = torch.empty((len(mkeys), 2048), dtype=torch.uint8, device=dev)
+    q = torch.empty((len(mkeys), 512), dtype=torch.int8, device=dev)
+    cnt = torch.empty(len(mkeys), dtype=torch.int32, device=dev)
+    for _ in range(3):
+        encode_keys(t, pool, dmk, mc=mc, q=q, counts=cnt)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(steps):
+        encode_keys(t, pool, dmk, mc=mc, q=q, counts=cnt)
+    e1.record()
+    torch.cuda.synchronize()
+    mc_ms = e0.elapsed_time(e1) / steps
+    nbr = oracle.neighbor_table(mkeys, mkeys)
+    omc, oq, _ = oracle.mc_encode(rows, nbr, threads=1)
+    mc_ok = bool(np.array_equal(mc.cpu().numpy(), omc) and np.array_equal(q.cpu().numpy(), oq))
+    # the reference algorithm on the host, same inputs: the C restatement
+    # (sequential, one thread, like the reference under the GIL)
+    o = oracle.OracleHashSet(1 << 17, 1 << 17)
+    ct = []
+    for _ in range(3):
+        a = time.perf_counter()
+        oc = o.insert_batch(keys)[0]
+        of = o.find_batch(probe)[0]
+        oe = o.erase_batch(keys)[0]
+        ct.append(time.perf_counter() - a)
+    cpu_ok = bool(int(oc.sum()) == 80_000 and int(of.sum()) == 100_000 and int(oe.sum()) == 80_000)
+    a = time.perf_counter()
+    oracle.mc_encode(rows, nbr, threads=1)
+    cpu_mc_s = time.perf_counter() - a
+    return {"workload": "config 1: 100k int3 keys (~20% duplicates) insert + find (with 100k absent probes) + "
+                        "erase on BlockHashSet(2^17, 2^17); MC + quantised encode of 10k random 8^3 blocks",
+            "hash": {"value": n_ops / (ms / 1e3) / 1e6, "unit": "M ops/s", "ms_per_step": ms, "ops_per_step": n_ops,
+                     "gpu_launches_per_step": prof.launches / steps,
+                     "e2e": {"value": n_ops / (e2e_ms / 1e3) / 1e6, "unit": "M ops/s",
+                             "h2d_bytes_per_step": (len(keys) + len(probe)) * 12,
+                             "d2h_bytes_per_step": len(keys) * 2 + len(probe),
+                             "note": "pinned host keys -> device, the three BlockHashSet calls, flags -> host"}},
+            "mc": {"value": len(mkeys) / (mc_ms / 1e3), "unit": "blocks/s", "ms_per_step": mc_ms, "ok": mc_ok},
+            "ok": bool(ok),
+            "cpu_reference": {"hash": {"value": n_ops / min(ct) / 1e6, "unit": "M ops/s", "cores": 1, "kind": "port",
+                                       "ok": cpu_ok},
+                              "mc": {"value": len(mkeys) / cpu_mc_s, "unit": "blocks/s", "cores": 1, "kind": "port"},
+                              "sample": "the whole config-1 workload (C restatement of the reference algorithm, "
+                                        "sequential, one thread); the reference Python itself measured 0.40/0.82/0.38 "
+                                        "M ops/s and 8.6k blocks/s/core (SURVEY §6)"}}
 
 
 def mc_full_parity(t, pool, keys, mc, q, counts, threads: int, chunk: int = 1 << 17):
@@ -536,7 +670,7 @@ def run_mc(args, dev, world=1):
                                              f"on {cpu_cores()} host threads, {parity_s:.1f} s",
            "gpu_launches": launches, "clocks": clk,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                        "traffic": ncu_traffic("k_mc_encode"), "kernel": "vsb::k_mc_encode<true,false,false>",
+                        "traffic": ncu_traffic("k_mc_encode", N), "kernel": "vsb::k_mc_encode<true,false,false>",
                         "kernel_ms": k_ms, "bytes_per_launch": N * BYTES_PER_BLOCK, "peak_source": src,
                         "bytes_per_block": "6144 TSDF read + 2048 MC + 512 quantised (SURVEY §8d)"},
            "compact": {"value": world * N / (c_ms / 1e3), "unit": "blocks/s", "ms_per_step": c_ms,
@@ -1005,13 +1139,28 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     from paper_1805_03709_b200 import workloads
 
+    # config 2 (10M keys, 2^22-op batches) on one GPU; config 5 (1e9 keys
+    # sharded by hash, 2^24-op batches per GPU) when the job spans N > 1 GPUs
+    # or --config5-slice G asks for one GPU's share of a G-GPU run
+    c5 = world if world > 1 else args.config5_slice
+    if args.live is None:
+        args.live = 1_000_000_000 // c5 if c5 > 1 else 10_000_000
+    if args.batch_log2 is None:
+        args.batch_log2 = 24 if c5 > 1 else 22
+    if c5 > 1 and args.steps == 300:
+        args.steps = 50  # 2^24-op batches: the pre-generated inputs stay within HBM
     spec = workloads.MixSpec(live=args.live, load_factor=0.7, batch=1 << args.batch_log2, bucket_frac=args.bucket_frac)
     threads = args.cpu_threads or cpu_cores()
-    config = {"workload": "config 2: 10M-key block hash set, 50/30/20 insert/find/erase mix, load factor 0.7, "
-                          f"batches of 2^{args.batch_log2} ops (one launch per batch)",
+    wl = ("config 2: 10M-key block hash set, 50/30/20 insert/find/erase mix, load factor 0.7, "
+          f"batches of 2^{args.batch_log2} ops (one launch per batch)") if c5 <= 1 else (
+          f"config 5: {spec.live * c5 / 1e9:.2g}B-key block hash set sharded by hash over {c5} GPUs "
+          f"({spec.live:,} live keys per GPU), 50/30/20 mix, load factor 0.7, 2^{args.batch_log2}-op batches per GPU"
+          + ("" if world > 1 else f"; ONE GPU's slice of a {c5}-GPU run (no routing)"))
+    config = {"workload": wl,
               "live_keys_per_gpu": spec.live, "slots_per_gpu": spec.slots, "batch_ops": spec.batch,
               "mix": spec.counts, "key_space": "int3 in [-2^20, 2^20)^3 (injective id map)",
-              "l2": "inputs larger than L2: 229 MB table + fresh 55 MB batch per step",
+              "l2": f"inputs larger than L2: {spec.slots * 16 / 1e6:.0f} MB table + fresh "
+                    f"{spec.batch * 14 / 1e6:.0f} MB batch per step",
               "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU"}
     if world > 1:
         config["exchange"] = ("peer stores into CUDA-IPC windows over NVLink (csrc/shard.cu)" if args.exchange != "collective"
@@ -1047,6 +1196,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
+        # communicator init lines (rank / nranks) for the launcher's records
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         if one_gpu:
             dist.init_process_group("gloo")
@@ -1069,6 +1221,10 @@ def main():
             traceback.print_exc()
             return {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
+    c1 = None
+    if not args.no_config1 and world == 1:
+        _free_cuda()
+        c1 = section(run_config1, args, dev)
     mc = None
     if not args.no_mc:
         _free_cuda()
@@ -1125,7 +1281,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": config,
                 "parity_ok": h["ok"], "roofline": h["roofline"], "gpu_launches": h["gpu_launches"],
-                "clocks": h["clocks"], "cpu_baseline": cpu, "e2e": h.get("e2e"), "mc": mc, "stream": stream, "server": server, "rc": rc}
+                "clocks": h["clocks"], "cpu_baseline": cpu, "e2e": h.get("e2e"), "config1": c1, "mc": mc, "stream": stream, "server": server, "rc": rc}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
