@@ -811,7 +811,8 @@ def run_stream(args, dev):
         st = torch.cuda.current_stream(dev)
         _lib.check(lib.vs_affected_dedup(scratch.handle, _lib.ptr(upd_all[t]), U, _lib.ptr(aff_keys[t]),
                                          _lib.ptr(aff_log[t]), ctypes.c_void_p(st.cuda_stream)))
-        # no host sync: the fan-out takes the device-side affected count
+        # no host sync: the fan-out (one launch, k_multi_fan_small) takes the
+        # device-side affected count
         fan_out(clients, aff_keys[t], sync=False, n_dev=aff_log[t])
         extract_random_many(clients, X, seeds[t], n_out=ex_log[t], keys_out=ex_keys[t])  # one launch, 16 clients
         if t % STREAM_EVERY == STREAM_EVERY - 1:
@@ -916,12 +917,14 @@ def run_stream(args, dev):
                       f"replay on the C restatement adopting the GPU's extracted keys; affected dedup == the "
                       f"reference's dict order ({parity_s:.1f} s)",
             "gpu_launches": prof.launches, "clocks": clk,
-            "roofline": {"bound": "hbm", "kernel": "fan-out chain (k_multi_insert + fixup + scan + FIFO append)",
+            "roofline": {"bound": "hbm", "kernel": "fan-out (k_multi_fan_small: inserts + fixup + scan + FIFO append)",
                          "achieved": fan_bytes / (fan_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": fan_bytes / (fan_ms / 1e3) / 1e9 / peak, "traffic": None, "kernel_ms": fan_ms,
                          "bytes_per_launch": fan_bytes, "peak_source": src,
                          "note": f"48 B per (client, key) insert (SURVEY §8d) x {C} clients x {A} affected keys; "
                                  "latency-bound: a tick's fan-out is ~65k inserts"},
+            "tick_path": "3 launches per tick: k_dedup_small -> k_multi_fan_small (inserts + created fixup + "
+                         "block scan + FIFO append, one CTA per client) -> k_multi_extract",
             "note": "inserts count created-or-not key inserts into every set; removes = extracted + reset keys; "
                     "no host sync inside a tick (device-side affected count bounds the fan-out)"}
 

@@ -123,6 +123,8 @@ def load() -> ctypes.CDLL:
                 "(there is no CPU fallback)")
         lib = ctypes.CDLL(str(LIB_PATH))
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("VSB_LIB") and not hasattr(lib, name):
+                continue  # A/B runs against an older library build (scripts/ab.py)
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

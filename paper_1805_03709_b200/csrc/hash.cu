@@ -13,6 +13,7 @@
 #define VSB_PDL 1
 #endif
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(kOpBlock) k_probe_sol(TableView T, uint64_t n,
 // One op of any kind on one key, then its post pass, in a single thread
 // (the per-key compatibility path: BlockHashSet.insert/remove/__contains__).
 __global__ void k_single(TableView T, const int32_t* __restrict__ kio, uint8_t op, uint8_t* __restrict__ res,
-                         int32_t* __restrict__ idx) {
+                         int32_t* __restrict__ idx, uint32_t* __restrict__ done, uint32_t seq) {
   const int32_t x = kio[0], y = kio[1], z = kio[2];
   int delta = 0;
   if (op == VS_OP_INSERT) {
@@ -312,6 +313,9 @@ __global__ void k_single(TableView T, const int32_t* __restrict__ kio, uint8_t o
     *idx = pos;
   }
   if (delta) atomicAdd((unsigned long long*)&T.ctl->size[0], (unsigned long long)(long long)delta);
+  // results first, then the completion word the host spins on (mapped memory)
+  __threadfence_system();
+  *(volatile uint32_t*)done = seq;
 }
 
 // Post pass after k_insert / k_apply: created flags to the lowest op index
@@ -751,6 +755,7 @@ vs_status vs_table_destroy(vs_table* t) {
   cudaFree(t->chunk_counts);
   cudaFree(t->chunk_offsets);
   cudaFree(t->pos_work);
+  if (t->stage_host) cudaFreeHost(t->stage_host);
   delete t;
   return VS_OK;
 }
@@ -892,8 +897,27 @@ vs_status vs_table_single(vs_table* t, int op, const int32_t key_host[3], uint8_
   hk[1] = key_host[1];
   hk[2] = key_host[2];
   int32_t* dk = (int32_t*)t->stage_dev;
-  { k_single<<<1, 1, 0, s>>>(t->next_view(), dk, (uint8_t)op, (uint8_t*)(t->stage_dev + 20), dk + 4); vsb::count_launch(); }
-  VS_CK(cudaStreamSynchronize(s));
+  const uint32_t seq = ++t->stage_seq;
+  { k_single<<<1, 1, 0, s>>>(t->next_view(), dk, (uint8_t)op, (uint8_t*)(t->stage_dev + 20), dk + 4,
+                            (uint32_t*)(t->stage_dev + 28), seq); vsb::count_launch(); }
+  VS_CK(cudaGetLastError());
+  // Wait by spinning on the completion word the kernel writes last: a per-key
+  // call then costs the launch and the op itself, not a stream
+  // synchronisation.  A busy stream (the key queued behind long work) or a
+  // fault falls back to the blocking synchronisation after ~50 us.
+  volatile uint32_t* done = (volatile uint32_t*)(t->stage_host + 28);
+  const auto t0 = std::chrono::steady_clock::now();
+  bool spun = false;
+  while (*done != seq) {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(50)) {
+      spun = true;
+      break;
+    }
+  }
+  if (spun) VS_CK(cudaStreamSynchronize(s));
   *index_host = ((volatile int32_t*)t->stage_host)[4];
   *result_host = ((volatile uint8_t*)t->stage_host)[20];
   if (op == VS_OP_INSERT && *index_host < 0) {

@@ -25,6 +25,9 @@
 #include "scan.cuh"
 #include "table.h"
 
+#ifndef VSB_FAN_SMALL
+#define VSB_FAN_SMALL 1  // one-launch fan-out for n <= 4096 keys (k_multi_fan_small)
+#endif
 #ifndef VSB_DEDUP_MIX
 #define VSB_DEDUP_MIX 1
 #endif
@@ -99,6 +102,115 @@ __global__ void k_fifo_tail(const __grid_constant__ FifoViews F, bool fifo, cons
   const uint64_t cnt = off[(uint64_t)(c + 1) * n] - off[(uint64_t)c * n];
   if (fifo) *F.tail[c] += cnt;
   if (n_created) n_created[c] = cnt;
+}
+
+// A tick's fan-out (n <= kFanKeys affected keys) in ONE launch: one CTA per
+// client runs its inserts (every thread issues the bucket loads of its keys
+// before walking any chain), then -- after a CTA barrier, so every duplicate
+// claim of this client is in -- the created-flag fixup, a block scan of the
+// created flags in key order, the FIFO append and the tail update.  The
+// multi-kernel chain above (insert -> fixup -> 3-kernel scan -> append ->
+// tail) stays for large fan-outs (fresh fills).
+constexpr int kFanThreads = 1024;
+constexpr int kFanPer = 4;
+constexpr uint32_t kFanKeys = kFanThreads * kFanPer;  // 4096 (a 512-key update tick)
+
+__global__ void __launch_bounds__(kFanThreads) k_multi_fan_small(const __grid_constant__ SetViews V,
+                                                                 const __grid_constant__ FifoViews F, bool fifo,
+                                                                 const int32_t* __restrict__ keys, uint32_t n,
+                                                                 const uint64_t* __restrict__ n_dev,
+                                                                 uint8_t* __restrict__ created,
+                                                                 uint64_t* __restrict__ n_created) {
+  pdl_wait();
+  __shared__ uint8_t s_cr[kFanKeys];
+  __shared__ uint32_t s_warp[kFanThreads / 32];
+  __shared__ uint64_t s_tail;
+  const int c = blockIdx.x;
+  const TableView& T = V.v[c];
+  const uint32_t t = threadIdx.x;
+  const uint32_t nv = n_dev && *n_dev < n ? (uint32_t)*n_dev : n;
+  // ---- inserts: key i = t + k * kFanThreads (coalesced), bucket loads first
+  int32_t x[kFanPer], y[kFanPer], z[kFanPer], pos[kFanPer];
+  int4 pre[kFanPer];
+#pragma unroll
+  for (int k = 0; k < kFanPer; ++k) {
+    const uint32_t i = t + k * kFanThreads;
+    if (i < nv) {
+      x[k] = keys[3 * i], y[k] = keys[3 * i + 1], z[k] = keys[3 * i + 2];
+      pre[k] = ld_bucket(T.e + bucket_of(T, x[k], y[k], z[k]));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kFanPer; ++k) {
+    const uint32_t i = t + k * kFanThreads;
+    if (i < nv) {
+      const InsertResult r = insert_key(T, x[k], y[k], z[k], (int32_t)i, &pre[k]);
+      s_cr[i] = r.created;
+      pos[k] = r.pos;
+    } else if (i < n) {
+      s_cr[i] = 0;
+    }
+  }
+  __syncthreads();  // all of this client's inserts (and duplicate claims) done
+  // ---- created flags to the lowest op index among duplicates, FRESH cleared
+#pragma unroll
+  for (int k = 0; k < kFanPer; ++k) {
+    const uint32_t i = t + k * kFanThreads;
+    if (i < nv && s_cr[i]) post_op(T, keys, i, 0 /*VS_OP_INSERT*/, s_cr, pos[k]);
+  }
+  __syncthreads();
+  // ---- exclusive scan of the flags in key order: thread t owns [4t, 4t+4)
+  uint32_t own = 0;
+#pragma unroll
+  for (int k = 0; k < kFanPer; ++k) {
+    const uint32_t i = t * kFanPer + k;
+    own += i < n ? s_cr[i] : 0u;
+  }
+  uint32_t incl = own;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if ((int)lane_id() >= d) incl += v;
+  }
+  if (lane_id() == 31) s_warp[t >> 5] = incl;
+  if (t == 0) s_tail = fifo ? *F.tail[c] : 0;
+  __syncthreads();
+  if (t < 32) {
+    uint32_t w = s_warp[t];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, w, d);
+      if ((int)t >= d) w += v;
+    }
+    s_warp[t] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  const uint32_t total = s_warp[kFanThreads / 32 - 1];
+  uint32_t rank = ((t >> 5) ? s_warp[(t >> 5) - 1] : 0u) + incl - own;
+  // ---- FIFO append (deque.append order = affected order) + created flags out
+#pragma unroll
+  for (int k = 0; k < kFanPer; ++k) {
+    const uint32_t i = t * kFanPer + k;
+    if (i >= n) break;
+    const uint8_t cr = s_cr[i];
+    if (created) created[(uint64_t)c * n + i] = cr;
+    if (cr && fifo) {
+      const uint64_t p = (s_tail + rank) % F.cap[c];
+      int32_t* dst = F.keys[c] + 3 * p;
+      dst[0] = keys[3 * i];
+      dst[1] = keys[3 * i + 1];
+      dst[2] = keys[3 * i + 2];
+    }
+    rank += cr;
+  }
+  if (t == 0) {
+    if (fifo) *F.tail[c] = s_tail + total;
+    if (n_created) n_created[c] = total;
+    if (total) {
+      const uint32_t w = blockIdx.x;  // one live-key counter stripe per client CTA
+      atomicAdd((unsigned long long*)&T.ctl->size[(w % kSizeStripes) * kSizeStride], (unsigned long long)total);
+    }
+  }
 }
 
 // Frustum-AABB visibility of a block (server.py:375-387): every plane
@@ -575,6 +687,21 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
     set_error("keys/created must be non-NULL");
     return VS_ERR_INVALID;
   }
+  const bool fifo = fifo_keys_host && fifo_cap_host && fifo_tail_host;
+  FifoViews F{};
+  if (fifo) {
+    for (int c = 0; c < n_sets; ++c) {
+      F.keys[c] = fifo_keys_host[c];
+      F.cap[c] = fifo_cap_host[c] ? fifo_cap_host[c] : 1;
+      F.tail[c] = fifo_tail_host[c];
+    }
+  }
+  if (n <= kFanKeys && VSB_FAN_SMALL) {  // a tick: one launch, no scratch
+    { VS_CK(launch_pdl(k_multi_fan_small, n_sets, kFanThreads, 0, s, V, F, fifo, keys, (uint32_t)n, n_dev, created,
+                       n_created)); vsb::count_launch(); }
+    VS_CK_LAUNCH("vs_stream_insert_many");
+    return VS_OK;
+  }
   const uint64_t total = (uint64_t)n_sets * n;
   // one stream-ordered allocation carved into the three scratch arrays
   const size_t b_index = (4 * total + 255) & ~(size_t)255, b_off = (8 * (total + 1) + 255) & ~(size_t)255;
@@ -588,15 +715,6 @@ vs_status vs_stream_insert_many(vs_table* const* sets_host, int n_sets, const in
   { VS_CK(launch_pdl(k_multi_insert, grid, 256, 0, s, V, keys, n, n_dev, created, index)); vsb::count_launch(); }
   { VS_CK(launch_pdl(k_multi_fixup, grid, 256, 0, s, V, keys, n, created, index)); vsb::count_launch(); }
   cudaError_t e = exclusive_scan<uint8_t>(created, total, off, work, s);
-  const bool fifo = fifo_keys_host && fifo_cap_host && fifo_tail_host;
-  FifoViews F{};
-  if (fifo) {
-    for (int c = 0; c < n_sets; ++c) {
-      F.keys[c] = fifo_keys_host[c];
-      F.cap[c] = fifo_cap_host[c] ? fifo_cap_host[c] : 1;
-      F.tail[c] = fifo_tail_host[c];
-    }
-  }
   if (e == cudaSuccess && fifo) { e = launch_pdl(k_fifo_append, grid, 256, 0, s, F, keys, n, created, off); vsb::count_launch(); }
   if (e == cudaSuccess) { e = launch_pdl(k_fifo_tail, 1, 32, 0, s, F, fifo, off, n, n_sets, n_created); vsb::count_launch(); }
   cudaFreeAsync(scratch_mem, s);

@@ -26,6 +26,7 @@ struct vs_table {
   int32_t* pos_work = nullptr;        // lazily allocated, cap entries
   uint8_t* stage_host = nullptr;      // pinned staging of the single-key path (32 B)
   uint8_t* stage_dev = nullptr;
+  uint32_t stage_seq = 0;             // completion sequence of the single-key path
 
   // view for ONE launch; next_epoch() gives it a fresh claim tag
   vsb::TableView view() const {
