@@ -1202,6 +1202,7 @@ def main():
         # communicator init lines (rank / nranks) for the launcher's records
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout keeps the one JSON line
         torch.cuda.set_device(local)
         if one_gpu:
             dist.init_process_group("gloo")
