@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--no-server", action="store_true")
     p.add_argument("--rc-frames", type=int, default=20)
     p.add_argument("--stream-ticks", type=int, default=200)
+    p.add_argument("--stream-separate", action="store_true",
+                   help="config-4 ticks as three calls (dedup, fan-out, extraction) instead of vs_stream_tick")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
@@ -785,7 +787,7 @@ def run_stream(args, dev):
 
     import oracle
     from paper_1805_03709_b200 import (BlockHashSet, StreamSet, _lib, extract_random_many, fan_out,
-                                       remove_everywhere, workloads)
+                                       remove_everywhere, stream_tick, workloads)
 
     scene_np = workloads.room_block_keys()
     keys = torch.from_numpy(scene_np).to(dev)
@@ -808,13 +810,18 @@ def run_stream(args, dev):
     seeds = [[(t * C + c) * 2654435761 + 17 for c in range(C)] for t in range(ticks + 1)]
 
     def tick(t):
-        st = torch.cuda.current_stream(dev)
-        _lib.check(lib.vs_affected_dedup(scratch.handle, _lib.ptr(upd_all[t]), U, _lib.ptr(aff_keys[t]),
-                                         _lib.ptr(aff_log[t]), ctypes.c_void_p(st.cuda_stream)))
-        # no host sync: the fan-out (one launch, k_multi_fan_small) takes the
-        # device-side affected count
-        fan_out(clients, aff_keys[t], sync=False, n_dev=aff_log[t])
-        extract_random_many(clients, X, seeds[t], n_out=ex_log[t], keys_out=ex_keys[t])  # one launch, 16 clients
+        if not args.stream_separate:
+            # ONE launch: dedup -> fan-out into all 16 sets -> 16 extractions
+            stream_tick(clients, upd_all[t], X, seeds[t], affected_out=aff_keys[t], n_affected=aff_log[t],
+                        keys_out=ex_keys[t], n_out=ex_log[t])
+        else:
+            st = torch.cuda.current_stream(dev)
+            _lib.check(lib.vs_affected_dedup(scratch.handle, _lib.ptr(upd_all[t]), U, _lib.ptr(aff_keys[t]),
+                                             _lib.ptr(aff_log[t]), ctypes.c_void_p(st.cuda_stream)))
+            # no host sync: the fan-out (one launch, k_multi_fan_small) takes the
+            # device-side affected count
+            fan_out(clients, aff_keys[t], sync=False, n_dev=aff_log[t])
+            extract_random_many(clients, X, seeds[t], n_out=ex_log[t], keys_out=ex_keys[t])  # one launch
         if t % STREAM_EVERY == STREAM_EVERY - 1:
             victim = clients[(t // STREAM_EVERY) % C]
             victim.clear()
@@ -923,8 +930,10 @@ def run_stream(args, dev):
                          "bytes_per_launch": fan_bytes, "peak_source": src,
                          "note": f"48 B per (client, key) insert (SURVEY §8d) x {C} clients x {A} affected keys; "
                                  "latency-bound: a tick's fan-out is ~65k inserts"},
-            "tick_path": "3 launches per tick: k_dedup_small -> k_multi_fan_small (inserts + created fixup + "
-                         "block scan + FIFO append, one CTA per client) -> k_multi_extract",
+            "tick_path": ("3 launches per tick: k_dedup_small -> k_multi_fan_small -> k_multi_extract"
+                          if args.stream_separate else
+                          "ONE launch per tick (vs_stream_tick): per client one CTA runs the affected dedup, "
+                          "the fan-out (inserts, created fixup, block scan, FIFO append) and its extraction"),
             "note": "inserts count created-or-not key inserts into every set; removes = extracted + reset keys; "
                     "no host sync inside a tick (device-side affected count bounds the fan-out)"}
 

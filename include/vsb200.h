@@ -279,6 +279,24 @@ vs_status vs_stream_insert_many(vs_table *const *sets_host, int n_sets,
                                 const uint64_t *fifo_cap_host, uint64_t *const *fifo_tail_host,
                                 uint64_t *n_created, vs_stream_t stream);
 
+/* One stream-set tick in ONE launch (up to 32 client sets):
+ *   affected = ordered first-occurrence dedup of affected_mc_blocks(k) over
+ *              the u updated keys (mc_encoding.py:108-115, server.py:304-307)
+ *              -> affected_out (device int32[8u][3]), *n_affected (device u64);
+ *   insert_many(affected) into every set with the FIFO append of the created
+ *              keys (server.py:314-315; fifo_* as vs_stream_insert_many),
+ *              n_created[c] (device u64[C], may be NULL);
+ *   extract_batch(max_extract) from every set (concurrent_hash.py:382-402,
+ *              seeds_host[c] as vs_stream_extract_random) -> keys_out[c],
+ *              n_out[c].
+ * Equivalent to vs_affected_dedup + vs_stream_insert_many +
+ * vs_stream_extract_random on the same stream; 1 <= u <= 512.  Asynchronous. */
+vs_status vs_stream_tick(vs_table *const *sets_host, int n_sets, const int32_t *updated, uint64_t u,
+                         int32_t *const *fifo_keys_host, const uint64_t *fifo_cap_host,
+                         uint64_t *const *fifo_tail_host, uint64_t max_extract, const uint64_t *seeds_host,
+                         int32_t *affected_out, uint64_t *n_affected, uint64_t *n_created,
+                         int32_t *keys_out, uint64_t *n_out, vs_stream_t stream);
+
 /* extract_batch (concurrent_hash.py:366-402) on up to 32 sets in ONE launch:
  * set c scans its live entries in position order from a start position
  * derived from seeds_host[c] (wrapping), removes and returns the first max_n:

@@ -30,14 +30,14 @@ from .mc_encoding import (
     recompute_mc_block,
     recompute_mc_blocks,
 )
-from .server import GpuServerCore, StreamSet, extract_random_many, fan_out, remove_everywhere
+from .server import GpuServerCore, StreamSet, extract_random_many, fan_out, remove_everywhere, stream_tick
 from .voxel_model import BLOCK_EDGE, TsdfBlock
 
 __all__ = [
     "BLOCK_EDGE", "BlockHashMap", "BlockHashSet", "BlockKey", "CapacityExhausted", "FreeListStack",
     "GpuServerCore", "McBlock", "McVoxel", "NativeUnavailable", "StreamSet", "TsdfBlock",
     "affected_mc_blocks", "apply_cutoff", "compact", "compute_mc_index", "encode_blocks", "encode_keys", "face_packs",
-    "extract_random_many", "fan_out", "hash_key", "hash_keys", "neighbors", "pack_mc_batch", "recompute_mc_block", "recompute_mc_blocks",
+    "extract_random_many", "stream_tick", "fan_out", "hash_key", "hash_keys", "neighbors", "pack_mc_batch", "recompute_mc_block", "recompute_mc_blocks",
     "remove_everywhere",
 ]
 

@@ -213,6 +213,265 @@ __global__ void __launch_bounds__(kFanThreads) k_multi_fan_small(const __grid_co
   }
 }
 
+// ---- One stream-set tick per launch (k_stream_tick): for every client, ONE
+// CTA of 1,024 threads runs, back to back,
+//   1. the affected dedup of the tick's updated keys (mc_encoding.py:108-115,
+//      server.py:304-307: expand x8 in product((0,-1), repeat=3) order,
+//      first occurrence wins) in shared memory -- every CTA computes the same
+//      list (deterministic), CTA 0 also writes it out;
+//   2. the fan-out into its client's set (server.py:314-315): inserts, the
+//      created-flag fixup, a block scan of the flags in key order and the
+//      FIFO append (as k_multi_fan_small);
+//   3. the client's extract_random(max_n) (concurrent_hash.py:382-402,
+//      server.py:334-363): live entries in position order from the seeded
+//      rotating start, the first max_n taken and removed; vacated excess
+//      entries go straight back to the free list (this CTA is the only one
+//      touching its table, and its inserts are done).
+// Three launches and two grid-wide dependencies per tick become one launch.
+constexpr int kTickThreads = 1024;
+constexpr uint32_t kTickMaxU = 512;
+constexpr uint32_t kTickKeys = 8 * kTickMaxU;                 // 4,096 affected keys
+constexpr uint32_t kTickSlots = 2 * kTickKeys;                // dedup table, load <= 0.5
+constexpr int kTickPer = (int)(kTickKeys / kTickThreads);     // 4
+constexpr int kTickScanK = 4;                                 // positions per thread per extraction round
+constexpr size_t kTickSmem = 12 * (size_t)kTickKeys + 4 * (size_t)kTickSlots;  // 80 KB
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* wsum, uint32_t* total) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= (uint32_t)d) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = wsum[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= (uint32_t)d) w += y;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  *total = wsum[31];
+  const uint32_t r = incl - v + (warp ? wsum[warp - 1] : 0u);
+  __syncthreads();  // wsum free for the next scan
+  return r;
+}
+
+__global__ void __launch_bounds__(kTickThreads) k_stream_tick(const __grid_constant__ SetViews V,
+                                                              const __grid_constant__ FifoViews F,
+                                                              const __grid_constant__ FifoViews S,
+                                                              const int32_t* __restrict__ updated, uint32_t u,
+                                                              uint32_t max_n, int32_t* __restrict__ aff_out,
+                                                              uint64_t* __restrict__ n_aff,
+                                                              uint64_t* __restrict__ n_created,
+                                                              int32_t* __restrict__ keys_out,
+                                                              uint64_t* __restrict__ n_out) {
+  pdl_wait();
+  extern __shared__ int32_t dsm[];
+  int32_t* kx = dsm;  // [kTickKeys] x, then y, then z; later the compacted keys (xyz interleaved)
+  int32_t* ky = kx + kTickKeys;
+  int32_t* kz = ky + kTickKeys;
+  uint32_t* slot = (uint32_t*)(kz + kTickKeys);
+  __shared__ uint32_t wsum[32];
+  __shared__ uint8_t s_cr[kTickKeys];
+  __shared__ uint32_t wcnt[kTickScanK][32];
+  const int c = blockIdx.x;
+  const TableView& T = V.v[c];
+  const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+  uint32_t total;
+
+  // ---- 1. affected dedup (thread t owns expanded keys [4t, 4t+4): input order)
+  const uint32_t m = 8 * u;
+  for (uint32_t i = t; i < kTickSlots; i += kTickThreads) slot[i] = 0xFFFFFFFFu;
+  int32_t x[kTickPer], y[kTickPer], z[kTickPer];
+  uint32_t where[kTickPer];
+#pragma unroll
+  for (int k = 0; k < kTickPer; ++k) {
+    const uint32_t j = t * kTickPer + k;
+    if (j < m) {
+      const uint32_t i = j >> 3, d = j & 7;
+      x[k] = updated[3 * i] - (int32_t)((d >> 2) & 1);
+      y[k] = updated[3 * i + 1] - (int32_t)((d >> 1) & 1);
+      z[k] = updated[3 * i + 2] - (int32_t)(d & 1);
+      kx[j] = x[k], ky[j] = y[k], kz[j] = z[k];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kTickPer; ++k) {
+    const uint32_t j = t * kTickPer + k;
+    if (j >= m) continue;
+    uint32_t h = hash_raw(x[k], y[k], z[k]);
+    h ^= h >> 16;  // murmur3 finaliser: neighbouring keys share low hash bits
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    h &= kTickSlots - 1;
+    for (;;) {
+      const uint32_t old = atomicCAS(&slot[h], 0xFFFFFFFFu, j);
+      if (old == 0xFFFFFFFFu) break;
+      if (kx[old] == x[k] && ky[old] == y[k] && kz[old] == z[k]) {
+        atomicMin(&slot[h], j);
+        break;
+      }
+      h = (h + 1) & (kTickSlots - 1);
+    }
+    where[k] = h;
+  }
+  __syncthreads();
+  uint32_t first = 0, cnt = 0;
+#pragma unroll
+  for (int k = 0; k < kTickPer; ++k) {
+    const uint32_t j = t * kTickPer + k;
+    if (j < m && slot[where[k]] == j) {
+      first |= 1u << k;
+      ++cnt;
+    }
+  }
+  uint32_t o = block_exclusive_scan(cnt, wsum, &total);  // (every probe is done: kx.. are free now)
+  int32_t* stage = kx;  // compacted affected keys, xyz interleaved
+#pragma unroll
+  for (int k = 0; k < kTickPer; ++k) {
+    if (first & (1u << k)) {
+      stage[3 * o] = x[k], stage[3 * o + 1] = y[k], stage[3 * o + 2] = z[k];
+      ++o;
+    }
+  }
+  __syncthreads();
+  const uint32_t n = total;
+  if (c == 0) {
+    for (uint32_t i = t; i < 3 * n; i += kTickThreads) aff_out[i] = stage[i];
+    if (t == 0 && n_aff) *n_aff = n;
+  }
+
+  // ---- 2. fan-out into this client's set: key i = t + k * 1024
+  int32_t pos[kTickPer];
+  int4 pre[kTickPer];
+#pragma unroll
+  for (int k = 0; k < kTickPer; ++k) {
+    const uint32_t i = t + k * kTickThreads;
+    if (i < n) pre[k] = ld_bucket(T.e + bucket_of(T, stage[3 * i], stage[3 * i + 1], stage[3 * i + 2]));
+  }
+#pragma unroll
+  for (int k = 0; k < kTickPer; ++k) {
+    const uint32_t i = t + k * kTickThreads;
+    if (i < n) {
+      const InsertResult r = insert_key(T, stage[3 * i], stage[3 * i + 1], stage[3 * i + 2], (int32_t)i, &pre[k]);
+      s_cr[i] = r.created;
+      pos[k] = r.pos;
+    }
+  }
+  __syncthreads();  // every insert and duplicate claim of this client is in
+#pragma unroll
+  for (int k = 0; k < kTickPer; ++k) {
+    const uint32_t i = t + k * kTickThreads;
+    if (i < n && s_cr[i])
+      post_op_t(
+          T,
+          [&](uint64_t mm) {
+            return stage[3 * mm] == stage[3 * i] && stage[3 * mm + 1] == stage[3 * i + 1] &&
+                   stage[3 * mm + 2] == stage[3 * i + 2];
+          },
+          i, 0 /*VS_OP_INSERT*/, s_cr, pos[k]);
+  }
+  __syncthreads();
+  uint32_t own = 0;
+#pragma unroll
+  for (int k = 0; k < kTickPer; ++k) {
+    const uint32_t i = t * kTickPer + k;
+    own += i < n ? s_cr[i] : 0u;
+  }
+  uint32_t created_total;
+  uint32_t rank = block_exclusive_scan(own, wsum, &created_total);
+  const uint64_t tail = *F.tail[c];
+#pragma unroll
+  for (int k = 0; k < kTickPer; ++k) {
+    const uint32_t i = t * kTickPer + k;
+    if (i < n && s_cr[i]) {
+      int32_t* dst = F.keys[c] + 3 * ((tail + rank) % F.cap[c]);
+      dst[0] = stage[3 * i], dst[1] = stage[3 * i + 1], dst[2] = stage[3 * i + 2];
+      ++rank;
+    }
+  }
+  __syncthreads();  // every thread read the tail
+  if (t == 0) {
+    *F.tail[c] = tail + created_total;
+    if (n_created) n_created[c] = created_total;
+  }
+
+  // ---- 3. extract_random(max_n): rotating start (k_multi_extract's seed mix)
+  const uint32_t cap = T.n + T.excess;
+  uint64_t sd = S.cap[c] + 0x9E3779B97F4A7C15ull;
+  sd = (sd ^ (sd >> 30)) * 0xBF58476D1CE4E5B9ull;
+  sd = (sd ^ (sd >> 27)) * 0x94D049BB133111EBull;
+  sd ^= sd >> 31;
+  const uint32_t start = (uint32_t)(sd % cap);
+  int32_t* out = keys_out + (uint64_t)c * max_n * 3;
+  uint64_t found = 0;
+  constexpr uint64_t kRound = (uint64_t)kTickThreads * kTickScanK;
+  for (uint64_t base = 0; base < cap && found < max_n; base += kRound) {
+    int4 e[kTickScanK];
+    bool live[kTickScanK];
+    uint32_t bal[kTickScanK];
+#pragma unroll
+    for (int k = 0; k < kTickScanK; ++k) {
+      const uint64_t q = base + (uint64_t)k * kTickThreads + t;
+      uint64_t p = (uint64_t)start + q;
+      p = p >= cap ? p - cap : p;
+      live[k] = false;
+      if (q < cap) {
+        e[k] = ld_entry(T.e + p);
+        live[k] = ((uint32_t)e[k].w & kOcc) != 0;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kTickScanK; ++k) {
+      bal[k] = __ballot_sync(0xffffffffu, live[k]);
+      if (lane == 0) wcnt[k][warp] = __popc(bal[k]);
+    }
+    __syncthreads();
+    uint64_t before = found, round_total = 0;
+#pragma unroll
+    for (int k = 0; k < kTickScanK; ++k) {
+      uint32_t lower = 0, all = 0;
+      for (uint32_t w = 0; w < 32; ++w) {
+        const uint32_t v = wcnt[k][w];
+        lower += w < warp ? v : 0u;
+        all += v;
+      }
+      if (live[k]) {
+        const uint64_t d = before + lower + __popc(bal[k] & lanemask_lt());
+        if (d < max_n) {
+          out[3 * d] = e[k].x, out[3 * d + 1] = e[k].y, out[3 * d + 2] = e[k].z;
+        }
+      }
+      before += all;
+      round_total += all;
+    }
+    found += round_total;
+    __syncthreads();  // wcnt reused by the next round
+  }
+  const uint64_t mn = found < max_n ? found : max_n;
+  __threadfence_block();
+  __syncthreads();  // the taken keys are written
+  int delta = (int)created_total * (t == 0);
+  for (uint64_t j = t; j < mn; j += kTickThreads) {
+    const int32_t p = erase_key(T, out[3 * j], out[3 * j + 1], out[3 * j + 2]);
+    if (p >= 0) {
+      --delta;
+      if (p >= (int32_t)T.n) push_free(T, (uint32_t)p);  // no pops after the barrier above
+    }
+  }
+  add_size_cta(T, delta);
+  if (t == 0) n_out[c] = mn;
+}
+
 // Frustum-AABB visibility of a block (server.py:375-387): every plane
 // (nx, ny, nz, d) must satisfy nx*px + ny*py + nz*pz + d >= -margin at the box
 // vertex furthest along the normal.  Evaluated in double with explicitly
@@ -780,6 +1039,44 @@ __global__ void k_mc_pack(const int32_t* __restrict__ keys, const int32_t* __res
   for (int j = lane; j < VS_MC_BLOCK_BYTES / 4; j += 32) dst[3 + j] = __ldcs(src + j);
 }
 
+
+vs_status vs_stream_tick(vs_table* const* sets_host, int n_sets, const int32_t* updated, uint64_t u,
+                         int32_t* const* fifo_keys_host, const uint64_t* fifo_cap_host,
+                         uint64_t* const* fifo_tail_host, uint64_t max_extract, const uint64_t* seeds_host,
+                         int32_t* affected_out, uint64_t* n_affected, uint64_t* n_created, int32_t* keys_out,
+                         uint64_t* n_out, vs_stream_t stream) {
+  SetViews V;
+  if (!sets_host || !updated || !fifo_keys_host || !fifo_cap_host || !fifo_tail_host || !seeds_host || !affected_out ||
+      !n_affected || !n_out || (max_extract && !keys_out)) {
+    set_error("vs_stream_tick: sets/updated/fifos/seeds/affected_out/n_affected/n_out must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  if (u < 1 || u > kTickMaxU || max_extract > 0xFFFFFFFFull) {
+    set_error("vs_stream_tick: 1 <= u <= 512 updated keys per tick (larger updates: the separate calls)");
+    return VS_ERR_INVALID;
+  }
+  vs_status st = fill_views(sets_host, n_sets, V);
+  if (st != VS_OK) return st;
+  DeviceGuard g(sets_host[0]->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  FifoViews F{}, S{};
+  for (int c = 0; c < n_sets; ++c) {
+    F.keys[c] = fifo_keys_host[c];
+    F.cap[c] = fifo_cap_host[c] ? fifo_cap_host[c] : 1;
+    F.tail[c] = fifo_tail_host[c];
+    S.cap[c] = seeds_host[c];
+  }
+  static bool attr_set[64] = {};  // the shared-memory opt-in is per device
+  const int d = sets_host[0]->device;
+  if (d < 0 || d >= 64 || !attr_set[d]) {
+    VS_CK(cudaFuncSetAttribute(k_stream_tick, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTickSmem));
+    if (d >= 0 && d < 64) attr_set[d] = true;
+  }
+  { VS_CK(launch_pdl(k_stream_tick, n_sets, kTickThreads, kTickSmem, s, V, F, S, updated, (uint32_t)u,
+                     (uint32_t)max_extract, affected_out, n_affected, n_created, keys_out, n_out)); vsb::count_launch(); }
+  VS_CK_LAUNCH("vs_stream_tick");
+  return VS_OK;
+}
 
 vs_status vs_stream_extract_random(vs_table* const* sets_host, int n_sets, uint64_t max_n,
                                    const uint64_t* seeds_host, int32_t* keys_out, uint64_t* n_out,

@@ -288,6 +288,50 @@ def extract_random_many(sets: Sequence[StreamSet], max_n: int, seeds: Optional[S
     return keys, n
 
 
+def stream_tick(sets: Sequence[StreamSet], updated, max_extract: int, seeds: Optional[Sequence[int]] = None, *,
+                affected_out=None, n_affected=None, keys_out=None, n_out=None, n_created=None):
+    """One tick of the server's stream-set path in ONE launch per 32 clients:
+    the affected dedup of the updated TSDF keys (server.py:304-307), the
+    fan-out of the affected keys into every client set with the FIFO append
+    (server.py:314-315), and an extract_random(max_extract) per client
+    (server.py:334-363) -- ``affected_dedup`` + ``fan_out`` +
+    ``extract_random_many`` fused (k_stream_tick).  1 <= len(updated) <= 512.
+
+    Returns (affected int32[8U,3], n_affected int64[1], keys int32[C,max_n,3],
+    n int64[C]) device tensors (or the given ``*_out`` buffers); nothing
+    synchronises."""
+    import random
+
+    torch = sets[0]._torch
+    dev = sets[0].device
+    k = _as_keys(updated, dev)
+    U = k.shape[0]
+    C = len(sets)
+    if not 1 <= U <= 512:
+        raise ValueError("stream_tick takes 1..512 updated keys (larger updates: affected_dedup + fan_out)")
+    if C > _MAX_SETS_PER_LAUNCH:
+        raise ValueError(f"stream_tick takes at most {_MAX_SETS_PER_LAUNCH} client sets per call")
+    aff = affected_out if affected_out is not None else torch.empty((8 * U, 3), dtype=torch.int32, device=dev)
+    na = n_affected if n_affected is not None else torch.empty(1, dtype=torch.int64, device=dev)
+    X = max(max_extract, 1)
+    keys = keys_out if keys_out is not None else torch.empty((C, X, 3), dtype=torch.int32, device=dev)
+    n = n_out if n_out is not None else torch.empty(C, dtype=torch.int64, device=dev)
+    for st in sets:
+        if st._tail_bound + 8 * U - st._head > st._fifo.shape[0]:
+            st._ensure_fifo(8 * U)
+    a = _group_args(list(sets))
+    tables = a["tables"]
+    sd = (ctypes.c_uint64 * C)(*(seeds if seeds else [random.getrandbits(64) for _ in range(C)]))
+    s = _order_streams(tables)
+    check(_lib.load().vs_stream_tick(a["handles"], C, ptr(k), U, a["fifos"], a["caps"], a["tails"], max_extract, sd,
+                                     ptr(aff), ptr(na), ptr(n_created), ptr(keys), ptr(n),
+                                     ctypes.c_void_p(s.cuda_stream)), "stream_tick")
+    _mark_done(tables, s)
+    for st in sets:
+        st._tail_bound += 8 * U
+    return aff, na, keys, n
+
+
 def remove_everywhere(sets: Sequence[StreamSet], keys) -> None:
     """Remove keys from every client set (server.py:433-435), one launch per 32."""
     if not sets:

@@ -220,6 +220,65 @@ def test_config4_tick_loop_vs_oracle(dev):
         assert g.extract_ordered(10 ** 6) == r.extract_ordered(10 ** 6)
 
 
+def test_stream_tick_fused_vs_oracle(dev):
+    """vs_stream_tick (dedup + fan-out + extraction in ONE launch): the
+    affected list equals the reference's dict-order dedup, every client's
+    pending set and FIFO (stale entries included) stay equal to the oracle
+    through reconnects and resets, extraction counts = min(max_n, size),
+    tables audit clean (the extraction recycles in the same launch)."""
+    import torch
+
+    from paper_1805_03709_b200 import StreamSet, fan_out, remove_everywhere, stream_tick, workloads
+
+    scene = workloads.room_block_keys()
+    scene = scene[(scene[:, 0] <= -170) & (scene[:, 2] <= -170)]
+    scene_t = [tuple(k) for k in scene.tolist()]
+    rng = np.random.default_rng(10)
+    C, X = 5, 60
+    # 28k structured keys collide heavily under the normative hash: 2^15 + 2^15
+    # entries keep the excess region clear of exhaustion (checked below)
+    gpu = [StreamSet(1 << 15, 1 << 15, fifo_capacity=1 << 12) for _ in range(C)]
+    ref = [oracle.OracleStreamSet() for _ in range(C)]
+    fan_out(gpu, scene)
+    for r in ref:
+        r.insert_many(scene_t)
+    for t in range(30):
+        U = int(rng.integers(1, 513)) if t % 3 else 512
+        idx = rng.integers(0, len(scene_t), U)
+        if t == 4:  # colliding updates: many duplicates among the expanded keys
+            idx = np.repeat(idx[:8], U // 8 + 1)[:U]
+        upd = [scene_t[i] for i in idx]
+        aff_want = oracle.affected_dedup(upd)
+        aff, na, keys, n = stream_tick(gpu, torch.from_numpy(scene[idx]).to(dev), X, seeds=[t * 7 + c for c in range(C)])
+        assert int(na.item()) == len(aff_want)
+        assert [tuple(k) for k in aff[: len(aff_want)].cpu().tolist()] == aff_want
+        for c, r in enumerate(ref):
+            r.insert_many(aff_want)
+            got = [tuple(k) for k in keys[c, : int(n[c])].cpu().tolist()]
+            assert len(got) == len(set(got)) == min(X, r.size())
+            for k in got:
+                assert r.remove(k)
+        if t % 10 == 9:
+            v = t // 10 % C
+            gpu[v].clear()
+            ref[v] = oracle.OracleStreamSet()
+            fan_out([gpu[v]], scene)
+            ref[v].insert_many(scene_t)
+            reset = [scene_t[i] for i in rng.integers(0, len(scene_t), 32)]
+            remove_everywhere(gpu, reset)
+            for r in ref:
+                for k in reset:
+                    r.remove(k)
+    for g, r in zip(gpu, ref):
+        g._set.check_capacity()
+        assert g.size() == len(r.set)
+        assert set(g.snapshot()) == r.set
+        assert g.fifo_entries() == list(r.order)
+        a = g._set.audit()
+        assert a["duplicates"] == 0 and a["unreachable_live"] == 0 and a["free_reachable"] == 0
+        assert a["free"] + a["reachable_excess"] == g._set.excess_capacity
+
+
 def test_extract_random_many_properties(dev):
     """Windowed multi-client extraction: distinct keys, subset of the set,
     count = min(max_n, size), post-set = pre-set minus returned, rotation
