@@ -214,27 +214,34 @@ __global__ void __launch_bounds__(kFanThreads) k_multi_fan_small(const __grid_co
 }
 
 // ---- One stream-set tick per launch (k_stream_tick): for every client, ONE
-// CTA of 1,024 threads runs, back to back,
+// CLUSTER of kTickCtas CTAs (1,024 threads each) runs, back to back,
 //   1. the affected dedup of the tick's updated keys (mc_encoding.py:108-115,
 //      server.py:304-307: expand x8 in product((0,-1), repeat=3) order,
 //      first occurrence wins) in shared memory -- every CTA computes the same
-//      list (deterministic), CTA 0 also writes it out;
-//   2. the fan-out into its client's set (server.py:314-315): inserts, the
-//      created-flag fixup, a block scan of the flags in key order and the
-//      FIFO append (as k_multi_fan_small);
+//      list (deterministic), the first CTA of the grid also writes it out;
+//   2. the fan-out into its client's set (server.py:314-315): CTA r inserts
+//      keys [1024r, 1024r + 1024), one per thread; the created flags are
+//      ranked by a block scan plus the lower CTAs' totals (read through
+//      distributed shared memory), so the FIFO append is in key order;
 //   3. the client's extract_random(max_n) (concurrent_hash.py:382-402,
-//      server.py:334-363): live entries in position order from the seeded
-//      rotating start, the first max_n taken and removed; vacated excess
-//      entries go straight back to the free list (this CTA is the only one
-//      touching its table, and its inserts are done).
+//      server.py:334-363): the cluster scans kTickCtas contiguous chunks per
+//      round from the seeded rotating start, exchanges the chunk counts over
+//      DSMEM, writes the first max_n live entries in position order and
+//      removes them (spread over the cluster); vacated excess entries go
+//      straight back to the free list (only this cluster touches its table,
+//      and its inserts are done).
 // Three launches and two grid-wide dependencies per tick become one launch.
+// The fan-out keys are distinct (they come out of the dedup), so the
+// created-flag fixup never resolves a duplicate across CTAs.
 constexpr int kTickThreads = 1024;
+constexpr int kTickCtas = 4;
 constexpr uint32_t kTickMaxU = 512;
-constexpr uint32_t kTickKeys = 8 * kTickMaxU;                 // 4,096 affected keys
+constexpr uint32_t kTickKeys = 8 * kTickMaxU;                 // 4,096 affected keys = kTickCtas x 1,024
 constexpr uint32_t kTickSlots = 2 * kTickKeys;                // dedup table, load <= 0.5
-constexpr int kTickPer = (int)(kTickKeys / kTickThreads);     // 4
+constexpr int kTickPer = (int)(kTickKeys / kTickThreads);     // 4 expanded keys per thread in the dedup
 constexpr int kTickScanK = 4;                                 // positions per thread per extraction round
 constexpr size_t kTickSmem = 12 * (size_t)kTickKeys + 4 * (size_t)kTickSlots;  // 80 KB
+static_assert(kTickKeys == (uint32_t)kTickCtas * kTickThreads, "one fan-out key per thread");
 
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* wsum, uint32_t* total) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -262,25 +269,24 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* w
   return r;
 }
 
-__global__ void __launch_bounds__(kTickThreads) k_stream_tick(const __grid_constant__ SetViews V,
-                                                              const __grid_constant__ FifoViews F,
-                                                              const __grid_constant__ FifoViews S,
-                                                              const int32_t* __restrict__ updated, uint32_t u,
-                                                              uint32_t max_n, int32_t* __restrict__ aff_out,
-                                                              uint64_t* __restrict__ n_aff,
-                                                              uint64_t* __restrict__ n_created,
-                                                              int32_t* __restrict__ keys_out,
-                                                              uint64_t* __restrict__ n_out) {
+__global__ void __cluster_dims__(kTickCtas, 1, 1) __launch_bounds__(kTickThreads)
+    k_stream_tick(const __grid_constant__ SetViews V, const __grid_constant__ FifoViews F,
+                  const __grid_constant__ FifoViews S, const int32_t* __restrict__ updated, uint32_t u,
+                  uint32_t max_n, int32_t* __restrict__ aff_out, uint64_t* __restrict__ n_aff,
+                  uint64_t* __restrict__ n_created, int32_t* __restrict__ keys_out, uint64_t* __restrict__ n_out) {
   pdl_wait();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ int32_t dsm[];
   int32_t* kx = dsm;  // [kTickKeys] x, then y, then z; later the compacted keys (xyz interleaved)
   int32_t* ky = kx + kTickKeys;
   int32_t* kz = ky + kTickKeys;
   uint32_t* slot = (uint32_t*)(kz + kTickKeys);
   __shared__ uint32_t wsum[32];
-  __shared__ uint8_t s_cr[kTickKeys];
   __shared__ uint32_t wcnt[kTickScanK][32];
-  const int c = blockIdx.x;
+  __shared__ uint32_t chunk_cnt;  // read by the other CTAs of the cluster
+  const int c = blockIdx.x / kTickCtas;
+  const uint32_t rank = cluster.block_rank();
   const TableView& T = V.v[c];
   const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
   uint32_t total;
@@ -345,65 +351,43 @@ __global__ void __launch_bounds__(kTickThreads) k_stream_tick(const __grid_const
   }
   __syncthreads();
   const uint32_t n = total;
-  if (c == 0) {
+  if (blockIdx.x == 0) {
     for (uint32_t i = t; i < 3 * n; i += kTickThreads) aff_out[i] = stage[i];
     if (t == 0 && n_aff) *n_aff = n;
   }
 
-  // ---- 2. fan-out into this client's set: key i = t + k * 1024
-  int32_t pos[kTickPer];
-  int4 pre[kTickPer];
-#pragma unroll
-  for (int k = 0; k < kTickPer; ++k) {
-    const uint32_t i = t + k * kTickThreads;
-    if (i < n) pre[k] = ld_bucket(T.e + bucket_of(T, stage[3 * i], stage[3 * i + 1], stage[3 * i + 2]));
+  // ---- 2. fan-out: CTA `rank` inserts key i = 1024 rank + t
+  const uint32_t i = rank * kTickThreads + t;
+  const uint64_t tail = *F.tail[c];  // read by every CTA before the cluster barrier below
+  uint8_t cr = 0;
+  if (i < n) {
+    const int32_t qx = stage[3 * i], qy = stage[3 * i + 1], qz = stage[3 * i + 2];
+    const InsertResult r = insert_key(T, qx, qy, qz, (int32_t)i);
+    cr = r.created;
+    // created flag of a distinct key: only FRESH to clear (post_op's duplicate
+    // resolution cannot trigger)
+    if (cr) atomicAnd(&T.e[r.pos].meta, ~kFresh);
   }
-#pragma unroll
-  for (int k = 0; k < kTickPer; ++k) {
-    const uint32_t i = t + k * kTickThreads;
-    if (i < n) {
-      const InsertResult r = insert_key(T, stage[3 * i], stage[3 * i + 1], stage[3 * i + 2], (int32_t)i, &pre[k]);
-      s_cr[i] = r.created;
-      pos[k] = r.pos;
-    }
+  uint32_t local_total;
+  const uint32_t lrank = block_exclusive_scan(cr, wsum, &local_total);
+  if (t == 0) chunk_cnt = local_total;
+  cluster.sync();  // chunk totals published; every insert of the cluster done; every tail read
+  uint32_t lower = 0, created_total = 0;
+  for (uint32_t r = 0; r < (uint32_t)kTickCtas; ++r) {
+    const uint32_t v = *cluster.map_shared_rank(&chunk_cnt, r);
+    lower += r < rank ? v : 0u;
+    created_total += v;
   }
-  __syncthreads();  // every insert and duplicate claim of this client is in
-#pragma unroll
-  for (int k = 0; k < kTickPer; ++k) {
-    const uint32_t i = t + k * kTickThreads;
-    if (i < n && s_cr[i])
-      post_op_t(
-          T,
-          [&](uint64_t mm) {
-            return stage[3 * mm] == stage[3 * i] && stage[3 * mm + 1] == stage[3 * i + 1] &&
-                   stage[3 * mm + 2] == stage[3 * i + 2];
-          },
-          i, 0 /*VS_OP_INSERT*/, s_cr, pos[k]);
+  if (cr) {
+    int32_t* dst = F.keys[c] + 3 * ((tail + lower + lrank) % F.cap[c]);
+    dst[0] = stage[3 * i], dst[1] = stage[3 * i + 1], dst[2] = stage[3 * i + 2];
   }
-  __syncthreads();
-  uint32_t own = 0;
-#pragma unroll
-  for (int k = 0; k < kTickPer; ++k) {
-    const uint32_t i = t * kTickPer + k;
-    own += i < n ? s_cr[i] : 0u;
-  }
-  uint32_t created_total;
-  uint32_t rank = block_exclusive_scan(own, wsum, &created_total);
-  const uint64_t tail = *F.tail[c];
-#pragma unroll
-  for (int k = 0; k < kTickPer; ++k) {
-    const uint32_t i = t * kTickPer + k;
-    if (i < n && s_cr[i]) {
-      int32_t* dst = F.keys[c] + 3 * ((tail + rank) % F.cap[c]);
-      dst[0] = stage[3 * i], dst[1] = stage[3 * i + 1], dst[2] = stage[3 * i + 2];
-      ++rank;
-    }
-  }
-  __syncthreads();  // every thread read the tail
-  if (t == 0) {
+  if (rank == 0 && t == 0) {
     *F.tail[c] = tail + created_total;
     if (n_created) n_created[c] = created_total;
   }
+  int delta = t == 0 ? (int)local_total : 0;
+  cluster.sync();  // chunk_cnt is reused below
 
   // ---- 3. extract_random(max_n): rotating start (k_multi_extract's seed mix)
   const uint32_t cap = T.n + T.excess;
@@ -413,15 +397,16 @@ __global__ void __launch_bounds__(kTickThreads) k_stream_tick(const __grid_const
   sd ^= sd >> 31;
   const uint32_t start = (uint32_t)(sd % cap);
   int32_t* out = keys_out + (uint64_t)c * max_n * 3;
-  uint64_t found = 0;
-  constexpr uint64_t kRound = (uint64_t)kTickThreads * kTickScanK;
-  for (uint64_t base = 0; base < cap && found < max_n; base += kRound) {
+  uint64_t found = 0;  // identical in every CTA of the cluster
+  constexpr uint64_t kChunk = (uint64_t)kTickThreads * kTickScanK;
+  for (uint64_t base = 0; base < cap && found < max_n; base += kChunk * kTickCtas) {
+    const uint64_t c0 = base + rank * kChunk;
     int4 e[kTickScanK];
     bool live[kTickScanK];
     uint32_t bal[kTickScanK];
 #pragma unroll
     for (int k = 0; k < kTickScanK; ++k) {
-      const uint64_t q = base + (uint64_t)k * kTickThreads + t;
+      const uint64_t q = c0 + (uint64_t)k * kTickThreads + t;
       uint64_t p = (uint64_t)start + q;
       p = p >= cap ? p - cap : p;
       live[k] = false;
@@ -436,40 +421,51 @@ __global__ void __launch_bounds__(kTickThreads) k_stream_tick(const __grid_const
       if (lane == 0) wcnt[k][warp] = __popc(bal[k]);
     }
     __syncthreads();
-    uint64_t before = found, round_total = 0;
+    if (t == 0) {
+      uint32_t a2 = 0;
+      for (int k = 0; k < kTickScanK; ++k)
+        for (uint32_t w = 0; w < 32; ++w) a2 += wcnt[k][w];
+      chunk_cnt = a2;
+    }
+    cluster.sync();  // every chunk count published
+    uint64_t lo = 0, all_chunks = 0;
+    for (uint32_t r = 0; r < (uint32_t)kTickCtas; ++r) {
+      const uint32_t v = *cluster.map_shared_rank(&chunk_cnt, r);
+      lo += r < rank ? v : 0u;
+      all_chunks += v;
+    }
+    uint64_t before = found + lo;
 #pragma unroll
     for (int k = 0; k < kTickScanK; ++k) {
-      uint32_t lower = 0, all = 0;
+      uint32_t lw = 0, all = 0;
       for (uint32_t w = 0; w < 32; ++w) {
         const uint32_t v = wcnt[k][w];
-        lower += w < warp ? v : 0u;
+        lw += w < warp ? v : 0u;
         all += v;
       }
       if (live[k]) {
-        const uint64_t d = before + lower + __popc(bal[k] & lanemask_lt());
+        const uint64_t d = before + lw + __popc(bal[k] & lanemask_lt());
         if (d < max_n) {
           out[3 * d] = e[k].x, out[3 * d + 1] = e[k].y, out[3 * d + 2] = e[k].z;
         }
       }
       before += all;
-      round_total += all;
     }
-    found += round_total;
-    __syncthreads();  // wcnt reused by the next round
+    found += all_chunks;
+    cluster.sync();  // chunk_cnt / wcnt reused by the next round
   }
   const uint64_t mn = found < max_n ? found : max_n;
-  __threadfence_block();
-  __syncthreads();  // the taken keys are written
-  int delta = (int)created_total * (t == 0);
-  for (uint64_t j = t; j < mn; j += kTickThreads) {
+  __threadfence();
+  cluster.sync();  // keys_out complete (written by the whole cluster) before the removals
+  for (uint64_t j = (uint64_t)rank * kTickThreads + t; j < mn; j += (uint64_t)kTickCtas * kTickThreads) {
     const int32_t p = erase_key(T, out[3 * j], out[3 * j + 1], out[3 * j + 2]);
     if (p >= 0) {
       --delta;
-      if (p >= (int32_t)T.n) push_free(T, (uint32_t)p);  // no pops after the barrier above
+      if (p >= (int32_t)T.n) push_free(T, (uint32_t)p);  // every insert of this table is done
     }
   }
   add_size_cta(T, delta);
-  if (t == 0) n_out[c] = mn;
+  if (rank == 0 && t == 0) n_out[c] = mn;
 }
 
 // Frustum-AABB visibility of a block (server.py:375-387): every plane
@@ -1072,7 +1068,7 @@ vs_status vs_stream_tick(vs_table* const* sets_host, int n_sets, const int32_t* 
     VS_CK(cudaFuncSetAttribute(k_stream_tick, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTickSmem));
     if (d >= 0 && d < 64) attr_set[d] = true;
   }
-  { VS_CK(launch_pdl(k_stream_tick, n_sets, kTickThreads, kTickSmem, s, V, F, S, updated, (uint32_t)u,
+  { VS_CK(launch_pdl(k_stream_tick, n_sets * kTickCtas, kTickThreads, kTickSmem, s, V, F, S, updated, (uint32_t)u,
                      (uint32_t)max_extract, affected_out, n_affected, n_created, keys_out, n_out)); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_stream_tick");
   return VS_OK;
