@@ -297,6 +297,21 @@ vs_status vs_stream_tick(vs_table *const *sets_host, int n_sets, const int32_t *
                          int32_t *affected_out, uint64_t *n_affected, uint64_t *n_created,
                          int32_t *keys_out, uint64_t *n_out, vs_stream_t stream);
 
+/* GpuServerCore.on_tsdf_batch without host synchronisation (server.py:299-315),
+ * in ONE host call on `stream`: tsdf_map.put of the u wire rows (latest write
+ * wins) into tsdf_pool (+ their face packs into tsdf_faces, may be NULL),
+ * affected dedup -> affected_out (device int32[8u][3]) / *n_affected, mc_map
+ * put of the affected keys, recompute of their MC + quantised bytes straight
+ * into mc_pool / q_pool at the MC map positions, insert_many into the n_sets
+ * client sets with the FIFO append (arrays as vs_stream_insert_many).  A
+ * capacity failure is sticky (vs_table_check on either map). */
+vs_status vs_server_tick(vs_table *tsdf_map, vs_table *mc_map, vs_table *dedup_scratch,
+                         const int32_t *keys, const uint8_t *rows, uint64_t u,
+                         uint8_t *tsdf_pool, uint8_t *tsdf_faces, uint8_t *mc_pool, int8_t *q_pool,
+                         vs_table *const *sets_host, int n_sets, int32_t *const *fifo_keys_host,
+                         const uint64_t *fifo_cap_host, uint64_t *const *fifo_tail_host,
+                         int32_t *affected_out, uint64_t *n_affected, vs_stream_t stream);
+
 /* extract_batch (concurrent_hash.py:366-402) on up to 32 sets in ONE launch:
  * set c scans its live entries in position order from a start position
  * derived from seeds_host[c] (wrapping), removes and returns the first max_n:

@@ -81,6 +81,8 @@ SIGNATURES: dict[str, tuple] = {
     "vs_stream_insert_many": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _vp, _u64, _vp, _vp,
                                      ctypes.POINTER(_vp), _pu64, ctypes.POINTER(_vp), _vp, _vp]),
     "vs_stream_extract_random": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _u64, _pu64, _vp, _vp, _vp]),
+    "vs_server_tick": (_i32, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp), ctypes.c_int,
+                              _vp, _vp, _vp, _vp, _vp, _vp]),
     "vs_stream_tick": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _vp, _u64, _vp, _vp, _vp, _u64, _pu64, _vp, _vp, _vp,
                               _vp, _vp, _vp]),
     "vs_stream_extract_visible": (_i32, [ctypes.POINTER(_vp), ctypes.c_int, _u64, _pu64,

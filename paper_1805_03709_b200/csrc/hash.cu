@@ -891,6 +891,10 @@ vs_status vs_table_single(vs_table* t, int op, const int32_t key_host[3], uint8_
     // straight in host memory, so a per-key call is one launch + one sync
     VS_CK(cudaHostAlloc((void**)&t->stage_host, 32, cudaHostAllocMapped));
     VS_CK(cudaHostGetDevicePointer((void**)&t->stage_dev, t->stage_host, 0));
+    // pinned blocks are recycled across tables: clear the completion word so
+    // a stale value from a previous owner can never equal this table's seq
+    memset(t->stage_host, 0, 32);
+    t->stage_seq = 0;
   }
   volatile int32_t* hk = (volatile int32_t*)t->stage_host;
   hk[0] = key_host[0];

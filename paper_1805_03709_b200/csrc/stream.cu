@@ -1244,4 +1244,55 @@ vs_status vs_stream_extract_ordered(vs_table* set, const int32_t* fifo_keys, uin
   return st;
 }
 
+// GpuServerCore.on_tsdf_batch (server.py:299-315) without host
+// synchronisation, in ONE host call: the library issues the whole chain
+// (TSDF put with latest-write-wins rows, face packs of the written rows,
+// affected dedup, mc_map put, recompute into the MC / quantised pools at the
+// MC map positions, fan-out into every client set) on one stream -- the
+// per-call host work of the Python path was the tick's critical path.
+vs_status vs_server_tick(vs_table* tsdf_map, vs_table* mc_map, vs_table* dedup_scratch, const int32_t* keys,
+                         const uint8_t* rows, uint64_t u, uint8_t* tsdf_pool, uint8_t* tsdf_faces, uint8_t* mc_pool,
+                         int8_t* q_pool, vs_table* const* sets_host, int n_sets, int32_t* const* fifo_keys_host,
+                         const uint64_t* fifo_cap_host, uint64_t* const* fifo_tail_host, int32_t* affected_out,
+                         uint64_t* n_affected, vs_stream_t stream) {
+  if (!tsdf_map || !mc_map || !dedup_scratch || !affected_out || !n_affected || n_sets < 0 ||
+      (n_sets > 0 && (!sets_host || !fifo_keys_host || !fifo_cap_host || !fifo_tail_host))) {
+    set_error("vs_server_tick: maps/scratch/affected_out/n_affected (and the client arrays) must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  if (u == 0) {
+    cudaStream_t s = (cudaStream_t)stream;
+    VS_CK(cudaMemsetAsync(n_affected, 0, 8, s));
+    return VS_OK;
+  }
+  DeviceGuard g(tsdf_map->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t m = 8 * u;
+  // scratch: TSDF positions [u], MC positions [8u], created flags of the MC put [8u]
+  // and of the fan-out [32 x 8u]
+  const uint64_t cfan = (uint64_t)(n_sets > kMaxSets ? kMaxSets : n_sets) * m;
+  const size_t b_pos = (4 * u + 255) & ~(size_t)255, b_mpos = (4 * m + 255) & ~(size_t)255,
+               b_cr = (m + 255) & ~(size_t)255;
+  char* mem = nullptr;
+  VS_CK(cudaMallocAsync((void**)&mem, b_pos + b_mpos + b_cr + (cfan ? cfan : 1), s));
+  int32_t* pos = (int32_t*)mem;
+  int32_t* mpos = (int32_t*)(mem + b_pos);
+  uint8_t* cr = (uint8_t*)(mem + b_pos + b_mpos);
+  uint8_t* cr_fan = (uint8_t*)(mem + b_pos + b_mpos + b_cr);
+  vs_status st = vs_tsdf_put(tsdf_map, keys, rows, u, tsdf_pool, pos, stream);
+  if (st == VS_OK && tsdf_faces) st = vs_mc_faces(tsdf_pool, pos, u, tsdf_faces, stream);
+  if (st == VS_OK) st = vs_affected_dedup(dedup_scratch, keys, u, affected_out, n_affected, stream);
+  if (st == VS_OK) st = vs_table_insert_bounded(mc_map, affected_out, m, n_affected, cr, mpos, stream);
+  if (st == VS_OK)
+    st = vs_mc_encode_keys_ex(tsdf_map, tsdf_pool, tsdf_faces, affected_out, m, n_affected, mpos, mc_pool,
+                              q_pool, nullptr, nullptr, nullptr, nullptr, nullptr, 0, stream);
+  for (int g0 = 0; st == VS_OK && g0 < n_sets; g0 += kMaxSets) {
+    const int C = n_sets - g0 < kMaxSets ? n_sets - g0 : kMaxSets;
+    st = vs_stream_insert_many(sets_host + g0, C, affected_out, m, n_affected, cr_fan, fifo_keys_host + g0,
+                               fifo_cap_host + g0, fifo_tail_host + g0, nullptr, stream);
+  }
+  cudaFreeAsync(mem, s);
+  return st;
+}
+
 }  // extern "C"

@@ -429,10 +429,35 @@ class GpuServerCore:
         if U == 0:
             return k if sync else (k, torch.zeros(1, dtype=torch.int64, device=dev))
         lib = _lib.load()
-        if sync:
-            # exact sequential failure semantics first (the reference raises at
-            # the first block that finds the excess list empty)
-            self.tsdf_map.insert_many_exact(k)
+        if 8 * U > self._dedup.bucket_count:
+            self._dedup = BlockHashSet(16 * U, 16 * U, device=dev)
+        if not sync:
+            # the whole chain in ONE host call (vs_server_tick): the per-call
+            # host work of the separate calls below was the tick's critical path
+            rows = rows.contiguous()
+            affected = torch.empty((8 * U, 3), dtype=torch.int32, device=dev)
+            n_dev = torch.empty(1, dtype=torch.int64, device=dev)
+            streams = self.streams()
+            for st in streams:
+                if st._tail_bound + 8 * U - st._head > st._fifo.shape[0]:
+                    st._ensure_fifo(8 * U)
+            a = _group_args(streams) if streams else None
+            tables = [self.tsdf_map, self.mc_map, self._dedup] + (a["tables"] if a else [])
+            s = _order_streams(tables)
+            null = ctypes.c_void_p(None)
+            check(lib.vs_server_tick(self.tsdf_map.handle, self.mc_map.handle, self._dedup.handle, ptr(k), ptr(rows),
+                                     U, ptr(self.tsdf_pool), ptr(self.tsdf_faces), ptr(self.mc_pool),
+                                     ptr(self.q_pool), a["handles"] if a else None, len(streams),
+                                     a["fifos"] if a else null, a["caps"] if a else null,
+                                     a["tails"] if a else null, ptr(affected), ptr(n_dev),
+                                     ctypes.c_void_p(s.cuda_stream)), "server_tick")
+            _mark_done(tables, s)
+            for st in streams:
+                st._tail_bound += 8 * U
+            return affected, n_dev
+        # exact sequential failure semantics first (the reference raises at
+        # the first block that finds the excess list empty)
+        self.tsdf_map.insert_many_exact(k)
         pos = torch.empty(U, dtype=torch.int32, device=dev)
         rows = rows.contiguous()
         st = _order_streams([self.tsdf_map])
@@ -440,36 +465,22 @@ class GpuServerCore:
                               ctypes.c_void_p(st.cuda_stream)), "tsdf_put")
         _mark_done([self.tsdf_map], st)
         face_packs(self.tsdf_pool, rows=pos, faces=self.tsdf_faces)  # halo side table of the written rows
-        if 8 * U > self._dedup.bucket_count:
-            self._dedup = BlockHashSet(16 * U, 16 * U, device=dev)
         affected = torch.empty((8 * U, 3), dtype=torch.int32, device=dev)
         n_dev = torch.empty(1, dtype=torch.int64, device=dev)
         s = _order_streams([self._dedup])
         check(lib.vs_affected_dedup(self._dedup.handle, ptr(k), U, ptr(affected), ptr(n_dev),
                                     ctypes.c_void_p(s.cuda_stream)), "affected_dedup")
         _mark_done([self._dedup], s)
-        if sync:
-            A = int(n_dev.item())
-            affected = affected[:A]
-            _, mpos = self.mc_map.insert_many_exact(affected)  # mc_map.put (positions of every key)
-            n_bound = None
-        else:
-            mpos = torch.empty(8 * U, dtype=torch.int32, device=dev)
-            created = torch.empty(8 * U, dtype=torch.uint8, device=dev)
-            s = _order_streams([self.mc_map])
-            check(lib.vs_table_insert_bounded(self.mc_map.handle, ptr(affected), 8 * U, ptr(n_dev), ptr(created),
-                                              ptr(mpos), ctypes.c_void_p(s.cuda_stream)), "mc_map insert")
-            _mark_done([self.mc_map], s)
-            n_bound = n_dev
+        A = int(n_dev.item())
+        affected = affected[:A]
+        _, mpos = self.mc_map.insert_many_exact(affected)  # mc_map.put (positions of every key)
         # recompute straight into the MC / quantised pools at the map positions
         encode_keys(self.tsdf_map, self.tsdf_pool, affected, mc=self.mc_pool, q=self.q_pool, counts=False,
-                    faces=self.tsdf_faces, out_rows=mpos, n_dev=n_bound)
+                    faces=self.tsdf_faces, out_rows=mpos)
         streams = self.streams()
         if streams:
-            fan_out(streams, affected, sync=False, n_dev=n_bound)
-        if sync:
-            return affected
-        return affected, n_dev
+            fan_out(streams, affected, sync=False)
+        return affected
 
     def check(self) -> None:
         """Raise CapacityExhausted if a sync=False update ran out of entries."""

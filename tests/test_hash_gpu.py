@@ -411,3 +411,21 @@ def test_host_threads_disjoint_key_spaces(dev):
         else:
             assert set(s.snapshot_keys()) == set(expected)
         audit_clean(s, len(expected))
+
+
+def test_per_key_path_across_recycled_staging(dev):
+    """The per-key path (vs_table_single) waits on a completion word in mapped
+    pinned memory; pinned blocks are recycled across tables, so a new table
+    must never see a previous table's final word as its own completion."""
+    from paper_1805_03709_b200 import BlockHashSet
+
+    for rnd in range(4):
+        s = BlockHashSet(64, 64)
+        for k in range(40 + 10 * rnd):  # seq runs past the previous table's last value
+            assert s.insert((k, rnd, 0))
+            assert (k, rnd, 0) in s
+            assert (k, rnd, 1) not in s
+        for k in range(0, 40 + 10 * rnd, 2):
+            assert s.remove((k, rnd, 0))
+        assert s.approx_size() == (40 + 10 * rnd) // 2
+        del s

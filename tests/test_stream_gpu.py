@@ -138,9 +138,11 @@ def test_affected_dedup_order(dev, u, span):
         assert got == oracle.affected_dedup(upd.tolist())
 
 
-def test_server_core_replays_reference_server(dev, golden):
+@pytest.mark.parametrize("sync", [True, False])
+def test_server_core_replays_reference_server(dev, golden, sync):
     """Server.on_tsdf_batch / on_reset_blocks / fresh attach, replayed on the
-    GPU core with the reference's exact TSDF bytes (server_blocks.npz)."""
+    GPU core with the reference's exact TSDF bytes (server_blocks.npz);
+    sync=False runs each batch as ONE vs_server_tick call."""
     from paper_1805_03709_b200 import GpuServerCore
 
     g = json.loads((golden / "server_seq.json").read_text())
@@ -152,7 +154,7 @@ def test_server_core_replays_reference_server(dev, golden):
         keys = d["keys"][sel]
         assert keys.tolist() == entry["updated"]
         before = [len(c.fifo_entries()) for c in clients]
-        core.on_tsdf_batch(keys, d["blocks"][sel])
+        core.on_tsdf_batch(keys, d["blocks"][sel], sync=sync)
         for c, cl in enumerate(clients):
             assert [list(k) for k in cl.fifo_entries()[before[c]:]] == entry["appended"][c]
             assert sorted(list(k) for k in cl.snapshot()) == entry["pending"][c]
