@@ -290,32 +290,33 @@ __global__ void __launch_bounds__(kOpBlock) k_probe_sol(TableView T, uint64_t n,
 
 // One op of any kind on one key, then its post pass, in a single thread
 // (the per-key compatibility path: BlockHashSet.insert/remove/__contains__).
-__global__ void k_single(TableView T, const int32_t* __restrict__ kio, uint8_t op, uint8_t* __restrict__ res,
-                         int32_t* __restrict__ idx, uint32_t* __restrict__ done, uint32_t seq) {
-  const int32_t x = kio[0], y = kio[1], z = kio[2];
+__global__ void k_single(TableView T, int32_t x, int32_t y, int32_t z, uint8_t op,
+                         unsigned long long* __restrict__ word, uint32_t seq) {
   int delta = 0;
+  int32_t pos;
+  uint32_t res;
   if (op == VS_OP_INSERT) {
     const InsertResult r = insert_key(T, x, y, z, 0);
-    *res = r.created;
-    *idx = r.pos;
+    res = r.created;
+    pos = r.pos;
     delta = r.created;
     if (r.created) atomicAnd(&T.e[r.pos].meta, ~kFresh);
   } else if (op == VS_OP_ERASE) {
-    const int32_t pos = erase_key(T, x, y, z);
-    *res = pos >= 0;
-    *idx = pos;
+    pos = erase_key(T, x, y, z);
+    res = pos >= 0;
     delta = -(pos >= 0);
     if (pos >= (int32_t)T.n) push_free(T, (uint32_t)pos);  // no pops in this launch
   } else {
     uint32_t meta;
-    const int32_t pos = find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
-    *res = pos >= 0;
-    *idx = pos;
+    pos = find_pos(T, x, y, z, bucket_of(T, x, y, z), &meta);
+    res = pos >= 0;
   }
   if (delta) atomicAdd((unsigned long long*)&T.ctl->size[0], (unsigned long long)(long long)delta);
-  // results first, then the completion word the host spins on (mapped memory)
-  __threadfence_system();
-  *(volatile uint32_t*)done = seq;
+  // result and completion in ONE 8-byte store to mapped host memory (a single
+  // PCIe write, so the host never sees one without the other):
+  // bit 63 = flag, bits 32-62 = sequence number, bits 0-31 = position
+  *(volatile unsigned long long*)word = ((unsigned long long)res << 63) |
+                                       ((unsigned long long)(seq & 0x7FFFFFFFu) << 32) | (uint32_t)pos;
 }
 
 // Post pass after k_insert / k_apply: created flags to the lowest op index
@@ -887,32 +888,28 @@ vs_status vs_table_single(vs_table* t, int op, const int32_t key_host[3], uint8_
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   if (!t->stage_host) {
-    // mapped pinned staging: the kernel reads the key and writes the result
-    // straight in host memory, so a per-key call is one launch + one sync
+    // mapped pinned staging: the kernel writes the result straight into host
+    // memory, so a per-key call is one launch + a spin on that word
     VS_CK(cudaHostAlloc((void**)&t->stage_host, 32, cudaHostAllocMapped));
     VS_CK(cudaHostGetDevicePointer((void**)&t->stage_dev, t->stage_host, 0));
-    // pinned blocks are recycled across tables: clear the completion word so
-    // a stale value from a previous owner can never equal this table's seq
+    // pinned blocks are recycled across tables: clear the result word so a
+    // stale value from a previous owner can never carry this table's seq
     memset(t->stage_host, 0, 32);
     t->stage_seq = 0;
   }
-  volatile int32_t* hk = (volatile int32_t*)t->stage_host;
-  hk[0] = key_host[0];
-  hk[1] = key_host[1];
-  hk[2] = key_host[2];
-  int32_t* dk = (int32_t*)t->stage_dev;
-  const uint32_t seq = ++t->stage_seq;
-  { k_single<<<1, 1, 0, s>>>(t->next_view(), dk, (uint8_t)op, (uint8_t*)(t->stage_dev + 20), dk + 4,
-                            (uint32_t*)(t->stage_dev + 28), seq); vsb::count_launch(); }
+  uint32_t seq = (++t->stage_seq) & 0x7FFFFFFFu;
+  if (seq == 0) seq = (++t->stage_seq) & 0x7FFFFFFFu;  // 0 is the cleared word's
+  volatile unsigned long long* word = (volatile unsigned long long*)t->stage_host;
+  { k_single<<<1, 1, 0, s>>>(t->next_view(), key_host[0], key_host[1], key_host[2], (uint8_t)op,
+                            (unsigned long long*)t->stage_dev, seq); vsb::count_launch(); }
   VS_CK(cudaGetLastError());
-  // Wait by spinning on the completion word the kernel writes last: a per-key
-  // call then costs the launch and the op itself, not a stream
-  // synchronisation.  A busy stream (the key queued behind long work) or a
-  // fault falls back to the blocking synchronisation after ~50 us.
-  volatile uint32_t* done = (volatile uint32_t*)(t->stage_host + 28);
+  // Wait by spinning on the word the kernel writes: a per-key call then
+  // costs the launch and the op itself, not a stream synchronisation.  A busy
+  // stream (the key queued behind long work) or a fault falls back to the
+  // blocking synchronisation after ~50 us.
   const auto t0 = std::chrono::steady_clock::now();
   bool spun = false;
-  while (*done != seq) {
+  while (((*word >> 32) & 0x7FFFFFFFull) != seq) {
 #if defined(__x86_64__)
     __builtin_ia32_pause();
 #endif
@@ -922,8 +919,9 @@ vs_status vs_table_single(vs_table* t, int op, const int32_t key_host[3], uint8_
     }
   }
   if (spun) VS_CK(cudaStreamSynchronize(s));
-  *index_host = ((volatile int32_t*)t->stage_host)[4];
-  *result_host = ((volatile uint8_t*)t->stage_host)[20];
+  const unsigned long long w = *word;
+  *index_host = (int32_t)(uint32_t)(w & 0xFFFFFFFFull);
+  *result_host = (uint8_t)(w >> 63);
   if (op == VS_OP_INSERT && *index_host < 0) {
     unsigned int zero = 0;
     VS_CK(cudaMemcpy(&t->ctl->error, &zero, sizeof(zero), cudaMemcpyHostToDevice));
