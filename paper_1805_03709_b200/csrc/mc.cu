@@ -181,7 +181,16 @@ struct McSmem {
   int32_t nb[2][kLook][8];  // neighbour rows of two lookup batches
   uint32_t wsum[4];         // kCells: per-warp non-empty counts of the block
   uint32_t cbase;           // kCells: reserved start of the block's cell range
+  uint32_t pair_lut[32];    // pair4 of every 5-bit row slice (VSB_MC_PAIR_LUT)
 };
+
+// Cube-index assembly through a 32-entry table of pair4 (VSB_MC_PAIR_LUT):
+// entry i sits in bank i, so any mix of lane indices is conflict-free, and
+// one shared load replaces pair4's eight integer ops (the scattered-halo
+// encode calls it 8 times per thread and block).
+#ifndef VSB_MC_PAIR_LUT
+#define VSB_MC_PAIR_LUT 1
+#endif
 
 // Sweep order (experiment knob VSB_MC_REVERSE): block of sweep index i.
 #ifndef VSB_MC_REVERSE
@@ -381,6 +390,7 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     for (int b = 0; b < kStages; ++b) mbar_init(&sm.mbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (t < 32) sm.pair_lut[t] = pair4((uint32_t)t);  // visible after the first barrier
   lookup_batch<kFromKeys>(sm, 0, T, keys, nbr, n, 0);
   __syncthreads();
   if (t == 0)
@@ -519,10 +529,18 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     } else {
       const uint32_t* gi = sm.grid_in[s];
       const uint32_t* go = sm.grid_ob[s];
+#if VSB_MC_PAIR_LUT
+      const uint32_t* L = sm.pair_lut;
+      I = L[(gi[r00] >> x0) & 31u] | (L[(gi[r00 + 1] >> x0) & 31u] << 2) | (L[(gi[r00 + 9] >> x0) & 31u] << 4) |
+          (L[(gi[r00 + 10] >> x0) & 31u] << 6);
+      O = L[(go[r00] >> x0) & 31u] | (L[(go[r00 + 1] >> x0) & 31u] << 2) | (L[(go[r00 + 9] >> x0) & 31u] << 4) |
+          (L[(go[r00 + 10] >> x0) & 31u] << 6);
+#else
       I = pair4(gi[r00] >> x0) | (pair4(gi[r00 + 1] >> x0) << 2) | (pair4(gi[r00 + 9] >> x0) << 4) |
           (pair4(gi[r00 + 10] >> x0) << 6);
       O = pair4(go[r00] >> x0) | (pair4(go[r00 + 1] >> x0) << 2) | (pair4(go[r00 + 9] >> x0) << 4) |
           (pair4(go[r00 + 10] >> x0) << 6);
+#endif
     }
     // keep a byte only where all 8 corners are observed and it is not 255
     const uint32_t keep = __vcmpeq4(O, 0xFFFFFFFFu) & ~__vcmpeq4(I, 0xFFFFFFFFu);
