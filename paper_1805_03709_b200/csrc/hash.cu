@@ -757,6 +757,9 @@ vs_status vs_table_destroy(vs_table* t) {
   cudaFree(t->chunk_offsets);
   cudaFree(t->pos_work);
   if (t->stage_host) cudaFreeHost(t->stage_host);
+  if (t->side) cudaStreamDestroy(t->side);
+  if (t->ev_fork) cudaEventDestroy(t->ev_fork);
+  if (t->ev_join) cudaEventDestroy(t->ev_join);
   delete t;
   return VS_OK;
 }

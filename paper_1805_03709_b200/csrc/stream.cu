@@ -1279,10 +1279,23 @@ vs_status vs_server_tick(vs_table* tsdf_map, vs_table* mc_map, vs_table* dedup_s
   int32_t* mpos = (int32_t*)(mem + b_pos);
   uint8_t* cr = (uint8_t*)(mem + b_pos + b_mpos);
   uint8_t* cr_fan = (uint8_t*)(mem + b_pos + b_mpos + b_cr);
-  vs_status st = vs_tsdf_put(tsdf_map, keys, rows, u, tsdf_pool, pos, stream);
+  // Two independent chains, on two streams: the TSDF put (+ face packs) on
+  // `stream`, the affected dedup + MC map put (they need only the keys) on
+  // a side stream; they join before the encode, which needs both.
+  if (!tsdf_map->side) {
+    VS_CK(cudaStreamCreateWithFlags(&tsdf_map->side, cudaStreamNonBlocking));
+    VS_CK(cudaEventCreateWithFlags(&tsdf_map->ev_fork, cudaEventDisableTiming));
+    VS_CK(cudaEventCreateWithFlags(&tsdf_map->ev_join, cudaEventDisableTiming));
+  }
+  cudaStream_t side = tsdf_map->side;
+  VS_CK(cudaEventRecord(tsdf_map->ev_fork, s));
+  VS_CK(cudaStreamWaitEvent(side, tsdf_map->ev_fork, 0));
+  vs_status st = vs_affected_dedup(dedup_scratch, keys, u, affected_out, n_affected, (vs_stream_t)side);
+  if (st == VS_OK) st = vs_table_insert_bounded(mc_map, affected_out, m, n_affected, cr, mpos, (vs_stream_t)side);
+  if (st == VS_OK) st = vs_tsdf_put(tsdf_map, keys, rows, u, tsdf_pool, pos, stream);
   if (st == VS_OK && tsdf_faces) st = vs_mc_faces(tsdf_pool, pos, u, tsdf_faces, stream);
-  if (st == VS_OK) st = vs_affected_dedup(dedup_scratch, keys, u, affected_out, n_affected, stream);
-  if (st == VS_OK) st = vs_table_insert_bounded(mc_map, affected_out, m, n_affected, cr, mpos, stream);
+  VS_CK(cudaEventRecord(tsdf_map->ev_join, side));
+  VS_CK(cudaStreamWaitEvent(s, tsdf_map->ev_join, 0));
   if (st == VS_OK)
     st = vs_mc_encode_keys_ex(tsdf_map, tsdf_pool, tsdf_faces, affected_out, m, n_affected, mpos, mc_pool,
                               q_pool, nullptr, nullptr, nullptr, nullptr, nullptr, 0, stream);

@@ -27,6 +27,10 @@ struct vs_table {
   uint8_t* stage_host = nullptr;      // pinned staging of the single-key path (32 B)
   uint8_t* stage_dev = nullptr;
   uint32_t stage_seq = 0;             // completion sequence of the single-key path
+  // side stream + fork/join events of vs_server_tick (lazily created; the
+  // TSDF map's table owns them)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   // view for ONE launch; next_epoch() gives it a fresh claim tag
   vsb::TableView view() const {
