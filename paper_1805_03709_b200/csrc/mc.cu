@@ -27,6 +27,7 @@
 //     the TSDF rows that neighbouring blocks will read as halo.
 #include <cstdint>
 
+#include "faces.cuh"
 #include "hash_ops.cuh"
 #include "scan.cuh"
 #include "table.h"
@@ -105,10 +106,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   } while (!ok);
 }
 
-__device__ __forceinline__ uint32_t inside_bit(uint32_t b) { return (b > 0x80000000u && b <= 0xFF800000u) ? 1u : 0u; }
-__device__ __forceinline__ uint32_t observed_bit(uint32_t b) {
-  return ((int32_t)b > 0 && b <= 0x7F800000u) ? 1u : 0u;
-}
 
 // Quantised TSDF byte (NEW; normative definition in oracle/mc_oracle.c and
 // DESIGN.md A17): observed ? clamp(rint_half_even(tsdf * 127), -127, 127)
@@ -312,7 +309,6 @@ __device__ __forceinline__ void issue_centre(McSmem& sm, uint64_t j, const uint8
 // instead of 217 scattered 8-B voxels (~117 DRAM bursts when they miss L2).
 // Packs are maintained where rows change (ingest, integration) with
 // vs_mc_faces.
-constexpr int kFaceBytes = 48;
 
 __device__ __forceinline__ int face_kind(int c) { return (c & 1) ? 0 : (c == 4 ? 2 : 1); }  // c: 1..7
 
@@ -328,34 +324,14 @@ __device__ __forceinline__ uint32_t byte64(uint32_t lo, uint32_t hi, int k) {
   return ((k < 4 ? lo >> (8 * k) : hi >> (8 * (k - 4))) & 0xFFu);
 }
 
-// One warp per row: lane l takes bits l and l + 32 of each face.
+// One warp per row (face_pack_warp, faces.cuh).
 __global__ void __launch_bounds__(256) k_mc_faces(const uint8_t* __restrict__ pool, const int32_t* __restrict__ rows,
                                                   uint64_t n, uint8_t* __restrict__ faces) {
   const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t lane = threadIdx.x & 31u;
   if (w >= n) return;
   const int32_t row = rows ? rows[w] : (int32_t)w;
   if (row < 0) return;
-  const uint8_t* src = pool + (uint64_t)row * VS_TSDF_BLOCK_BYTES;
-  uint32_t word[3][4];
-#pragma unroll
-  for (int f = 0; f < 3; ++f) {
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int i = (int)lane + 32 * half;
-      const int a = i & 7, b = i >> 3;
-      const int flat = f == 0 ? 8 * a + 64 * b : (f == 1 ? a + 64 * b : a + 8 * b);
-      const uint32_t* v = (const uint32_t*)(src + 12 * flat);
-      const uint32_t in = __ballot_sync(0xFFFFFFFFu, inside_bit(__ldg(v)));
-      const uint32_t ob = __ballot_sync(0xFFFFFFFFu, observed_bit(__ldg(v + 1)));
-      word[f][half] = in;
-      word[f][2 + half] = ob;
-    }
-  }
-#pragma unroll
-  for (int f = 0; f < 3; ++f)
-    if (lane == (uint32_t)f)
-      ((uint4*)(faces + (uint64_t)row * kFaceBytes))[f] = make_uint4(word[f][0], word[f][1], word[f][2], word[f][3]);
+  face_pack_warp(pool + (uint64_t)row * VS_TSDF_BLOCK_BYTES, faces + (uint64_t)row * kFaceBytes);
 }
 
 // Optional fused compaction (kCells): the block's non-empty

@@ -20,6 +20,7 @@
 
 #include <cooperative_groups.h>
 
+#include "faces.cuh"
 #include "hash_ops.cuh"
 #include "pdl.cuh"
 #include "scan.cuh"
@@ -1008,7 +1009,7 @@ __global__ void k_put_claim(TableView T, const int32_t* __restrict__ pos, uint64
 }
 
 __global__ void k_put_rows(TableView T, const int32_t* __restrict__ pos, uint64_t n, const uint4* __restrict__ rows,
-                           uint4* __restrict__ pool) {
+                           uint4* __restrict__ pool, uint8_t* __restrict__ faces) {
   const uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= n) return;
@@ -1018,6 +1019,8 @@ __global__ void k_put_rows(TableView T, const int32_t* __restrict__ pos, uint64_
   uint4* dst = pool + (uint64_t)p * (VS_TSDF_BLOCK_BYTES / 16);
 #pragma unroll 4
   for (int j = lane; j < VS_TSDF_BLOCK_BYTES / 16; j += 32) dst[j] = __ldcs(src + j);
+  // the encoder's halo side table for this row, from the same source bytes
+  if (faces) face_pack_warp((const uint8_t*)src, faces + (uint64_t)p * kFaceBytes);
 }
 
 // MC_BATCH payload (wire.py:292-299): u32 count, then per block the key as
@@ -1096,8 +1099,16 @@ vs_status vs_stream_extract_visible(vs_table* const* sets_host, int n_sets, uint
   return multi_extract(sets_host, n_sets, max_n, seeds_host, F, keys_out, n_out, stream);
 }
 
+static vs_status tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows, uint64_t n, uint8_t* pool,
+                          int32_t* index, uint8_t* faces, vs_stream_t stream);
+
 vs_status vs_tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows, uint64_t n, uint8_t* pool,
                       int32_t* index, vs_stream_t stream) {
+  return tsdf_put(t, keys, rows, n, pool, index, nullptr, stream);
+}
+
+static vs_status tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows, uint64_t n, uint8_t* pool,
+                          int32_t* index, uint8_t* faces, vs_stream_t stream) {
   if (!t || !index || (n && (!keys || !rows || !pool))) {
     set_error("table/keys/rows/pool/index must be non-NULL");
     return VS_ERR_INVALID;
@@ -1116,7 +1127,7 @@ vs_status vs_tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows, uin
   if (st != VS_OK) return st;
   const TableView v = t->next_view();
   { k_put_claim<<<grid_for(n, 256), 256, 0, s>>>(v, index, n); vsb::count_launch(); }
-  { k_put_rows<<<grid_for(32 * n, 256), 256, 0, s>>>(v, index, n, (const uint4*)rows, (uint4*)pool); vsb::count_launch(); }
+  { k_put_rows<<<grid_for(32 * n, 256), 256, 0, s>>>(v, index, n, (const uint4*)rows, (uint4*)pool, faces); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_tsdf_put");
   return VS_OK;
 }
@@ -1292,8 +1303,7 @@ vs_status vs_server_tick(vs_table* tsdf_map, vs_table* mc_map, vs_table* dedup_s
   VS_CK(cudaStreamWaitEvent(side, tsdf_map->ev_fork, 0));
   vs_status st = vs_affected_dedup(dedup_scratch, keys, u, affected_out, n_affected, (vs_stream_t)side);
   if (st == VS_OK) st = vs_table_insert_bounded(mc_map, affected_out, m, n_affected, cr, mpos, (vs_stream_t)side);
-  if (st == VS_OK) st = vs_tsdf_put(tsdf_map, keys, rows, u, tsdf_pool, pos, stream);
-  if (st == VS_OK && tsdf_faces) st = vs_mc_faces(tsdf_pool, pos, u, tsdf_faces, stream);
+  if (st == VS_OK) st = tsdf_put(tsdf_map, keys, rows, u, tsdf_pool, pos, tsdf_faces, stream);  // + face packs
   VS_CK(cudaEventRecord(tsdf_map->ev_join, side));
   VS_CK(cudaStreamWaitEvent(s, tsdf_map->ev_join, 0));
   if (st == VS_OK)
