@@ -424,7 +424,9 @@ class GpuServerCore:
         torch = self._torch
         dev = self.device
         k = _as_keys(keys, dev)
-        rows = torch.as_tensor(rows).to(dev, torch.uint8).reshape(-1, TSDF_BLOCK_BYTES)
+        if not (isinstance(rows, torch.Tensor) and rows.dtype == torch.uint8 and rows.device == dev):
+            rows = torch.as_tensor(rows).to(dev, torch.uint8)
+        rows = rows.reshape(-1, TSDF_BLOCK_BYTES)
         U = k.shape[0]
         if U == 0:
             return k if sync else (k, torch.zeros(1, dtype=torch.int64, device=dev))
@@ -435,25 +437,28 @@ class GpuServerCore:
             # the whole chain in ONE host call (vs_server_tick): the per-call
             # host work of the separate calls below was the tick's critical path
             rows = rows.contiguous()
-            affected = torch.empty((8 * U, 3), dtype=torch.int32, device=dev)
-            n_dev = torch.empty(1, dtype=torch.int64, device=dev)
+            # one allocation for both outputs (views), raw pointers as ints:
+            # this wrapper's own cost is part of the tick when the host paces it
+            out = torch.empty(24 * U + 2, dtype=torch.int32, device=dev)
+            affected = out[: 24 * U].view(8 * U, 3)
+            n_dev = out[24 * U:].view(torch.int64)
             streams = self.streams()
+            need = 8 * U
             for st in streams:
-                if st._tail_bound + 8 * U - st._head > st._fifo.shape[0]:
-                    st._ensure_fifo(8 * U)
+                if st._tail_bound + need - st._head > st._fifo.shape[0]:
+                    st._ensure_fifo(need)
             a = _group_args(streams) if streams else None
             tables = [self.tsdf_map, self.mc_map, self._dedup] + (a["tables"] if a else [])
             s = _order_streams(tables)
-            null = ctypes.c_void_p(None)
-            check(lib.vs_server_tick(self.tsdf_map.handle, self.mc_map.handle, self._dedup.handle, ptr(k), ptr(rows),
-                                     U, ptr(self.tsdf_pool), ptr(self.tsdf_faces), ptr(self.mc_pool),
-                                     ptr(self.q_pool), a["handles"] if a else None, len(streams),
-                                     a["fifos"] if a else null, a["caps"] if a else null,
-                                     a["tails"] if a else null, ptr(affected), ptr(n_dev),
-                                     ctypes.c_void_p(s.cuda_stream)), "server_tick")
+            check(lib.vs_server_tick(self.tsdf_map.handle, self.mc_map.handle, self._dedup.handle, k.data_ptr(),
+                                     rows.data_ptr(), U, self.tsdf_pool.data_ptr(), self.tsdf_faces.data_ptr(),
+                                     self.mc_pool.data_ptr(), self.q_pool.data_ptr(), a["handles"] if a else None,
+                                     len(streams), a["fifos"] if a else None, a["caps"] if a else None,
+                                     a["tails"] if a else None, affected.data_ptr(), n_dev.data_ptr(),
+                                     s.cuda_stream), "server_tick")
             _mark_done(tables, s)
             for st in streams:
-                st._tail_bound += 8 * U
+                st._tail_bound += need
             return affected, n_dev
         # exact sequential failure semantics first (the reference raises at
         # the first block that finds the excess list empty)

@@ -23,7 +23,7 @@ for a in range(0, len(scene), 1 << 16):
 for c in range(16):
     core.attach(bytes([c]) * 16)
 rng = np.random.default_rng(1)
-T = 45
+T = 85
 upd = torch.from_numpy(scene_np[rng.integers(0, len(scene_np), (T, 512))]).to(dev)
 rows = torch.stack([workloads.room_tsdf_rows(upd[t]) for t in range(T)])
 torch.cuda.synchronize()
@@ -31,13 +31,21 @@ for t in range(5):
     core.on_tsdf_batch(upd[t], rows[t], sync=False)
 torch.cuda.synchronize()
 torch.cuda._sleep(200_000_000)  # keep the GPU busy (~0.1 s): 40 ticks stay within the launch queue
-pr = cProfile.Profile()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()  # after the sleep kernel: the ticks below are all queued when it ends
 t0 = time.perf_counter()
+for t in range(5, T // 2):
+    core.on_tsdf_batch(upd[t], rows[t], sync=False)
+dt = (time.perf_counter() - t0) / (T // 2 - 5)
+e1.record()
+torch.cuda.synchronize()
+print(f"host per tick (no profiler): {dt * 1e6:.1f} us; device per tick, queued back to back: "
+      f"{e0.elapsed_time(e1) * 1e3 / (T // 2 - 5):.1f} us")
+torch.cuda._sleep(200_000_000)
+pr = cProfile.Profile()
 pr.enable()
-for t in range(5, T):
+for t in range(T // 2, T):
     core.on_tsdf_batch(upd[t], rows[t], sync=False)
 pr.disable()
-dt = (time.perf_counter() - t0) / (T - 5)
 torch.cuda.synchronize()
-print(f"host per tick: {dt * 1e6:.1f} us")
-pstats.Stats(pr).sort_stats("tottime").print_stats(12)
+pstats.Stats(pr).sort_stats("tottime").print_stats(8)
