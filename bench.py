@@ -447,7 +447,9 @@ def run_config1(args, dev):
     ok = True
     for _ in range(3):
         ok &= check(*step(dk, dp))
-    steps = 50
+    for _ in range(20):  # settle clocks / allocator (the steps are ~0.15 ms each)
+        step(dk, dp)
+    steps = 200
     res = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()

@@ -25,6 +25,7 @@ SECTIONS = {
     "stream": ["--no-cpu", "--no-mc", "--no-rc", "--no-e2e", "--no-server", "--steps", "5"],
     "server": ["--no-cpu", "--no-mc", "--no-rc", "--no-e2e", "--no-stream", "--steps", "5"],
     "rc": ["--no-cpu", "--no-mc", "--no-stream", "--no-e2e", "--no-server", "--steps", "5"],
+    "config1": ["--no-cpu", "--no-mc", "--no-stream", "--no-rc", "--no-e2e", "--no-server", "--steps", "3"],
 }
 
 
@@ -32,6 +33,10 @@ def pick(d: dict, section: str):
     if section == "hash":
         return {"value": round(d["value"]), "kernel_ms": round(d["roofline"]["kernel_ms"], 4),
                 "ms_per_step": round(d["ms_per_step"], 4), "ok": d["parity_ok"]}
+    if section == "config1":
+        c = d.get("config1") or {}
+        return {"hash_M_ops": round(c.get("hash", {}).get("value", 0)), "ms": c.get("hash", {}).get("ms_per_step"),
+                "mc_blocks": c.get("mc", {}).get("value"), "ok": c.get("ok"), "error": c.get("error")}
     s = d.get(section) or {}
     out = {k: s.get(k) for k in ("value", "ms_per_step", "ms_per_tick", "ok", "error") if k in s}
     if "roofline" in s:
