@@ -281,6 +281,29 @@ def test_stream_tick_fused_vs_oracle(dev):
         assert a["free"] + a["reachable_excess"] == g._set.excess_capacity
 
 
+def test_stream_tick_edges(dev):
+    """vs_stream_tick with a single updated key and no extraction, with
+    max_n larger than every set, and the argument checks."""
+    import torch
+
+    from paper_1805_03709_b200 import StreamSet, stream_tick
+
+    sets = [StreamSet(1 << 10, 1 << 10) for _ in range(3)]
+    aff, na, keys, n = stream_tick(sets, torch.tensor([[5, 6, 7]], dtype=torch.int32, device=dev), 0, seeds=[1, 2, 3])
+    want = oracle.affected_dedup([(5, 6, 7)])
+    assert int(na.item()) == 8 and [tuple(k) for k in aff.cpu().tolist()] == want
+    assert n.cpu().tolist() == [0, 0, 0]
+    for st in sets:
+        assert sorted(st.snapshot()) == sorted(want) and st.fifo_entries() == want
+    aff, na, keys, n = stream_tick(sets, torch.tensor([[5, 6, 7]], dtype=torch.int32, device=dev), 100, seeds=[4, 5, 6])
+    assert n.cpu().tolist() == [8, 8, 8]  # nothing new was created: all 8 pending keys come out
+    for c, st in enumerate(sets):
+        assert sorted(tuple(k) for k in keys[c, :8].cpu().tolist()) == sorted(want)
+        assert st.size() == 0
+    with pytest.raises(ValueError):
+        stream_tick(sets, torch.zeros((513, 3), dtype=torch.int32, device=dev), 1)
+
+
 def test_extract_random_many_properties(dev):
     """Windowed multi-client extraction: distinct keys, subset of the set,
     count = min(max_n, size), post-set = pre-set minus returned, rotation
