@@ -14,13 +14,15 @@ from paper_1805_03709_b200 import BlockHashSet, workloads
 from paper_1805_03709_b200.shard import ShardedBlockHashSet
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
+live = int(sys.argv[2]) if len(sys.argv) > 2 else 10_000_000
+blog = int(sys.argv[3]) if len(sys.argv) > 3 else 22
 dev = torch.device("cuda", 0)
 dist.init_process_group("gloo", init_method=f"file://{tempfile.mkdtemp()}/pg", rank=0, world_size=1)
-spec = workloads.MixSpec(live=10_000_000, load_factor=0.7, batch=1 << 22)
+spec = workloads.MixSpec(live=live, load_factor=0.7, batch=1 << blog)
 res = {}
 for mode in ("table", "peer"):
     s = BlockHashSet(spec.bucket_count, spec.excess, device=dev)
-    sh = ShardedBlockHashSet(s, exchange="peer", max_batch=1 << 22) if mode == "peer" else None
+    sh = ShardedBlockHashSet(s, exchange="peer", max_batch=spec.batch) if mode == "peer" else None
     for a in range(0, spec.live, 1 << 22):
         k = workloads.id_to_key_torch(torch.arange(a, min(spec.live, a + (1 << 22)), device=dev))
         s.insert_keys(k)

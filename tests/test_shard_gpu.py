@@ -134,20 +134,23 @@ def test_peer_single_rank_equals_table(tmp_path, dev):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [3, 8])
-def test_peer_route_world_on_one_gpu(dev, world):
+@pytest.mark.parametrize("world,big", [(3, False), (8, False), (3, True), (8, True)])
+def test_peer_route_world_on_one_gpu(dev, world, big):
     """An 8-rank (and a 3-rank) node simulated in one process on one GPU:
     every rank's batch on its own stream through the real windows, flags and
     kernels (OneGpuShardGroup).  Per-op results equal the A18 expectation,
     every key lives on its owner, sizes add up, cross-rank duplicate fresh
-    inserts resolve to the lowest rank, and every table audits clean."""
+    inserts resolve to the lowest rank, and every table audits clean.
+    big: 1 GiB tables, so the route partitions by (owner, bucket region) and
+    owners apply region by region (shard.cu VSB_SHARD_REGIONS)."""
     import torch
 
     from paper_1805_03709_b200 import BlockHashSet, workloads
     from paper_1805_03709_b200.shard import OneGpuShardGroup, owner_of
 
     spec = workloads.MixSpec(live=40_000, load_factor=0.7, batch=1 << 13)
-    tabs = [BlockHashSet(spec.bucket_count, spec.excess, device=dev) for _ in range(world)]
+    nb, ex = (1 << 25, 1 << 25) if big else (spec.bucket_count, spec.excess)
+    tabs = [BlockHashSet(nb, ex, device=dev) for _ in range(world)]
     g = OneGpuShardGroup(tabs, max_batch=spec.live)
     z = lambda n: torch.zeros(n, dtype=torch.uint8, device=dev)  # noqa: E731
     init = [workloads.id_to_key_torch(torch.arange(r << 40, (r << 40) + spec.live, device=dev)) for r in range(world)]
