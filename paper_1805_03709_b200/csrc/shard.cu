@@ -43,6 +43,7 @@
 namespace vsb {
 
 constexpr int kMaxWorld = 32;
+constexpr uint32_t kMaxKeys = 128;  // partition keys: (owner, bucket region) pairs
 constexpr int kPartThreads = 256;
 constexpr int kPartRounds = 8;
 constexpr int kShardOpBlock = 128;
@@ -187,11 +188,12 @@ __device__ __forceinline__ void stage_tile(const int32_t* __restrict__ keys, con
 __global__ void __launch_bounds__(kPartThreads) k_wpart_count(const int32_t* __restrict__ keys, uint64_t n, ShardView V,
                                                               uint32_t nwt, uint32_t* __restrict__ tile_cnt) {
   pdl_wait();
-  __shared__ uint32_t c[kPartThreads / 32][kMaxWorld];
+  __shared__ uint32_t c[kPartThreads / 32][kMaxKeys];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t wt = blockIdx.x * (kPartThreads / 32) + warp;
   if (wt >= nwt) return;
-  c[warp][lane] = 0;
+  const uint32_t NV = (uint32_t)V.world * V.nreg;
+  for (uint32_t q = lane; q < NV; q += 32) c[warp][q] = 0;
   __syncwarp();
   __shared__ WarpStage stage[kPartThreads / 32];
   WarpStage& S = stage[warp];
@@ -206,7 +208,21 @@ __global__ void __launch_bounds__(kPartThreads) k_wpart_count(const int32_t* __r
     if (o != 0xFFFFFFFFu && (int)lane == __ffs(m) - 1) c[warp][o] += __popc(m);
     __syncwarp();
   }
-  if (lane < (uint32_t)V.world * V.nreg) tile_cnt[(size_t)lane * nwt + wt] = c[warp][lane];
+  for (uint32_t q = lane; q < NV; q += 32) tile_cnt[(size_t)q * nwt + wt] = c[warp][q];
+}
+
+// Start of every partition key's records inside its owner's region: the
+// totals of the owner's lower bucket regions (one thread per key), and the
+// per-owner record counts for the owners' headers.
+__global__ void k_wpart_base(const uint32_t* __restrict__ totals, uint32_t world, uint32_t nreg,
+                             uint32_t* __restrict__ base, uint32_t* __restrict__ owner_cnt) {
+  pdl_wait();
+  const uint32_t q = threadIdx.x;
+  if (q >= world * nreg) return;
+  uint32_t b = 0;
+  for (uint32_t p = q - q % nreg; p < q; ++p) b += totals[p];
+  base[q] = b;
+  if (q % nreg == nreg - 1) owner_cnt[q / nreg] = b + totals[q];
 }
 
 // CTA o: exclusive scan of owner o's counts per GROUP of kTilesPerCta warp
@@ -283,25 +299,24 @@ __global__ void __launch_bounds__(kPartThreads) k_wpart_push(ShardView V, const 
                                                              const uint8_t* __restrict__ ops, uint64_t n, uint32_t nwt,
                                                              const uint32_t* __restrict__ tile_cnt,
                                                              const uint32_t* __restrict__ grp_off,
-                                                             const uint32_t* __restrict__ totals,
+                                                             const uint32_t* __restrict__ base,
+                                                             const uint32_t* __restrict__ owner_cnt,
                                                              unsigned long long epoch, unsigned int* ctr) {
   pdl_wait();
-  __shared__ uint32_t run[kPartThreads / 32][kMaxWorld];
+  __shared__ uint32_t run[kPartThreads / 32][kMaxKeys];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t wt = blockIdx.x * (kPartThreads / 32) + warp;
   const int G = V.world;
-  const uint32_t NV = (uint32_t)G * V.nreg;  // partition keys (<= 32)
+  const uint32_t NV = (uint32_t)G * V.nreg;  // partition keys (<= kMaxKeys)
   if (wt < nwt) {
     // tile offset = the group's offset + the tiles of earlier warps in the
-    // group + the owner's lower regions
-    uint32_t off0 = 0;
-    if (lane < NV) {
-      const uint32_t ngrp = (nwt + kTilesPerCta - 1) / kTilesPerCta;
-      off0 = grp_off[(size_t)lane * ngrp + blockIdx.x];
-      for (uint32_t w = 0; w < warp; ++w) off0 += tile_cnt[(size_t)lane * nwt + blockIdx.x * kTilesPerCta + w];
-      for (uint32_t q = lane - lane % V.nreg; q < lane; ++q) off0 += totals[q];
+    // group + the start of the key's bucket region inside its owner's region
+    const uint32_t ngrp = (nwt + kTilesPerCta - 1) / kTilesPerCta;
+    for (uint32_t q = lane; q < NV; q += 32) {
+      uint32_t off0 = grp_off[(size_t)q * ngrp + blockIdx.x] + base[q];
+      for (uint32_t w = 0; w < warp; ++w) off0 += tile_cnt[(size_t)q * nwt + blockIdx.x * kTilesPerCta + w];
+      run[warp][q] = off0;
     }
-    run[warp][lane] = off0;
     __syncwarp();
     const uint64_t t0 = (uint64_t)wt * kWTile;
     __shared__ WarpStage stage[kPartThreads / 32];
@@ -332,9 +347,7 @@ __global__ void __launch_bounds__(kPartThreads) k_wpart_push(ShardView V, const 
   if (last_cta(ctr) && (int)threadIdx.x < G) {
     __threadfence_system();
     ShardHdr* h = hdr_of(V, threadIdx.x);
-    unsigned long long cnt = 0;
-    for (uint32_t q = 0; q < V.nreg; ++q) cnt += totals[threadIdx.x * V.nreg + q];
-    st_relaxed_sys(&h->cnt[V.rank], cnt);
+    st_relaxed_sys(&h->cnt[V.rank], owner_cnt[threadIdx.x]);
     st_release_sys(&h->push_flag[V.rank], epoch);
   }
 }
@@ -540,8 +553,8 @@ struct vs_shard {
     // region order pays off only when the table is far larger than the L2
     // (at world 1: 125M keys, 2^24 ops 1.50 -> 1.28 ms; 10M keys 0.33 -> 0.36 ms)
     const bool big = (uint64_t)table->cap * sizeof(Entry) >= (1ull << 30);
-    const uint32_t cap_r = (uint32_t)(kMaxWorld / world < VSB_SHARD_REGIONS_MAX ? kMaxWorld / world
-                                                                                : VSB_SHARD_REGIONS_MAX);
+    const uint32_t cap_r = (uint32_t)(kMaxKeys / world < VSB_SHARD_REGIONS_MAX ? kMaxKeys / world
+                                                                              : VSB_SHARD_REGIONS_MAX);
     v.nreg = VSB_SHARD_REGIONS && big ? cap_r : 1u;
     v.tn = table->n;
     v.tmagic = table->magic;
@@ -573,9 +586,9 @@ vs_status vs_shard_create(vs_table* local, int rank, int world, uint64_t max_bat
   if (e == cudaSuccess) e = cudaMemset(s->win, 0, kHdrBytes);
   // warp tiles (kWTile ops) are the finest partition granularity
   const size_t nwt_max = (max_batch + kWTile - 1) / kWTile;
-  if (e == cudaSuccess) e = cudaMalloc(&s->tile_cnt, (size_t)kMaxWorld * nwt_max * 4);  // (owner, region) rows
-  if (e == cudaSuccess) e = cudaMalloc(&s->grp_off, (size_t)kMaxWorld * nwt_max * 4);
-  if (e == cudaSuccess) e = cudaMalloc(&s->totals, kMaxWorld * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->tile_cnt, (size_t)kMaxKeys * nwt_max * 4);  // (owner, region) rows
+  if (e == cudaSuccess) e = cudaMalloc(&s->grp_off, (size_t)kMaxKeys * nwt_max * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&s->totals, 3 * kMaxKeys * 4);  // totals | base | per-owner counts
   if (e == cudaSuccess) e = cudaMalloc(&s->ctl, 128 * 4);
   if (e == cudaSuccess) e = cudaMemset(s->ctl, 0, 128 * 4);
   if (e == cudaSuccess) e = cudaMalloc(&s->res, (size_t)world * max_batch);
@@ -591,7 +604,8 @@ vs_status vs_shard_create(vs_table* local, int rank, int world, uint64_t max_bat
   // k_wait spins on peers whose launches sit behind it (one-process groups)
   {
     cudaFuncAttributes fa;
-    const void* fns[] = {(const void*)k_wpart_count, (const void*)k_wpart_scan, (const void*)k_wpart_push,
+    const void* fns[] = {(const void*)k_wpart_count, (const void*)k_wpart_scan, (const void*)k_wpart_base,
+                         (const void*)k_wpart_push,
                          (const void*)k_wait,        (const void*)k_shard_apply, (const void*)k_shard_post,
                          (const void*)k_shard_return};
     for (const void* f : fns)
@@ -686,11 +700,14 @@ vs_status vs_shard_apply(vs_shard* s, const int32_t* keys, const uint8_t* ops, u
       count_launch();
       VS_CK(launch_pdl(k_wpart_scan, s->world * V.nreg, 1024, 0, st, s->tile_cnt, nwt, s->grp_off, s->totals));
       count_launch();
+      VS_CK(launch_pdl(k_wpart_base, 1, kMaxKeys, 0, st, s->totals, (uint32_t)s->world, V.nreg, s->totals + kMaxKeys,
+                       s->totals + 2 * kMaxKeys));
+      count_launch();
     } else {
-      VS_CK(cudaMemsetAsync(s->totals, 0, kMaxWorld * 4, st));
+      VS_CK(cudaMemsetAsync(s->totals, 0, 3 * kMaxKeys * 4, st));
     }
     VS_CK(launch_pdl(k_wpart_push, ctas, kPartThreads, 0, st, V, keys, ops, n, nwt, s->tile_cnt, s->grp_off,
-                     s->totals, ep, s->ctl));
+                     s->totals + kMaxKeys, s->totals + 2 * kMaxKeys, ep, s->ctl));
     count_launch();
   }
   VS_CK(launch_pdl(k_wait, 1, 32, 0, st, own->push_flag, s->world, ep, s->ctl + 64, s->timeout_ns));
