@@ -522,6 +522,16 @@ class BlockHashMap(_HashCore):
             pos = self._find(key)
             return default if pos is None else self._values[pos]
 
+    def get_many(self, keys, default: Any = None) -> list:
+        """``[get(k) for k in keys]`` with ONE batched lookup (a per-key get
+        is one GPU round trip)."""
+        keys = list(keys)
+        if not keys:
+            return []
+        found, pos = self.find_keys(keys)
+        with self._mutex:
+            return [self._values[p] if f else default for f, p in zip(found.cpu().tolist(), pos.cpu().tolist())]
+
     def get_or_create(self, key: BlockKey, factory: Callable[[], Any]) -> tuple[Any, bool]:
         """Exactly one caller creates (concurrent_hash.py:462-478)."""
         with self._mutex:

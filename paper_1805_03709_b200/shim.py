@@ -11,6 +11,9 @@ modules, the maintainers' one-line integration:
         one encode launch per TSDF batch and one fan-out launch for all
         exploration clients instead of per-block / per-key Python loops
         (server.py:299-315)
+  voxelstream.server.Server.on_block_request                 -> batched:
+        one map lookup for the whole request instead of one per key, and
+        the VISIBLE_FIRST frustum test on the device (server.py:334-387)
 
 Modules bind names at import time (server.py:25, voxel_model.py:20,
 exploration.py:24), so both the defining module and the importers are
@@ -58,6 +61,7 @@ def install(package: str = "voxelstream", batched_server: bool = True) -> None:
             _set(rc, "StreamSet", gsrv.StreamSet)
         if batched_server and hasattr(srv, "Server"):
             _set(srv.Server, "on_tsdf_batch", _on_tsdf_batch)
+            _set(srv.Server, "on_block_request", _on_block_request)
     _set(top, "recompute_mc_block", gmc.recompute_mc_block)
 
 
@@ -95,3 +99,55 @@ def _on_tsdf_batch(self, batch) -> None:
     for s in streams:
         if not isinstance(s, gsrv.StreamSet):
             s.insert_many(affected)
+
+
+def _frustum_args(self, req, srv):
+    """The frustum _visibility_predicate builds (server.py:365-375), as the
+    (planes, margin, block size) the device predicate takes."""
+    voxel = self.cfg.voxel_size or 0.005
+    block_size = srv.BLOCK_EDGE * voxel
+    fx, fy, cx, cy, near, far = req.intrinsics
+    pose = srv.Pose.from_floats(req.pose)
+    intr = srv.CameraIntrinsics(fx=fx, fy=fy, cx=cx, cy=cy, width=int(2 * cx) or 640, height=int(2 * cy) or 480)
+    frustum = srv.Frustum(pose, intr, near=max(near, 1e-3), far=far, margin=block_size)
+    return frustum._planes, frustum.margin, block_size
+
+
+def _on_block_request(self, sess, req) -> None:
+    """server.py:334-363 with the same strategies and effects, but ONE
+    batched map lookup for the requested keys (mc_map.get per key is one GPU
+    round trip each), and for VISIBLE_FIRST on a GPU stream set the frustum
+    test on the device (extract_visible_first: decisions bit-identical to
+    _visibility_predicate, same random top-up)."""
+    from . import server as gsrv
+
+    if sess.stream is None:
+        return
+    srv = sys.modules[type(self).__module__]
+    wire = srv.wire
+    n = min(req.max_blocks, self.cfg.max_request_blocks)
+    stream = sess.stream
+    strategy = req.strategy
+    if strategy == wire.Strategy.VISIBLE_FIRST:
+        if isinstance(stream, gsrv.StreamSet):
+            planes, margin, block = _frustum_args(self, req, srv)
+            keys = stream.extract_visible_first(n, planes, margin, block)
+        else:
+            keys = stream.extract_matching(n, self._visibility_predicate(req))
+            if len(keys) < n:  # top up so requests stay full-sized
+                keys.extend(stream.extract_random(n - len(keys)))
+    elif strategy == wire.Strategy.GENERATION_ORDER:
+        keys = stream.extract_ordered(n)
+    else:
+        keys = stream.extract_random(n)
+    sess.request_count += 1
+    with self._delivery_lock:
+        get_many = getattr(self.mc_map, "get_many", None)
+        raws = get_many(keys) if get_many is not None else [self.mc_map.get(k) for k in keys]
+        blocks = [(k, raw) for k, raw in zip(keys, raws) if raw is not None]  # deleted by a reset meanwhile
+        ok = sess.send(wire.McBatch(blocks), self.cfg.codec)
+    if ok:
+        sess.blocks_sent += len(blocks)
+    else:
+        # connection died mid-delivery: nothing may be lost
+        stream.insert_many(keys)

@@ -31,6 +31,9 @@ def _fake_package(name):
         def on_tsdf_batch(self, batch):
             return "reference"
 
+        def on_block_request(self, sess, req):
+            return "reference"
+
     mods["server"].Server = Server
     pkg.BlockHashSet = object
     pkg.BlockHashMap = object
@@ -58,6 +61,7 @@ def test_install_rebinds_hot_path_names_and_uninstall_restores():
         assert mods["server"].recompute_mc_block is gmc.recompute_mc_block
         assert pkg.BlockHashSet is gch.BlockHashSet
         assert mods["server"].Server.on_tsdf_batch is shim._on_tsdf_batch
+        assert mods["server"].Server.on_block_request is shim._on_block_request
     finally:
         shim.uninstall()
     assert mods["concurrent_hash"].BlockHashSet is object
@@ -65,3 +69,83 @@ def test_install_rebinds_hot_path_names_and_uninstall_restores():
     assert mods["server"].Server.on_tsdf_batch is original
     for k in [k for k in sys.modules if k.startswith("fakevs_ref")]:
         del sys.modules[k]
+
+
+def test_block_request_batches_the_map_lookups():
+    """shim._on_block_request (server.py:334-363): strategy dispatch, ONE
+    get_many for the whole request, keys deleted meanwhile dropped, the
+    request counted, and the keys given back when the send fails."""
+    import enum
+
+    from paper_1805_03709_b200 import shim
+
+    class Strategy(enum.IntEnum):
+        GENERATION_ORDER = 0
+        VISIBLE_FIRST = 1
+        RANDOM = 2
+
+    class McBatch:
+        def __init__(self, blocks):
+            self.blocks = blocks
+
+    mod = types.ModuleType("fake_block_server")
+    mod.wire = types.SimpleNamespace(Strategy=Strategy, McBatch=McBatch)
+    sys.modules[mod.__name__] = mod
+
+    class Stream:  # a host stream set (the device path is tested on the GPU)
+        def __init__(self, keys):
+            self.keys = list(keys)
+            self.back = []
+
+        def extract_random(self, n):
+            out, self.keys = self.keys[:n], self.keys[n:]
+            return out
+
+        def extract_ordered(self, n):
+            return self.extract_random(n)
+
+        def extract_matching(self, n, pred):
+            out = [k for k in self.keys if pred(k)][:n]
+            self.keys = [k for k in self.keys if k not in out]
+            return out
+
+        def insert_many(self, keys):
+            self.back.extend(keys)
+
+    class Map:
+        def __init__(self):
+            self.calls = 0
+
+        def get_many(self, keys):
+            self.calls += 1
+            return [None if k[0] == 3 else bytes([k[0]]) for k in keys]
+
+    class Sess:
+        def __init__(self, stream, ok=True):
+            self.stream, self.ok = stream, ok
+            self.request_count = self.blocks_sent = 0
+            self.sent = []
+
+        def send(self, msg, codec):
+            self.sent.append(msg.blocks)
+            return self.ok
+
+    Server = type("Server", (), {"__module__": mod.__name__})
+    srv = Server()
+    srv.cfg = types.SimpleNamespace(max_request_blocks=4, codec=None, voxel_size=0.01)
+    srv.mc_map = Map()
+    srv._delivery_lock = __import__("threading").Lock()
+    srv._visibility_predicate = lambda req: (lambda k: k[1] == 0)
+    keys = [(i, i % 2, 0) for i in range(10)]
+    for strategy, want in ((Strategy.RANDOM, [0, 1, 2, 3]), (Strategy.GENERATION_ORDER, [0, 1, 2, 3]),
+                           (Strategy.VISIBLE_FIRST, [0, 2, 4, 6])):  # max_request_blocks = 4
+        sess = Sess(Stream(keys))
+        req = types.SimpleNamespace(max_blocks=10, strategy=strategy)
+        shim._on_block_request(srv, sess, req)
+        got = [k[0] for k, _ in sess.sent[0]]
+        assert got == [k for k in want if k != 3], (strategy, got)
+        assert sess.request_count == 1 and sess.blocks_sent == len(got)
+    assert srv.mc_map.calls == 3  # one lookup per request, not one per key
+    sess = Sess(Stream(keys), ok=False)
+    shim._on_block_request(srv, sess, types.SimpleNamespace(max_blocks=2, strategy=Strategy.RANDOM))
+    assert sess.stream.back == [(0, 0, 0), (1, 1, 0)] and sess.blocks_sent == 0

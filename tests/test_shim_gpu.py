@@ -138,3 +138,88 @@ def test_gpu_server_core_sync_free_tick_matches_sync(dev, golden):
         f0, p0 = cores[0].mc_map.find_keys([k])
         f1, p1 = cores[1].mc_map.find_keys([k])
         assert torch.equal(cores[0].q_pool[p0.long()], cores[1].q_pool[p1.long()])
+
+
+# ---- on_block_request through the shim: the names server.py imports, stubbed
+# (the reference package is not on the GPU box)
+import enum as _enum
+import types as _types
+
+
+class _Strategy(_enum.IntEnum):
+    GENERATION_ORDER = 0
+    VISIBLE_FIRST = 1
+    RANDOM = 2
+
+
+class _McBatch:
+    def __init__(self, blocks):
+        self.blocks = blocks
+
+
+wire = _types.SimpleNamespace(Strategy=_Strategy, McBatch=_McBatch)
+BLOCK_EDGE = 8
+
+
+class Pose:
+    @staticmethod
+    def from_floats(v):
+        return tuple(v)
+
+
+class CameraIntrinsics:
+    def __init__(self, **kw):
+        self.kw = kw
+
+
+class Frustum:
+    """Stand-in with the two attributes the predicate uses: the half-space
+    x >= 0.2 (plus five planes every block passes)."""
+
+    def __init__(self, pose, intr, near, far, margin):
+        self.margin = margin
+        self._planes = [(1.0, 0.0, 0.0, -0.2)] + [(0.0, 0.0, 0.0, 1.0)] * 5
+
+
+class _Sess:
+    def __init__(self, stream):
+        self.stream = stream
+        self.request_count = self.blocks_sent = 0
+        self.sent = []
+
+    def send(self, msg, codec):
+        self.sent.append(msg.blocks)
+        return True
+
+
+def test_shim_block_request_device_frustum_and_batched_gets(dev):
+    """VISIBLE_FIRST through shim._on_block_request on a GPU stream set: the
+    frustum from the request goes to the device predicate (visible keys
+    first, random top-up), payloads come from ONE batched map lookup, keys
+    deleted from the map meanwhile are dropped."""
+    import threading
+
+    from paper_1805_03709_b200 import BlockHashMap, StreamSet, shim
+
+    srv = StubServer()
+    srv.mc_map = BlockHashMap(1 << 10, 1 << 10)
+    srv.cfg = _types.SimpleNamespace(max_request_blocks=64, codec=None, voxel_size=0.01)
+    srv._delivery_lock = threading.Lock()
+    keys = [(x, y, 0) for x in range(-8, 8) for y in range(4)]  # 64 keys; x >= 0 is visible with block 0.08
+    for k in keys:
+        srv.mc_map.put(k, bytes([k[0] & 0xFF, k[1]]))
+    srv.mc_map.remove((5, 1, 0))  # deleted by a reset after it became pending
+    stream = StreamSet(1 << 8, 1 << 8)
+    stream.insert_many(keys)
+    sess = _Sess(stream)
+    req = _types.SimpleNamespace(max_blocks=40, strategy=_Strategy.VISIBLE_FIRST, intrinsics=(1.0, 1.0, 320.0, 240.0,
+                                 0.1, 10.0), pose=(0.0,) * 7)
+    shim._on_block_request(srv, sess, req)
+    block = 0.08
+    visible = [k for k in keys if k[0] * block + block - 0.2 >= -block]  # the stand-in frustum, margin = block
+    got = [k for k, _ in sess.sent[0]]
+    n_vis = min(40, len(visible))
+    assert all(k in visible for k in got[: n_vis - 1])  # visible keys first (one of them was deleted)
+    assert len(got) == 40 - 1 and (5, 1, 0) not in got
+    assert all(raw == bytes([k[0] & 0xFF, k[1]]) for k, raw in sess.sent[0])
+    assert sess.blocks_sent == len(got) and stream.size() == len(keys) - 40
