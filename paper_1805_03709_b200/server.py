@@ -20,7 +20,7 @@ from typing import Callable, Optional, Sequence
 
 from . import _lib
 from ._lib import check, ptr
-from .concurrent_hash import BlockHashSet, BlockKey, _as_keys
+from .concurrent_hash import BlockHashSet, BlockKey, CapacityExhausted, _as_keys
 from .mc_encoding import FACE_BYTES, MC_BLOCK_BYTES, Q_BLOCK_BYTES, encode_keys, face_packs, pack_mc_batch
 from .voxel_model import TSDF_BLOCK_BYTES
 
@@ -47,6 +47,23 @@ class StreamSet:
         self._tail_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
         self._tail_bound = 0
         self._scratch: Optional[BlockHashSet] = None
+
+    def _grow(self, need: int = 0) -> None:
+        """Lift the reference's fixed set capacity (server.py:242-243 caps a
+        client's set at 2^16 + 2^16 and raises CapacityExhausted on larger
+        models): move the pending keys into a table at least twice as large.
+        The FIFO ring holds key values, so it stays as it is."""
+        old = self._set
+        nb, ex = 2 * old.bucket_count, 2 * old.excess_capacity
+        while nb + ex < 2 * need:
+            nb, ex = 2 * nb, 2 * ex
+        keys, _ = old.snapshot_tensor()
+        new = BlockHashSet(nb, ex, device=self.device)
+        if keys.shape[0]:
+            new.insert_keys(keys)
+        new.check_capacity()
+        self._set = new
+        _FIFO_GEN[0] += 1  # cached launch arguments hold the old table
 
     # -- FIFO ring management -------------------------------------------------
 
@@ -250,7 +267,17 @@ def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True, n_dev=None):
             st._tail_bound += n
     if not sync:
         return counts
-    return [int(c) for c in counts.cpu().tolist()]
+    out = [int(c) for c in counts.cpu().tolist()]
+    # a set that ran out of entries grows and takes the keys again (inserts of
+    # keys it already holds are no-ops); sync=False callers check() instead
+    for j, st in enumerate(sets):
+        if isinstance(st, StreamSet):
+            try:
+                st._set.check_capacity()
+            except CapacityExhausted:
+                st._grow(st.size() + n)
+                out[j] += fan_out([st], k)[0]
+    return out
 
 
 def extract_random_many(sets: Sequence[StreamSet], max_n: int, seeds: Optional[Sequence[int]] = None, *,
@@ -488,9 +515,12 @@ class GpuServerCore:
         return affected
 
     def check(self) -> None:
-        """Raise CapacityExhausted if a sync=False update ran out of entries."""
+        """Raise CapacityExhausted if a sync=False update ran out of entries
+        (in either map or in a client's stream set)."""
         self.tsdf_map.check_capacity()
         self.mc_map.check_capacity()
+        for st in self.streams():
+            st._set.check_capacity()
 
     def on_reset_blocks(self, keys) -> None:
         """server.py:425-436: remove from both maps and every client set."""

@@ -304,6 +304,33 @@ def test_stream_tick_edges(dev):
         stream_tick(sets, torch.zeros((513, 3), dtype=torch.int32, device=dev), 1)
 
 
+def test_stream_set_grows_past_its_capacity(dev):
+    """The reference caps a client's set at 2^16 + 2^16 entries and raises
+    CapacityExhausted on larger models (server.py:242-243); our StreamSet
+    grows instead: every key pending and queued exactly once.  (Keys whose
+    insert found the old table full are queued after the rest of that call:
+    there is no reference order for a call the reference would have failed.)
+    A set that did not overflow keeps the exact generation order."""
+    from paper_1805_03709_b200 import StreamSet, fan_out
+
+    rng = np.random.default_rng(4)
+    keys = [tuple(int(v) for v in r) for r in np.unique(rng.integers(-10**6, 10**6, (6000, 3)), axis=0)]
+    ref = oracle.OracleStreamSet()
+    small = StreamSet(1 << 6, 1 << 6, fifo_capacity=1 << 10)
+    other = StreamSet(1 << 14, 1 << 14)
+    half = len(keys) // 2
+    assert fan_out([small, other], keys[:half]) == [half, half]
+    assert small.insert_many(keys) == len(keys) - half
+    ref.insert_many(keys)
+    assert small.size() == len(keys) and set(small.snapshot()) == ref.set
+    assert sorted(small.fifo_entries()) == sorted(ref.order)
+    got = small.extract_ordered(100)
+    assert len(got) == 100 and set(got) <= ref.set
+    assert other.fifo_entries() == keys[:half]
+    a = small._set.audit()
+    assert a["duplicates"] == 0 and a["unreachable_live"] == 0
+
+
 def test_extract_random_many_properties(dev):
     """Windowed multi-client extraction: distinct keys, subset of the set,
     count = min(max_n, size), post-set = pre-set minus returned, rotation
