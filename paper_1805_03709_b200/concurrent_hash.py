@@ -350,6 +350,21 @@ class _HashCore:
     def __contains__(self, key: BlockKey) -> bool:
         return self._find(key) is not None
 
+    def remove_many(self, keys) -> int:
+        """``sum(remove(k) for k in keys)`` in one launch (a per-key remove is
+        one GPU round trip); map values of the removed keys are dropped."""
+        keys = list(keys) if not hasattr(keys, "shape") else keys
+        if len(keys) == 0:
+            return 0
+        erased, pos = self.erase_keys(keys)
+        e = erased.cpu().tolist()
+        if self._values is not None:
+            with self._mutex:
+                for f, p in zip(e, pos.cpu().tolist()):
+                    if f:
+                        self._values[p] = None
+        return int(sum(e))
+
     def snapshot_keys(self) -> list[BlockKey]:
         keys, _ = self.snapshot_tensor()
         return [tuple(k) for k in keys.cpu().tolist()]

@@ -14,6 +14,9 @@ modules, the maintainers' one-line integration:
   voxelstream.server.Server.on_block_request                 -> batched:
         one map lookup for the whole request instead of one per key, and
         the VISIBLE_FIRST frustum test on the device (server.py:334-387)
+  voxelstream.server.Server.on_reset_blocks                  -> batched:
+        one remove launch per map and one for every client set instead of
+        K x (2 + clients) per-key removes (server.py:425-436)
 
 Modules bind names at import time (server.py:25, voxel_model.py:20,
 exploration.py:24), so both the defining module and the importers are
@@ -62,6 +65,7 @@ def install(package: str = "voxelstream", batched_server: bool = True) -> None:
         if batched_server and hasattr(srv, "Server"):
             _set(srv.Server, "on_tsdf_batch", _on_tsdf_batch)
             _set(srv.Server, "on_block_request", _on_block_request)
+            _set(srv.Server, "on_reset_blocks", _on_reset_blocks)
     _set(top, "recompute_mc_block", gmc.recompute_mc_block)
 
 
@@ -151,3 +155,31 @@ def _on_block_request(self, sess, req) -> None:
     else:
         # connection died mid-delivery: nothing may be lost
         stream.insert_many(keys)
+
+
+def _on_reset_blocks(self, keys) -> None:
+    """server.py:425-436 with the same effects (keys gone from both maps and
+    every exploration client's set, DeleteBlocks sent to each client), the
+    removes batched: one launch per map, one for all GPU client sets."""
+    from . import server as gsrv
+
+    if not keys:
+        return
+    srv = sys.modules[type(self).__module__]
+    wire = srv.wire
+    ecs = self._exploration_sessions()
+    with self._delivery_lock:
+        for m in (self.tsdf_map, self.mc_map):
+            if hasattr(m, "remove_many"):
+                m.remove_many(keys)
+            else:
+                for key in keys:
+                    m.remove(key)
+        gpu = [ec.stream for ec in ecs if isinstance(ec.stream, gsrv.StreamSet)]
+        if gpu:
+            gsrv.remove_everywhere(gpu, keys)
+        for ec in ecs:
+            if not isinstance(ec.stream, gsrv.StreamSet):
+                for key in keys:
+                    ec.stream.remove(key)
+            ec.send(wire.DeleteBlocks(keys), self.cfg.codec)

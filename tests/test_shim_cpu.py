@@ -34,6 +34,9 @@ def _fake_package(name):
         def on_block_request(self, sess, req):
             return "reference"
 
+        def on_reset_blocks(self, keys):
+            return "reference"
+
     mods["server"].Server = Server
     pkg.BlockHashSet = object
     pkg.BlockHashMap = object
@@ -62,6 +65,7 @@ def test_install_rebinds_hot_path_names_and_uninstall_restores():
         assert pkg.BlockHashSet is gch.BlockHashSet
         assert mods["server"].Server.on_tsdf_batch is shim._on_tsdf_batch
         assert mods["server"].Server.on_block_request is shim._on_block_request
+        assert mods["server"].Server.on_reset_blocks is shim._on_reset_blocks
     finally:
         shim.uninstall()
     assert mods["concurrent_hash"].BlockHashSet is object
@@ -149,3 +153,61 @@ def test_block_request_batches_the_map_lookups():
     sess = Sess(Stream(keys), ok=False)
     shim._on_block_request(srv, sess, types.SimpleNamespace(max_blocks=2, strategy=Strategy.RANDOM))
     assert sess.stream.back == [(0, 0, 0), (1, 1, 0)] and sess.blocks_sent == 0
+
+
+def test_reset_blocks_batched_removes():
+    """shim._on_reset_blocks (server.py:425-436): keys leave both maps (one
+    remove_many each) and every client's set, every client gets DeleteBlocks."""
+    from paper_1805_03709_b200 import shim
+
+    class DeleteBlocks:
+        def __init__(self, keys):
+            self.keys = keys
+
+    mod = types.ModuleType("fake_reset_server")
+    mod.wire = types.SimpleNamespace(DeleteBlocks=DeleteBlocks)
+    sys.modules[mod.__name__] = mod
+
+    class Map:
+        def __init__(self, keys):
+            self.keys, self.calls = set(keys), 0
+
+        def remove_many(self, keys):
+            self.calls += 1
+            n = len(self.keys & set(keys))
+            self.keys -= set(keys)
+            return n
+
+    class HostSet:
+        def __init__(self, keys):
+            self.keys = set(keys)
+
+        def remove(self, key):
+            had = key in self.keys
+            self.keys.discard(key)
+            return had
+
+    class Ec:
+        def __init__(self, keys):
+            self.stream = HostSet(keys)
+            self.sent = []
+
+        def send(self, msg, codec):
+            self.sent.append(msg.keys)
+
+    allk = [(i, 0, 0) for i in range(10)]
+    Server = type("Server", (), {"__module__": mod.__name__})
+    srv = Server()
+    srv.cfg = types.SimpleNamespace(codec=None)
+    srv.tsdf_map, srv.mc_map = Map(allk), Map(allk)
+    ecs = [Ec(allk), Ec(allk[:5])]
+    srv._exploration_sessions = lambda: ecs
+    srv._delivery_lock = __import__("threading").Lock()
+    gone = allk[3:7]
+    shim._on_reset_blocks(srv, gone)
+    for m in (srv.tsdf_map, srv.mc_map):
+        assert m.keys == set(allk) - set(gone) and m.calls == 1
+    assert ecs[0].stream.keys == set(allk) - set(gone) and ecs[1].stream.keys == set(allk[:3])
+    assert all(ec.sent == [gone] for ec in ecs)
+    shim._on_reset_blocks(srv, [])
+    assert all(len(ec.sent) == 1 for ec in ecs)

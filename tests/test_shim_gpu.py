@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import hashlib
 import json
+import threading
 import sys
 
 import numpy as np
@@ -36,6 +37,11 @@ class _Batch:
 class _Session:
     def __init__(self, stream):
         self.stream = stream
+        self.sent = []
+
+    def send(self, msg, codec):
+        self.sent.append(msg.keys)
+        return True
 
 
 class StubServer:
@@ -70,7 +76,8 @@ class StubServer:
                 ec.stream.remove(key)
 
 
-def test_shim_on_tsdf_batch_replays_reference_server(dev, golden):
+@pytest.mark.parametrize("batched_reset", [False, True])
+def test_shim_on_tsdf_batch_replays_reference_server(dev, golden, batched_reset):
     from paper_1805_03709_b200 import shim
 
     assert sys.modules[StubServer.__module__].TsdfBlock is TsdfBlock
@@ -93,7 +100,14 @@ def test_shim_on_tsdf_batch_replays_reference_server(dev, golden):
             drop = [k for k in clients[1].snapshot() if k not in keep]
             clients[1].remove_many(drop)  # adopt the reference's random subset
         if "reset" in entry:
-            srv.on_reset_blocks([tuple(v) for v in entry["reset"]])
+            if batched_reset:  # shim._on_reset_blocks: batched removes + DeleteBlocks to each client
+                srv.cfg = _types.SimpleNamespace(codec=None)
+                srv._delivery_lock = threading.Lock()
+                shim._on_reset_blocks(srv, [tuple(v) for v in entry["reset"]])
+                assert all(s_.sent and s_.sent[-1] == [tuple(v) for v in entry["reset"]]
+                           for s_ in srv.sessions.values())
+            else:
+                srv.on_reset_blocks([tuple(v) for v in entry["reset"]])
             for c, cl in enumerate(clients):
                 assert sorted(list(k) for k in cl.snapshot()) == entry["pending_after_reset"][c]
     got = sorted(srv.mc_map.snapshot_keys())
@@ -157,7 +171,12 @@ class _McBatch:
         self.blocks = blocks
 
 
-wire = _types.SimpleNamespace(Strategy=_Strategy, McBatch=_McBatch)
+class _DeleteBlocks:
+    def __init__(self, keys):
+        self.keys = keys
+
+
+wire = _types.SimpleNamespace(Strategy=_Strategy, McBatch=_McBatch, DeleteBlocks=_DeleteBlocks)
 BLOCK_EDGE = 8
 
 
