@@ -37,8 +37,14 @@ def _set(obj, name: str, value) -> None:
         setattr(obj, name, value)
 
 
-def install(package: str = "voxelstream", batched_server: bool = True) -> None:
-    """Patch the (already importable) reference package in place."""
+def install(package: str = "voxelstream", batched_server: bool = True, client_maps: bool = True) -> None:
+    """Patch the (already importable) reference package in place.
+
+    client_maps=False keeps the reference's host maps in ``voxel_model`` and
+    ``exploration``: their per-key loops (VoxelModel.allocate_blocks /
+    integrate_frame, ExplorationClient) would pay one GPU round trip per key
+    (INTEGRATION.md); reconstruction clients get the batched
+    ``voxel_model.GpuVoxelModel`` instead."""
     import importlib
 
     from . import concurrent_hash as gch
@@ -52,7 +58,10 @@ def install(package: str = "voxelstream", batched_server: bool = True) -> None:
         except ImportError:
             continue
     top = sys.modules.get(package) or importlib.import_module(package)
+    client_side = {mods.get("voxel_model"), mods.get("exploration")} - {None}
     for mod in list(mods.values()) + [top]:
+        if not client_maps and mod in client_side:
+            continue
         _set(mod, "BlockHashSet", gch.BlockHashSet)
         _set(mod, "BlockHashMap", gch.BlockHashMap)
     srv = mods.get("server")

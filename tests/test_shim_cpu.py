@@ -211,3 +211,16 @@ def test_reset_blocks_batched_removes():
     assert all(ec.sent == [gone] for ec in ecs)
     shim._on_reset_blocks(srv, [])
     assert all(len(ec.sent) == 1 for ec in ecs)
+
+
+def test_install_can_keep_client_side_host_maps():
+    from paper_1805_03709_b200 import concurrent_hash as gch
+    from paper_1805_03709_b200 import shim
+
+    pkg, mods = _fake_package("fakevs_ref2")
+    shim.install("fakevs_ref2", client_maps=False)
+    try:
+        assert mods["server"].BlockHashMap is gch.BlockHashMap
+        assert mods["voxel_model"].BlockHashMap is object and mods["exploration"].BlockHashMap is object
+    finally:
+        shim.uninstall()
