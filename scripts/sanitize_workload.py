@@ -38,6 +38,12 @@ sets[0].extract_ordered(100); sets[0].fifo_entries(); sets[1].clear()
 core = GpuServerCore(1 << 10, 1 << 10, stream_buckets=1 << 9, stream_excess=1 << 9)
 cl = core.attach(b"a" * 16)
 core.on_tsdf_batch(keys[:20], rows[:20]); core.on_reset_blocks(keys[:5])
+# one-call server tick (side-stream fork/join) + fused stream tick + set growth
+aff, n_aff = core.on_tsdf_batch(keys[20:60], rows[20:60], sync=False); core.check()
+from paper_1805_03709_b200 import stream_tick
+stream_tick(sets, torch.from_numpy(keys[:200]).to(dev), 32, seeds=[1, 2, 3])
+tiny = StreamSet(4, 4, fifo_capacity=64)
+fan_out([tiny], keys[:300], sync=True); assert len(tiny) >= 300 if hasattr(tiny, "__len__") else True
 # face packs + both encoder halo paths
 from paper_1805_03709_b200 import face_packs
 fp = face_packs(pool, rows=pos)
@@ -56,6 +62,10 @@ sh.apply(workloads.id_to_key_torch(torch.arange(spec.live, device=dev)[:spec.bat
          torch.zeros(spec.batch, dtype=torch.uint8, device=dev))
 r2 = sh.apply(workloads.id_to_key_torch(ids), ops)
 sh.check()
+# region-ordered partition (tables >= 1 GiB): 2^26 entries, small batch
+big = ShardedBlockHashSet(BlockHashSet(1 << 25, 1 << 25), exchange="peer", max_batch=1 << 12)
+big.apply(workloads.id_to_key_torch(torch.arange(1 << 12, device=dev)), torch.zeros(1 << 12, dtype=torch.uint8, device=dev))
+big.check(); del big
 dist.destroy_process_group()
 # RC fusion kernels on a small frame
 import types

@@ -18,7 +18,8 @@ CAPS = [("apply", "r02_apply", "k_apply (config 2, one 2^22-op mixed batch)"),
         ("stream", "r02_stream", "config-4 tick kernels: k_dedup_small, k_multi_fan_small, k_multi_extract"),
         ("server", "r02_server", "SURVEY 3.1 on_tsdf_batch kernels: k_put_rows, k_mc_encode<1,1,0> (faces, out_rows)"),
         ("rc", "r02_rc", "RC fusion: k_rc_cull_table, k_rc_integrate"),
-        ("shard", "r02_shard", "peer-shard route at world 1: k_wpart_push, k_shard_apply, k_shard_return")]
+        ("shard", "r02_shard", "peer-shard route at world 1, config-5 slice (125M keys, 2^24-op batches, 16 bucket regions): "
+                            "k_wpart_count, k_wpart_base, k_wpart_push, k_shard_apply, k_shard_return")]
 
 
 def raw_all(rep):
@@ -46,14 +47,17 @@ def stalls(rep, kernel, n=12):
     return [(s, 100 * s / tot, f, l, src) for s, f, l, src in sorted(res, reverse=True)[:n]]
 
 
-def main(src="gpurun_out", tag="r02"):
+def main(src="gpurun_out", tag="r02", only=""):
     for name, rep, what in CAPS:
+        if only and name not in only.split(","):
+            continue
         path = f"{src}/{rep}.ncu-rep"
         if not pathlib.Path(path).exists():
             print("missing", path)
             continue
         lines = [f"# ncu --set full --clock-control none summary ({tag}): {what}",
-                 f"# from {rep}.ncu-rep, command in scripts/gpu_r02_ncu.sh"]
+                 f"# from {rep}.ncu-rep, command in scripts/gpu_r02_ncu.sh"
+                 + (" (re-captured by scripts/gpu_r02_final2.sh)" if name == "shard" else "")]
         seen = set()
         for kname, d in raw_all(path):
             lines.append(f"## {kname[:120]}")
