@@ -26,6 +26,9 @@
 //   * outputs are written with streaming stores (evict-first) so the L2 keeps
 //     the TSDF rows that neighbouring blocks will read as halo.
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "faces.cuh"
 #include "hash_ops.cuh"
@@ -179,6 +182,7 @@ struct McSmem {
   uint32_t wsum[4];         // kCells: per-warp non-empty counts of the block
   uint32_t cbase;           // kCells: reserved start of the block's cell range
   uint32_t pair_lut[32];    // pair4 of every 5-bit row slice (VSB_MC_PAIR_LUT)
+  unsigned long long tk[4]; // VSB_MC_TICKET: ticket of lookup batch k in slot k & 3
 };
 
 // Cube-index assembly through a 32-entry table of pair4 (VSB_MC_PAIR_LUT):
@@ -194,6 +198,43 @@ struct McSmem {
 #define VSB_MC_REVERSE 0
 #endif
 __device__ __forceinline__ uint64_t sweep_block(uint64_t i, uint64_t n) { return VSB_MC_REVERSE ? n - 1 - i : i; }
+
+// Work distribution.  VSB_MC_TICKET=1 (default): every lookup batch is 16
+// CONSECUTIVE sweep indices claimed from a per-stream ticket counter (one
+// atomicAdd per 16 blocks, claimed two batches ahead), so CTAs take work in
+// sweep order as they free up: the grid-wide wavefront stays a few batches
+// wide and a block's +x neighbour (97% of consecutive room keys) is read by
+// the same CTA one block later.  VSB_MC_TICKET=0: static grid stride
+// (iteration j of CTA c takes sweep index c + j*G); measured, the CTAs then
+// drift apart by up to 1.4 ms of a 4 ms launch (profiles/r02_mc_drift.txt),
+// so neighbour rows leave L2 between their halo read and their own encode.
+#ifndef VSB_MC_TICKET
+#define VSB_MC_TICKET 1
+#endif
+// next: the ticket counter; done: CTAs finished.  The last CTA to finish
+// zeroes both, so the next launch on the same stream starts from 0.
+struct McTickets {
+  unsigned long long next, done;
+};
+// VSB_MC_DRIFT (measurement build): globaltimer of every CTA at iterations
+// 64, 256, 640 and 1024 and at its end, read back by vs_mc_drift_read.
+#ifndef VSB_MC_DRIFT
+#define VSB_MC_DRIFT 0
+#endif
+#if VSB_MC_DRIFT
+__device__ unsigned long long g_mc_drift[5][4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+#endif
+
+// Sweep index of the CTA's j-th block (>= n: past the end); dyn: the
+// launch uses tickets (large launches, see launch_mc_t).
+__device__ __forceinline__ uint64_t iter_sblk(const McSmem& sm, uint64_t j, bool dyn) {
+  return dyn ? (uint64_t)sm.tk[(j / kLook) & 3] * kLook + (j % kLook) : blockIdx.x + j * (uint64_t)gridDim.x;
+}
 
 // Neighbour row of block `blk` for corner-block c.
 template <bool kFromKeys>
@@ -218,13 +259,15 @@ __device__ __forceinline__ int32_t load_nbr(const TableView& T, const int32_t* _
 // All 128 threads resolve the 8 neighbour rows of the CTA's next kLook
 // blocks at once (iterations j0 .. j0+15): one chain-walk latency per 16
 // blocks instead of one per block.
-template <bool kFromKeys>
+template <bool kFromKeys, bool kDyn>
 __device__ __forceinline__ void lookup_batch(McSmem& sm, int buf, const TableView& T, const int32_t* keys,
-                                             const int32_t* nbr, uint64_t n, uint64_t j0) {
+                                             const int32_t* nbr, uint64_t n, uint64_t j0, McTickets* tix) {
   const int t = threadIdx.x;
   const int slot = t >> 3, c = t & 7;
-  const uint64_t sblk = blockIdx.x + (j0 + slot) * (uint64_t)gridDim.x;  // sweep index
+  const uint64_t sblk = iter_sblk(sm, j0 + slot, kDyn);  // sweep index
   sm.nb[buf][slot][c] = sblk < n ? load_nbr<kFromKeys>(T, keys, nbr, sweep_block(sblk, n), c) : -1;
+  // the ticket of the batch after next (visible after this iteration's barriers)
+  if (kDyn && t == 0) sm.tk[(j0 / kLook + 2) & 3] = atomicAdd(&tix->next, 1ull);
 }
 
 // Per-thread halo items (thread t owns items t and t + 128 of 217).
@@ -342,7 +385,7 @@ __global__ void __launch_bounds__(256) k_mc_faces(const uint8_t* __restrict__ po
 // vs_mc_compact gives the exact-prefix layout).  out_rows (optional): the
 // MC / quantised outputs of block i go to row out_rows[i] (e.g. the MC map
 // position of the block's key) instead of row i.
-template <bool kFromKeys, bool kFaces, bool kCells>
+template <bool kFromKeys, bool kFaces, bool kCells, bool kDyn>
 __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS : VSB_MC_MINBLOCKS_NBR) k_mc_encode(TableView T, const uint8_t* __restrict__ pool,
                                                           const uint8_t* __restrict__ faces,
                                                           const int32_t* __restrict__ keys,
@@ -353,30 +396,36 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
                                                           uint32_t* __restrict__ counts,
                                                           unsigned long long* cursor, uint32_t* __restrict__ offsets,
                                                           uint16_t* __restrict__ cell_flat,
-                                                          uint32_t* __restrict__ cell_mc, uint64_t cell_cap) {
+                                                          uint32_t* __restrict__ cell_mc, uint64_t cell_cap,
+                                                          McTickets* tix) {
   __shared__ McSmem sm;
   if (n_dev) n = min(n, *n_dev);  // a device-produced count (no host sync in the server tick)
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
-  const uint64_t G = gridDim.x;
-  // blocks of this CTA: blockIdx.x + j*G for j < nj
-  const uint64_t nj = blockIdx.x < n ? (n - 1 - blockIdx.x) / G + 1 : 0;
+  // the CTA's j-th block exists iff its sweep index is < n (a prefix of j)
+  constexpr bool dyn = kDyn;
+  auto has = [&](uint64_t j) { return iter_sblk(sm, j, dyn) < n; };
 
   if (t == 0) {
     for (int b = 0; b < kStages; ++b) mbar_init(&sm.mbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (dyn) {
+      sm.tk[0] = atomicAdd(&tix->next, 1ull);
+      sm.tk[1] = atomicAdd(&tix->next, 1ull);
+    }
   }
   if (t < 32) sm.pair_lut[t] = pair4((uint32_t)t);  // visible after the first barrier
-  lookup_batch<kFromKeys>(sm, 0, T, keys, nbr, n, 0);
+  if (dyn) __syncthreads();
+  lookup_batch<kFromKeys, kDyn>(sm, 0, T, keys, nbr, n, 0, tix);
   __syncthreads();
   if (t == 0)
-    for (uint64_t j = 0; j < kAhead && j < nj; ++j) issue_centre(sm, j, pool);
+    for (uint64_t j = 0; j < kAhead && has(j); ++j) issue_centre(sm, j, pool);
   uint32_t phases = 0u;  // bit b = parity of mbar[b]
   // halo of the block processed next, loaded one iteration ahead
   const HaloDesc hd = halo_desc();
   HaloRegs hal;
   uint4 fpk = make_uint4(0u, 0u, 0u, 0u);  // kFaces: thread t < 7 holds neighbour t+1's pack, one block ahead
-  if (nj) {
+  if (has(0)) {
     if (kFaces) {
       if (t < 7) fpk = load_face(faces, nb_of(sm, 0)[t + 1], t + 1);
     } else {
@@ -384,16 +433,23 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     }
   }
 
-  for (uint64_t j = 0; j < nj; ++j) {
-    const uint64_t blk = sweep_block(blockIdx.x + j * G, n);
+  uint64_t j = 0;
+  for (; has(j); ++j) {
+    const uint64_t blk = sweep_block(iter_sblk(sm, j, dyn), n);
+#if VSB_MC_DRIFT
+    if (t == 0 && blockIdx.x < 4096) {
+      const int m = j == 64 ? 0 : j == 256 ? 1 : j == 640 ? 2 : j == 1024 ? 3 : -1;
+      if (m >= 0) g_mc_drift[m][blockIdx.x] = gtimer();
+    }
+#endif
     const int s = (int)(j & 1);
     const int b = (int)(j % kStages);
     const int slot = (int)(j % kLook);
     const int32_t* nbc = nb_of(sm, j);
     const int32_t centre = nbc[0];
     // the next lookup batch must be ready before block j + kAhead is issued
-    if (slot == kLook - kAhead && j + kAhead < nj)
-      lookup_batch<kFromKeys>(sm, (int)(((j / kLook) + 1) & 1), T, keys, nbr, n, (j / kLook + 1) * kLook);
+    if (slot == kLook - kAhead && (dyn || has(j + kAhead)))
+      lookup_batch<kFromKeys, kDyn>(sm, (int)(((j / kLook) + 1) & 1), T, keys, nbr, n, (j / kLook + 1) * kLook, tix);
     if (kFaces) {
       if (t < 7) sm.pk[s][t] = fpk;  // every grid row is then written whole: no zeroing, no atomics
     } else {
@@ -403,12 +459,12 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
       }
     }
     __syncthreads();  // (A) lookups + packs ready, grids zeroed, buf[(j+kAhead)%kStages] no longer read
-    if (t == 0 && j + kAhead < nj) issue_centre(sm, j + kAhead, pool);
+    if (t == 0 && has(j + kAhead)) issue_centre(sm, j + kAhead, pool);
     const int64_t orow = out_rows ? (int64_t)__ldg(out_rows + blk) : (int64_t)blk;  // < 0: no output row
     uint32_t* mc_blk = mc_out && orow >= 0 ? mc_out + (uint64_t)orow * VS_BLOCK_VOXELS : nullptr;
     int8_t* q_blk = q_out && orow >= 0 ? q_out + (uint64_t)orow * VS_BLOCK_VOXELS : nullptr;
     const HaloRegs cur = hal;
-    if (j + 1 < nj) {
+    if (has(j + 1)) {
       if (kFaces) {
         if (t < 7) fpk = load_face(faces, nb_of(sm, j + 1)[t + 1], t + 1);
       } else {
@@ -566,6 +622,16 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
       if (lane == 0 && nz) atomicAdd(counts + blk, nz);
     }
   }
+#if VSB_MC_DRIFT
+  if (t == 0 && blockIdx.x < 4096) g_mc_drift[4][blockIdx.x] = gtimer();
+#endif
+  if (dyn && t == 0) {
+    __threadfence();  // this CTA's claims precede its "done"
+    if (atomicAdd(&tix->done, 1ull) == gridDim.x - 1) {
+      tix->next = 0ull;  // every CTA is past its last claim
+      tix->done = 0ull;
+    }
+  }
 }
 
 __global__ void k_mc_neighbors(TableView T, const int32_t* __restrict__ keys, uint64_t n,
@@ -618,6 +684,31 @@ struct McOut {
   uint64_t cell_cap;
 };
 
+// One zeroed ticket counter per (device, stream), kept for the process:
+// launches on one stream run in order and the kernel's last CTA re-zeroes
+// the counter, so it needs no memset per launch; launches on different
+// streams never share one.  Allocated in chunks of 256 on first use.
+static McTickets* stream_tickets(cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, McTickets*> slots;
+  static McTickets* chunk = nullptr;
+  static int chunk_dev = -1, chunk_used = 256;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = slots.find({dev, s});
+  if (it != slots.end()) return it->second;
+  if (chunk_used == 256 || chunk_dev != dev) {
+    McTickets* c = nullptr;
+    if (cudaMalloc(&c, 256 * sizeof(McTickets)) != cudaSuccess) return nullptr;
+    if (cudaMemset(c, 0, 256 * sizeof(McTickets)) != cudaSuccess) return nullptr;
+    chunk = c, chunk_dev = dev, chunk_used = 0;
+  }
+  McTickets* t = chunk + chunk_used++;
+  slots[{dev, s}] = t;
+  return t;
+}
+
 template <bool kFromKeys, bool kFaces, bool kCells>
 static vs_status launch_mc_t(const TableView& T, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
                              const int32_t* nbr, uint64_t n, const McOut& o, cudaStream_t s) {
@@ -626,18 +717,26 @@ static vs_status launch_mc_t(const TableView& T, const uint8_t* pool, const uint
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mc_encode<kFromKeys, kFaces, kCells>, kMcThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mc_encode<kFromKeys, kFaces, kCells, false>, kMcThreads, 0);
     if (per_sm < 1) per_sm = 1;
     grid = sms * per_sm;
   }
   const uint64_t g = n < (uint64_t)grid ? n : (uint64_t)grid;
   if (o.counts) VS_CK(cudaMemsetAsync(o.counts, 0, 4 * n, s));
   if (kCells) VS_CK(cudaMemsetAsync(o.cursor, 0, 8, s));
+  // tickets only where every CTA gets several batches: a small launch (the
+  // server tick's ~4k blocks) would otherwise run 16 blocks back to back in
+  // few CTAs instead of 2-3 blocks in each
+  McTickets* tix = nullptr;
+  if (VSB_MC_TICKET && n >= (uint64_t)g * kLook * 4) {
+    tix = stream_tickets(s);
+    if (!tix) return VS_ERR_CUDA;
+  }
   {
     ProfScope prof(1, s);
-    k_mc_encode<kFromKeys, kFaces, kCells><<<(unsigned)g, kMcThreads, 0, s>>>(
-        T, pool, faces, keys, nbr, n, o.n_dev, o.out_rows, (uint32_t*)o.mc, o.q, o.counts, o.cursor, o.offsets, o.cell_flat,
-        o.cell_mc, o.cell_cap);
+    auto kern = tix ? k_mc_encode<kFromKeys, kFaces, kCells, true> : k_mc_encode<kFromKeys, kFaces, kCells, false>;
+    kern<<<(unsigned)g, kMcThreads, 0, s>>>(T, pool, faces, keys, nbr, n, o.n_dev, o.out_rows, (uint32_t*)o.mc, o.q,
+                                            o.counts, o.cursor, o.offsets, o.cell_flat, o.cell_mc, o.cell_cap, tix);
     vsb::count_launch();
   }
   VS_CK_LAUNCH("k_mc_encode");
@@ -769,3 +868,10 @@ vs_status vs_mc_compact(const uint8_t* mc, const uint32_t* counts, uint64_t n, u
 }
 
 }  // extern "C"
+
+#if VSB_MC_DRIFT
+// measurement build only: copies the drift timestamps (5 x 4096 u64) out
+extern "C" int vs_mc_drift_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vsb::g_mc_drift, sizeof(vsb::g_mc_drift)) == cudaSuccess ? 0 : 1;
+}
+#endif
