@@ -288,6 +288,13 @@ __device__ __forceinline__ bool rc_block_candidate(const RcParams& P, const floa
   return true;
 }
 
+// Work distribution of k_rc_integrate: 1 = blocks claimed from a counter
+// (balanced: blocks differ in cost -- voxels outside the image skip their
+// loads), 0 = static grid stride.
+#ifndef VSB_RC_TICKET
+#define VSB_RC_TICKET 1
+#endif
+
 // Persistent CTAs (128 threads, 4 voxels each) walk the blocks that survived
 // culling.  Per block a thread first projects its 4 voxels, then issues every
 // independent load at once (depth sample + the 12-B voxel record, as three
@@ -298,13 +305,20 @@ __global__ void __launch_bounds__(128) k_rc_integrate(const int32_t* __restrict_
                                                       const Entry* __restrict__ ent, const uint32_t* __restrict__ list, const uint64_t* __restrict__ n_list,
                                                       const float* __restrict__ depth, const uint8_t* __restrict__ color,
                                                       const __grid_constant__ RcParams P, uint8_t* __restrict__ pool,
-                                                      uint8_t* __restrict__ touched) {
+                                                      uint8_t* __restrict__ touched, unsigned long long* tick) {
   pdl_wait();
   const uint64_t n_live = *n_list;
+  // tick (VSB_RC_TICKET): blocks are claimed one at a time from a zeroed
+  // counter, the next claim issued while the current block is processed
+  __shared__ unsigned long long claim[2];
+  if (tick && threadIdx.x == 0) claim[0] = atomicAdd(tick, 1ull);
+  if (tick) __syncthreads();
+  int cb = 0;
   const float fx = (float)P.fx, fy = (float)P.fy, cx = (float)P.cx, cy = (float)P.cy;
   const float mu = (float)P.mu, neg_mu = (float)(-P.mu), maxw = (float)P.max_weight;
   const int lx = threadIdx.x & 7, ly = (threadIdx.x >> 3) & 7, lz0 = threadIdx.x >> 6;  // f = tid + 128k: lz = lz0 + 2k
-  for (uint64_t li = blockIdx.x; li < n_live; li += gridDim.x) {
+  for (uint64_t li = tick ? claim[0] : blockIdx.x; li < n_live;) {
+    if (tick && threadIdx.x == 0) claim[cb ^ 1] = atomicAdd(tick, 1ull);
     const uint64_t i = list[li];
     // block source: (keys, pos) arrays, or the table's entry slots (row = slot)
     int32_t kx, ky, kz;
@@ -373,6 +387,13 @@ __global__ void __launch_bounds__(128) k_rc_integrate(const int32_t* __restrict_
       any = true;
     }
     if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) touched[i] = 1;
+    if (tick) {
+      __syncthreads();  // the next claim is visible; claim[cb] is free again
+      cb ^= 1;
+      li = claim[cb];
+    } else {
+      li += gridDim.x;
+    }
   }
 }
 
@@ -451,14 +472,16 @@ vs_status vs_rc_integrate(const int32_t* keys, const int32_t* pos, uint64_t n, c
   VS_CK(cudaMallocAsync((void**)&keep, n, s));
   VS_CK(cudaMallocAsync((void**)&off, 8 * (n + 1), s));
   VS_CK(cudaMallocAsync((void**)&work, 8 * (scan_tiles(n) + 1), s));
-  VS_CK(cudaMallocAsync((void**)&list, 4 * n, s));
+  VS_CK(cudaMallocAsync((void**)&list, 4 * n + 16, s));
+  unsigned long long* tick = VSB_RC_TICKET ? (unsigned long long*)(list + n + (n & 1)) : nullptr;
+  if (tick) VS_CK(cudaMemsetAsync(tick, 0, 8, s));
   VS_CK(cudaMemsetAsync(touched, 0, n, s));
   {
     ProfScope prof(3, s);
     { VS_CK(launch_pdl(k_rc_cull, grid_for(n, 256), 256, 0, s, keys, n, depth, P, keep)); vsb::count_launch(); }
     VS_CK(exclusive_scan<uint8_t>(keep, n, off, work, s));
     { VS_CK(launch_pdl(k_rc_gather, grid_for(n, 256), 256, 0, s, keep, off, n, list)); vsb::count_launch(); }
-    { VS_CK(launch_pdl(k_rc_integrate, integrate_grid(n), 128, 0, s, keys, pos, nullptr, list, off + n, depth, color, P, pool, touched)); vsb::count_launch(); }
+    { VS_CK(launch_pdl(k_rc_integrate, integrate_grid(n), 128, 0, s, keys, pos, nullptr, list, off + n, depth, color, P, pool, touched, tick)); vsb::count_launch(); }
   }
   cudaFreeAsync(keep, s);
   cudaFreeAsync(off, s);
@@ -486,13 +509,15 @@ vs_status vs_rc_integrate_table(const vs_table* t, const float* depth, const uin
   VS_CK(cudaMallocAsync((void**)&touched, n, s));
   VS_CK(cudaMallocAsync((void**)&off, 8 * (n + 1), s));
   VS_CK(cudaMallocAsync((void**)&work, 8 * (scan_tiles(n) + 1), s));
-  VS_CK(cudaMallocAsync((void**)&list, 4 * n, s));
+  VS_CK(cudaMallocAsync((void**)&list, 4 * n + 16, s));
+  unsigned long long* tick = VSB_RC_TICKET ? (unsigned long long*)(list + n + (n & 1)) : nullptr;
+  if (tick) VS_CK(cudaMemsetAsync(tick, 0, 8, s));
   VS_CK(cudaMemsetAsync(touched, 0, n, s));
   {
     ProfScope prof(3, s);
     VS_CK(cudaMemsetAsync(off + n, 0, 8, s));
     { VS_CK(launch_pdl(k_rc_cull_table, grid_for(n, 256), 256, 0, s, t->e, t->cap, depth, P, list, (unsigned long long*)(off + n))); vsb::count_launch(); }
-    { VS_CK(launch_pdl(k_rc_integrate, integrate_grid(n), 128, 0, s, nullptr, nullptr, t->e, list, off + n, depth, color, P, pool, touched)); vsb::count_launch(); }
+    { VS_CK(launch_pdl(k_rc_integrate, integrate_grid(n), 128, 0, s, nullptr, nullptr, t->e, list, off + n, depth, color, P, pool, touched, tick)); vsb::count_launch(); }
   }
   VS_CK(exclusive_scan<uint8_t>(touched, n, off, work, s));
   { VS_CK(launch_pdl(k_rc_touched_keys, grid_for(n, 256), 256, 0, s, touched, off, t->cap, t->e, touched_keys_out)); vsb::count_launch(); }
