@@ -10,10 +10,9 @@ namespace vsb {
 // predicates on the IEEE bits, independent of FTZ/DAZ:
 //   inside   <=> 0x80000000 <  bits <= 0xFF800000   (tsdf < 0, NaN false)
 //   observed <=> 0 < (int32)bits <= 0x7F800000       (weight > 0, NaN false)
-__device__ __forceinline__ uint32_t inside_bit(uint32_t b) { return (b > 0x80000000u && b <= 0xFF800000u) ? 1u : 0u; }
-__device__ __forceinline__ uint32_t observed_bit(uint32_t b) {
-  return ((int32_t)b > 0 && b <= 0x7F800000u) ? 1u : 0u;
-}
+// each as ONE unsigned range check (wrap-around subtraction)
+__device__ __forceinline__ uint32_t inside_bit(uint32_t b) { return (b - 0x80000001u) < 0x7F800000u ? 1u : 0u; }
+__device__ __forceinline__ uint32_t observed_bit(uint32_t b) { return (b - 1u) < 0x7F800000u ? 1u : 0u; }
 
 constexpr int kFaceBytes = 48;
 

@@ -232,8 +232,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // Sweep index of the CTA's j-th block (>= n: past the end); dyn: the
 // launch uses tickets (large launches, see launch_mc_t).
-__device__ __forceinline__ uint64_t iter_sblk(const McSmem& sm, uint64_t j, bool dyn) {
-  return dyn ? (uint64_t)sm.tk[(j / kLook) & 3] * kLook + (j % kLook) : blockIdx.x + j * (uint64_t)gridDim.x;
+__device__ __forceinline__ uint64_t iter_sblk(const McSmem& sm, uint32_t j, bool dyn) {
+  return dyn ? (uint64_t)sm.tk[(j / kLook) & 3] * kLook + (j % kLook) : blockIdx.x + (uint64_t)j * gridDim.x;
 }
 
 // Neighbour row of block `blk` for corner-block c.
@@ -324,11 +324,11 @@ __device__ __forceinline__ void halo_prefetch(HaloRegs& h, const HaloDesc& d, co
 }
 
 // Neighbour rows of the CTA's j-th block (j counts this CTA's blocks).
-__device__ __forceinline__ const int32_t* nb_of(const McSmem& sm, uint64_t j) {
+__device__ __forceinline__ const int32_t* nb_of(const McSmem& sm, uint32_t j) {
   return sm.nb[(j / kLook) & 1][j % kLook];
 }
 
-__device__ __forceinline__ void issue_centre(McSmem& sm, uint64_t j, const uint8_t* __restrict__ pool) {
+__device__ __forceinline__ void issue_centre(McSmem& sm, uint32_t j, const uint8_t* __restrict__ pool) {
   const int32_t row = nb_of(sm, j)[0];
   if (row < 0) return;
   const int b = (int)(j % kStages);
@@ -402,9 +402,10 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
   if (n_dev) n = min(n, *n_dev);  // a device-produced count (no host sync in the server tick)
   const int t = threadIdx.x;
   const int lane = t & 31, warp = t >> 5;
-  // the CTA's j-th block exists iff its sweep index is < n (a prefix of j)
+  // the CTA's j-th block exists iff its sweep index is < n (a prefix of j);
+  // each iteration evaluates the sweep index of j + 1 once (= j + kAhead)
   constexpr bool dyn = kDyn;
-  auto has = [&](uint64_t j) { return iter_sblk(sm, j, dyn) < n; };
+  static_assert(kAhead == 1, "the loop carries one look-ahead sweep index");
 
   if (t == 0) {
     for (int b = 0; b < kStages; ++b) mbar_init(&sm.mbar[b], 1);
@@ -418,14 +419,14 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
   if (dyn) __syncthreads();
   lookup_batch<kFromKeys, kDyn>(sm, 0, T, keys, nbr, n, 0, tix);
   __syncthreads();
-  if (t == 0)
-    for (uint64_t j = 0; j < kAhead && has(j); ++j) issue_centre(sm, j, pool);
+  uint64_t sb = iter_sblk(sm, 0, dyn);  // sweep index of iteration j
+  if (t == 0 && sb < n) issue_centre(sm, 0, pool);
   uint32_t phases = 0u;  // bit b = parity of mbar[b]
   // halo of the block processed next, loaded one iteration ahead
   const HaloDesc hd = halo_desc();
   HaloRegs hal;
   uint4 fpk = make_uint4(0u, 0u, 0u, 0u);  // kFaces: thread t < 7 holds neighbour t+1's pack, one block ahead
-  if (has(0)) {
+  if (sb < n) {
     if (kFaces) {
       if (t < 7) fpk = load_face(faces, nb_of(sm, 0)[t + 1], t + 1);
     } else {
@@ -433,9 +434,9 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     }
   }
 
-  uint64_t j = 0;
-  for (; has(j); ++j) {
-    const uint64_t blk = sweep_block(iter_sblk(sm, j, dyn), n);
+  uint64_t sb1 = 0;  // sweep index of iteration j + 1
+  for (uint32_t j = 0; sb < n; ++j, sb = sb1) {
+    const uint64_t blk = sweep_block(sb, n);
 #if VSB_MC_DRIFT
     if (t == 0 && blockIdx.x < 4096) {
       const int m = j == 64 ? 0 : j == 256 ? 1 : j == 640 ? 2 : j == 1024 ? 3 : -1;
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     const int32_t* nbc = nb_of(sm, j);
     const int32_t centre = nbc[0];
     // the next lookup batch must be ready before block j + kAhead is issued
-    if (slot == kLook - kAhead && (dyn || has(j + kAhead)))
+    if (slot == kLook - kAhead && (dyn || blockIdx.x + (uint64_t)(j + kAhead) * gridDim.x < n))
       lookup_batch<kFromKeys, kDyn>(sm, (int)(((j / kLook) + 1) & 1), T, keys, nbr, n, (j / kLook + 1) * kLook, tix);
     if (kFaces) {
       if (t < 7) sm.pk[s][t] = fpk;  // every grid row is then written whole: no zeroing, no atomics
@@ -459,12 +460,13 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
       }
     }
     __syncthreads();  // (A) lookups + packs ready, grids zeroed, buf[(j+kAhead)%kStages] no longer read
-    if (t == 0 && has(j + kAhead)) issue_centre(sm, j + kAhead, pool);
+    sb1 = iter_sblk(sm, j + 1, dyn);  // the next batch's ticket is visible by now
+    if (t == 0 && sb1 < n) issue_centre(sm, j + kAhead, pool);
     const int64_t orow = out_rows ? (int64_t)__ldg(out_rows + blk) : (int64_t)blk;  // < 0: no output row
     uint32_t* mc_blk = mc_out && orow >= 0 ? mc_out + (uint64_t)orow * VS_BLOCK_VOXELS : nullptr;
     int8_t* q_blk = q_out && orow >= 0 ? q_out + (uint64_t)orow * VS_BLOCK_VOXELS : nullptr;
     const HaloRegs cur = hal;
-    if (has(j + 1)) {
+    if (sb1 < n) {
       if (kFaces) {
         if (t < 7) fpk = load_face(faces, nb_of(sm, j + 1)[t + 1], t + 1);
       } else {
