@@ -234,6 +234,27 @@ __global__ void __launch_bounds__(kFanThreads) k_multi_fan_small(const __grid_co
 // Three launches and two grid-wide dependencies per tick become one launch.
 // The fan-out keys are distinct (they come out of the dedup), so the
 // created-flag fixup never resolves a duplicate across CTAs.
+// VSB_TICK_PROF (measurement build): globaltimer at the phase boundaries of
+// every CTA of k_stream_tick, read back by vs_tick_prof_read
+#ifndef VSB_TICK_PROF
+#define VSB_TICK_PROF 0
+#endif
+#if VSB_TICK_PROF
+__device__ unsigned long long g_tick_prof[8][256];
+#define TICK_MARK(m)                                                              \
+  do {                                                                            \
+    if (threadIdx.x == 0 && blockIdx.x < 256) {                                   \
+      unsigned long long v_;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v_));                      \
+      g_tick_prof[m][blockIdx.x] = v_;                                            \
+    }                                                                             \
+  } while (0)
+#else
+#define TICK_MARK(m) \
+  do {               \
+  } while (0)
+#endif
+
 constexpr int kTickThreads = 1024;
 constexpr int kTickCtas = 4;
 constexpr uint32_t kTickMaxU = 512;
@@ -276,6 +297,7 @@ __global__ void __cluster_dims__(kTickCtas, 1, 1) __launch_bounds__(kTickThreads
                   uint32_t max_n, int32_t* __restrict__ aff_out, uint64_t* __restrict__ n_aff,
                   uint64_t* __restrict__ n_created, int32_t* __restrict__ keys_out, uint64_t* __restrict__ n_out) {
   pdl_wait();
+  TICK_MARK(0);
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ int32_t dsm[];
@@ -357,6 +379,7 @@ __global__ void __cluster_dims__(kTickCtas, 1, 1) __launch_bounds__(kTickThreads
     if (t == 0 && n_aff) *n_aff = n;
   }
 
+  TICK_MARK(1);  // dedup done
   // ---- 2. fan-out: CTA `rank` inserts key i = 1024 rank + t
   const uint32_t i = rank * kTickThreads + t;
   const uint64_t tail = *F.tail[c];  // read by every CTA before the cluster barrier below
@@ -369,6 +392,7 @@ __global__ void __cluster_dims__(kTickCtas, 1, 1) __launch_bounds__(kTickThreads
     // resolution cannot trigger)
     if (cr) atomicAnd(&T.e[r.pos].meta, ~kFresh);
   }
+  TICK_MARK(2);  // this thread-0's insert done
   uint32_t local_total;
   const uint32_t lrank = block_exclusive_scan(cr, wsum, &local_total);
   if (t == 0) chunk_cnt = local_total;
@@ -389,6 +413,7 @@ __global__ void __cluster_dims__(kTickCtas, 1, 1) __launch_bounds__(kTickThreads
   }
   int delta = t == 0 ? (int)local_total : 0;
   cluster.sync();  // chunk_cnt is reused below
+  TICK_MARK(3);  // FIFO append done
 
   // ---- 3. extract_random(max_n): rotating start (k_multi_extract's seed mix)
   const uint32_t cap = T.n + T.excess;
@@ -458,6 +483,7 @@ __global__ void __cluster_dims__(kTickCtas, 1, 1) __launch_bounds__(kTickThreads
   const uint64_t mn = found < max_n ? found : max_n;
   __threadfence();
   cluster.sync();  // keys_out complete (written by the whole cluster) before the removals
+  TICK_MARK(4);  // extraction scan done
   for (uint64_t j = (uint64_t)rank * kTickThreads + t; j < mn; j += (uint64_t)kTickCtas * kTickThreads) {
     const int32_t p = erase_key(T, out[3 * j], out[3 * j + 1], out[3 * j + 2]);
     if (p >= 0) {
@@ -467,6 +493,10 @@ __global__ void __cluster_dims__(kTickCtas, 1, 1) __launch_bounds__(kTickThreads
   }
   add_size_cta(T, delta);
   if (rank == 0 && t == 0) n_out[c] = mn;
+#if VSB_TICK_PROF
+  __syncthreads();
+  TICK_MARK(5);  // removals done
+#endif
 }
 
 // Frustum-AABB visibility of a block (server.py:375-387): every plane
@@ -1319,3 +1349,10 @@ vs_status vs_server_tick(vs_table* tsdf_map, vs_table* mc_map, vs_table* dedup_s
 }
 
 }  // extern "C"
+
+#if VSB_TICK_PROF
+// measurement build only: the phase timestamps (8 x 256 u64)
+extern "C" int vs_tick_prof_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vsb::g_tick_prof, sizeof(vsb::g_tick_prof)) == cudaSuccess ? 0 : 1;
+}
+#endif
