@@ -43,6 +43,9 @@ constexpr int kOpBlock = VSB_HASH_BLOCK;  // threads per CTA of the op kernels
 
 // ------------------------------------------------------- launch accounting
 
+#ifndef VSB_PROF_RESERVE
+#define VSB_PROF_RESERVE 8192
+#endif
 static std::atomic<uint64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
@@ -632,6 +635,15 @@ vs_status vs_profile_begin(void) {
     g_ev_pool.push_back(r.b);
   }
   g_prof_recs.clear();
+#if VSB_PROF_RESERVE
+  // event creation inside a timed region (~2 per profiled launch) costs host
+  // time on the launch path: create the region's events up front
+  while (g_ev_pool.size() < (size_t)VSB_PROF_RESERVE) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    g_ev_pool.push_back(e);
+  }
+#endif
   g_prof_on = true;
   g_prof_launch0 = g_launches.load();
   return VS_OK;
