@@ -257,3 +257,39 @@ def test_face_packs_track_row_updates(dev):
         a = encode_blocks(pool, nbr)
         b = encode_blocks(pool, nbr, faces=faces)
         assert all(torch.equal(x, y) for x, y in zip(a, b)), step
+
+
+@pytest.mark.gpu
+def test_ticketed_work_distribution_vs_oracle(dev):
+    """Launches of >= 4 lookup batches per CTA take their blocks from the
+    per-stream ticket counter (mc.cu launch_mc_t); 114k room blocks exercise
+    that path for every encoder variant, twice on one stream (the last CTA
+    re-zeroes the counter) and once on a second stream, against the oracle."""
+    import torch
+
+    from paper_1805_03709_b200 import encode_blocks, encode_keys, face_packs
+
+    keys = workloads.room_block_keys()
+    keys = keys[(keys[:, 0] <= -120) & (keys[:, 2] <= -120)]
+    assert len(keys) > 148 * 10 * 16 * 4  # above the ticket threshold of a full grid
+    kt = torch.from_numpy(keys).to(dev)
+    rows = workloads.room_tsdf_rows(kt)
+    t, pool = table_with_pool(keys, rows.cpu().numpy(), dev, n=1 << 17, excess=1 << 17)
+    nbr = oracle.neighbor_table(keys, keys)
+    omc, oq, oc = oracle.mc_encode(rows.cpu().numpy(), nbr, threads=8)
+    _, pos = t.find_keys(keys)
+    fp = face_packs(pool, rows=pos)
+    side = torch.cuda.Stream(dev)
+    for run in range(3):
+        with torch.cuda.stream(side if run == 2 else torch.cuda.current_stream(dev)):
+            outs = [encode_keys(t, pool, keys), encode_keys(t, pool, keys, faces=fp),
+                    encode_blocks(pool, torch.from_numpy(np.where(nbr >= 0, pos.cpu().numpy()[np.maximum(nbr, 0)], -1)
+                                                         .astype(np.int32)).to(dev))]
+            mc4, q4, c4, (offs, flat, cells, cur) = encode_keys(t, pool, keys, cells=True)
+        torch.cuda.synchronize()
+        for mc, q, c in outs + [(mc4, q4, c4)]:
+            assert np.array_equal(mc.cpu().numpy(), omc)
+            assert np.array_equal(q.cpu().numpy(), oq)
+            assert np.array_equal(c.cpu().numpy().astype(np.uint32), oc)
+        assert int(cur.item()) == int(oc.sum())
+        check_cells_scatter_back(mc4, c4, offs, flat, cells)
