@@ -331,6 +331,7 @@ __global__ void __cluster_dims__(kTickCtas, 1, 1) __launch_bounds__(kTickThreads
     }
   }
   __syncthreads();
+  TICK_MARK(6);  // expanded keys loaded and staged
 #pragma unroll
   for (int k = 0; k < kTickPer; ++k) {
     const uint32_t j = t * kTickPer + k;
@@ -354,6 +355,7 @@ __global__ void __cluster_dims__(kTickCtas, 1, 1) __launch_bounds__(kTickThreads
     where[k] = h;
   }
   __syncthreads();
+  TICK_MARK(7);  // hash probes done
   uint32_t first = 0, cnt = 0;
 #pragma unroll
   for (int k = 0; k < kTickPer; ++k) {

@@ -30,11 +30,13 @@ for t in range(60):
     times.append(e0.elapsed_time(e1) * 1e3)
     buf = np.zeros((8, 256), np.uint64)
     assert lib.vs_tick_prof_read(buf.ctypes.data_as(ctypes.c_void_p)) == 0
-    b = buf[:6, :4 * C].astype(np.int64)
+    b = buf[:8, :4 * C].astype(np.int64)
     t0 = b[0].min()
-    rows.append(np.stack([b[0] - t0, b[1] - b[0], b[2] - b[1], b[3] - b[2], b[4] - b[3], b[5] - b[4], b[5] - t0]))
+    rows.append(np.stack([b[0] - t0, b[1] - b[0], b[2] - b[1], b[3] - b[2], b[4] - b[3], b[5] - b[4], b[5] - t0,
+                          b[6] - b[0], b[7] - b[6], b[1] - b[7]]))
 r = np.stack(rows) / 1e3  # ticks x 7 x CTAs, us
-names = ["start skew", "dedup", "insert (thread 0)", "scan+append", "extract scan", "removals", "end (from first start)"]
+names = ["start skew", "dedup", "insert (thread 0)", "scan+append", "extract scan", "removals", "end (from first start)",
+         "dedup: load+stage", "dedup: hash probes", "dedup: flags+scan+compact"]
 out = {"event_us_median": round(float(np.median(times)), 1)}
 for i, nm in enumerate(names):
     out[nm] = {"median": round(float(np.median(r[:, i])), 2), "p90": round(float(np.percentile(r[:, i], 90)), 2),
