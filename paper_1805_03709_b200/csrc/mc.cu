@@ -689,16 +689,22 @@ struct McOut {
 // One zeroed ticket counter per (device, stream), kept for the process:
 // launches on one stream run in order and the kernel's last CTA re-zeroes
 // the counter, so it needs no memset per launch; launches on different
-// streams never share one.  Allocated in chunks of 256 on first use.
+// streams never share one.  Allocated in chunks of 256 on first use (a
+// synchronous cudaMalloc: make the first large encode on a stream outside
+// any graph capture).
 static McTickets* stream_tickets(cudaStream_t s) {
   static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, McTickets*> slots;
+  static std::map<std::pair<int, unsigned long long>, McTickets*> slots;
   static McTickets* chunk = nullptr;
   static int chunk_dev = -1, chunk_used = 256;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  // keyed by the stream's unique id, not its handle: cudaStreamPerThread is
+  // one handle for a different stream on every host thread
+  unsigned long long sid = 0;
+  if (cudaStreamGetId(s, &sid) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> lk(mu);
-  auto it = slots.find({dev, s});
+  auto it = slots.find({dev, sid});
   if (it != slots.end()) return it->second;
   if (chunk_used == 256 || chunk_dev != dev) {
     McTickets* c = nullptr;
@@ -707,7 +713,7 @@ static McTickets* stream_tickets(cudaStream_t s) {
     chunk = c, chunk_dev = dev, chunk_used = 0;
   }
   McTickets* t = chunk + chunk_used++;
-  slots[{dev, s}] = t;
+  slots[{dev, sid}] = t;
   return t;
 }
 
