@@ -450,17 +450,22 @@ def run_config1(args, dev):
     for _ in range(20):  # settle clocks / allocator (the steps are ~0.15 ms each)
         step(dk, dp)
     steps = 200
-    res = []
+    # keep only the last steps' outputs: holding all 200 steps' result
+    # tensors (~2 MB each) made the caching allocator cudaMalloc new segments
+    # inside the timed loop (synchronous, ms each: 0.6-4.8 ms steps)
+    from collections import deque
+
+    res = deque(maxlen=3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    with _lib.Profile() as prof:
+    with _lib.Profile(events=False) as prof:
         e0.record()
         for _ in range(steps):
             res.append(step(dk, dp))
         e1.record()
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    ok &= all(check(*r) for r in res[-3:])
+    ok &= all(check(*r) for r in res)
     ok &= s.approx_size() == 0
     # e2e: pinned host keys in, the three flag vectors out, every step
     hk, hp = torch.from_numpy(keys).pin_memory(), torch.from_numpy(probe).pin_memory()
@@ -885,7 +890,7 @@ def run_stream(args, dev):
     time.sleep(0.12)
     t0 = time.perf_counter()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(ticks + 1)]
-    with _lib.Profile() as prof:
+    with _lib.Profile(events=False) as prof:
         for t in range(1, ticks + 1):
             evs[t - 1].record()
             tick(t)
@@ -1053,7 +1058,7 @@ def run_server(args, dev):
     time.sleep(0.12)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     h0 = time.perf_counter()
-    with _lib.Profile() as prof:
+    with _lib.Profile(events=False) as prof:
         e0.record()
         for t in range(3, 3 + T):
             core.on_tsdf_batch(upd[t], rows[t], sync=False)

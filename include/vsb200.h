@@ -64,6 +64,9 @@ int32_t vs_abi_version(void);
  * launches issued in between. */
 vs_status vs_profile_begin(void);
 vs_status vs_profile_end(double ms_host[4], uint64_t count_host[4], uint64_t *launches_host);
+/* Kernels this library has launched since it was loaded (no events: for
+ * host-paced timed regions where profiling events would add host work). */
+uint64_t vs_launch_count(void);
 
 /* ---------------------------------------------------------------- hash --- */
 
@@ -304,7 +307,9 @@ vs_status vs_stream_tick(vs_table *const *sets_host, int n_sets, const int32_t *
  * put of the affected keys, recompute of their MC + quantised bytes straight
  * into mc_pool / q_pool at the MC map positions, insert_many into the n_sets
  * client sets with the FIFO append (arrays as vs_stream_insert_many).  A
- * capacity failure is sticky (vs_table_check on either map). */
+ * capacity failure is sticky (vs_table_check on either map).  Calls on one
+ * tsdf_map must be stream-ordered (they mutate it); the call's scratch is
+ * kept on tsdf_map between calls (grow-only, freed by vs_table_destroy). */
 vs_status vs_server_tick(vs_table *tsdf_map, vs_table *mc_map, vs_table *dedup_scratch,
                          const int32_t *keys, const uint8_t *rows, uint64_t u,
                          uint8_t *tsdf_pool, uint8_t *tsdf_faces, uint8_t *mc_pool, int8_t *q_pool,

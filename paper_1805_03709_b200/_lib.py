@@ -50,6 +50,7 @@ SIGNATURES: dict[str, tuple] = {
     "vs_last_error": (ctypes.c_char_p, []),
     "vs_abi_version": (_i32, []),
     "vs_profile_begin": (_i32, []),
+    "vs_launch_count": (ctypes.c_uint64, []),
     "vs_profile_end": (_i32, [ctypes.POINTER(ctypes.c_double * 4), ctypes.POINTER(ctypes.c_uint64 * 4), _pu64]),
     "vs_hash_keys": (_i32, [_vp, _u64, _u32, _vp, _vp]),
     "vs_table_create": (_i32, [_u64, _u64, ctypes.c_int, ctypes.POINTER(_vp)]),
@@ -183,11 +184,24 @@ class Profile:
 
     TAGS = ("hash", "mc", "stream", "other")
 
+    def __init__(self, events: bool = True):
+        # events=False: count launches only (no per-launch event records on
+        # the host path of a host-paced timed region)
+        self.events = events
+
     def __enter__(self):
-        check(load().vs_profile_begin())
+        if self.events:
+            check(load().vs_profile_begin())
+        else:
+            self._n0 = int(load().vs_launch_count())
         return self
 
     def __exit__(self, *exc):
+        if not self.events:
+            self.ms = {t: 0.0 for t in self.TAGS}
+            self.count = {t: 0 for t in self.TAGS}
+            self.launches = int(load().vs_launch_count()) - self._n0
+            return False
         ms = (ctypes.c_double * 4)()
         cnt = (ctypes.c_uint64 * 4)()
         launches = ctypes.c_uint64()

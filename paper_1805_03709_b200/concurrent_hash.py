@@ -114,6 +114,12 @@ def _as_keys(keys, device):
     return t.contiguous()
 
 
+# bumped whenever any table records a launch (_HashCore._done, server._mark_done):
+# a caller that recorded it right after its own launches knows, while it is
+# unchanged, that no table saw a launch since (stream-ordering fast paths)
+LAUNCH_GEN = [0]
+
+
 class _HashCore:
     """One GPU table (bucket region + excess region), shared by set and map."""
 
@@ -177,6 +183,7 @@ class _HashCore:
     def _done(self, s) -> None:
         self._last_stream = s
         self._last_sid = s.cuda_stream
+        LAUNCH_GEN[0] += 1
 
     def _keys(self, keys):
         return _as_keys(keys, self.device)

@@ -628,6 +628,8 @@ extern "C" {
 const char* vs_last_error(void) { return g_last_error.c_str(); }
 int32_t vs_abi_version(void) { return 2; }  // 2: faces argument of the MC encoders, n_dev of vs_stream_insert_many
 
+uint64_t vs_launch_count(void) { return g_launches.load(); }
+
 vs_status vs_profile_begin(void) {
   std::lock_guard<std::mutex> g(g_prof_mu);
   for (auto& r : g_prof_recs) {
@@ -772,6 +774,7 @@ vs_status vs_table_destroy(vs_table* t) {
   if (t->side) cudaStreamDestroy(t->side);
   if (t->ev_fork) cudaEventDestroy(t->ev_fork);
   if (t->ev_join) cudaEventDestroy(t->ev_join);
+  if (t->tick_mem) cudaFree(t->tick_mem);
   delete t;
   return VS_OK;
 }

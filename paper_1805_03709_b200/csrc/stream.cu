@@ -1132,15 +1132,17 @@ vs_status vs_stream_extract_visible(vs_table* const* sets_host, int n_sets, uint
 }
 
 static vs_status tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows, uint64_t n, uint8_t* pool,
-                          int32_t* index, uint8_t* faces, vs_stream_t stream);
+                          int32_t* index, uint8_t* faces, vs_stream_t stream, uint8_t* created_scratch = nullptr);
 
 vs_status vs_tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows, uint64_t n, uint8_t* pool,
                       int32_t* index, vs_stream_t stream) {
   return tsdf_put(t, keys, rows, n, pool, index, nullptr, stream);
 }
 
+// created_scratch (optional, n bytes): the insert's created flags go there
+// instead of a stream-ordered allocation
 static vs_status tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows, uint64_t n, uint8_t* pool,
-                          int32_t* index, uint8_t* faces, vs_stream_t stream) {
+                          int32_t* index, uint8_t* faces, vs_stream_t stream, uint8_t* created_scratch) {
   if (!t || !index || (n && (!keys || !rows || !pool))) {
     set_error("table/keys/rows/pool/index must be non-NULL");
     return VS_ERR_INVALID;
@@ -1152,10 +1154,10 @@ static vs_status tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows,
   if (n == 0) return VS_OK;
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
-  uint8_t* created = nullptr;
-  VS_CK(cudaMallocAsync((void**)&created, n, s));
+  uint8_t* created = created_scratch;
+  if (!created) VS_CK(cudaMallocAsync((void**)&created, n, s));
   vs_status st = vs_table_insert(t, keys, n, created, index, stream);
-  cudaFreeAsync(created, s);
+  if (!created_scratch) cudaFreeAsync(created, s);
   if (st != VS_OK) return st;
   const TableView v = t->next_view();
   { k_put_claim<<<grid_for(n, 256), 256, 0, s>>>(v, index, n); vsb::count_launch(); }
@@ -1315,13 +1317,21 @@ vs_status vs_server_tick(vs_table* tsdf_map, vs_table* mc_map, vs_table* dedup_s
   // and of the fan-out [32 x 8u]
   const uint64_t cfan = (uint64_t)(n_sets > kMaxSets ? kMaxSets : n_sets) * m;
   const size_t b_pos = (4 * u + 255) & ~(size_t)255, b_mpos = (4 * m + 255) & ~(size_t)255,
-               b_cr = (m + 255) & ~(size_t)255;
-  char* mem = nullptr;
-  VS_CK(cudaMallocAsync((void**)&mem, b_pos + b_mpos + b_cr + (cfan ? cfan : 1), s));
+               b_cr = (m + 255) & ~(size_t)255, b_tcr = (u + 255) & ~(size_t)255;
+  const size_t need = b_pos + b_mpos + b_cr + b_tcr + (cfan ? cfan : 1);
+  if (tsdf_map->tick_mem_bytes < need) {  // grow-only scratch kept on the map (stream-ordered reuse)
+    if (tsdf_map->tick_mem) VS_CK(cudaFreeAsync(tsdf_map->tick_mem, s));
+    tsdf_map->tick_mem = nullptr;
+    tsdf_map->tick_mem_bytes = 0;
+    VS_CK(cudaMallocAsync((void**)&tsdf_map->tick_mem, need, s));
+    tsdf_map->tick_mem_bytes = need;
+  }
+  char* mem = tsdf_map->tick_mem;
   int32_t* pos = (int32_t*)mem;
   int32_t* mpos = (int32_t*)(mem + b_pos);
   uint8_t* cr = (uint8_t*)(mem + b_pos + b_mpos);
-  uint8_t* cr_fan = (uint8_t*)(mem + b_pos + b_mpos + b_cr);
+  uint8_t* tcr = (uint8_t*)(mem + b_pos + b_mpos + b_cr);
+  uint8_t* cr_fan = (uint8_t*)(mem + b_pos + b_mpos + b_cr + b_tcr);
   // Two independent chains, on two streams: the TSDF put (+ face packs) on
   // `stream`, the affected dedup + MC map put (they need only the keys) on
   // a side stream; they join before the encode, which needs both.
@@ -1335,7 +1345,7 @@ vs_status vs_server_tick(vs_table* tsdf_map, vs_table* mc_map, vs_table* dedup_s
   VS_CK(cudaStreamWaitEvent(side, tsdf_map->ev_fork, 0));
   vs_status st = vs_affected_dedup(dedup_scratch, keys, u, affected_out, n_affected, (vs_stream_t)side);
   if (st == VS_OK) st = vs_table_insert_bounded(mc_map, affected_out, m, n_affected, cr, mpos, (vs_stream_t)side);
-  if (st == VS_OK) st = tsdf_put(tsdf_map, keys, rows, u, tsdf_pool, pos, tsdf_faces, stream);  // + face packs
+  if (st == VS_OK) st = tsdf_put(tsdf_map, keys, rows, u, tsdf_pool, pos, tsdf_faces, stream, tcr);  // + face packs
   VS_CK(cudaEventRecord(tsdf_map->ev_join, side));
   VS_CK(cudaStreamWaitEvent(s, tsdf_map->ev_join, 0));
   if (st == VS_OK)
@@ -1346,7 +1356,6 @@ vs_status vs_server_tick(vs_table* tsdf_map, vs_table* mc_map, vs_table* dedup_s
     st = vs_stream_insert_many(sets_host + g0, C, affected_out, m, n_affected, cr_fan, fifo_keys_host + g0,
                                fifo_cap_host + g0, fifo_tail_host + g0, nullptr, stream);
   }
-  cudaFreeAsync(mem, s);
   return st;
 }
 

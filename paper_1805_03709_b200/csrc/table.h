@@ -31,6 +31,10 @@ struct vs_table {
   // TSDF map's table owns them)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // vs_server_tick's scratch (positions, created flags), grow-only and kept
+  // between ticks: calls on one map are stream-ordered (they mutate it)
+  char* tick_mem = nullptr;
+  size_t tick_mem_bytes = 0;
 
   // view for ONE launch; next_epoch() gives it a fresh claim tag
   vsb::TableView view() const {

@@ -20,7 +20,7 @@ from typing import Callable, Optional, Sequence
 
 from . import _lib
 from ._lib import check, ptr
-from .concurrent_hash import BlockHashSet, BlockKey, CapacityExhausted, _as_keys
+from .concurrent_hash import LAUNCH_GEN as _MARK_GEN, BlockHashSet, BlockKey, CapacityExhausted, _as_keys
 from .mc_encoding import FACE_BYTES, MC_BLOCK_BYTES, Q_BLOCK_BYTES, encode_keys, face_packs, pack_mc_batch
 from .voxel_model import TSDF_BLOCK_BYTES
 
@@ -195,6 +195,7 @@ def _mark_done(tables, s) -> None:
     for t in tables:
         t._last_stream = s
         t._last_sid = sid
+    _MARK_GEN[0] += 1
 
 
 # ctypes argument arrays of a client group, reused while the group's sets and
@@ -402,6 +403,7 @@ class GpuServerCore:
         self.mc_pool = torch.zeros((cap, MC_BLOCK_BYTES), dtype=torch.uint8, device=self.device)
         self.q_pool = torch.zeros((cap, Q_BLOCK_BYTES), dtype=torch.int8, device=self.device)
         self._dedup = BlockHashSet(16 * max_batch, 16 * max_batch, device=self.device)
+        self._tick_cache = None  # on_tsdf_batch(sync=False) per-group launch constants
         self._stream_sizes = (stream_buckets, stream_excess)
         self.retention_s = retention_s
         self.sessions: dict[bytes, dict] = {}
@@ -471,19 +473,40 @@ class GpuServerCore:
             n_dev = out[24 * U:].view(torch.int64)
             streams = self.streams()
             need = 8 * U
-            for st in streams:
-                if st._tail_bound + need - st._head > st._fifo.shape[0]:
-                    st._ensure_fifo(need)
-            a = _group_args(streams) if streams else None
-            tables = [self.tsdf_map, self.mc_map, self._dedup] + (a["tables"] if a else [])
-            s = _order_streams(tables)
-            check(lib.vs_server_tick(self.tsdf_map.handle, self.mc_map.handle, self._dedup.handle, k.data_ptr(),
-                                     rows.data_ptr(), U, self.tsdf_pool.data_ptr(), self.tsdf_faces.data_ptr(),
-                                     self.mc_pool.data_ptr(), self.q_pool.data_ptr(), a["handles"] if a else None,
-                                     len(streams), a["fifos"] if a else None, a["caps"] if a else None,
-                                     a["tails"] if a else None, affected.data_ptr(), n_dev.data_ptr(),
-                                     s.cuda_stream), "server_tick")
-            _mark_done(tables, s)
+            # per-tick constants of this client group (tables, ctypes arrays,
+            # pool pointers, ring capacities), rebuilt when the group, a ring
+            # or a table changes
+            key = (tuple(map(id, streams)), _FIFO_GEN[0], id(self._dedup))
+            tc = self._tick_cache
+            caps = tc["caps"] if tc is not None and tc["key"] == key else [st.fifo_capacity for st in streams]
+            for st, cap in zip(streams, caps):
+                if st._tail_bound + need - st._head > cap:
+                    st._ensure_fifo(need)  # may reallocate the ring (bumps _FIFO_GEN: the key below changes)
+            key = (key[0], _FIFO_GEN[0], key[2])
+            if tc is None or tc["key"] != key:
+                a = _group_args(streams) if streams else None
+                tc = self._tick_cache = {
+                    "key": key, "tables": [self.tsdf_map, self.mc_map, self._dedup] + (a["tables"] if a else []),
+                    "caps": [st.fifo_capacity for st in streams], "mark": None, "sid": None,
+                    "args": (self.tsdf_map.handle, self.mc_map.handle, self._dedup.handle),
+                    "pools": (self.tsdf_pool.data_ptr(), self.tsdf_faces.data_ptr(), self.mc_pool.data_ptr(),
+                              self.q_pool.data_ptr()),
+                    "group": (a["handles"] if a else None, len(streams), a["fifos"] if a else None,
+                              a["caps"] if a else None, a["tails"] if a else None)}
+            cur = torch.cuda.current_stream(dev)
+            sid = cur.cuda_stream
+            if tc["mark"] == _MARK_GEN[0] and tc["sid"] == sid:
+                s = cur  # back to back with this core's previous tick on the same stream: already ordered
+            else:
+                s = _order_streams(tc["tables"])
+            t0, t1, t2 = tc["args"]
+            p0, p1, p2, p3 = tc["pools"]
+            g0, g1, g2, g3, g4 = tc["group"]
+            check(lib.vs_server_tick(t0, t1, t2, k.data_ptr(), rows.data_ptr(), U, p0, p1, p2, p3, g0, g1, g2, g3,
+                                     g4, affected.data_ptr(), n_dev.data_ptr(), sid), "server_tick")
+            if tc["mark"] != _MARK_GEN[0] or tc["sid"] != sid:
+                _mark_done(tc["tables"], s)
+                tc["mark"], tc["sid"] = _MARK_GEN[0], sid
             for st in streams:
                 st._tail_bound += need
             return affected, n_dev
