@@ -1108,3 +1108,16 @@ vs_status vs_table_audit(vs_table* t, uint64_t out_host[6], vs_stream_t stream) 
 }
 
 }  // extern "C"
+
+namespace vsb {
+vs_status table_insert_fresh(vs_table* t, const int32_t* keys, uint64_t n, const uint64_t* n_dev, uint8_t* created,
+                             int32_t* index, cudaStream_t s) {
+  vs_status st = check_batch(t, n);
+  if (st != VS_OK || n == 0) return st;
+  DeviceGuard g(t->device);
+  const TableView v = t->next_view();
+  { VS_CK(launch_pdl(k_insert, grid_for(n, kOpBlock), kOpBlock, 0, s, v, keys, n, n_dev, created, index)); vsb::count_launch(); }
+  VS_CK_LAUNCH("table_insert_fresh");
+  return VS_OK;
+}
+}  // namespace vsb

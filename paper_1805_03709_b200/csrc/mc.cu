@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
                                                           unsigned long long* cursor, uint32_t* __restrict__ offsets,
                                                           uint16_t* __restrict__ cell_flat,
                                                           uint32_t* __restrict__ cell_mc, uint64_t cell_cap,
-                                                          McTickets* tix) {
+                                                          McTickets* tix, Entry* __restrict__ fresh_e) {
   __shared__ McSmem sm;
   if (n_dev) n = min(n, *n_dev);  // a device-produced count (no host sync in the server tick)
   const int t = threadIdx.x;
@@ -463,6 +463,9 @@ __global__ void __launch_bounds__(kMcThreads, kFromKeys ? VSB_MC_MINBLOCKS_KEYS 
     sb1 = iter_sblk(sm, j + 1, dyn);  // the next batch's ticket is visible by now
     if (t == 0 && sb1 < n) issue_centre(sm, j + kAhead, pool);
     const int64_t orow = out_rows ? (int64_t)__ldg(out_rows + blk) : (int64_t)blk;  // < 0: no output row
+    // the MC map entry this block's output row belongs to was created FRESH by
+    // the same tick's post-less insert: settle it here (one word per block)
+    if (fresh_e && t == 0 && orow >= 0) atomicAnd(&fresh_e[orow].meta, ~kFresh);
     uint32_t* mc_blk = mc_out && orow >= 0 ? mc_out + (uint64_t)orow * VS_BLOCK_VOXELS : nullptr;
     int8_t* q_blk = q_out && orow >= 0 ? q_out + (uint64_t)orow * VS_BLOCK_VOXELS : nullptr;
     const HaloRegs cur = hal;
@@ -684,6 +687,7 @@ struct McOut {
   uint16_t* cell_flat;
   uint32_t* cell_mc;
   uint64_t cell_cap;
+  Entry* fresh_e = nullptr;  // clear FRESH on fresh_e[out_rows[i]] (mc_encode_keys_clear)
 };
 
 // One zeroed ticket counter per (device, stream), kept for the process:
@@ -744,7 +748,8 @@ static vs_status launch_mc_t(const TableView& T, const uint8_t* pool, const uint
     ProfScope prof(1, s);
     auto kern = tix ? k_mc_encode<kFromKeys, kFaces, kCells, true> : k_mc_encode<kFromKeys, kFaces, kCells, false>;
     kern<<<(unsigned)g, kMcThreads, 0, s>>>(T, pool, faces, keys, nbr, n, o.n_dev, o.out_rows, (uint32_t*)o.mc, o.q,
-                                            o.counts, o.cursor, o.offsets, o.cell_flat, o.cell_mc, o.cell_cap, tix);
+                                            o.counts, o.cursor, o.offsets, o.cell_flat, o.cell_mc, o.cell_cap, tix,
+                                            o.fresh_e);
     vsb::count_launch();
   }
   VS_CK_LAUNCH("k_mc_encode");
@@ -876,6 +881,20 @@ vs_status vs_mc_compact(const uint8_t* mc, const uint32_t* counts, uint64_t n, u
 }
 
 }  // extern "C"
+
+namespace vsb {
+vs_status mc_encode_keys_clear(const vs_table* t, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
+                               uint64_t n, const uint64_t* n_dev, const int32_t* out_rows, uint8_t* mc_out,
+                               int8_t* q_out, Entry* fresh_e, cudaStream_t s) {
+  if (!t || !out_rows || (n && (!pool || !keys))) {
+    set_error("table/pool/keys/out_rows must be non-NULL");
+    return VS_ERR_INVALID;
+  }
+  DeviceGuard g(t->device);
+  McOut o{n_dev, out_rows, mc_out, q_out, nullptr, nullptr, nullptr, nullptr, nullptr, 0, fresh_e};
+  return launch_mc<true>(t->view(), pool, faces, keys, nullptr, n, o, s);
+}
+}  // namespace vsb
 
 #if VSB_MC_DRIFT
 // measurement build only: copies the drift timestamps (5 x 4096 u64) out

@@ -1038,6 +1038,8 @@ __global__ void k_put_claim(TableView T, const int32_t* __restrict__ pos, uint64
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || pos[i] < 0) return;
   atomicMin(&T.claim[pos[i]], T.tag | (unsigned long long)(0xFFFFFFFFu - (uint32_t)i));
+  // the insert before this launch ran without its post pass: settle FRESH
+  atomicAnd(&T.e[pos[i]].meta, ~kFresh);
 }
 
 __global__ void k_put_rows(TableView T, const int32_t* __restrict__ pos, uint64_t n, const uint4* __restrict__ rows,
@@ -1156,7 +1158,9 @@ static vs_status tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows,
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t* created = created_scratch;
   if (!created) VS_CK(cudaMallocAsync((void**)&created, n, s));
-  vs_status st = vs_table_insert(t, keys, n, created, index, stream);
+  // positions only (a put has no created flag): the insert's post pass is
+  // folded into k_put_claim (FRESH clear); a capacity failure stays sticky
+  vs_status st = table_insert_fresh(t, keys, n, nullptr, created, index, s);
   if (!created_scratch) cudaFreeAsync(created, s);
   if (st != VS_OK) return st;
   const TableView v = t->next_view();
@@ -1344,13 +1348,14 @@ vs_status vs_server_tick(vs_table* tsdf_map, vs_table* mc_map, vs_table* dedup_s
   VS_CK(cudaEventRecord(tsdf_map->ev_fork, s));
   VS_CK(cudaStreamWaitEvent(side, tsdf_map->ev_fork, 0));
   vs_status st = vs_affected_dedup(dedup_scratch, keys, u, affected_out, n_affected, (vs_stream_t)side);
-  if (st == VS_OK) st = vs_table_insert_bounded(mc_map, affected_out, m, n_affected, cr, mpos, (vs_stream_t)side);
+  // mc_map.put positions; FRESH on the created entries is settled by the encode below
+  if (st == VS_OK) st = table_insert_fresh(mc_map, affected_out, m, n_affected, cr, mpos, side);
   if (st == VS_OK) st = tsdf_put(tsdf_map, keys, rows, u, tsdf_pool, pos, tsdf_faces, stream, tcr);  // + face packs
   VS_CK(cudaEventRecord(tsdf_map->ev_join, side));
   VS_CK(cudaStreamWaitEvent(s, tsdf_map->ev_join, 0));
   if (st == VS_OK)
-    st = vs_mc_encode_keys_ex(tsdf_map, tsdf_pool, tsdf_faces, affected_out, m, n_affected, mpos, mc_pool,
-                              q_pool, nullptr, nullptr, nullptr, nullptr, nullptr, 0, stream);
+    st = mc_encode_keys_clear(tsdf_map, tsdf_pool, tsdf_faces, affected_out, m, n_affected, mpos, mc_pool, q_pool,
+                              mc_map->view().e, s);
   for (int g0 = 0; st == VS_OK && g0 < n_sets; g0 += kMaxSets) {
     const int C = n_sets - g0 < kMaxSets ? n_sets - g0 : kMaxSets;
     st = vs_stream_insert_many(sets_host + g0, C, affected_out, m, n_affected, cr_fan, fifo_keys_host + g0,

@@ -103,6 +103,17 @@ void launch_recycle(const vsb::TableView& v, const int32_t* pos, const uint8_t* 
                     const uint64_t* n_dev, uint64_t n, cudaStream_t s);
 vs_status erase_device_count(vs_table* t, const int32_t* keys, const uint64_t* n_dev, uint64_t max_n,
                              cudaStream_t s);
+// Insert launch WITHOUT its post pass: positions final, created flags
+// provisional (in-batch duplicates unresolved), created entries left FRESH --
+// the caller clears FRESH on every returned position in a later launch of
+// the same chain (vs_server_tick / tsdf_put fold it into their next kernel).
+vs_status table_insert_fresh(vs_table* t, const int32_t* keys, uint64_t n, const uint64_t* n_dev,
+                             uint8_t* created, int32_t* index, cudaStream_t s);
+// vs_mc_encode_keys_ex plus: clear FRESH on entry out_rows[i] of `fresh_e`
+// (the MC map whose positions are the output rows) for every encoded block.
+vs_status mc_encode_keys_clear(const vs_table* t, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
+                               uint64_t n, const uint64_t* n_dev, const int32_t* out_rows, uint8_t* mc_out,
+                               int8_t* q_out, Entry* fresh_e, cudaStream_t s);
 
 }  // namespace vsb
 
