@@ -113,9 +113,13 @@ __global__ void k_reset_ctl(TableView T) {
   if (threadIdx.x == 0) T.ctl->error = 0;
 }
 
-__global__ void __launch_bounds__(kOpBlock) k_insert(TableView T, const int32_t* __restrict__ keys, uint64_t n,
-                                                     const uint64_t* __restrict__ n_dev,
-                                                     uint8_t* __restrict__ created, int32_t* __restrict__ index) {
+// kPut: a TSDF put (latest write wins, no created flag): duplicates claim
+// nothing, and every op instead claims its position for the row copy with
+// the highest op index (k_put_rows, same launch tag).
+template <bool kPut>
+__global__ void __launch_bounds__(kOpBlock) k_insert_t(TableView T, const int32_t* __restrict__ keys, uint64_t n,
+                                                       const uint64_t* __restrict__ n_dev,
+                                                       uint8_t* __restrict__ created, int32_t* __restrict__ index) {
   pdl_wait();
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nv = n_dev && *n_dev < n ? *n_dev : n;  // ops past a device count: created 0, index -1
@@ -126,13 +130,15 @@ __global__ void __launch_bounds__(kOpBlock) k_insert(TableView T, const int32_t*
   }
   if (i < nv) {
     const int32_t x = keys[3 * i], y = keys[3 * i + 1], z = keys[3 * i + 2];
-    const InsertResult r = insert_key(T, x, y, z, (int32_t)i);
+    const InsertResult r = insert_key<!kPut>(T, x, y, z, (int32_t)i);
     created[i] = r.created;
     index[i] = r.pos;
     delta = r.created;
+    if (kPut && r.pos >= 0) atomicMin(&T.claim[r.pos], T.tag | (unsigned long long)(0xFFFFFFFFu - (uint32_t)i));
   }
   add_size_cta(T, delta);
 }
+#define k_insert k_insert_t<false>
 
 __global__ void __launch_bounds__(kOpBlock) k_find(TableView T, const int32_t* __restrict__ keys, uint64_t n,
                                                    uint8_t* __restrict__ found, int32_t* __restrict__ index) {
@@ -1110,6 +1116,18 @@ vs_status vs_table_audit(vs_table* t, uint64_t out_host[6], vs_stream_t stream) 
 }  // extern "C"
 
 namespace vsb {
+vs_status table_put_insert(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* created, int32_t* index,
+                           cudaStream_t s, TableView* view_out) {
+  vs_status st = check_batch(t, n);
+  if (st != VS_OK || n == 0) return st;
+  DeviceGuard g(t->device);
+  const TableView v = t->next_view();
+  *view_out = v;
+  { VS_CK(launch_pdl(k_insert_t<true>, grid_for(n, kOpBlock), kOpBlock, 0, s, v, keys, n, (const uint64_t*)nullptr, created, index)); vsb::count_launch(); }
+  VS_CK_LAUNCH("table_put_insert");
+  return VS_OK;
+}
+
 vs_status table_insert_fresh(vs_table* t, const int32_t* keys, uint64_t n, const uint64_t* n_dev, uint8_t* created,
                              int32_t* index, cudaStream_t s) {
   vs_status st = check_batch(t, n);

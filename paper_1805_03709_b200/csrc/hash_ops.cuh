@@ -293,7 +293,7 @@ __device__ __forceinline__ void post_op(const TableView& T, const int32_t* __res
 // for an erase.
 __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_t x, int32_t y, int32_t z, bool ins,
                                                       int32_t op, uint32_t b, uint32_t snap, int32_t fpos = -1,
-                                                      uint32_t fprev = 0, bool mixed = true) {
+                                                      uint32_t fprev = 0, bool mixed = true, bool dup_claims = true) {
   uint32_t* bmeta = &T.e[b].meta;
 #pragma unroll 1
   for (int attempt = 0;; ++attempt) {
@@ -377,7 +377,7 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
     if (ins) {
       if (found >= 0) {  // inserted by another op since the lookup
         unlock_relaxed(bmeta, old);
-        if (fmeta & kFresh) claim_min(T, found, op);
+        if (dup_claims && (fmeta & kFresh)) claim_min(T, found, op);
         return {found, 0};
       }
       if (!(old & kOcc)) {
@@ -447,6 +447,9 @@ __device__ __forceinline__ InsertResult mutate_locked(const TableView& T, int32_
 // the key is absent, the locked claim (mutate_locked).  `pre` (optional):
 // the bucket entry loaded ahead of time (a stale snapshot is harmless: every
 // mutation re-validates under the lock).
+// kDupClaims = false (a put: positions only, no created flag): in-batch
+// duplicates claim nothing, so the caller may use the claim array itself.
+template <bool kDupClaims = true>
 __device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x, int32_t y, int32_t z, int32_t op,
                                                    const int4* pre = nullptr) {
   const uint32_t b = bucket_of(T, x, y, z);
@@ -454,10 +457,11 @@ __device__ __forceinline__ InsertResult insert_key(const TableView& T, int32_t x
   const int4 s0 = pre ? *pre : ld_bucket(T.e + b);
   const int32_t pos = find_pos_from(T, x, y, z, b, s0, &fmeta);
   if (pos >= 0) {
-    if (fmeta & kFresh) claim_min(T, pos, op);
+    if (kDupClaims && (fmeta & kFresh)) claim_min(T, pos, op);
     return {pos, 0};
   }
-  return mutate_locked(T, x, y, z, true, op, b, (uint32_t)s0.w, -1, 0, /*mixed=*/false);  // insert-only launches
+  return mutate_locked(T, x, y, z, true, op, b, (uint32_t)s0.w, -1, 0, /*mixed=*/false,
+                       kDupClaims);  // insert-only launches
 }
 
 // remove (concurrent_hash.py:251-295).  Returns the vacated position or -1.

@@ -1034,13 +1034,6 @@ static vs_status multi_extract(vs_table* const* sets_host, int n_sets, uint64_t 
 // position wins the claim word (epoch-tagged atomicMin of ~op), then the
 // winners copy their 6,144-byte wire rows into the pool (one warp per row,
 // 16-byte vector copies).
-__global__ void k_put_claim(TableView T, const int32_t* __restrict__ pos, uint64_t n) {
-  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || pos[i] < 0) return;
-  atomicMin(&T.claim[pos[i]], T.tag | (unsigned long long)(0xFFFFFFFFu - (uint32_t)i));
-  // the insert before this launch ran without its post pass: settle FRESH
-  atomicAnd(&T.e[pos[i]].meta, ~kFresh);
-}
 
 __global__ void k_put_rows(TableView T, const int32_t* __restrict__ pos, uint64_t n, const uint4* __restrict__ rows,
                            uint4* __restrict__ pool, uint8_t* __restrict__ faces) {
@@ -1048,7 +1041,10 @@ __global__ void k_put_rows(TableView T, const int32_t* __restrict__ pos, uint64_
   const int lane = threadIdx.x & 31;
   if (i >= n) return;
   const int32_t p = pos[i];
-  if (p < 0 || T.claim[p] != (T.tag | (unsigned long long)(0xFFFFFFFFu - (uint32_t)i))) return;
+  if (p < 0) return;
+  // the insert before this launch ran without a post pass: settle FRESH
+  if (lane == 0) atomicAnd(&T.e[p].meta, ~kFresh);
+  if (T.claim[p] != (T.tag | (unsigned long long)(0xFFFFFFFFu - (uint32_t)i))) return;
   const uint4* src = rows + i * (VS_TSDF_BLOCK_BYTES / 16);
   uint4* dst = pool + (uint64_t)p * (VS_TSDF_BLOCK_BYTES / 16);
 #pragma unroll 4
@@ -1158,13 +1154,13 @@ static vs_status tsdf_put(vs_table* t, const int32_t* keys, const uint8_t* rows,
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t* created = created_scratch;
   if (!created) VS_CK(cudaMallocAsync((void**)&created, n, s));
-  // positions only (a put has no created flag): the insert's post pass is
-  // folded into k_put_claim (FRESH clear); a capacity failure stays sticky
-  vs_status st = table_insert_fresh(t, keys, n, nullptr, created, index, s);
+  // ONE insert launch that also claims each position for the latest write
+  // (no created resolution: a put has no created flag), then the row copy,
+  // which settles FRESH (the insert's post pass); capacity failures stay sticky
+  TableView v;
+  vs_status st = table_put_insert(t, keys, n, created, index, s, &v);
   if (!created_scratch) cudaFreeAsync(created, s);
   if (st != VS_OK) return st;
-  const TableView v = t->next_view();
-  { k_put_claim<<<grid_for(n, 256), 256, 0, s>>>(v, index, n); vsb::count_launch(); }
   { k_put_rows<<<grid_for(32 * n, 256), 256, 0, s>>>(v, index, n, (const uint4*)rows, (uint4*)pool, faces); vsb::count_launch(); }
   VS_CK_LAUNCH("vs_tsdf_put");
   return VS_OK;

@@ -109,6 +109,11 @@ vs_status erase_device_count(vs_table* t, const int32_t* keys, const uint64_t* n
 // the same chain (vs_server_tick / tsdf_put fold it into their next kernel).
 vs_status table_insert_fresh(vs_table* t, const int32_t* keys, uint64_t n, const uint64_t* n_dev,
                              uint8_t* created, int32_t* index, cudaStream_t s);
+// The insert of a TSDF put: positions, no created resolution, each op claims
+// its position for the row copy (highest op index wins); the launch's view
+// (its claim tag) goes to *view_out for k_put_rows, which also settles FRESH.
+vs_status table_put_insert(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* created, int32_t* index,
+                           cudaStream_t s, TableView* view_out);
 // vs_mc_encode_keys_ex plus: clear FRESH on entry out_rows[i] of `fresh_e`
 // (the MC map whose positions are the output rows) for every encoded block.
 vs_status mc_encode_keys_clear(const vs_table* t, const uint8_t* pool, const uint8_t* faces, const int32_t* keys,
