@@ -15,6 +15,8 @@ in the reference and is out of scope.
 from __future__ import annotations
 
 import ctypes
+import functools
+import threading
 import time
 from typing import Callable, Optional, Sequence
 
@@ -25,6 +27,25 @@ from .mc_encoding import FACE_BYTES, MC_BLOCK_BYTES, Q_BLOCK_BYTES, encode_keys,
 from .voxel_model import TSDF_BLOCK_BYTES
 
 _MAX_SETS_PER_LAUNCH = 32
+
+
+# One re-entrant lock for the server layer: its calls read and update host
+# bookkeeping (FIFO ring bounds, the tables' last-launch streams, the tick's
+# cached launch constants) around their launches, and the reference's Server
+# calls these from several session threads (transport.py:157-160).  Launches
+# stay asynchronous; only the host-side sequence is serialised, which costs
+# nothing measurable (the calls are host-bound under the GIL anyway,
+# DESIGN.md section 1).
+_LOCK = threading.RLock()
+
+
+def _locked(fn):
+    @functools.wraps(fn)
+    def wrapper(*a, **kw):
+        with _LOCK:
+            return fn(*a, **kw)
+
+    return wrapper
 
 
 class StreamSet:
@@ -104,37 +125,47 @@ class StreamSet:
         self._tail_bound = tail - self._head
         self._head = 0
 
+    @_locked
     def fifo_entries(self) -> list[BlockKey]:
         """The generation-order queue incl. stale entries (tests/inspection)."""
         return [tuple(k) for k in self._ring_view().cpu().tolist()]
 
     # -- reference API ------------------------------------------------------
 
+    @_locked
     def insert(self, key: BlockKey) -> bool:
         return self.insert_many([key]) == 1
 
+    @_locked
     def insert_many(self, keys) -> int:
         return fan_out([self], keys)[0]
 
+    @_locked
     def remove(self, key: BlockKey) -> bool:
         return self._set.remove(key)
 
+    @_locked
     def remove_many(self, keys) -> int:
         erased, _ = self._set.erase_keys(keys)
         return int(erased.sum().item())
 
+    @_locked
     def size(self) -> int:
         return self._set.approx_size()
 
+    @_locked
     def snapshot(self) -> list[BlockKey]:
         return self._set.snapshot_keys()
 
+    @_locked
     def extract_random(self, max_n: int) -> list[BlockKey]:
         return self._set.extract_batch(max_n)
 
+    @_locked
     def extract_matching(self, max_n: int, predicate: Callable) -> list[BlockKey]:
         return self._set.extract_matching(max_n, predicate)
 
+    @_locked
     def extract_visible_first(self, max_n: int, planes, margin: float, block_size: float) -> list[BlockKey]:
         """VISIBLE_FIRST (server.py:339-344): frustum-visible keys first, then
         a random top-up so requests stay full-sized."""
@@ -143,10 +174,12 @@ class StreamSet:
             keys.extend(self.extract_random(max_n - len(keys)))
         return keys
 
+    @_locked
     def extract_ordered(self, max_n: int) -> list[BlockKey]:
         keys = self.extract_ordered_keys(max_n)
         return [tuple(k) for k in keys.cpu().tolist()]
 
+    @_locked
     def extract_ordered_keys(self, max_n: int):
         """Device version of extract_ordered (server.py:86-95) -> int32[m,3]."""
         torch = self._torch
@@ -167,6 +200,7 @@ class StreamSet:
         self._head = int(head.value)
         return out[: int(n_out.value)]
 
+    @_locked
     def clear(self) -> None:
         """Bulk reset (fresh reconnect of a retained client)."""
         self._set.clear()
@@ -229,6 +263,7 @@ def _group_args(group):
     return args
 
 
+@_locked
 def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True, n_dev=None):
     """``for s in sets: s.insert_many(keys)`` in one launch per 32 clients.
 
@@ -281,6 +316,7 @@ def fan_out(sets: Sequence[StreamSet], keys, *, sync: bool = True, n_dev=None):
     return out
 
 
+@_locked
 def extract_random_many(sets: Sequence[StreamSet], max_n: int, seeds: Optional[Sequence[int]] = None, *,
                         n_out=None, keys_out=None):
     """``[s.extract_random(max_n) for s in sets]`` in one launch per 32
@@ -316,6 +352,7 @@ def extract_random_many(sets: Sequence[StreamSet], max_n: int, seeds: Optional[S
     return keys, n
 
 
+@_locked
 def stream_tick(sets: Sequence[StreamSet], updated, max_extract: int, seeds: Optional[Sequence[int]] = None, *,
                 affected_out=None, n_affected=None, keys_out=None, n_out=None, n_created=None):
     """One tick of the server's stream-set path in ONE launch per 32 clients:
@@ -360,6 +397,7 @@ def stream_tick(sets: Sequence[StreamSet], updated, max_extract: int, seeds: Opt
     return aff, na, keys, n
 
 
+@_locked
 def remove_everywhere(sets: Sequence[StreamSet], keys) -> None:
     """Remove keys from every client set (server.py:433-435), one launch per 32."""
     if not sets:
@@ -410,6 +448,7 @@ class GpuServerCore:
 
     # -- sessions (server.py:221-249) ---------------------------------------
 
+    @_locked
     def attach(self, client_id: bytes) -> StreamSet:
         """Returning client within retention keeps its set; otherwise a new
         set filled with every MC key (snapshot order)."""
@@ -424,6 +463,7 @@ class GpuServerCore:
         fan_out([stream], keys)
         return stream
 
+    @_locked
     def detach(self, client_id: bytes) -> None:
         sess = self.sessions.get(client_id)
         if sess is not None:
@@ -435,6 +475,7 @@ class GpuServerCore:
 
     # -- model updates (server.py:299-315) ----------------------------------
 
+    @_locked
     def on_tsdf_batch(self, keys, rows, *, sync: bool = True):
         """Ingest U TSDF blocks (int32[U,3], uint8[U,6144] wire rows) and
         propagate (server.py:299-315): TSDF put (latest write wins), face
@@ -537,6 +578,7 @@ class GpuServerCore:
             fan_out(streams, affected, sync=False)
         return affected
 
+    @_locked
     def check(self) -> None:
         """Raise CapacityExhausted if a sync=False update ran out of entries
         (in either map or in a client's stream set)."""
@@ -545,6 +587,7 @@ class GpuServerCore:
         for st in self.streams():
             st._set.check_capacity()
 
+    @_locked
     def on_reset_blocks(self, keys) -> None:
         """server.py:425-436: remove from both maps and every client set."""
         k = _as_keys(keys, self.device)
@@ -554,6 +597,7 @@ class GpuServerCore:
         _, mpos = self.mc_map.erase_keys(k)
         remove_everywhere(self.streams(), k)
 
+    @_locked
     def on_block_request(self, client_id: bytes, max_blocks: int, strategy: int, planes=None,
                          margin: float = 0.0, block_size: float = 0.04) -> tuple[list, bytes]:
         """server.py:334-363 without the transport: extract by strategy
@@ -577,12 +621,14 @@ class GpuServerCore:
         kept = [kk for kk, f in zip(keys, found.cpu().tolist()) if f]
         return kept, bytes(payload.cpu().numpy().tobytes())
 
+    @_locked
     def mc_payload(self, key: BlockKey) -> Optional[bytes]:
         found, pos = self.mc_map.find_keys([key])
         if not bool(found[0].item()):
             return None
         return bytes(self.mc_pool[int(pos[0].item())].cpu().numpy().tobytes())
 
+    @_locked
     def tsdf_payload(self, key: BlockKey) -> Optional[bytes]:
         found, pos = self.tsdf_map.find_keys([key])
         if not bool(found[0].item()):

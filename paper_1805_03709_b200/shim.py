@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import sys
 from typing import Any
+from . import server as _gserver
 
 _saved: list[tuple[Any, str, Any]] = []
 
@@ -84,6 +85,7 @@ def uninstall() -> None:
         setattr(obj, name, value)
 
 
+@_gserver._locked
 def _on_tsdf_batch(self, batch) -> None:
     """server.py:299-315 with one GPU encode + one fan-out launch per batch.
 
@@ -126,6 +128,7 @@ def _frustum_args(self, req, srv):
     return frustum._planes, frustum.margin, block_size
 
 
+@_gserver._locked
 def _on_block_request(self, sess, req) -> None:
     """server.py:334-363 with the same strategies and effects, but ONE
     batched map lookup for the requested keys (mc_map.get per key is one GPU
@@ -166,6 +169,7 @@ def _on_block_request(self, sess, req) -> None:
         stream.insert_many(keys)
 
 
+@_gserver._locked
 def _on_reset_blocks(self, keys) -> None:
     """server.py:425-436 with the same effects (keys gone from both maps and
     every exploration client's set, DeleteBlocks sent to each client), the

@@ -423,3 +423,66 @@ def test_tsdf_ingest_latest_write_wins(dev):
     core.on_tsdf_batch(keys[:1], rows2)
     assert core.tsdf_payload((2, 2, 2)) == rows2[0].tobytes()
     assert core.tsdf_map.approx_size() == 3
+
+
+def test_server_core_concurrent_session_threads(dev):
+    """The reference Server calls on_tsdf_batch and on_block_request from
+    different session threads (transport.py:157-160).  Ticks on one thread
+    and block requests of two clients on two others, each thread on its own
+    CUDA stream: no exception, every table passes its audit, no capacity
+    error, and what each client received plus what it still holds is exactly
+    the set of MC keys the ticks produced (nothing lost; a key updated again
+    after its delivery is pending again, as in the reference)."""
+    import threading
+
+    import torch
+
+    from paper_1805_03709_b200 import GpuServerCore, workloads
+
+    scene = workloads.room_block_keys()[:40_000]
+    core = GpuServerCore(1 << 17, 1 << 17, stream_buckets=1 << 17, stream_excess=1 << 17, max_batch=1 << 10,
+                         device=dev)
+    ids = [bytes([c]) * 16 for c in range(2)]
+    for cid in ids:
+        core.attach(cid)
+    rng = np.random.default_rng(3)
+    upd = [scene[rng.integers(0, len(scene), 512)] for _ in range(24)]
+    rows = [workloads.room_tsdf_rows(torch.from_numpy(u).to(dev)) for u in upd]
+    got = {cid: [] for cid in ids}
+    errors = []
+
+    def ticks():
+        try:
+            with torch.cuda.stream(torch.cuda.Stream(dev)):
+                for u, r in zip(upd, rows):
+                    core.on_tsdf_batch(u, r, sync=False)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    def requests(cid, strategy):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream(dev)):
+                for _ in range(40):
+                    keys, _ = core.on_block_request(cid, 256, strategy)
+                    got[cid].extend(keys)
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=ticks)] + [threading.Thread(target=requests, args=(cid, s))
+                                             for cid, s in zip(ids, (0, 2))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    core.check()
+    for t in [core.tsdf_map, core.mc_map] + [core.sessions[cid]["stream"]._set for cid in ids]:
+        a = t.audit()
+        assert a["duplicates"] == 0 and a["unreachable_live"] == 0 and a["free_reachable"] == 0, a
+    produced = {tuple(k) for k in core.mc_map.snapshot_keys()}
+    for cid in ids:
+        st = core.sessions[cid]["stream"]
+        sent = {tuple(k) for k in got[cid]}
+        pending = {tuple(k) for k in st.snapshot()}
+        assert sent and pending | sent == produced
