@@ -50,6 +50,13 @@ fp = face_packs(pool, rows=pos)
 mc3, q3, c3 = encode_keys(tt, pool, keys, faces=fp)
 mc4, q4, c4 = encode_blocks(pool, nb, faces=fp)
 assert torch.equal(mc, mc3) and torch.equal(mc, mc4)
+# ticketed work distribution of the encoder (launches of >= 4 lookup batches per CTA)
+rk = workloads.room_block_keys()
+rk = rk[(rk[:, 0] <= -120) & (rk[:, 2] <= -120)]
+rt = BlockHashSet(1 << 17, 1 << 17); _, rpos = rt.insert_keys(rk)
+rpool = torch.zeros((rt.capacity, 6144), dtype=torch.uint8, device=dev)
+rpool[rpos.long()] = workloads.room_tsdf_rows(torch.from_numpy(rk).to(dev))
+encode_keys(rt, rpool, rk); del rpool
 # fan-out bounded by a device count
 fan_out(sets, keys[:300], n_dev=torch.tensor([123], dtype=torch.int64, device=dev))
 # peer-sharded route at world 1 (partition, push, waits, routed apply/post/return)
