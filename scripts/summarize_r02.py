@@ -16,7 +16,7 @@ CAPS = [("apply", "r02_apply", "k_apply (config 2, one 2^22-op mixed batch)"),
         ("mc", "r02_mc", "k_mc_encode<1,0,0> (config 3 full encode, 2,080,160 blocks)"),
         ("mcaux", "r02_mcaux", "k_mc_faces / k_mc_compact (config 3 incremental packs, two-pass compaction)"),
         ("stream", "r02_stream", "config-4 tick kernels: k_dedup_small, k_multi_fan_small, k_multi_extract"),
-        ("server", "r02_server", "SURVEY 3.1 on_tsdf_batch kernels: k_put_rows, k_mc_encode<1,1,0> (faces, out_rows)"),
+        ("server", "r02_server", "SURVEY 3.1 on_tsdf_batch kernels (6 launches per tick): k_dedup_small, k_insert_t (MC map; TSDF put with its latest-write claims), k_put_rows, k_mc_encode<1,1,0,0> (faces, out_rows, FRESH settle), k_multi_fan_small"),
         ("rc", "r02_rc", "RC fusion: k_rc_cull_table, k_rc_integrate"),
         ("shard", "r02_shard", "peer-shard route at world 1, config-5 slice (125M keys, 2^24-op batches, 16 bucket regions): "
                             "k_wpart_count, k_wpart_base, k_wpart_push, k_shard_apply, k_shard_return")]
@@ -57,7 +57,7 @@ def main(src="gpurun_out", tag="r02", only=""):
             continue
         lines = [f"# ncu --set full --clock-control none summary ({tag}): {what}",
                  f"# from {rep}.ncu-rep, command in scripts/gpu_r02_ncu.sh"
-                 + (" (re-captured by scripts/gpu_r02_final2.sh)" if name == "shard" else "")]
+                 + (" (re-captured after the late changes)" if name in ("shard", "server") else "")]
         seen = set()
         for kname, d in raw_all(path):
             lines.append(f"## {kname[:120]}")
