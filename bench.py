@@ -275,7 +275,11 @@ def run_hash(args, dev, rank, world):
     lo, hi = base, base + spec.live
     n_total = args.warmup + args.steps
     batches = []
-    for step in range(n_total + (0 if args.no_e2e else min(args.steps, 20))):
+    # e2e window: 3x the timed steps (up to 60 distinct batches, ~65 ms of
+    # PCIe-bound transfers at config 2), long enough that host-side transients
+    # of a few ms do not swing the figure
+    n_e2e = 0 if args.no_e2e else min(3 * args.steps, 60)
+    for step in range(n_total + n_e2e):
         ids, ops, expect = workloads.mix_batch_ids(spec, step, lo, hi, gen, dev)
         ids = torch.where(ids >= workloads.MISS_BASE, ids + (rank << 50), ids)
         batches.append((workloads.id_to_key_torch(ids), ops, expect))
