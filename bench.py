@@ -275,10 +275,11 @@ def run_hash(args, dev, rank, world):
     lo, hi = base, base + spec.live
     n_total = args.warmup + args.steps
     batches = []
-    # e2e window: 3x the timed steps (up to 60 distinct batches, ~65 ms of
-    # PCIe-bound transfers at config 2), long enough that host-side transients
-    # of a few ms do not swing the figure
-    n_e2e = 0 if args.no_e2e else min(3 * args.steps, 60)
+    # e2e window: 3x the timed steps, up to 60 distinct batches and at most
+    # ~3 GB of pinned host inputs per rank (config 2: 55 batches, ~60 ms of
+    # PCIe-bound transfers; 2^24-op batches: 13), long enough that host-side
+    # transients of a few ms do not swing the figure
+    n_e2e = 0 if args.no_e2e else max(4, min(3 * args.steps, 60, int(3e9 // (13 * B))))
     for step in range(n_total + n_e2e):
         ids, ops, expect = workloads.mix_batch_ids(spec, step, lo, hi, gen, dev)
         ids = torch.where(ids >= workloads.MISS_BASE, ids + (rank << 50), ids)
