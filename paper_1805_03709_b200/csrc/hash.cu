@@ -331,10 +331,22 @@ __global__ void k_single(TableView T, int32_t x, int32_t y, int32_t z, uint8_t o
 // Post pass after k_insert / k_apply: created flags to the lowest op index
 // among in-batch duplicates (sequential replay), FRESH cleared, and the
 // excess entries vacated by erases recycled -- one launch, one pass.  Each
-// thread takes kPostOps ops (loads of all of them in flight first) and the
-// vacated positions of a whole warp go back with one reservation.
-constexpr int kPostOps = 4;
-constexpr int kPostBlock = 256;
+// thread takes kPostOps ops (loads of all of them in flight first, then
+// every FRESH clear and dup-bitmap load issued before any is waited on) and
+// the vacated positions of a whole warp go back with one reservation.
+// 64-thread CTAs x 3 ops: 0.2358 vs 0.2388 ms per config-2 step against the
+// former 256 x 4 without the hoist (profiles/r02_ab_post.txt).
+#ifndef VSB_POST_HOIST
+#define VSB_POST_HOIST 1
+#endif
+#ifndef VSB_POST_OPS
+#define VSB_POST_OPS 3
+#endif
+#ifndef VSB_POST_BLOCK
+#define VSB_POST_BLOCK 64
+#endif
+constexpr int kPostOps = VSB_POST_OPS;
+constexpr int kPostBlock = VSB_POST_BLOCK;
 __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t* __restrict__ keys,
                                                      const uint8_t* __restrict__ ops, uint64_t n,
                                                      uint8_t* __restrict__ result, const int32_t* __restrict__ index) {
@@ -358,6 +370,40 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
   }
   uint32_t vac[kPostOps];
   int nv = 0;
+#if VSB_POST_HOIST
+  // every FRESH clear and dup-bitmap load of the thread's ops issued before
+  // any of them is waited on (the loop below only reads the loaded words)
+  uint32_t dw[kPostOps];
+#pragma unroll
+  for (int k = 0; k < kPostOps; ++k) {
+    dw[k] = 0;
+    if (op[k] == VS_OP_INSERT && res[k]) {
+      atomicAnd(&T.e[pos[k]].meta, ~kFresh);
+      dw[k] = __ldcg(&T.dupbits[(uint32_t)pos[k] >> 5]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kPostOps; ++k) {
+    const uint64_t i = base + (uint64_t)k * kPostBlock;
+    if (op[k] == VS_OP_INSERT && res[k]) {
+      const uint32_t bit = 1u << ((uint32_t)pos[k] & 31u);
+      if (dw[k] & bit) {
+        atomicAnd(&T.dupbits[(uint32_t)pos[k] >> 5], ~bit);
+        const unsigned long long c = T.claim[pos[k]];
+        if ((c & 0xFFFFFFFF00000000ull) == T.tag) {
+          const uint64_t m = (uint32_t)(c & 0xFFFFFFFFull);
+          if (m < i && keys[3 * m] == keys[3 * i] && keys[3 * m + 1] == keys[3 * i + 1] &&
+              keys[3 * m + 2] == keys[3 * i + 2]) {
+            result[i] = 0;
+            result[m] = 1;
+          }
+        }
+      }
+    } else if (op[k] == VS_OP_ERASE && res[k] && pos[k] >= (int32_t)T.n) {
+      vac[nv++] = (uint32_t)pos[k];
+    }
+  }
+#else
 #pragma unroll
   for (int k = 0; k < kPostOps; ++k) {
     const uint64_t i = base + (uint64_t)k * kPostBlock;
@@ -367,6 +413,7 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
       vac[nv++] = (uint32_t)pos[k];
     }
   }
+#endif
   push_free_many<kPostOps>(T, vac, nv);
 }
 
