@@ -12,6 +12,14 @@
 #ifndef VSB_PDL
 #define VSB_PDL 1
 #endif
+// k_apply launched as a programmatic dependent of the previous launch (1),
+// and the post pass releasing its dependents right after its own wait (1).
+#ifndef VSB_PDL_APPLY
+#define VSB_PDL_APPLY 0
+#endif
+#ifndef VSB_POST_TRIGGER
+#define VSB_POST_TRIGGER 0
+#endif
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -209,6 +217,11 @@ constexpr int kOpsPerThread = VSB_HASH_OPS_PER_THREAD;
 __global__ void __launch_bounds__(kOpBlock) k_apply(TableView T, const int32_t* __restrict__ keys,
                                                     const uint8_t* __restrict__ ops, uint64_t n,
                                                     uint8_t* __restrict__ result, int32_t* __restrict__ index) {
+#if VSB_PDL_APPLY
+  // launched as a programmatic dependent of the previous batch's post pass
+  // (its launch overlaps that pass's tail): wait before touching anything
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   const uint64_t base = (uint64_t)blockIdx.x * (kOpBlock * kOpsPerThread) + threadIdx.x;
   int32_t x[kOpsPerThread], y[kOpsPerThread], z[kOpsPerThread];
   uint8_t op[kOpsPerThread];
@@ -266,6 +279,17 @@ static cudaError_t launch_apply(const TableView& v, const int32_t* keys, const u
   attr[0].val.accessPolicyWindow.hitRatio = bytes > carve ? (float)carve / (float)bytes : 1.0f;
   attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
   attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_apply, v, keys, ops, n, result, index);
+#elif VSB_PDL_APPLY
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(apply_grid(n));
+  cfg.blockDim = dim3(kOpBlock);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = n >= (1u << 16);
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_apply, v, keys, ops, n, result, index);
@@ -354,6 +378,9 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
   // launched as a programmatic dependent of the op kernel: everything below
   // reads its results, so wait for its grid to complete and flush
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+#if VSB_POST_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;");
 #endif
   const uint64_t base = (uint64_t)blockIdx.x * (kPostBlock * kPostOps) + threadIdx.x;
   uint8_t op[kPostOps], res[kPostOps];
