@@ -359,9 +359,10 @@ __global__ void k_single(TableView T, int32_t x, int32_t y, int32_t z, uint8_t o
 // every FRESH clear and dup-bitmap load issued before any is waited on) and
 // the vacated positions of a whole warp go back with one reservation.
 // 64-thread CTAs x 3 ops: 0.2358 vs 0.2388 ms per config-2 step against the
-// former 256 x 4 without the hoist (profiles/r02_ab_post.txt).
+// former 256 x 4 without the hoist; with the free-list reservation issued
+// first (VSB_POST_HOIST=2) 0.2347 (profiles/r02_ab_post.txt).
 #ifndef VSB_POST_HOIST
-#define VSB_POST_HOIST 1
+#define VSB_POST_HOIST 2
 #endif
 #ifndef VSB_POST_OPS
 #define VSB_POST_OPS 3
@@ -398,6 +399,14 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
   uint32_t vac[kPostOps];
   int nv = 0;
 #if VSB_POST_HOIST
+#if VSB_POST_HOIST == 2
+  // the vacated positions first: the warp's free-list reservation is in
+  // flight while the FRESH clears and dup-bitmap loads below are issued
+#pragma unroll
+  for (int k = 0; k < kPostOps; ++k)
+    if (op[k] == VS_OP_ERASE && res[k] && pos[k] >= (int32_t)T.n) vac[nv++] = (uint32_t)pos[k];
+  const PushRes pr = push_reserve(T, nv);
+#endif
   // every FRESH clear and dup-bitmap load of the thread's ops issued before
   // any of them is waited on (the loop below only reads the loaded words)
   uint32_t dw[kPostOps];
@@ -409,6 +418,9 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
       dw[k] = __ldcg(&T.dupbits[(uint32_t)pos[k] >> 5]);
     }
   }
+#if VSB_POST_HOIST == 2
+  push_commit<kPostOps>(T, pr, vac, nv);
+#endif
 #pragma unroll
   for (int k = 0; k < kPostOps; ++k) {
     const uint64_t i = base + (uint64_t)k * kPostBlock;
@@ -426,7 +438,7 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
           }
         }
       }
-    } else if (op[k] == VS_OP_ERASE && res[k] && pos[k] >= (int32_t)T.n) {
+    } else if (VSB_POST_HOIST != 2 && op[k] == VS_OP_ERASE && res[k] && pos[k] >= (int32_t)T.n) {
       vac[nv++] = (uint32_t)pos[k];
     }
   }
@@ -441,7 +453,7 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
     }
   }
 #endif
-  push_free_many<kPostOps>(T, vac, nv);
+  if (VSB_POST_HOIST != 2) push_free_many<kPostOps>(T, vac, nv);
 }
 
 // k_post as a programmatic dependent launch (VSB_PDL): its launch and CTA

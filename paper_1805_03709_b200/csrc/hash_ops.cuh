@@ -188,6 +188,46 @@ __device__ __forceinline__ void push_free_many(const TableView& T, const uint32_
     if (j < nv) push_free(T, v[j]);
 }
 
+// push_free_many split in two, so the caller can issue other memory work
+// while lane 0's reservation atomic is in flight: push_reserve scans the
+// warp's counts and issues the atomic, push_commit waits for it and stores.
+struct PushRes {
+  uint32_t incl, total, s;
+  long long old;  // lane 0: the reservation's old top (not yet waited on)
+};
+__device__ __forceinline__ PushRes push_reserve(const TableView& T, int nv) {
+  const uint32_t lane = lane_id();
+  PushRes r;
+  r.incl = (uint32_t)nv;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, r.incl, d);
+    if ((int)lane >= d) r.incl += y;
+  }
+  r.total = __shfl_sync(0xFFFFFFFFu, r.incl, 31);
+  r.s = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % T.stripes;
+  r.old = 0;
+  if (r.total && lane == 0)
+    r.old = (long long)atomicAdd((unsigned long long*)(T.tops + (size_t)r.s * kTopStride), (unsigned long long)r.total);
+  return r;
+}
+template <int kMaxPush>
+__device__ __forceinline__ void push_commit(const TableView& T, PushRes r, const uint32_t (&v)[kMaxPush], int nv) {
+  if (r.total == 0) return;
+  const long long old = __shfl_sync(0xFFFFFFFFu, r.old, 0);
+  if (old + (long long)r.total <= (long long)T.stripe_cap) {
+    uint32_t* dst = T.free_stack + (size_t)r.s * T.stripe_cap + (size_t)old + (r.incl - (uint32_t)nv);
+#pragma unroll
+    for (int j = 0; j < kMaxPush; ++j)
+      if (j < nv) dst[j] = v[j];
+    return;
+  }
+  if (lane_id() == 0) atomicAdd((unsigned long long*)(T.tops + (size_t)r.s * kTopStride), (unsigned long long)(-(long long)r.total));
+#pragma unroll
+  for (int j = 0; j < kMaxPush; ++j)
+    if (j < nv) push_free(T, v[j]);
+}
+
 // Lock-free retrieval (_find + _scan_chain, concurrent_hash.py:127-157).
 // Returns the position or -1; *meta_out = meta of the matching entry.
 // ... starting from an already loaded bucket entry `s` (lets a thread
