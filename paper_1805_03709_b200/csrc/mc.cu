@@ -153,7 +153,14 @@ __device__ __forceinline__ void halo_item(int i, int& c, int& flat, int& row, in
   }
 }
 
-constexpr int kLook = kMcThreads / 8;  // blocks per batched neighbour lookup (16)
+// Blocks per batched neighbour lookup = blocks per work ticket (16: one find
+// per thread; VSB_MC_LOOK = 8 or 4 leaves threads idle in the lookup but
+// shortens a ticket, so consecutive keys are encoded closer in time).
+#ifndef VSB_MC_LOOK
+#define VSB_MC_LOOK 16
+#endif
+constexpr int kLook = VSB_MC_LOOK;
+static_assert(kLook * 8 <= kMcThreads && (kLook & (kLook - 1)) == 0, "one find per thread");
 #ifndef VSB_MC_STAGES
 #define VSB_MC_STAGES 2
 #endif
@@ -264,8 +271,10 @@ __device__ __forceinline__ void lookup_batch(McSmem& sm, int buf, const TableVie
                                              const int32_t* nbr, uint64_t n, uint64_t j0, McTickets* tix) {
   const int t = threadIdx.x;
   const int slot = t >> 3, c = t & 7;
-  const uint64_t sblk = iter_sblk(sm, j0 + slot, kDyn);  // sweep index
-  sm.nb[buf][slot][c] = sblk < n ? load_nbr<kFromKeys>(T, keys, nbr, sweep_block(sblk, n), c) : -1;
+  if (slot < kLook) {
+    const uint64_t sblk = iter_sblk(sm, j0 + slot, kDyn);  // sweep index
+    sm.nb[buf][slot][c] = sblk < n ? load_nbr<kFromKeys>(T, keys, nbr, sweep_block(sblk, n), c) : -1;
+  }
   // the ticket of the batch after next (visible after this iteration's barriers)
   if (kDyn && t == 0) sm.tk[(j0 / kLook + 2) & 3] = atomicAdd(&tix->next, 1ull);
 }
