@@ -46,6 +46,15 @@ struct Ctl {
 #define VSB_HASH_STRIPES 128
 #endif
 constexpr uint32_t kMaxStripes = VSB_HASH_STRIPES;  // free-list stripes
+// Fewer stripes for small excess regions: at least kStripeMinEntries entries
+// per stripe, down to kMinStripes (a table that erases its whole set pushes
+// into full stripes less often: config 1 0.117 -> 0.080 ms per step at 32
+// stripes, config 2 unchanged at 128; profiles/r02_ab_stripes.txt).
+#ifndef VSB_HASH_STRIPE_MIN_ENTRIES
+#define VSB_HASH_STRIPE_MIN_ENTRIES 4096
+#endif
+constexpr uint32_t kStripeMinEntries = VSB_HASH_STRIPE_MIN_ENTRIES;
+constexpr uint32_t kMinStripes = 32;
 constexpr uint32_t kTopStride = 32;   // long longs between stripe tops (256 B)
 
 // By-value view passed to kernels.

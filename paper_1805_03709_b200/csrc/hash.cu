@@ -817,7 +817,11 @@ vs_status vs_table_create(uint64_t bucket_count, uint64_t excess_capacity, int d
   t->n = (uint32_t)bucket_count;
   t->excess = (uint32_t)excess_capacity;
   t->cap = t->n + t->excess;
-  t->stripes = t->excess < kMaxStripes ? t->excess : kMaxStripes;
+  {
+    uint32_t st = t->excess / kStripeMinEntries;
+    st = st < kMinStripes ? kMinStripes : st > kMaxStripes ? kMaxStripes : st;
+    t->stripes = t->excess < st ? t->excess : st;
+  }
   t->stripe_cap = (t->excess + t->stripes - 1) / t->stripes;
   t->magic = fastmod_magic(t->n);
   t->nchunks = (t->cap + kChunk - 1) / kChunk;
