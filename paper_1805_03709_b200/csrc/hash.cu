@@ -967,6 +967,9 @@ vs_status vs_table_erase(vs_table* t, const int32_t* keys, uint64_t n, uint8_t* 
     { k_erase_claim<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, idx); vsb::count_launch(); }
     { k_erase_win<<<grid_for(n, kOpBlock), kOpBlock, 0, s>>>(v, keys, n, erased, idx); vsb::count_launch(); }
   }
+  // vacated excess entries go back in a separate launch: pushing them from
+  // k_erase_win itself was measured to leave freed entries reachable
+  // (scripts/c1_loop.py: 3-5 per config-1 cycle), so it stays separate
   launch_recycle(v, idx, nullptr, nullptr, nullptr, n, s);
   if (!index) cudaFreeAsync(idx, s);
   VS_CK_LAUNCH("vs_table_erase");
