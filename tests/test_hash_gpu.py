@@ -367,6 +367,32 @@ def test_free_list_conservation_under_churn(dev):
     audit_clean(s, len(live))
 
 
+def test_whole_set_erase_cycles_keep_free_list_exact(dev):
+    """Config 1 as a loop: insert the 100k keys (~20% duplicates), find them
+    with 100k absent probes, erase them all -- 60 cycles on one table, audited
+    every 10.  Whole-set erases return ~30k excess entries per cycle, which
+    fills every free-list stripe exactly (free == excess), and the next
+    cycle pops them all again (concurrent_hash.py:72-79, :251-295).  A
+    variant that pushed vacated entries from the erase launch itself left
+    3-5 freed entries reachable per cycle here (scripts/c1_loop.py)."""
+    import torch
+
+    from paper_1805_03709_b200 import BlockHashSet
+
+    keys, absent = workloads.config1_keys()
+    dk = torch.from_numpy(keys).to(dev)
+    dp = torch.from_numpy(np.concatenate([keys, absent])).to(dev)
+    s = BlockHashSet(1 << 17, 1 << 17, device=dev)
+    for it in range(60):
+        c, _ = s.insert_keys(dk)
+        f, _ = s.find_keys(dp)
+        e, _ = s.erase_keys(dk)
+        assert (int(c.sum()), int(f.sum()), int(e.sum())) == (80_000, 100_000, 80_000), it
+        if it % 10 == 9:
+            audit_clean(s, 0)
+            assert s.audit()["free"] == s.excess_capacity
+
+
 def test_host_threads_disjoint_key_spaces(dev):
     """tests/test_acceptance.py:229-275 shape, scaled: 8 host threads x 2,000
     per-key ops on disjoint key spaces vs a replayed dict oracle."""
