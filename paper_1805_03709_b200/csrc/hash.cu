@@ -360,18 +360,23 @@ __global__ void k_single(TableView T, int32_t x, int32_t y, int32_t z, uint8_t o
 // the vacated positions of a whole warp go back with one reservation.
 // 64-thread CTAs x 3 ops: 0.2358 vs 0.2388 ms per config-2 step against the
 // former 256 x 4 without the hoist; with the free-list reservation issued
-// first (VSB_POST_HOIST=2) 0.2347 (profiles/r02_ab_post.txt).
+// first (VSB_POST_HOIST=2) 0.2347; 4 consecutive ops per thread through
+// three vector loads (VSB_POST_VEC, aligned arrays) 0.2341 (profiles/r02_ab_post.txt).
+#ifndef VSB_POST_VEC
+#define VSB_POST_VEC 1
+#endif
 #ifndef VSB_POST_HOIST
 #define VSB_POST_HOIST 2
 #endif
 #ifndef VSB_POST_OPS
-#define VSB_POST_OPS 3
+#define VSB_POST_OPS 4
 #endif
 #ifndef VSB_POST_BLOCK
 #define VSB_POST_BLOCK 64
 #endif
 constexpr int kPostOps = VSB_POST_OPS;
 constexpr int kPostBlock = VSB_POST_BLOCK;
+template <bool kVec>
 __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t* __restrict__ keys,
                                                      const uint8_t* __restrict__ ops, uint64_t n,
                                                      uint8_t* __restrict__ result, const int32_t* __restrict__ index) {
@@ -383,17 +388,36 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
 #if VSB_POST_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;");
 #endif
-  const uint64_t base = (uint64_t)blockIdx.x * (kPostBlock * kPostOps) + threadIdx.x;
+  // kVec (4 ops per thread, 4-aligned op/result and 16-aligned index
+  // arrays): a thread's ops are CONSECUTIVE and come in with three vector
+  // loads; otherwise they sit kPostBlock apart (scalar, coalesced per k)
+  const uint64_t base = kVec ? ((uint64_t)blockIdx.x * kPostBlock + threadIdx.x) * kPostOps
+                             : (uint64_t)blockIdx.x * (kPostBlock * kPostOps) + threadIdx.x;
+  constexpr uint64_t kStep = kVec ? 1 : kPostBlock;
   uint8_t op[kPostOps], res[kPostOps];
   int32_t pos[kPostOps];
+  if (kVec && base + kPostOps <= n) {
+    static_assert(!kVec || kPostOps == 4, "vector post loads take 4 ops per thread");
+    const uint32_t ow = ops ? *(const uint32_t*)(ops + base) : 0u;  // VS_OP_INSERT == 0
+    const uint32_t rw = *(const uint32_t*)(result + base);
+    const int4 pw = *(const int4*)(index + base);
+    const int32_t pv[4] = {pw.x, pw.y, pw.z, pw.w};
 #pragma unroll
-  for (int k = 0; k < kPostOps; ++k) {
-    const uint64_t i = base + (uint64_t)k * kPostBlock;
-    op[k] = 0xFF;
-    if (i < n) {
-      op[k] = ops ? ops[i] : (uint8_t)VS_OP_INSERT;
-      res[k] = result[i];
-      pos[k] = index[i];
+    for (int k = 0; k < kPostOps; ++k) {
+      op[k] = (uint8_t)(ow >> (8 * k));
+      res[k] = (uint8_t)(rw >> (8 * k));
+      pos[k] = pv[k & 3];
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kPostOps; ++k) {
+      const uint64_t i = base + (uint64_t)k * kStep;
+      op[k] = 0xFF;
+      if (i < n) {
+        op[k] = ops ? ops[i] : (uint8_t)VS_OP_INSERT;
+        res[k] = result[i];
+        pos[k] = index[i];
+      }
     }
   }
   uint32_t vac[kPostOps];
@@ -423,7 +447,7 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
 #endif
 #pragma unroll
   for (int k = 0; k < kPostOps; ++k) {
-    const uint64_t i = base + (uint64_t)k * kPostBlock;
+    const uint64_t i = base + (uint64_t)k * kStep;
     if (op[k] == VS_OP_INSERT && res[k]) {
       const uint32_t bit = 1u << ((uint32_t)pos[k] & 31u);
       if (dw[k] & bit) {
@@ -445,7 +469,7 @@ __global__ void __launch_bounds__(kPostBlock) k_post(TableView T, const int32_t*
 #else
 #pragma unroll
   for (int k = 0; k < kPostOps; ++k) {
-    const uint64_t i = base + (uint64_t)k * kPostBlock;
+    const uint64_t i = base + (uint64_t)k * kStep;
     if (op[k] == VS_OP_INSERT && res[k]) {
       post_op(T, keys, i, VS_OP_INSERT, result, pos[k]);
     } else if (op[k] == VS_OP_ERASE && res[k] && pos[k] >= (int32_t)T.n) {
@@ -470,7 +494,10 @@ static cudaError_t launch_post(const TableView& v, const int32_t* keys, const ui
   attr[0].val.programmaticStreamSerializationAllowed = VSB_PDL && n >= (1u << 16);
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_post, v, keys, ops, n, result, index);
+  const bool vec = VSB_POST_VEC && kPostOps == 4 && (((uintptr_t)ops | (uintptr_t)result) & 3u) == 0 &&
+                   ((uintptr_t)index & 15u) == 0;
+  return vec ? cudaLaunchKernelEx(&cfg, k_post<VSB_POST_VEC != 0>, v, keys, ops, n, result, index)
+             : cudaLaunchKernelEx(&cfg, k_post<false>, v, keys, ops, n, result, index);
 }
 
 // Push vacated excess positions back onto the striped free list (warp-
